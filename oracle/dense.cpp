@@ -1,0 +1,293 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY (see dense.hpp).
+#include "dense.hpp"
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <numeric>
+#include <stdexcept>
+
+namespace oracle {
+
+Mat Mat::transpose() const {
+  Mat t(c, r);
+  for (index_t i = 0; i < r; ++i)
+    for (index_t j = 0; j < c; ++j) t(j, i) = (*this)(i, j);
+  return t;
+}
+
+double Mat::max_abs() const {
+  double m = 0.0;
+  for (double v : a) m = std::max(m, std::abs(v));
+  return m;
+}
+
+Mat matmul(const Mat& A, const Mat& B) {
+  if (A.c != B.r) throw std::invalid_argument("matmul shape");
+  Mat C(A.r, B.c);
+  for (index_t i = 0; i < A.r; ++i)
+    for (index_t k = 0; k < A.c; ++k) {
+      const double aik = A(i, k);
+      if (aik == 0.0) continue;
+      for (index_t j = 0; j < B.c; ++j) C(i, j) += aik * B(k, j);
+    }
+  return C;
+}
+
+Mat matmul_tn(const Mat& A, const Mat& B) {
+  if (A.r != B.r) throw std::invalid_argument("matmul_tn shape");
+  Mat C(A.c, B.c);
+  for (index_t k = 0; k < A.r; ++k)
+    for (index_t i = 0; i < A.c; ++i) {
+      const double aki = A(k, i);
+      if (aki == 0.0) continue;
+      for (index_t j = 0; j < B.c; ++j) C(i, j) += aki * B(k, j);
+    }
+  return C;
+}
+
+Mat matmul_nt(const Mat& A, const Mat& B) {
+  if (A.c != B.c) throw std::invalid_argument("matmul_nt shape");
+  Mat C(A.r, B.r);
+  for (index_t i = 0; i < A.r; ++i)
+    for (index_t j = 0; j < B.r; ++j) {
+      double s = 0.0;
+      for (index_t k = 0; k < A.c; ++k) s += A(i, k) * B(j, k);
+      C(i, j) = s;
+    }
+  return C;
+}
+
+// Unblocked left-looking Cholesky over the lower triangle, failing on a
+// non-positive pivot (Eigen llt_inplace::unblocked semantics).
+bool llt_lower(Mat& P) {
+  const index_t n = P.r;
+  for (index_t j = 0; j < n; ++j) {
+    double d = P(j, j);
+    for (index_t k = 0; k < j; ++k) d -= P(j, k) * P(j, k);
+    if (!(d > 0.0)) return false;
+    d = std::sqrt(d);
+    P(j, j) = d;
+    for (index_t i = j + 1; i < n; ++i) {
+      double s = P(i, j);
+      for (index_t k = 0; k < j; ++k) s -= P(i, k) * P(j, k);
+      P(i, j) = s / d;
+    }
+  }
+  for (index_t i = 0; i < n; ++i)
+    for (index_t j = i + 1; j < n; ++j) P(i, j) = 0.0;
+  return true;
+}
+
+void trsm_lower_left(const Mat& L, Mat& Y) {
+  const index_t n = L.r;
+  for (index_t i = 0; i < n; ++i) {
+    for (index_t k = 0; k < i; ++k) {
+      const double lik = L(i, k);
+      if (lik == 0.0) continue;
+      for (index_t j = 0; j < Y.c; ++j) Y(i, j) -= lik * Y(k, j);
+    }
+    const double d = L(i, i);
+    for (index_t j = 0; j < Y.c; ++j) Y(i, j) /= d;
+  }
+}
+
+void trsv_lower(const Mat& L, double* y) {
+  const index_t n = L.r;
+  for (index_t i = 0; i < n; ++i) {
+    double s = y[i];
+    for (index_t k = 0; k < i; ++k) s -= L(i, k) * y[k];
+    y[i] = s / L(i, i);
+  }
+}
+
+void trsv_lower_t(const Mat& L, double* y) {
+  const index_t n = L.r;
+  for (index_t i = n - 1; i >= 0; --i) {
+    double s = y[i];
+    for (index_t k = i + 1; k < n; ++k) s -= L(k, i) * y[k];
+    y[i] = s / L(i, i);
+  }
+}
+
+double gauge_weight(index_t k) {
+  // 1 + 0.5 * frac((k+1) * (sqrt(5)-1)/2): positive, irregular, deterministic.
+  const double x = static_cast<double>(k + 1) * 0.6180339887498949;
+  return 1.0 + 0.5 * (x - std::floor(x));
+}
+
+namespace {
+
+// Householder QR of A (m x n, row-major, in place), LAPACK sign convention.
+// On return the upper trapezoid of A holds R (min(m,n) x n); below is junk.
+void householder_r(Mat& A) {
+  const index_t m = A.r, n = A.c;
+  const index_t kmax = std::min(m, n);
+  std::vector<double> v(static_cast<size_t>(m));
+  for (index_t k = 0; k < kmax; ++k) {
+    double nrm2 = 0.0;
+    for (index_t i = k; i < m; ++i) nrm2 += A(i, k) * A(i, k);
+    const double nrm = std::sqrt(nrm2);
+    if (nrm == 0.0) continue;
+    const double xk = A(k, k);
+    const double beta = xk >= 0.0 ? -nrm : nrm;
+    // v = x - beta e_k, tau = 2 / v^T v
+    v[static_cast<size_t>(k)] = xk - beta;
+    double vtv = v[static_cast<size_t>(k)] * v[static_cast<size_t>(k)];
+    for (index_t i = k + 1; i < m; ++i) {
+      v[static_cast<size_t>(i)] = A(i, k);
+      vtv += A(i, k) * A(i, k);
+    }
+    const double tau = 2.0 / vtv;
+    A(k, k) = beta;
+    for (index_t i = k + 1; i < m; ++i) A(i, k) = 0.0;
+    for (index_t j = k + 1; j < n; ++j) {
+      double s = 0.0;
+      for (index_t i = k; i < m; ++i) s += v[static_cast<size_t>(i)] * A(i, j);
+      s *= tau;
+      for (index_t i = k; i < m; ++i) A(i, j) -= s * v[static_cast<size_t>(i)];
+    }
+  }
+}
+
+}  // namespace
+
+SvdLeft svd_left(const Mat& F) {
+  const index_t b = F.r, f = F.c;
+  SvdLeft out;
+  const index_t m = std::min(b, f);
+  // R = triu(qr(F^T)), m x b.
+  Mat T = F.transpose();  // f x b
+  householder_r(T);
+  Mat R(m, b);
+  for (index_t i = 0; i < m; ++i)
+    for (index_t j = i; j < b; ++j) R(i, j) = T(i, j);
+
+  // One-sided Jacobi on the columns of R; V accumulates the rotations.
+  Mat V = Mat::identity(b);
+  const double tol = std::sqrt(static_cast<double>(std::max<index_t>(m, 1))) * DBL_EPSILON;
+  int sweep = 0;
+  for (; sweep < 100; ++sweep) {
+    bool rotated = false;
+    for (index_t p = 0; p < b - 1; ++p) {
+      for (index_t q = p + 1; q < b; ++q) {
+        double alpha = 0.0, beta = 0.0, gamma = 0.0;
+        for (index_t i = 0; i < m; ++i) {
+          alpha += R(i, p) * R(i, p);
+          beta += R(i, q) * R(i, q);
+          gamma += R(i, p) * R(i, q);
+        }
+        if (alpha == 0.0 || beta == 0.0) continue;
+        if (!(std::abs(gamma) > tol * std::sqrt(alpha) * std::sqrt(beta))) continue;
+        rotated = true;
+        const double zeta = (beta - alpha) / (2.0 * gamma);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / std::sqrt(1.0 + t * t);
+        const double sn = cs * t;
+        for (index_t i = 0; i < m; ++i) {
+          const double ap = R(i, p), aq = R(i, q);
+          R(i, p) = cs * ap - sn * aq;
+          R(i, q) = sn * ap + cs * aq;
+        }
+        for (index_t i = 0; i < b; ++i) {
+          const double vp = V(i, p), vq = V(i, q);
+          V(i, p) = cs * vp - sn * vq;
+          V(i, q) = sn * vp + cs * vq;
+        }
+      }
+    }
+    if (!rotated) break;
+  }
+  out.sweeps = sweep + 1;
+
+  std::vector<double> norms(static_cast<size_t>(b));
+  for (index_t j = 0; j < b; ++j) {
+    double s = 0.0;
+    for (index_t i = 0; i < m; ++i) s += R(i, j) * R(i, j);
+    norms[static_cast<size_t>(j)] = std::sqrt(s);
+  }
+  std::vector<index_t> order(static_cast<size_t>(b));
+  std::iota(order.begin(), order.end(), index_t{0});
+  std::stable_sort(order.begin(), order.end(), [&](index_t x, index_t y) {
+    return norms[static_cast<size_t>(x)] > norms[static_cast<size_t>(y)];
+  });
+  out.V = Mat(b, b);
+  for (index_t k = 0; k < b; ++k)
+    for (index_t i = 0; i < b; ++i) out.V(i, k) = V(i, order[static_cast<size_t>(k)]);
+  out.sigma.resize(static_cast<size_t>(m));
+  for (index_t k = 0; k < m; ++k) out.sigma[static_cast<size_t>(k)] = norms[static_cast<size_t>(order[static_cast<size_t>(k)])];
+  return out;
+}
+
+Mat canonical_basis(const Mat& V, index_t r) {
+  const index_t b = V.r;
+  Mat U(b, b);
+  // U1: sign-fixed leading singular vectors.
+  Mat A(b, r);
+  for (index_t k = 0; k < r; ++k) {
+    double g = 0.0;
+    for (index_t i = 0; i < b; ++i) g += gauge_weight(i) * V(i, k);
+    const double s = g >= 0.0 ? 1.0 : -1.0;
+    for (index_t i = 0; i < b; ++i) {
+      U(i, k) = s * V(i, k);
+      A(i, k) = U(i, k);
+    }
+  }
+  // Householder QR of U1 with generic sign rule; Q = H_0 ... H_{r-1}.
+  std::vector<std::vector<double>> vs(static_cast<size_t>(r));
+  std::vector<double> taus(static_cast<size_t>(r), 0.0);
+  for (index_t k = 0; k < r; ++k) {
+    double nrm2 = 0.0, rest2 = 0.0, g = 0.0;
+    for (index_t i = k; i < b; ++i) {
+      nrm2 += A(i, k) * A(i, k);
+      if (i > k) rest2 += A(i, k) * A(i, k);
+      g += gauge_weight(i) * A(i, k);
+    }
+    const double nrm = std::sqrt(nrm2);
+    std::vector<double>& v = vs[static_cast<size_t>(k)];
+    v.assign(static_cast<size_t>(b), 0.0);
+    if (nrm == 0.0) continue;
+    const double s = g >= 0.0 ? 1.0 : -1.0;
+    const double xk = A(k, k);
+    const double beta = -s * nrm;
+    double vk;
+    if (xk == 0.0 || (xk > 0.0) == (s > 0.0)) {
+      vk = xk - beta;  // same signs: no cancellation
+    } else {
+      vk = -rest2 / (xk + beta);  // Parlett: x_k - beta = (x_k^2 - nrm^2)/(x_k + beta)
+    }
+    v[static_cast<size_t>(k)] = vk;
+    double vtv = vk * vk;
+    for (index_t i = k + 1; i < b; ++i) {
+      v[static_cast<size_t>(i)] = A(i, k);
+      vtv += A(i, k) * A(i, k);
+    }
+    const double tau = vtv > 0.0 ? 2.0 / vtv : 0.0;
+    taus[static_cast<size_t>(k)] = tau;
+    for (index_t j = k; j < r; ++j) {
+      double d = 0.0;
+      for (index_t i = k; i < b; ++i) d += v[static_cast<size_t>(i)] * A(i, j);
+      d *= tau;
+      for (index_t i = k; i < b; ++i) A(i, j) -= d * v[static_cast<size_t>(i)];
+    }
+  }
+  // Q[:, r:] = H_0 ... H_{r-1} E_{r:}
+  Mat Q(b, b - r);
+  for (index_t j = 0; j < b - r; ++j) Q(r + j, j) = 1.0;
+  for (index_t k = r - 1; k >= 0; --k) {
+    const std::vector<double>& v = vs[static_cast<size_t>(k)];
+    const double tau = taus[static_cast<size_t>(k)];
+    if (tau == 0.0) continue;
+    for (index_t j = 0; j < b - r; ++j) {
+      double d = 0.0;
+      for (index_t i = k; i < b; ++i) d += v[static_cast<size_t>(i)] * Q(i, j);
+      d *= tau;
+      for (index_t i = k; i < b; ++i) Q(i, j) -= d * v[static_cast<size_t>(i)];
+    }
+  }
+  for (index_t i = 0; i < b; ++i)
+    for (index_t j = 0; j < b - r; ++j) U(i, r + j) = Q(i, j);
+  return U;
+}
+
+}  // namespace oracle
