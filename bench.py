@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 CE hot path: factorize -> PCG (BASELINE.json configs[1] by default).
+
+One "step" = ce_factorize of the device-resident CSB matrix (host plan, device factor)
+followed by a device PCG solve to the config's tolerance.  `value` = factorization
+unknowns/s over all ranks (N x n x K / max-over-ranks factor time).  Each rank runs
+its own copy of the workload (replicas; SURVEY.md §8e subdomain sharding is the
+next step), so scaling is weak.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--cfg C] [--grid NX NY NZ]
+  python bench.py --impl reference ...   # CPU oracle restatement (rank 0 only)
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "factorization unknowns/sec (fp64) + PCG solve time; % of HBM/FP64 roofline"
+# CPU sample of the same workload family (stencil, B, eps) sized for ~10 s of oracle work
+CPU_SAMPLE_GRID = {1: (128, 128, 0), 2: (192, 192, 0), 3: (192, 192, 0), 4: (16, 16, 16), 5: (16, 16, 16)}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--cfg", type=int, default=2)
+    ap.add_argument("--grid", type=int, nargs=3, default=[0, 0, 0])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload_name(cfg, grid):
+    names = {1: "2D Poisson 128x128 B=8 eps=1e-4 PCG 1e-8", 2: "2D Poisson 1024x1024 B=16 eps=1e-6 PCG 1e-10",
+             3: "2D variable-k diffusion 2048x2048 B=16 eps=1e-6 PCG 1e-8",
+             4: "3D Poisson 128^3 B=32 eps=1e-5 PCG 1e-8", 5: "3D variable-k diffusion 256^3 B=32 eps=1e-4 PCG 1e-6"}
+    s = f"cfg{cfg}: {names[cfg]}"
+    if any(grid):
+        s += f" (grid override {grid[0]}x{grid[1]}x{grid[2]})"
+    return s
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        cmd = ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+               "--format=csv,noheader,nounits", "-lms", "200"]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.3)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if "Active" in s[3 + k]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def fp64_gemm_tflops(torch, dev):
+    """Achievable FP64 (DMMA) peak via cuBLAS DGEMM, the FP64 roofline denominator."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    for _ in range(2):
+        torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, 2 * n ** 3 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    del a, b
+    torch.cuda.empty_cache()
+    return best
+
+
+def cpu_oracle_run(cfg, grid, solve=True):
+    """Time the CPU oracle restatement (single thread, as the reference) on one sample."""
+    cli = os.path.join(ROOT, "oracle", "oracle_cli")
+    if not os.path.exists(cli):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "-j8"], check=True, capture_output=True)
+    args = [cli, str(cfg)] + [str(g) for g in grid if g > 0]
+    if not solve:
+        args.append("--no-solve")
+    out = subprocess.run(args, check=True, capture_output=True, text=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    grid = CPU_SAMPLE_GRID[args.cfg]
+    for _ in range(args.warmup):
+        cpu_oracle_run(args.cfg, grid)
+    vals, fac, pcg_s = [], [], []
+    t0 = time.time()
+    for _ in range(args.steps):
+        r = cpu_oracle_run(args.cfg, grid)
+        vals.append(r["unknowns_per_sec"])
+        fac.append(r["factor_seconds"])
+        pcg_s.append(r.get("pcg_seconds", 0.0))
+    wall = time.time() - t0
+    v = statistics.mean(vals)
+    sample = (f"oracle/oracle_cli cfg{args.cfg} on a {grid[0]}x{grid[1]}" + (f"x{grid[2]}" if grid[2] else "") +
+              f" grid (n={r['n']}, same stencil/B/eps), full factorization + PCG, 1 thread")
+    line = {"metric": METRIC, "value": v, "unit": "unknowns/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args.cfg, list(grid)), "cfg": args.cfg},
+            "pcg_solve_ms": 1e3 * statistics.mean(pcg_s), "factor_ms": 1e3 * statistics.mean(fac),
+            "cpu_baseline": {"value": v, "unit": "unknowns/s", "cores": 1, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_product(args):
+    import torch
+    import paper_1603_09133_b200 as ce
+    from paper_1603_09133_b200._lib import lib
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    prob = ce.Problem(args.cfg, *args.grid)
+    n = prob.n
+    ctx = ce.Context.get(local)
+    host_a = prob.matrix()
+    a = ce.DeviceMatrix(host_a, ctx)
+    b = torch.from_numpy(prob.rhs).to(dev)
+    strategy = prob.strategy()
+    popts = ce.PcgOptions(tol=prob.tol, maxit=1000)
+    import ctypes as C
+    sp = C.c_void_p()
+    lib.ce_ctx_stream(ctx.handle, C.byref(sp))
+    stream = torch.cuda.ExternalStream(sp.value, device=dev)
+
+    fp64_peak = fp64_gemm_tflops(torch, dev)
+    peaks, peak_kind = measured_peaks()
+
+    def step(record):
+        with torch.cuda.stream(stream):
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            f = ce.ce_factorize(a, prob.plan, strategy, ce.FactorOptions(), ctx)
+            e1.record(stream)
+            rep, x = ce.pcg(a, n, b, f, popts)
+            e2.record(stream)
+        e2.synchronize()
+        st = f.stats
+        if record is not None:
+            record.append(dict(fac=e0.elapsed_time(e1) * 1e-3, pcg=e1.elapsed_time(e2) * 1e-3, its=rep.iterations,
+                               resid=rep.final_true_residual, conv=rep.converged, sweep=st["sweep_kernel_seconds"],
+                               abytes=st["algorithmic_bytes"], aflops=st["algorithmic_flops"], levels=st["n_levels"],
+                               tail=st["tail_dim"], host=st["total_seconds"]))
+        del f
+
+    for _ in range(args.warmup):
+        step(None)
+    clocks = ClockSampler(local)
+    recs = []
+    barrier()
+    clocks.start()
+    launches0 = lib.ce_launch_count()
+    t_wall = time.time()
+    for _ in range(args.steps):
+        step(recs)
+    barrier()
+    wall = time.time() - t_wall
+    launches = lib.ce_launch_count() - launches0
+    ck = clocks.stop()
+
+    fac_total = allmax(sum(r["fac"] for r in recs))
+    step_total = allmax(sum(r["fac"] + r["pcg"] for r in recs))
+    value = world * n * args.steps / fac_total
+    sweep_t = sum(r["sweep"] for r in recs) / len(recs)
+    abytes = recs[-1]["abytes"]
+    aflops = recs[-1]["aflops"]
+    gbs = abytes / sweep_t / 1e9
+    tfl = aflops / sweep_t / 1e12
+    f_hbm = gbs / peaks["hbm_gbs"]
+    f_fp64 = tfl / fp64_peak
+    bound = "hbm" if f_hbm >= f_fp64 else "fp64"
+
+    # end-to-end through the public API with host buffers: H2D upload of A and b, factorize, PCG, D2H x
+    e2e_t = []
+    h2d = host_a.values.nbytes + host_a.offsets.nbytes + host_a.row_ptr.nbytes + host_a.col_idx.nbytes + \
+        host_a.val_ptr.nbytes + prob.rhs.nbytes
+    for _ in range(args.e2e_steps):
+        barrier()
+        t0 = time.time()
+        a2 = ce.DeviceMatrix(host_a, ctx)
+        f2 = ce.ce_factorize(a2, prob.plan, strategy, ce.FactorOptions(), ctx)
+        rep2, x2 = ce.pcg(a2, n, prob.rhs, f2, popts)
+        e2e_t.append(time.time() - t0)
+        del f2, a2
+    e2e_val = world * n / allmax(statistics.mean(e2e_t))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        grid = CPU_SAMPLE_GRID[args.cfg]
+        r = cpu_oracle_run(args.cfg, grid, solve=False)
+        cpu = {"value": r["unknowns_per_sec"], "unit": "unknowns/s", "cores": 1, "kind": "port",
+               "sample": f"oracle/oracle_cli cfg{args.cfg} on a {grid[0]}x{grid[1]}" + (f"x{grid[2]}" if grid[2] else "")
+               + f" grid (n={r['n']}), full factorization, 1 thread of {os.cpu_count()}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "unknowns/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * step_total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE cfg generator, seeded N(0,1) rhs)",
+            "config": {"workload": workload_name(args.cfg, args.grid), "cfg": args.cfg, "n": n,
+                       "parallelism": f"replicas x{world}", "l2": "inputs > L2 (A is %.2f GB)" % (host_a.values.nbytes / 1e9)},
+            "factor_ms": 1e3 * fac_total / args.steps, "pcg_solve_ms": 1e3 * (step_total - fac_total) / args.steps,
+            "pcg_iterations": recs[-1]["its"], "pcg_true_residual": recs[-1]["resid"], "pcg_converged": recs[-1]["conv"],
+            "levels": recs[-1]["levels"], "tail_dim": recs[-1]["tail"],
+            "roofline": {"bound": bound, "kernel": "level sweep (compress+eliminate), summed over levels",
+                         "achieved": gbs if bound == "hbm" else tfl,
+                         "peak": peaks["hbm_gbs"] if bound == "hbm" else fp64_peak,
+                         "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
+                         "frac": f_hbm if bound == "hbm" else f_fp64, "traffic": None,
+                         "hbm": {"achieved_gbs": gbs, "peak_gbs": peaks["hbm_gbs"], "frac": f_hbm, "peak_kind": peak_kind},
+                         "fp64": {"achieved_tflops": tfl, "peak_tflops": fp64_peak, "frac": f_fp64,
+                                  "peak_kind": "measured live: cuBLAS DGEMM 8192^3"},
+                         "sweep_ms_per_step": 1e3 * sweep_t, "algorithmic_bytes": abytes, "algorithmic_flops": aflops},
+            "e2e": {"value": e2e_val, "unit": "unknowns/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 * n,
+                    "region": "H2D upload of A + b, factorize, PCG, D2H x (pageable host buffers)"},
+            "gpu_launches": int(launches),
+            "clocks": ck,
+            "wall_s": wall,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_product(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,191 @@
+/* ce_gpu.h — C-ABI of the B200-native compress-and-eliminate (CE) hot path.
+ *
+ * Drop-in boundary for the reference's public header set proj/include/ce/
+ * (SURVEY.md §8b).  Every entry point names the reference interface it
+ * replaces.  Plain pointers and sizes only; no exceptions cross the ABI.
+ * Return codes equal the reference CLI exit codes (proj/include/ce/cli.hpp:16-19):
+ *   CE_OK 0, CE_EUSAGE 1 (usage / IO / invalid argument / CUDA failure),
+ *   CE_EBREAKDOWN 2 (BreakdownError, proj/include/ce/types.hpp:26-36),
+ *   CE_ENOCONV 3 (Krylov non-convergence).
+ * The factor is device-resident and opaque.  There is no CPU fallback: every
+ * compute entry point fails with CE_EUSAGE when no sm_100 device is present.
+ */
+#ifndef CE_GPU_H
+#define CE_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CE_OK 0
+#define CE_EUSAGE 1
+#define CE_EBREAKDOWN 2
+#define CE_ENOCONV 3
+
+typedef struct ce_ctx ce_ctx;
+typedef struct ce_matrix ce_matrix;
+typedef struct ce_factor ce_factor;
+typedef struct ce_problem ce_problem;
+
+/* Host CSB matrix: the reference BlockSparseMatrix (proj/include/ce/block_matrix.hpp:23-63):
+ * a BlockPartition (m+1 offsets), a structurally symmetric BlockSparsityPattern with full
+ * diagonal (CSR over block rows, both triangles, sorted columns) and one dense row-major
+ * block per pattern slot (values[val_ptr[k] ...], b_i x b_j). */
+typedef struct {
+  int64_t n;                /* scalar dimension */
+  int64_t m;                /* block count */
+  const int64_t* offsets;   /* m + 1 */
+  const int64_t* row_ptr;   /* m + 1 */
+  const int64_t* col_idx;   /* nnzb */
+  const int64_t* val_ptr;   /* nnzb + 1 */
+  const double* values;
+} ce_csb_host;
+
+/* Host CoarseningPlan (proj/include/ce/problems.hpp:51-65): per plan level, the block -> group
+ * assignment (the reference's plan text format, problems.cpp:114-136).  The initial permutation
+ * is applied by the caller before assembling the CSB (cli.cpp:49-58), so it is not needed here. */
+typedef struct {
+  int64_t join;               /* J used once the plan levels are exhausted (factorization.cpp:18-26) */
+  int64_t n_levels;
+  const int64_t* level_blocks;  /* n_levels: blocks at each plan level */
+  const int64_t* assign;        /* concatenated assignments, sum(level_blocks) entries */
+} ce_plan_host;
+
+/* CompressionStrategy (proj/include/ce/compression.hpp:15-38). mode 0 = AdaptiveEps, 1 = FixedRank. */
+typedef struct {
+  int mode;
+  double eps;
+  int absolute;
+  int64_t rank;
+} ce_strategy;
+
+/* FactorOptions (proj/include/ce/factorization.hpp:74-77) + parity hook: forced ranks per
+ * (level, row), -1 = free (SURVEY.md §8c "--force-ranks"). */
+typedef struct {
+  int64_t dense_threshold;    /* default 2048 */
+  int64_t max_levels;         /* default 64 */
+  int64_t n_forced_levels;
+  const int64_t* forced_counts;
+  const int64_t* forced;      /* concatenated */
+} ce_factor_opts;
+
+/* Error context: BreakdownError{level, block} (types.hpp:26-36), block = -1 for the dense tail. */
+typedef struct {
+  int code;
+  int level;
+  int64_t block;
+  int64_t shift_retries;
+  char message[256];
+} ce_status;
+
+/* MinresOptions-shaped PCG options (proj/include/ce/minres.hpp:34-38). */
+typedef struct {
+  double tol;
+  int64_t maxit;
+  int track_true_residual;
+} ce_pcg_opts;
+
+/* SolveReport (proj/include/ce/minres.hpp:25-31). */
+typedef struct {
+  int converged;
+  int64_t iterations;
+  double final_recurrence_residual;
+  double final_true_residual;
+  double seconds;
+} ce_solve_report;
+
+/* FactorStats summary (proj/include/ce/factorization.hpp:56-72). */
+typedef struct {
+  int64_t n_levels;
+  int64_t tail_dim;
+  double factor_blocks;
+  double predicted_factor_blocks;
+  int64_t l_scalar_nnz;
+  int64_t l_payload_bytes;
+  int64_t q_payload_bytes;
+  int64_t tail_bytes;
+  int64_t shift_retries;
+  double total_seconds;         /* host wall time of ce_factorize */
+  double device_seconds;        /* CUDA-event time of the device work */
+  double sweep_kernel_seconds;  /* CUDA-event time of the level sweep kernels */
+  double algorithmic_bytes;     /* SURVEY.md §8d per-row byte contract, summed */
+  double algorithmic_flops;     /* SURVEY.md §8d per-row flop contract, summed */
+} ce_factor_stats;
+
+/* LevelStats (factorization.hpp:38-54) for level l (0-based). */
+typedef struct {
+  int64_t block_count, pattern_blocks, factor_blocks, eliminated, retained, max_rank;
+  double mean_rank;
+  double seconds;              /* CUDA-event time of the level's device work */
+  int64_t l_bytes, q_bytes, shift_retries;
+  int64_t max_block, max_far_cols, max_close;
+  double sweep_seconds;        /* CUDA-event time of the sweep kernel alone */
+  double algorithmic_bytes, algorithmic_flops;
+} ce_level_stats;
+
+/* ---- context / device ---- */
+int ce_ctx_create(int device, ce_ctx** out);
+void ce_ctx_destroy(ce_ctx* ctx);
+const char* ce_last_error(void);
+/* Number of sm_100 devices visible (0 when none). */
+int ce_device_count(void);
+/* The context's CUDA stream (cudaStream_t), for event timing by the caller. */
+int ce_ctx_stream(const ce_ctx* ctx, void** stream);
+/* Kernels launched by this library since it was loaded (launch accounting for benchmarks). */
+int64_t ce_launch_count(void);
+
+/* ---- operator: BlockSparseMatrix on the device ---- */
+/* Upload a host CSB (replaces BlockSparseMatrix construction, block_matrix.cpp:11-27). */
+int ce_matrix_upload(ce_ctx* ctx, const ce_csb_host* a, ce_matrix** out);
+void ce_matrix_free(ce_matrix* a);
+int64_t ce_matrix_dim(const ce_matrix* a);
+/* y = A x (replaces BlockSparseMatrix::matvec, block_matrix.cpp:92-105; ApplyFn at cli.cpp:198).
+ * on_device != 0: x, y are device pointers used on `stream`; else host arrays (copies included). */
+int ce_matvec(const ce_matrix* a, const double* x, double* y, int64_t n, int on_device, void* stream);
+
+/* ---- factorization ---- */
+/* Replaces ce_factorize(const BlockSparseMatrix&, const CoarseningPlan&, const CompressionStrategy&,
+ * const FactorOptions&) (factorization.hpp:121-123, factorization.cpp:336-461). */
+int ce_factorize(ce_ctx* ctx, const ce_matrix* a, const ce_plan_host* plan, const ce_strategy* s,
+                 const ce_factor_opts* opts, ce_factor** out, ce_status* st);
+void ce_factor_free(ce_factor* f);
+int64_t ce_factor_dim(const ce_factor* f);
+/* Preconditioner apply x = Q^T L^-T L^-1 Q b (replaces CEFactorization::solve,
+ * factorization.cpp:140-168; used as ApplyFn at cli.cpp:225). */
+int ce_apply_precond(const ce_factor* f, const double* b, double* x, int64_t n, int on_device, void* stream);
+/* Validation tools (factorization.cpp:170-257): which 0 = apply_operator (Q^T L L^T Q x),
+ * 1 = apply_q, 2 = apply_q_transpose.  Host arrays. */
+int ce_factor_apply_tool(const ce_factor* f, int which, const double* x, double* y, int64_t n);
+int ce_factor_get_stats(const ce_factor* f, ce_factor_stats* out);
+int ce_factor_get_level_stats(const ce_factor* f, int64_t level, ce_level_stats* out);
+/* Binary factor dump in the oracle's format, for parity checks. */
+int ce_factor_dump(const ce_factor* f, const char* path);
+
+/* ---- Krylov ---- */
+/* PCG with the minres contract (minres.hpp:46-47): x0 = 0, stop when the
+ * recurrence ||r||/||b|| <= tol, iterations = number of A*p products.  precond may be NULL
+ * (unpreconditioned).  on_device != 0: b, x are device pointers. */
+int ce_pcg(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const double* b, double* x, int64_t n,
+           int on_device, const ce_pcg_opts* opts, ce_solve_report* rep);
+
+/* ---- BASELINE problem generation (setup, untimed; SURVEY.md §8d conventions) ----
+ * cfg 1..5, optional grid override (0 = keep).  Builds the permuted CSB, plan and rhs on the host
+ * (replaces assemble_diffusion_3d + geometric_block_ordering + finish_load, problems.cpp:18-258,
+ * cli.cpp:33-58, extended with the 2-D/FV/random-k/RNG inputs BASELINE.json names). */
+int ce_problem_create(int cfg, int64_t nx, int64_t ny, int64_t nz, ce_problem** out);
+void ce_problem_free(ce_problem* p);
+/* Views into the problem (valid until ce_problem_free). */
+int ce_problem_csb(const ce_problem* p, ce_csb_host* out);
+int ce_problem_plan(const ce_problem* p, ce_plan_host* out);
+const double* ce_problem_rhs(const ce_problem* p);
+const int64_t* ce_problem_perm(const ce_problem* p);
+/* eps, tol, block of the config. */
+int ce_problem_params(const ce_problem* p, double* eps, double* tol, int64_t* block);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CE_GPU_H */

@@ -102,6 +102,32 @@ int oracle_problem_triplets(long long n, long long nnz, const long long* rows, c
 
 void oracle_problem_free(void* p) { delete static_cast<OProblem*>(p); }
 
+// Conditioning probe: multiply every off-diagonal-symmetric pair of stored values by
+// (1 + rel * z), z a deterministic N(0,1) draw; the matrix stays exactly symmetric.
+void oracle_problem_perturb(void* h, double rel, unsigned long long seed) {
+  auto* p = static_cast<OProblem*>(h);
+  auto& a = p->matrix;
+  const index_t m = a.partition().block_count();
+  for (index_t i = 0; i < m; ++i)
+    for (index_t j : a.pattern().row(i)) {
+      if (j > i) continue;
+      Mat& bij = a.block(i, j);
+      Mat& bji = a.block(j, i);
+      for (index_t r = 0; r < bij.r; ++r)
+        for (index_t c = 0; c < bij.c; ++c) {
+          if (i == j && c > r) continue;
+          const std::uint64_t key = static_cast<std::uint64_t>(((i * 1000003 + j) * 64 + r) * 64 + c);
+          const double f = 1.0 + rel * normal_sample(seed, 7, key);
+          bij(r, c) *= f;
+          if (i == j) {
+            if (c != r) bij(c, r) = bij(r, c);
+          } else {
+            bji(c, r) = bij(r, c);
+          }
+        }
+    }
+}
+
 long long oracle_problem_n(void* p) { return static_cast<OProblem*>(p)->matrix.dim(); }
 long long oracle_problem_m(void* p) { return static_cast<OProblem*>(p)->matrix.partition().block_count(); }
 long long oracle_problem_nnzb(void* p) { return static_cast<OProblem*>(p)->matrix.pattern().stored_blocks(); }

@@ -110,9 +110,12 @@ void trsv_lower_t(const Mat& L, double* y) {
   }
 }
 
-double gauge_weight(index_t k) {
-  // 1 + 0.5 * frac((k+1) * (sqrt(5)-1)/2): positive, irregular, deterministic.
-  const double x = static_cast<double>(k + 1) * 0.6180339887498949;
+double gauge_weight(index_t k) { return gauge_weight2(k, 0); }
+
+double gauge_weight2(index_t k, index_t j) {
+  // 1 + 0.5 * frac((k+1) * c_j), c_j = (sqrt(5)-1)/2 + j (sqrt(2)-1)/2: positive, irregular, deterministic.
+  const double cj = 0.6180339887498949 + 0.2071067811865475 * static_cast<double>(j);
+  const double x = static_cast<double>(k + 1) * cj;
   return 1.0 + 0.5 * (x - std::floor(x));
 }
 
@@ -219,20 +222,51 @@ SvdLeft svd_left(const Mat& F) {
   return out;
 }
 
-Mat canonical_basis(const Mat& V, index_t r) {
+Mat canonical_basis(const Mat& V, const std::vector<double>& sigma, index_t r) {
   const index_t b = V.r;
   Mat U(b, b);
-  // U1: sign-fixed leading singular vectors.
+  // U1: leading singular vectors; clusters of (numerically) equal singular values
+  // get the basis orth(P_c G_c) of their span, singletons a sign fix.
   Mat A(b, r);
-  for (index_t k = 0; k < r; ++k) {
-    double g = 0.0;
-    for (index_t i = 0; i < b; ++i) g += gauge_weight(i) * V(i, k);
-    const double s = g >= 0.0 ? 1.0 : -1.0;
-    for (index_t i = 0; i < b; ++i) {
-      U(i, k) = s * V(i, k);
-      A(i, k) = U(i, k);
+  const index_t ns = static_cast<index_t>(sigma.size());
+  index_t k0 = 0;
+  while (k0 < r) {
+    index_t k1 = k0 + 1;
+    while (k1 < r && k1 < ns && sigma[static_cast<size_t>(k1 - 1)] - sigma[static_cast<size_t>(k1)] <= kClusterTol * sigma[0]) ++k1;
+    const index_t c = k1 - k0;
+    if (c == 1) {
+      double g = 0.0;
+      for (index_t i = 0; i < b; ++i) g += gauge_weight(i) * V(i, k0);
+      const double s = g >= 0.0 ? 1.0 : -1.0;
+      for (index_t i = 0; i < b; ++i) A(i, k0) = s * V(i, k0);
+    } else {
+      // Z = U_c (U_c^T G_c)
+      for (index_t j = 0; j < c; ++j) {
+        for (index_t i = 0; i < b; ++i) A(i, k0 + j) = 0.0;
+        for (index_t q = 0; q < c; ++q) {
+          double m = 0.0;
+          for (index_t i = 0; i < b; ++i) m += V(i, k0 + q) * gauge_weight2(i, j);
+          for (index_t i = 0; i < b; ++i) A(i, k0 + j) += V(i, k0 + q) * m;
+        }
+      }
+      // modified Gram-Schmidt, two passes
+      for (index_t j = 0; j < c; ++j) {
+        for (int pass = 0; pass < 2; ++pass)
+          for (index_t q = 0; q < j; ++q) {
+            double d = 0.0;
+            for (index_t i = 0; i < b; ++i) d += A(i, k0 + q) * A(i, k0 + j);
+            for (index_t i = 0; i < b; ++i) A(i, k0 + j) -= d * A(i, k0 + q);
+          }
+        double nrm = 0.0;
+        for (index_t i = 0; i < b; ++i) nrm += A(i, k0 + j) * A(i, k0 + j);
+        nrm = std::sqrt(nrm);
+        for (index_t i = 0; i < b; ++i) A(i, k0 + j) /= nrm;
+      }
     }
+    k0 = k1;
   }
+  for (index_t k = 0; k < r; ++k)
+    for (index_t i = 0; i < b; ++i) U(i, k) = A(i, k);
   // Householder QR of U1 with generic sign rule; Q = H_0 ... H_{r-1}.
   std::vector<std::vector<double>> vs(static_cast<size_t>(r));
   std::vector<double> taus(static_cast<size_t>(r), 0.0);

@@ -63,6 +63,9 @@ void trsv_lower_t(const Mat& L, double* y);
 
 // Generic weights c_k used by the canonical gauge's sign rules.
 double gauge_weight(index_t k);
+double gauge_weight2(index_t k, index_t j);
+// Singular values closer than kClusterTol * sigma_1 share one canonical basis.
+constexpr double kClusterTol = 1e-9;
 
 struct SvdLeft {
   std::vector<double> sigma;  // min(rows, cols) singular values, descending
@@ -75,9 +78,11 @@ struct SvdLeft {
 SvdLeft svd_left(const Mat& F);
 
 // Canonical gauge: U = [U1 | U2] with U1 = first r columns of V, each sign-fixed
-// so sum_k c_k u_k >= 0, and U2 = trailing columns of the Householder QR Q of U1
+// so sum_k c_k u_k >= 0 -- or, for a cluster of singular values within
+// kClusterTol * sigma_1 of each other, the orthonormalised projection
+// orth(U_c U_c^T G_c) of fixed generic vectors -- and U2 = trailing columns of the Householder QR Q of U1
 // (reflector signs chosen by the same generic functional, Parlett's formula
 // when that choice cancels).
-Mat canonical_basis(const Mat& V, index_t r);
+Mat canonical_basis(const Mat& V, const std::vector<double>& sigma, index_t r);
 
 }  // namespace oracle

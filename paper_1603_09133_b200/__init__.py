@@ -1,0 +1,40 @@
+"""B200-native compress-and-eliminate (CE) factorization hot path.
+
+Python mirror of the reference's public interface for this path
+(``proj/include/ce/``): ``ce_factorize`` -> ``CEFactorization.solve`` used as
+the preconditioner of a Krylov solve (``pcg`` here, with the ``minres``
+contract of ``proj/include/ce/minres.hpp:46-47``).  Every call goes through
+the C-ABI library ``libce_gpu.so`` (``include/ce_gpu.h``), which runs
+hand-written sm_100a CUDA; there is no CPU fallback.
+"""
+
+from ._lib import lib, LibraryMissing  # noqa: F401
+from .ce import (  # noqa: F401
+    BreakdownError,
+    CEFactorization,
+    CompressionStrategy,
+    Context,
+    DeviceMatrix,
+    FactorOptions,
+    PcgOptions,
+    Problem,
+    SolveReport,
+    ce_factorize,
+    device_count,
+    pcg,
+)
+
+__all__ = [
+    "BreakdownError",
+    "CEFactorization",
+    "CompressionStrategy",
+    "Context",
+    "DeviceMatrix",
+    "FactorOptions",
+    "PcgOptions",
+    "Problem",
+    "SolveReport",
+    "ce_factorize",
+    "device_count",
+    "pcg",
+]

@@ -1,0 +1,386 @@
+"""Host-side mirror of the reference interface for the CE hot path.
+
+Reference names kept (proj/include/ce/):
+  CompressionStrategy    compression.hpp:15-38
+  FactorOptions          factorization.hpp:74-77
+  ce_factorize           factorization.hpp:121-123
+  CEFactorization.solve  factorization.hpp:90   (preconditioner apply)
+  CEFactorization.apply_q / apply_q_transpose / apply_operator   factorization.hpp:92-96
+  BreakdownError(level, block)   types.hpp:26-36
+  SolveReport            minres.hpp:25-31
+  pcg                    the minres contract (minres.hpp:46-47) with PCG, SURVEY.md §8b
+Vectors are numpy float64 arrays (host) or torch float64 CUDA tensors (device).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import lib
+
+CE_OK, CE_EUSAGE, CE_EBREAKDOWN, CE_ENOCONV = 0, 1, 2, 3
+
+
+class BreakdownError(RuntimeError):
+    """Pivot failure that survived the diagonal-shift retry (types.hpp:26-36)."""
+
+    def __init__(self, level: int, block: int, what: str):
+        super().__init__(what)
+        self.level = level
+        self.block = block
+
+
+def _check(rc: int):
+    if rc != CE_OK:
+        raise RuntimeError(L.last_error() or f"libce_gpu error {rc}")
+
+
+def device_count() -> int:
+    return int(lib.ce_device_count())
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+class Context:
+    """One GPU (ce_ctx).  Default per device via Context.get()."""
+
+    _default = {}
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _check(lib.ce_ctx_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    @classmethod
+    def get(cls, device: int = 0) -> "Context":
+        if device not in cls._default:
+            cls._default[device] = Context(device)
+        return cls._default[device]
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib.ce_ctx_destroy(self.handle)
+            self.handle = None
+
+
+@dataclass
+class CompressionStrategy:
+    """CE(eps) / CE(r) rule (compression.hpp:15-38)."""
+
+    mode: str = "eps"  # "eps" | "rank"
+    eps: float = 1e-6
+    absolute: bool = False
+    rank: int = 0
+
+    @staticmethod
+    def adaptive(eps: float, absolute: bool = False) -> "CompressionStrategy":
+        return CompressionStrategy("eps", eps, absolute, 0)
+
+    @staticmethod
+    def fixed_rank(rank: int) -> "CompressionStrategy":
+        return CompressionStrategy("rank", 0.0, False, rank)
+
+    def _c(self) -> L.Strategy:
+        return L.Strategy(1 if self.mode == "rank" else 0, float(self.eps), int(self.absolute), int(self.rank))
+
+    def describe(self) -> str:
+        if self.mode == "rank":
+            return f"rank={self.rank}"
+        return f"{'abseps' if self.absolute else 'eps'}={self.eps:g}"
+
+
+@dataclass
+class FactorOptions:
+    dense_threshold: int = 2048
+    max_levels: int = 64
+    forced_ranks: List[Sequence[int]] = field(default_factory=list)  # parity hook, -1 = free
+
+
+@dataclass
+class PcgOptions:
+    tol: float = 1e-10
+    maxit: int = 1000
+    track_true_residual: bool = False
+
+
+@dataclass
+class SolveReport:
+    converged: bool
+    iterations: int
+    final_recurrence_residual: float
+    final_true_residual: float
+    seconds: float
+
+
+class CoarseningPlan:
+    """Per-level block -> group assignments (problems.hpp:51-65 / plan text format)."""
+
+    def __init__(self, assigns: Sequence[Sequence[int]], join: int = 2):
+        self.assigns = [_i64(a) for a in assigns]
+        self.join = int(join)
+        self._blocks = _i64([len(a) for a in self.assigns])
+        self._flat = _i64(np.concatenate(self.assigns)) if self.assigns else _i64([0])
+
+    @staticmethod
+    def trivial() -> "CoarseningPlan":
+        return CoarseningPlan([], 2)
+
+    def _c(self) -> L.PlanHost:
+        return L.PlanHost(self.join, len(self.assigns), _ptr(self._blocks, C.c_int64), _ptr(self._flat, C.c_int64))
+
+
+class BlockSparseMatrix:
+    """Host CSB (block_matrix.hpp:23-63): both triangles, row-major blocks."""
+
+    def __init__(self, offsets, row_ptr, col_idx, val_ptr, values):
+        self.offsets = _i64(offsets)
+        self.row_ptr = _i64(row_ptr)
+        self.col_idx = _i64(col_idx)
+        self.val_ptr = _i64(val_ptr)
+        self.values = _f64(values)
+        self.n = int(self.offsets[-1])
+        self.m = len(self.offsets) - 1
+
+    def _c(self) -> L.CsbHost:
+        return L.CsbHost(self.n, self.m, _ptr(self.offsets, C.c_int64), _ptr(self.row_ptr, C.c_int64),
+                         _ptr(self.col_idx, C.c_int64), _ptr(self.val_ptr, C.c_int64),
+                         _ptr(self.values, C.c_double))
+
+    @staticmethod
+    def from_dense(a: np.ndarray, offsets: Sequence[int]) -> "BlockSparseMatrix":
+        """Blocks on the nonzero block pattern (+ full diagonal), like from_triplets (block_matrix.cpp:48-90)."""
+        a = np.asarray(a, dtype=np.float64)
+        offsets = _i64(offsets)
+        m = len(offsets) - 1
+        row_ptr, col_idx, val_ptr, vals = [0], [], [0], []
+        for i in range(m):
+            for j in range(m):
+                blk = a[offsets[i]:offsets[i + 1], offsets[j]:offsets[j + 1]]
+                if i == j or np.any(blk != 0) or np.any(a[offsets[j]:offsets[j + 1], offsets[i]:offsets[i + 1]] != 0):
+                    col_idx.append(j)
+                    vals.append(blk.ravel())
+                    val_ptr.append(val_ptr[-1] + blk.size)
+            row_ptr.append(len(col_idx))
+        return BlockSparseMatrix(offsets, row_ptr, col_idx, val_ptr, np.concatenate(vals))
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _stream_ptr(x):
+    import torch
+    return C.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)
+
+
+class DeviceMatrix:
+    """Device-resident operator A (ce_matrix); matvec replaces BlockSparseMatrix::matvec."""
+
+    def __init__(self, a: BlockSparseMatrix, ctx: Optional[Context] = None):
+        self.ctx = ctx or Context.get()
+        self.host = a
+        h = C.c_void_p()
+        _check(lib.ce_matrix_upload(self.ctx.handle, C.byref(a._c()), C.byref(h)))
+        self.handle = h
+        self.n = a.n
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib.ce_matrix_free(self.handle)
+            self.handle = None
+
+    def matvec(self, x):
+        if _is_torch(x):
+            import torch
+            y = torch.empty_like(x)
+            _check(lib.ce_matvec(self.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), self.n, 1,
+                                 _stream_ptr(x)))
+            return y
+        x = _f64(x)
+        if x.size != self.n:
+            raise ValueError("matvec dimension mismatch")
+        y = np.empty(self.n)
+        _check(lib.ce_matvec(self.handle, x.ctypes.data, y.ctypes.data, self.n, 0, None))
+        return y
+
+    __call__ = matvec
+
+
+class CEFactorization:
+    """Device-resident CE factor A ~ Q^T L L^T Q (factorization.hpp:81-102)."""
+
+    def __init__(self, handle, ctx: Context):
+        self.handle = handle
+        self.ctx = ctx
+        self.n = int(lib.ce_factor_dim(handle))
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib.ce_factor_free(self.handle)
+            self.handle = None
+
+    def solve(self, b):
+        """x = Q^T L^-T L^-1 Q b (factorization.cpp:140-168)."""
+        if _is_torch(b):
+            import torch
+            if b.numel() != self.n:
+                raise ValueError("solve dimension mismatch")
+            x = torch.empty_like(b)
+            _check(lib.ce_apply_precond(self.handle, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()), self.n, 1,
+                                        _stream_ptr(b)))
+            return x
+        b = _f64(b)
+        if b.size != self.n:
+            raise ValueError("solve dimension mismatch")
+        x = np.empty(self.n)
+        _check(lib.ce_apply_precond(self.handle, b.ctypes.data, x.ctypes.data, self.n, 0, None))
+        return x
+
+    __call__ = solve
+
+    def _tool(self, which: int, x) -> np.ndarray:
+        x = _f64(x)
+        if x.size != self.n:
+            raise ValueError("dimension mismatch")
+        y = np.empty(self.n)
+        _check(lib.ce_factor_apply_tool(self.handle, which, x.ctypes.data, y.ctypes.data, self.n))
+        return y
+
+    def apply_operator(self, x) -> np.ndarray:
+        return self._tool(0, x)
+
+    def apply_q(self, x) -> np.ndarray:
+        return self._tool(1, x)
+
+    def apply_q_transpose(self, y) -> np.ndarray:
+        return self._tool(2, y)
+
+    @property
+    def stats(self) -> dict:
+        s = L.FactorStats()
+        _check(lib.ce_factor_get_stats(self.handle, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in L.FactorStats._fields_}
+
+    def level_stats(self) -> List[dict]:
+        out = []
+        for lvl in range(self.stats["n_levels"]):
+            s = L.LevelStats()
+            _check(lib.ce_factor_get_level_stats(self.handle, lvl, C.byref(s)))
+            out.append({k: getattr(s, k) for k, _ in L.LevelStats._fields_})
+        return out
+
+    def dump(self, path: str):
+        _check(lib.ce_factor_dump(self.handle, path.encode()))
+
+
+def ce_factorize(a, plan: Optional[CoarseningPlan], strategy: CompressionStrategy,
+                 opts: Optional[FactorOptions] = None, ctx: Optional[Context] = None) -> CEFactorization:
+    """Multilevel CE factorization on the GPU (factorization.cpp:336-461)."""
+    opts = opts or FactorOptions()
+    if isinstance(a, BlockSparseMatrix):
+        a = DeviceMatrix(a, ctx)
+    ctx = a.ctx
+    plan = plan or CoarseningPlan.trivial()
+    counts = _i64([len(f) for f in opts.forced_ranks]) if opts.forced_ranks else _i64([0])
+    flat = _i64(np.concatenate([_i64(f) for f in opts.forced_ranks])) if opts.forced_ranks else _i64([0])
+    copts = L.FactorOpts(int(opts.dense_threshold), int(opts.max_levels), len(opts.forced_ranks),
+                         _ptr(counts, C.c_int64), _ptr(flat, C.c_int64))
+    st = L.Status()
+    h = C.c_void_p()
+    rc = lib.ce_factorize(ctx.handle, a.handle, C.byref(plan._c()), C.byref(strategy._c()), C.byref(copts),
+                          C.byref(h), C.byref(st))
+    if rc == CE_EBREAKDOWN:
+        raise BreakdownError(st.level, st.block, st.message.decode())
+    _check(rc)
+    f = CEFactorization(h, ctx)
+    f.shift_retries = st.shift_retries
+    return f
+
+
+def pcg(a: DeviceMatrix, n: int, b, precond: Optional[CEFactorization], opts: Optional[PcgOptions] = None):
+    """Preconditioned CG with the minres contract; returns (SolveReport, x).
+
+    `a` must be a DeviceMatrix and `precond` a CEFactorization or None (the
+    device loop has no host callbacks).  Non-convergence is reported in the
+    SolveReport, not raised, as in the reference."""
+    if not isinstance(a, DeviceMatrix):
+        raise TypeError("pcg runs on the device: `a` must be a DeviceMatrix")
+    if precond is not None and not isinstance(precond, CEFactorization):
+        raise TypeError("precond must be a CEFactorization or None")
+    opts = opts or PcgOptions()
+    co = L.PcgOpts(float(opts.tol), int(opts.maxit), int(opts.track_true_residual))
+    rep = L.Report()
+    ph = precond.handle if precond is not None else None
+    if _is_torch(b):
+        import torch
+        x = torch.empty_like(b)
+        rc = lib.ce_pcg(a.ctx.handle, a.handle, ph, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()), n, 1,
+                        C.byref(co), C.byref(rep))
+    else:
+        b = _f64(b)
+        x = np.empty(n)
+        rc = lib.ce_pcg(a.ctx.handle, a.handle, ph, b.ctypes.data, x.ctypes.data, n, 0, C.byref(co), C.byref(rep))
+    if rc not in (CE_OK, CE_ENOCONV):
+        _check(rc)
+    return SolveReport(bool(rep.converged), int(rep.iterations), rep.final_recurrence_residual,
+                       rep.final_true_residual, rep.seconds), x
+
+
+class Problem:
+    """A BASELINE.json configuration generated on the host."""
+
+    def __init__(self, cfg: int, nx: int = 0, ny: int = 0, nz: int = 0):
+        h = C.c_void_p()
+        _check(lib.ce_problem_create(int(cfg), int(nx), int(ny), int(nz), C.byref(h)))
+        self.handle = h
+        self.cfg = cfg
+        csb = L.CsbHost()
+        lib.ce_problem_csb(h, C.byref(csb))
+        self.n, self.m = csb.n, csb.m
+        nnzb = np.ctypeslib.as_array(csb.row_ptr, (self.m + 1,))[-1]
+        self.offsets = np.ctypeslib.as_array(csb.offsets, (self.m + 1,)).copy()
+        self.row_ptr = np.ctypeslib.as_array(csb.row_ptr, (self.m + 1,)).copy()
+        self.col_idx = np.ctypeslib.as_array(csb.col_idx, (nnzb,)).copy()
+        self.val_ptr = np.ctypeslib.as_array(csb.val_ptr, (nnzb + 1,)).copy()
+        self.values = np.ctypeslib.as_array(csb.values, (int(self.val_ptr[-1]),)).copy()
+        self.rhs = np.ctypeslib.as_array(lib.ce_problem_rhs(h), (self.n,)).copy()
+        self.perm = np.ctypeslib.as_array(lib.ce_problem_perm(h), (self.n,)).copy()
+        plan = L.PlanHost()
+        lib.ce_problem_plan(h, C.byref(plan))
+        blocks = np.ctypeslib.as_array(plan.level_blocks, (plan.n_levels,)).copy() if plan.n_levels else []
+        flat = np.ctypeslib.as_array(plan.assign, (int(np.sum(blocks)),)).copy() if plan.n_levels else []
+        assigns, at = [], 0
+        for nb in blocks:
+            assigns.append(flat[at:at + nb])
+            at += nb
+        self.plan = CoarseningPlan(assigns, plan.join)
+        eps, tol, blk = C.c_double(), C.c_double(), C.c_int64()
+        lib.ce_problem_params(h, C.byref(eps), C.byref(tol), C.byref(blk))
+        self.eps, self.tol, self.block = eps.value, tol.value, blk.value
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib.ce_problem_free(self.handle)
+            self.handle = None
+
+    def matrix(self) -> BlockSparseMatrix:
+        return BlockSparseMatrix(self.offsets, self.row_ptr, self.col_idx, self.val_ptr, self.values)
+
+    def strategy(self) -> CompressionStrategy:
+        return CompressionStrategy.adaptive(self.eps)

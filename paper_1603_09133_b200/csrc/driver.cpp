@@ -1,0 +1,998 @@
+// Host driver of the B200 CE factorization: per-level symbolic planning,
+// the multilevel loop (ce_factorize, proj/src/factorization.cpp:336-461),
+// the device preconditioner apply (:140-168), device PCG, stats and dumps.
+#include "driver.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <sstream>
+
+#include "kernels.hpp"
+
+namespace ceg {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    std::ostringstream os;
+    os << "CUDA error " << cudaGetErrorString(e) << " in " << what;
+    throw CudaError(os.str());
+  }
+}
+
+namespace {
+
+constexpr int64_t kPairInlineWork = int64_t{1} << 19;  // FMA below which a row's Schur pairs stay in phase A
+constexpr int64_t kPairTileWork = int64_t{1} << 19;    // FMA per phase-B tile
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+struct Events {
+  cudaEvent_t a = nullptr, b = nullptr;
+  Events() {
+    CE_CUDA(cudaEventCreate(&a));
+    CE_CUDA(cudaEventCreate(&b));
+  }
+  ~Events() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  double seconds() {
+    float ms = 0.f;
+    CE_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return ms * 1e-3;
+  }
+};
+
+// pattern_square (proj/src/pattern.cpp:64-86), CSR in / CSR out.
+void square_pattern(int64_t m, const std::vector<int64_t>& ptr, const std::vector<int>& col, std::vector<int64_t>& sptr,
+                    std::vector<int>& scol) {
+  std::vector<int64_t> mark(static_cast<size_t>(m), -1);
+  std::vector<int> touched;
+  sptr.assign(static_cast<size_t>(m + 1), 0);
+  scol.clear();
+  for (int64_t i = 0; i < m; ++i) {
+    touched.clear();
+    for (int64_t k = ptr[static_cast<size_t>(i)]; k < ptr[static_cast<size_t>(i + 1)]; ++k) {
+      const int kk = col[static_cast<size_t>(k)];
+      for (int64_t e = ptr[static_cast<size_t>(kk)]; e < ptr[static_cast<size_t>(kk + 1)]; ++e) {
+        const int j = col[static_cast<size_t>(e)];
+        if (mark[static_cast<size_t>(j)] != i) {
+          mark[static_cast<size_t>(j)] = i;
+          touched.push_back(j);
+        }
+      }
+    }
+    std::sort(touched.begin(), touched.end());
+    scol.insert(scol.end(), touched.begin(), touched.end());
+    sptr[static_cast<size_t>(i + 1)] = static_cast<int64_t>(scol.size());
+  }
+}
+
+bool csr_contains(const std::vector<int64_t>& ptr, const std::vector<int>& col, int64_t i, int j) {
+  auto b = col.begin() + ptr[static_cast<size_t>(i)], e = col.begin() + ptr[static_cast<size_t>(i + 1)];
+  return std::binary_search(b, e, j);
+}
+
+int64_t csr_find(const std::vector<int64_t>& ptr, const std::vector<int>& col, int64_t i, int j) {
+  auto b = col.begin() + ptr[static_cast<size_t>(i)], e = col.begin() + ptr[static_cast<size_t>(i + 1)];
+  auto it = std::lower_bound(b, e, j);
+  if (it == e || *it != j) return -1;
+  return it - col.begin();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- planner
+LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vector<int> bcol) {
+  LevelPlan P;
+  const int64_t M = static_cast<int64_t>(bsz.size());
+  P.M = M;
+  P.bsz = std::move(bsz);
+  P.bptr = std::move(bptr);
+  P.bcol = std::move(bcol);
+  P.offsets.assign(static_cast<size_t>(M + 1), 0);
+  for (int64_t i = 0; i < M; ++i) P.offsets[static_cast<size_t>(i + 1)] = P.offsets[static_cast<size_t>(i)] + P.bsz[static_cast<size_t>(i)];
+  P.dim = P.offsets.back();
+  for (int b : P.bsz) P.bmax = std::max(P.bmax, b);
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t k = P.bptr[static_cast<size_t>(i)]; k < P.bptr[static_cast<size_t>(i + 1)]; ++k)
+      if (P.bcol[static_cast<size_t>(k)] <= i) ++P.lower_blocks;
+
+  square_pattern(M, P.bptr, P.bcol, P.sptr, P.scol);
+  const int64_t nnz = static_cast<int64_t>(P.scol.size());
+  P.skind.resize(static_cast<size_t>(nnz));
+  P.sslot.assign(static_cast<size_t>(nnz), -1);
+  int64_t slot = 0;
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e) {
+      const int j = P.scol[static_cast<size_t>(e)];
+      P.skind[static_cast<size_t>(e)] = j == i ? 0 : (csr_contains(P.bptr, P.bcol, i, j) ? 1 : 2);
+      if (j <= i) P.sslot[static_cast<size_t>(e)] = slot++;
+    }
+  P.nslots = slot;
+  P.slot_off.assign(static_cast<size_t>(slot), 0);
+  int64_t off = 0;
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e) {
+      const int j = P.scol[static_cast<size_t>(e)];
+      if (j > i) break;
+      P.slot_off[static_cast<size_t>(P.sslot[static_cast<size_t>(e)])] = off;
+      off += static_cast<int64_t>(P.bsz[static_cast<size_t>(i)]) * P.bsz[static_cast<size_t>(j)];
+    }
+  P.store_doubles = off;
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e) {
+      const int j = P.scol[static_cast<size_t>(e)];
+      if (j <= i) continue;
+      P.sslot[static_cast<size_t>(e)] = P.sslot[static_cast<size_t>(csr_find(P.sptr, P.scol, j, static_cast<int>(i)))];
+    }
+
+  P.cptr.assign(static_cast<size_t>(M + 1), 0);
+  P.csum.assign(static_cast<size_t>(M), 0);
+  P.fsum.assign(static_cast<size_t>(M), 0);
+  for (int64_t i = 0; i < M; ++i) {
+    int64_t c = 0;
+    for (int64_t k = P.bptr[static_cast<size_t>(i)]; k < P.bptr[static_cast<size_t>(i + 1)]; ++k) {
+      const int t = P.bcol[static_cast<size_t>(k)];
+      if (t == i) continue;
+      P.ccol.push_back(t);
+      P.croff.push_back(static_cast<int>(c));
+      c += P.bsz[static_cast<size_t>(t)];
+    }
+    P.csum[static_cast<size_t>(i)] = c;
+    P.cptr[static_cast<size_t>(i + 1)] = static_cast<int64_t>(P.ccol.size());
+    P.cmax = std::max<int64_t>(P.cmax, static_cast<int64_t>(P.cptr[static_cast<size_t>(i + 1)] - P.cptr[static_cast<size_t>(i)]));
+    int64_t f = 0;
+    for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e)
+      if (P.skind[static_cast<size_t>(e)] == 2) f += P.bsz[static_cast<size_t>(P.scol[static_cast<size_t>(e)])];
+    P.fsum[static_cast<size_t>(i)] = f;
+    P.fmax = std::max(P.fmax, f);
+  }
+  P.chol_off.resize(static_cast<size_t>(M));
+  P.g_off.resize(static_cast<size_t>(M));
+  P.basis_off.resize(static_cast<size_t>(M));
+  P.sigma_off.resize(static_cast<size_t>(M));
+  P.item_start.assign(static_cast<size_t>(M + 1), 0);
+  int64_t fo = 0, bo = 0, so = 0, it = 0;
+  for (int64_t i = 0; i < M; ++i) {
+    const int64_t b = P.bsz[static_cast<size_t>(i)];
+    P.chol_off[static_cast<size_t>(i)] = fo;
+    fo += b * b;
+    P.g_off[static_cast<size_t>(i)] = fo;
+    fo += (b + P.csum[static_cast<size_t>(i)]) * b;
+    P.basis_off[static_cast<size_t>(i)] = bo;
+    bo += b * b;
+    P.sigma_off[static_cast<size_t>(i)] = so;
+    so += std::min<int64_t>(b, P.fsum[static_cast<size_t>(i)]);
+    // Schur pair work: sum_{s<=t in close} b_s b_t * w, with w <= b
+    int64_t sq2 = 0;
+    for (int64_t k = P.cptr[static_cast<size_t>(i)]; k < P.cptr[static_cast<size_t>(i + 1)]; ++k) {
+      const int64_t bt = P.bsz[static_cast<size_t>(P.ccol[static_cast<size_t>(k)])];
+      sq2 += bt * bt;
+    }
+    const int64_t cs = P.csum[static_cast<size_t>(i)];
+    const int64_t work = (cs * cs + sq2) / 2 * b;
+    const int64_t nc = P.cptr[static_cast<size_t>(i + 1)] - P.cptr[static_cast<size_t>(i)];
+    const int64_t pairs = nc * (nc + 1) / 2;
+    int64_t tiles = 0;
+    if (work > kPairInlineWork && pairs > 1) tiles = std::min<int64_t>(pairs, (work + kPairTileWork - 1) / kPairTileWork);
+    P.item_start[static_cast<size_t>(i)] = it;
+    it += 1 + tiles;
+  }
+  P.item_start[static_cast<size_t>(M)] = it;
+  P.n_items = it;
+  P.fac_doubles = fo;
+  P.basis_doubles = bo;
+  P.sigma_doubles = so;
+  return P;
+}
+
+namespace {
+
+// Device copy of a plan's symbolic arrays (freed after the level).
+struct DevPlan {
+  DevArray<int> bsz, scol, ccol, croff;
+  DevArray<int64_t> sptr, sslot, slot_off, cptr, chol_off, g_off, basis_off, sigma_off, item_start, offsets, cl_slot;
+  DevArray<unsigned char> skind;
+  void upload(const LevelPlan& P, cudaStream_t s) {
+    bsz.upload(P.bsz, s);
+    scol.upload(P.scol, s);
+    ccol.upload(P.ccol, s);
+    croff.upload(P.croff, s);
+    sptr.upload(P.sptr, s);
+    sslot.upload(P.sslot, s);
+    slot_off.upload(P.slot_off, s);
+    cptr.upload(P.cptr, s);
+    chol_off.upload(P.chol_off, s);
+    g_off.upload(P.g_off, s);
+    basis_off.upload(P.basis_off, s);
+    sigma_off.upload(P.sigma_off, s);
+    item_start.upload(P.item_start, s);
+    offsets.upload(P.offsets, s);
+    skind.upload(P.skind, s);
+    std::vector<int64_t> cls(P.ccol.size());
+    for (int64_t i = 0; i < P.M; ++i)
+      for (int64_t k = P.cptr[static_cast<size_t>(i)]; k < P.cptr[static_cast<size_t>(i + 1)]; ++k)
+        cls[static_cast<size_t>(k)] = P.sslot[static_cast<size_t>(csr_find(P.sptr, P.scol, i, P.ccol[static_cast<size_t>(k)]))];
+    cl_slot.upload(cls, s);
+  }
+};
+
+std::vector<std::vector<int64_t>> pair_groups(int64_t blocks, int64_t join) {
+  std::vector<std::vector<int64_t>> g;
+  for (int64_t b = 0; b < blocks; b += join) {
+    std::vector<int64_t> m;
+    for (int64_t k = b; k < std::min(b + join, blocks); ++k) m.push_back(k);
+    g.push_back(std::move(m));
+  }
+  return g;
+}
+
+std::vector<std::vector<std::vector<int64_t>>> plan_levels_from(const ce_plan_host* plan) {
+  std::vector<std::vector<std::vector<int64_t>>> levels;
+  if (!plan) return levels;
+  int64_t at = 0;
+  for (int64_t l = 0; l < plan->n_levels; ++l) {
+    const int64_t nb = plan->level_blocks[l];
+    int64_t ng = 0;
+    for (int64_t b = 0; b < nb; ++b) ng = std::max(ng, plan->assign[at + b] + 1);
+    std::vector<std::vector<int64_t>> groups(static_cast<size_t>(ng));
+    for (int64_t b = 0; b < nb; ++b) {
+      const int64_t g = plan->assign[at + b];
+      if (g < 0 || g >= ng) throw std::invalid_argument("plan: negative group id");
+      groups[static_cast<size_t>(g)].push_back(b);
+    }
+    for (const auto& g : groups)
+      if (g.empty()) throw std::invalid_argument("empty group in coarsening level");
+    levels.push_back(std::move(groups));
+    at += nb;
+  }
+  return levels;
+}
+
+// Algorithmic bytes / flops of one row (SURVEY.md §8d contract).
+void row_counts(double b, double c, double f, double r, double w, double p, double P, bool U, bool svd, double& bytes,
+                double& flops) {
+  double words = 0.0, fl = 0.0;
+  if (f > 0) words += b * f;
+  if (svd) fl += 2 * b * b * f + 12 * b * b * b;
+  if (U) {
+    words += 2 * (b * b + b * c + b * f) + 2 * b * p + b * b;
+    fl += 4 * b * b * b + 2 * b * b * (c + f) + 2 * b * p;
+  }
+  if (w > 0) {
+    words += b * c + 2 * P + (w * (w + 1) / 2 + r * w + c * w);
+    fl += w * w * w / 3 + w * w * (r + c) + 2 * r * r * w + 2 * r * w * c + 2 * w * P;
+  }
+  bytes += 8 * words;
+  flops += fl;
+}
+
+}  // namespace
+
+Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, const ce_strategy* st,
+                  const ce_factor_opts* op, int64_t* shift_total) {
+  const double t_start = now_s();
+  cudaStream_t s = ctx->stream;
+  const int64_t dense_threshold = op ? op->dense_threshold : 2048;
+  const int64_t max_levels = op ? op->max_levels : 64;
+  std::vector<std::vector<int64_t>> forced;
+  if (op && op->n_forced_levels > 0) {
+    int64_t at = 0;
+    for (int64_t l = 0; l < op->n_forced_levels; ++l) {
+      forced.emplace_back(op->forced + at, op->forced + at + op->forced_counts[l]);
+      at += op->forced_counts[l];
+    }
+  }
+  const auto plan_levels = plan_levels_from(plan_host);
+  const int64_t join = plan_host ? plan_host->join : 2;
+  if (join < 1) throw std::invalid_argument("join must be positive");
+  if (!plan_levels.empty() && static_cast<int64_t>(plan_levels[0].size()) > 0) {
+    int64_t nb = 0;
+    for (const auto& g : plan_levels[0]) nb += static_cast<int64_t>(g.size());
+    if (nb != A->m) throw std::invalid_argument("plan partition does not match the matrix");
+  }
+
+  auto F = std::make_unique<Factor>();
+  F->ctx = ctx;
+  F->n = A->n;
+
+  // level-1 plan from A's block structure
+  std::vector<int> bsz(static_cast<size_t>(A->m));
+  for (int64_t i = 0; i < A->m; ++i) bsz[static_cast<size_t>(i)] = static_cast<int>(A->offsets[static_cast<size_t>(i + 1)] - A->offsets[static_cast<size_t>(i)]);
+  std::vector<int> bcol(A->col_idx.begin(), A->col_idx.end());
+  LevelPlan cur = plan_level(bsz, A->row_ptr, bcol);
+  DevPlan dcur;
+  dcur.upload(cur, s);
+  DevArray<double> store(static_cast<size_t>(cur.store_doubles));
+  store.zero(s);
+  Events ev_all;
+  CE_CUDA(cudaEventRecord(ev_all.a, s));
+  launch_init_store_from_matrix(cur.M, dcur.bsz.p, A->d_row_ptr.p, A->d_col_idx.p, A->d_val_ptr.p, A->d_values.p,
+                                dcur.sptr.p, dcur.scol.p, dcur.sslot.p, dcur.slot_off.p, store.p, s);
+  CE_CUDA(cudaGetLastError());
+
+  std::vector<int64_t> alive_map(static_cast<size_t>(A->m));
+  std::iota(alive_map.begin(), alive_map.end(), int64_t{0});
+  DevArray<int> d_err(4), d_shifts(1);
+  DevArray<unsigned long long> d_ticket(1);
+  int64_t shifts = 0;
+  int64_t elim_total = 0;
+
+  while (cur.dim > dense_threshold && static_cast<int64_t>(F->levels.size()) < max_levels) {
+    const size_t li = F->levels.size();
+    const auto plan_groups = li < plan_levels.size() ? plan_levels[li] : pair_groups(static_cast<int64_t>(alive_map.size()), join);
+    std::vector<std::vector<int64_t>> cur_groups;
+    std::vector<int64_t> slot_of_group(plan_groups.size(), -1);
+    for (size_t g = 0; g < plan_groups.size(); ++g) {
+      std::vector<int64_t> mem;
+      for (int64_t b : plan_groups[g]) {
+        if (b < 0 || b >= static_cast<int64_t>(alive_map.size())) throw std::invalid_argument("groups must partition the level's blocks");
+        if (alive_map[static_cast<size_t>(b)] >= 0) mem.push_back(alive_map[static_cast<size_t>(b)]);
+      }
+      if (!mem.empty()) {
+        slot_of_group[g] = static_cast<int64_t>(cur_groups.size());
+        cur_groups.push_back(std::move(mem));
+      }
+    }
+    {
+      std::vector<char> seen(static_cast<size_t>(cur.M), 0);
+      int64_t cov = 0;
+      for (const auto& g : cur_groups)
+        for (int64_t b : g) {
+          if (b < 0 || b >= cur.M || seen[static_cast<size_t>(b)]) throw std::invalid_argument("groups must partition the block index range");
+          seen[static_cast<size_t>(b)] = 1;
+          ++cov;
+        }
+      if (cov != cur.M) throw std::invalid_argument("groups must cover every block");
+    }
+
+    LevelFactor LF;
+    LF.M = cur.M;
+    LF.dim = cur.dim;
+    LF.pattern_blocks = cur.lower_blocks;
+    LF.max_far = cur.fmax;
+    LF.max_close = cur.cmax;
+    LF.d_rank.alloc(static_cast<size_t>(cur.M));
+    LF.d_width.alloc(static_cast<size_t>(cur.M));
+    LF.d_has_basis.alloc(static_cast<size_t>(cur.M));
+    LF.d_fcols.alloc(static_cast<size_t>(cur.M));
+    LF.d_nsig.alloc(static_cast<size_t>(cur.M));
+    LF.d_basis.alloc(static_cast<size_t>(cur.basis_doubles));
+    LF.d_sigma.alloc(static_cast<size_t>(std::max<int64_t>(cur.sigma_doubles, 1)));
+    LF.d_fac.alloc(static_cast<size_t>(cur.fac_doubles));
+    DevArray<int> d_done(static_cast<size_t>(cur.M));
+    d_done.zero(s);
+    d_err.zero(s);
+    d_shifts.zero(s);
+    d_ticket.zero(s);
+    DevArray<int> d_forced;
+    if (li < forced.size() && !forced[li].empty()) {
+      std::vector<int> fr(static_cast<size_t>(cur.M), -1);
+      for (size_t k = 0; k < forced[li].size() && k < fr.size(); ++k) fr[k] = static_cast<int>(forced[li][k]);
+      d_forced.upload(fr, s);
+    }
+
+    SweepArgs a{};
+    a.M = cur.M;
+    a.level = static_cast<int>(li) + 1;
+    a.bsz = dcur.bsz.p;
+    a.sq_ptr = dcur.sptr.p;
+    a.sq_col = dcur.scol.p;
+    a.sq_slot = dcur.sslot.p;
+    a.sq_kind = dcur.skind.p;
+    a.slot_off = dcur.slot_off.p;
+    a.store = store.p;
+    a.cl_ptr = dcur.cptr.p;
+    a.cl_col = dcur.ccol.p;
+    a.cl_roff = dcur.croff.p;
+    a.cl_slot = dcur.cl_slot.p;
+    a.rank = LF.d_rank.p;
+    a.width = LF.d_width.p;
+    a.has_basis = LF.d_has_basis.p;
+    a.fcols = LF.d_fcols.p;
+    a.nsig = LF.d_nsig.p;
+    a.basis = LF.d_basis.p;
+    a.basis_off = dcur.basis_off.p;
+    a.sigma = LF.d_sigma.p;
+    a.sigma_off = dcur.sigma_off.p;
+    a.fac = LF.d_fac.p;
+    a.chol_off = dcur.chol_off.p;
+    a.g_off = dcur.g_off.p;
+    a.item_start = dcur.item_start.p;
+    a.done = d_done.p;
+    a.ticket = d_ticket.p;
+    a.n_items = cur.n_items;
+    a.forced = d_forced.p;
+    a.mode = st ? st->mode : 0;
+    a.absolute = st ? st->absolute : 0;
+    a.eps = st ? st->eps : 1e-6;
+    a.fixed_rank = st ? static_cast<int>(st->rank) : 0;
+    a.err = d_err.p;
+    a.shifts = d_shifts.p;
+    a.bmax = std::max(cur.bmax, 1);
+    a.kcap = std::max(a.bmax, 128);
+    int64_t need = sweep_smem_doubles(a.bmax, a.kcap);
+    size_t smem = static_cast<size_t>(need) * sizeof(double);
+    DevArray<double> scratch;
+    int per_sm = 0;
+    if (smem <= 200 * 1024) {
+      per_sm = sweep_max_ctas_per_sm(smem);
+    }
+    if (per_sm < 1) {
+      a.use_global_scratch = 1;
+      smem = 0;
+      per_sm = std::max(1, sweep_max_ctas_per_sm(0));
+      per_sm = std::min(per_sm, 4);
+    }
+    int grid = ctx->sm_count * per_sm;
+    if (grid > cur.n_items) grid = static_cast<int>(std::max<int64_t>(cur.n_items, 1));
+    if (a.use_global_scratch) {
+      scratch.alloc(static_cast<size_t>(need) * static_cast<size_t>(grid));
+      a.scratch = scratch.p;
+      a.scratch_per_cta = need;
+    }
+    Events ev_lvl, ev_sw;
+    CE_CUDA(cudaEventRecord(ev_lvl.a, s));
+    CE_CUDA(cudaEventRecord(ev_sw.a, s));
+    launch_sweep(a, grid, smem, s);
+    CE_CUDA(cudaGetLastError());
+    CE_CUDA(cudaEventRecord(ev_sw.b, s));
+    int herr[4] = {0, 0, 0, 0};
+    int hsh = 0;
+    CE_CUDA(cudaMemcpyAsync(herr, d_err.p, sizeof herr, cudaMemcpyDeviceToHost, s));
+    CE_CUDA(cudaMemcpyAsync(&hsh, d_shifts.p, sizeof hsh, cudaMemcpyDeviceToHost, s));
+    CE_CUDA(cudaStreamSynchronize(s));
+    if (herr[0] == kErrBreakdown) {
+      const int64_t row = static_cast<int64_t>(herr[2]) | (static_cast<int64_t>(herr[3]) << 31);
+      std::ostringstream os;
+      os << "elimination breakdown at level " << herr[1] << ", block " << row
+         << ": trailing pivot not positive definite after shift";
+      throw Breakdown(herr[1], row, os.str());
+    }
+    if (herr[0] == kErrPattern) throw std::logic_error("update outside the squared pattern");
+    if (herr[0] != 0) throw std::logic_error("internal sweep error");
+    launch_pending_rotation(a, s);
+    CE_CUDA(cudaGetLastError());
+    LF.d_rank.download(LF.rank, s);
+    LF.d_width.download(LF.width, s);
+    LF.d_has_basis.download(LF.has_basis, s);
+    LF.d_fcols.download(LF.fcols, s);
+    LF.d_nsig.download(LF.nsig, s);
+    CE_CUDA(cudaStreamSynchronize(s));
+    int64_t eliminated = 0;
+    for (int w : LF.width) eliminated += w;
+    if (eliminated == 0) break;  // factorization.cpp:374 (store untouched: every r_i = b_i)
+    shifts += hsh;
+    LF.shift_retries = hsh;
+
+    // ---- remainder (level_matrix.cpp:185-248) + next level plan ----
+    const int64_t ng = static_cast<int64_t>(cur_groups.size());
+    std::vector<int64_t> group_of(static_cast<size_t>(cur.M));
+    for (int64_t g = 0; g < ng; ++g)
+      for (int64_t b : cur_groups[static_cast<size_t>(g)]) group_of[static_cast<size_t>(b)] = g;
+    std::vector<int64_t> gsize(static_cast<size_t>(ng), 0), alive(static_cast<size_t>(ng), -1);
+    for (int64_t g = 0; g < ng; ++g)
+      for (int64_t b : cur_groups[static_cast<size_t>(g)]) gsize[static_cast<size_t>(g)] += LF.rank[static_cast<size_t>(b)];
+    std::vector<int> nbsz;
+    for (int64_t g = 0; g < ng; ++g)
+      if (gsize[static_cast<size_t>(g)] > 0) {
+        alive[static_cast<size_t>(g)] = static_cast<int64_t>(nbsz.size());
+        nbsz.push_back(static_cast<int>(gsize[static_cast<size_t>(g)]));
+      }
+    // coarse pattern of sq over groups restricted to alive groups
+    const int64_t nM = static_cast<int64_t>(nbsz.size());
+    std::vector<int64_t> nptr(static_cast<size_t>(nM + 1), 0);
+    std::vector<int> ncol;
+    {
+      std::vector<int64_t> mark(static_cast<size_t>(ng), -1);
+      std::vector<int> row;
+      for (int64_t g = 0; g < ng; ++g) {
+        if (alive[static_cast<size_t>(g)] < 0) continue;
+        row.clear();
+        for (int64_t b : cur_groups[static_cast<size_t>(g)])
+          for (int64_t e = cur.sptr[static_cast<size_t>(b)]; e < cur.sptr[static_cast<size_t>(b + 1)]; ++e) {
+            const int64_t h = group_of[static_cast<size_t>(cur.scol[static_cast<size_t>(e)])];
+            if (alive[static_cast<size_t>(h)] < 0 || mark[static_cast<size_t>(h)] == g) continue;
+            mark[static_cast<size_t>(h)] = g;
+            row.push_back(static_cast<int>(alive[static_cast<size_t>(h)]));
+          }
+        std::sort(row.begin(), row.end());
+        ncol.insert(ncol.end(), row.begin(), row.end());
+        nptr[static_cast<size_t>(alive[static_cast<size_t>(g)] + 1)] = static_cast<int64_t>(ncol.size());
+      }
+    }
+    std::vector<int> next_block(static_cast<size_t>(cur.M), -1), next_loc(static_cast<size_t>(cur.M), 0);
+    for (int64_t g = 0; g < ng; ++g) {
+      int at = 0;
+      for (int64_t b : cur_groups[static_cast<size_t>(g)]) {
+        next_loc[static_cast<size_t>(b)] = at;
+        next_block[static_cast<size_t>(b)] = static_cast<int>(alive[static_cast<size_t>(g)]);
+        at += LF.rank[static_cast<size_t>(b)];
+      }
+    }
+    // gathers (factorization.cpp:76-85)
+    std::vector<int64_t> elim, kept;
+    for (int64_t b = 0; b < cur.M; ++b)
+      for (int64_t rr = LF.rank[static_cast<size_t>(b)]; rr < cur.bsz[static_cast<size_t>(b)]; ++rr) elim.push_back(cur.offsets[static_cast<size_t>(b)] + rr);
+    for (const auto& g : cur_groups)
+      for (int64_t b : g)
+        for (int64_t rr = 0; rr < LF.rank[static_cast<size_t>(b)]; ++rr) kept.push_back(cur.offsets[static_cast<size_t>(b)] + rr);
+    LF.n_elim = static_cast<int64_t>(elim.size());
+    LF.n_kept = static_cast<int64_t>(kept.size());
+    LF.d_elim_gather.upload(elim, s);
+    LF.d_kept_gather.upload(kept, s);
+
+    LevelPlan next;
+    DevPlan dnext;
+    DevArray<double> nstore;
+    if (nM > 0) {
+      next = plan_level(nbsz, nptr, ncol);
+      dnext.upload(next, s);
+      nstore.alloc(static_cast<size_t>(next.store_doubles));
+      nstore.zero(s);
+      DevArray<int> d_nb, d_nl;
+      d_nb.upload(next_block, s);
+      d_nl.upload(next_loc, s);
+      RemainderArgs ra{};
+      ra.M = cur.M;
+      ra.bsz = dcur.bsz.p;
+      ra.rank = LF.d_rank.p;
+      ra.sq_ptr = dcur.sptr.p;
+      ra.sq_col = dcur.scol.p;
+      ra.sq_slot = dcur.sslot.p;
+      ra.slot_off = dcur.slot_off.p;
+      ra.store = store.p;
+      ra.next_block = d_nb.p;
+      ra.next_loc = d_nl.p;
+      ra.nbsz = dnext.bsz.p;
+      ra.nsq_ptr = dnext.sptr.p;
+      ra.nsq_col = dnext.scol.p;
+      ra.nsq_slot = dnext.sslot.p;
+      ra.nslot_off = dnext.slot_off.p;
+      ra.nstore = nstore.p;
+      ra.err = d_err.p;
+      launch_remainder(ra, s);
+      CE_CUDA(cudaGetLastError());
+      CE_CUDA(cudaEventRecord(ev_lvl.b, s));
+      CE_CUDA(cudaMemcpyAsync(herr, d_err.p, sizeof herr, cudaMemcpyDeviceToHost, s));
+      CE_CUDA(cudaStreamSynchronize(s));
+      if (herr[0] != 0) throw std::logic_error("remainder block outside the coarse squared pattern");
+    } else {
+      CE_CUDA(cudaEventRecord(ev_lvl.b, s));
+      CE_CUDA(cudaStreamSynchronize(s));
+    }
+    LF.seconds = ev_lvl.seconds();
+    LF.sweep_seconds = ev_sw.seconds();
+    F->sweep_seconds += LF.sweep_seconds;
+
+    // host copies needed by apply / dump / stats
+    LF.bsz = cur.bsz;
+    LF.offsets = cur.offsets;
+    LF.cptr = cur.cptr;
+    LF.ccol = cur.ccol;
+    LF.croff = cur.croff;
+    LF.chol_off = cur.chol_off;
+    LF.g_off = cur.g_off;
+    LF.basis_off = cur.basis_off;
+    LF.sigma_off = cur.sigma_off;
+    LF.groups = cur_groups;
+    LF.d_bsz = std::move(dcur.bsz);
+    LF.d_offsets = std::move(dcur.offsets);
+    LF.d_cptr = std::move(dcur.cptr);
+    LF.d_ccol = std::move(dcur.ccol);
+    LF.d_croff = std::move(dcur.croff);
+    LF.d_chol_off = std::move(dcur.chol_off);
+    LF.d_g_off = std::move(dcur.g_off);
+    LF.d_basis_off = std::move(dcur.basis_off);
+    LF.d_sigma_off = std::move(dcur.sigma_off);
+
+    // stats (factorization.cpp:376-405) + §8d algorithmic counts
+    {
+      std::vector<int64_t> pend(static_cast<size_t>(cur.M), 0);
+      for (int64_t k = 0; k < cur.M; ++k)
+        for (int64_t e = cur.cptr[static_cast<size_t>(k)]; e < cur.cptr[static_cast<size_t>(k + 1)]; ++e) {
+          const int t = cur.ccol[static_cast<size_t>(e)];
+          if (t > k) pend[static_cast<size_t>(t)] += LF.width[static_cast<size_t>(k)];
+        }
+      double by = 0.0, fl = 0.0;
+      for (int64_t i = 0; i < cur.M; ++i) {
+        const double b = cur.bsz[static_cast<size_t>(i)], c = static_cast<double>(cur.csum[static_cast<size_t>(i)]);
+        const double r = LF.rank[static_cast<size_t>(i)], w = LF.width[static_cast<size_t>(i)];
+        double sq2 = 0.0;
+        for (int64_t e = cur.cptr[static_cast<size_t>(i)]; e < cur.cptr[static_cast<size_t>(i + 1)]; ++e) {
+          const double bt = cur.bsz[static_cast<size_t>(cur.ccol[static_cast<size_t>(e)])];
+          sq2 += bt * bt;
+        }
+        const double Pp = (c * c + sq2) / 2;
+        row_counts(b, c, static_cast<double>(LF.fcols[static_cast<size_t>(i)]), r, w,
+                   LF.has_basis[static_cast<size_t>(i)] ? static_cast<double>(pend[static_cast<size_t>(i)]) : 0.0, Pp,
+                   LF.has_basis[static_cast<size_t>(i)] != 0, LF.nsig[static_cast<size_t>(i)] > 0, by, fl);
+        const int64_t wi = LF.width[static_cast<size_t>(i)], ri = LF.rank[static_cast<size_t>(i)];
+        if (wi > 0) {
+          const int64_t cs = cur.csum[static_cast<size_t>(i)];
+          F->l_payload_bytes += (wi * wi + ri * wi + cs * wi) * 8;
+          F->l_scalar_nnz += wi * (wi + 1) / 2 + ri * wi + cs * wi;
+        }
+        if (LF.has_basis[static_cast<size_t>(i)]) F->q_payload_bytes += static_cast<int64_t>(b * b) * 8;
+      }
+      // remainder extraction traffic
+      double rem = 0.0;
+      for (int64_t sI = 0; sI < cur.M; ++sI)
+        for (int64_t e = cur.sptr[static_cast<size_t>(sI)]; e < cur.sptr[static_cast<size_t>(sI + 1)]; ++e) {
+          const int t = cur.scol[static_cast<size_t>(e)];
+          if (t > sI) break;
+          rem += static_cast<double>(LF.rank[static_cast<size_t>(sI)]) * LF.rank[static_cast<size_t>(t)];
+        }
+      by += 2 * 8 * rem;
+      LF.alg_bytes = by;
+      LF.alg_flops = fl;
+      F->factor_blocks += 2.0 * static_cast<double>(cur.lower_blocks);
+    }
+    elim_total += LF.n_elim;
+
+    std::vector<int64_t> next_alive(plan_groups.size(), -1);
+    for (size_t g = 0; g < plan_groups.size(); ++g)
+      if (slot_of_group[g] >= 0) next_alive[g] = alive[static_cast<size_t>(slot_of_group[g])];
+    alive_map = std::move(next_alive);
+    F->levels.push_back(std::move(LF));
+
+    cur = std::move(next);
+    dcur = std::move(dnext);
+    store = std::move(nstore);
+    if (nM == 0) break;
+  }
+
+  // ---- dense tail (factorization.cpp:419-436) ----
+  F->tail_dim = cur.M > 0 ? cur.dim : 0;
+  if (F->tail_dim > 0) {
+    const int64_t n = F->tail_dim;
+    F->d_tail_L.alloc(static_cast<size_t>(n * n));
+    F->d_tail_Linv.alloc(static_cast<size_t>(n * n));
+    F->d_tail_L.zero(s);
+    launch_densify(cur.M, dcur.bsz.p, dcur.offsets.p, dcur.sptr.p, dcur.scol.p, dcur.sslot.p, dcur.slot_off.p,
+                   store.p, F->d_tail_L.p, n, s);
+    CE_CUDA(cudaGetLastError());
+    DevArray<double> backup(static_cast<size_t>(n * n)), d_tr(1);
+    CE_CUDA(cudaMemcpyAsync(backup.p, F->d_tail_L.p, static_cast<size_t>(n * n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    dense_trace(backup.p, n, d_tr.p, s);
+    DevArray<int> d_fail(1);
+    d_fail.zero(s);
+    dense_cholesky(F->d_tail_L.p, n, d_fail.p, s);
+    int hf = 0;
+    CE_CUDA(cudaMemcpyAsync(&hf, d_fail.p, sizeof hf, cudaMemcpyDeviceToHost, s));
+    CE_CUDA(cudaStreamSynchronize(s));
+    if (hf) {
+      double tr = 0.0;
+      CE_CUDA(cudaMemcpy(&tr, d_tr.p, sizeof tr, cudaMemcpyDeviceToHost));
+      const double shift = 1e-12 * tr / static_cast<double>(n);
+      CE_CUDA(cudaMemcpyAsync(F->d_tail_L.p, backup.p, static_cast<size_t>(n * n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      dense_add_shift(F->d_tail_L.p, n, shift, s);
+      d_fail.zero(s);
+      dense_cholesky(F->d_tail_L.p, n, d_fail.p, s);
+      CE_CUDA(cudaMemcpyAsync(&hf, d_fail.p, sizeof hf, cudaMemcpyDeviceToHost, s));
+      CE_CUDA(cudaStreamSynchronize(s));
+      if (hf) {
+        std::ostringstream os;
+        os << "dense tail not positive definite after shift " << shift;
+        throw Breakdown(static_cast<int>(F->levels.size()) + 1, -1, os.str());
+      }
+    }
+    dense_tri_inverse(F->d_tail_L.p, F->d_tail_Linv.p, n, s);
+    CE_CUDA(cudaGetLastError());
+  }
+  CE_CUDA(cudaEventRecord(ev_all.b, s));
+  CE_CUDA(cudaStreamSynchronize(s));
+  F->device_seconds = ev_all.seconds();
+  F->tail_bytes = F->tail_dim * F->tail_dim * 8;
+  F->l_scalar_nnz += F->tail_dim * (F->tail_dim + 1) / 2;
+  F->factor_blocks += 0.5 * static_cast<double>(F->tail_dim) * static_cast<double>(F->tail_dim);
+  F->shift_retries = shifts;
+  if (shift_total) *shift_total = shifts;
+
+  // apply workspaces
+  F->w_v.alloc(static_cast<size_t>(std::max<int64_t>(F->n, 1)));
+  F->w_active.alloc(static_cast<size_t>(std::max<int64_t>(F->n, 1)));
+  F->w_elim.alloc(static_cast<size_t>(std::max<int64_t>(elim_total, 1)));
+  int64_t mmax = 1;
+  F->elim_base.clear();
+  int64_t eb = 0;
+  for (const auto& L : F->levels) {
+    mmax = std::max(mmax, L.M);
+    F->elim_base.push_back(eb);
+    eb += L.n_elim;
+  }
+  F->w_flags.alloc(static_cast<size_t>(mmax));
+  F->w_ticket.alloc(1);
+  F->total_seconds = now_s() - t_start;
+  return F.release();
+}
+
+// ---------------------------------------------------------------- apply
+namespace {
+ApplyLevelArgs level_args(const Factor& f, const LevelFactor& L, double* v) {
+  ApplyLevelArgs a{};
+  a.M = L.M;
+  a.bsz = L.d_bsz.p;
+  a.offsets = L.d_offsets.p;
+  a.rank = L.d_rank.p;
+  a.width = L.d_width.p;
+  a.has_basis = L.d_has_basis.p;
+  a.basis = L.d_basis.p;
+  a.basis_off = L.d_basis_off.p;
+  a.fac = L.d_fac.p;
+  a.chol_off = L.d_chol_off.p;
+  a.g_off = L.d_g_off.p;
+  a.cl_ptr = L.d_cptr.p;
+  a.cl_col = L.d_ccol.p;
+  a.cl_roff = L.d_croff.p;
+  a.v = v;
+  a.flags = f.w_flags.p;
+  a.ticket = f.w_ticket.p;
+  return a;
+}
+}  // namespace
+
+void apply_device(const Factor& f, const double* d_b, double* d_x, cudaStream_t s) {
+  const int grid = f.ctx->sm_count * 8;
+  double* active = f.w_active.p;
+  double* v = f.w_v.p;
+  CE_CUDA(cudaMemcpyAsync(active, d_b, static_cast<size_t>(f.n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  for (size_t l = 0; l < f.levels.size(); ++l) {
+    const LevelFactor& L = f.levels[l];
+    CE_CUDA(cudaMemcpyAsync(v, active, static_cast<size_t>(L.dim) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    ApplyLevelArgs a = level_args(f, L, v);
+    launch_basis_apply(a, 1, s);
+    CE_CUDA(cudaMemsetAsync(f.w_flags.p, 0, static_cast<size_t>(L.M) * sizeof(int), s));
+    CE_CUDA(cudaMemsetAsync(f.w_ticket.p, 0, sizeof(unsigned long long), s));
+    launch_forward_sweep(a, static_cast<int>(std::min<int64_t>(grid, L.M)), s);
+    launch_forward_retained(a, s);
+    launch_gather(v, L.d_elim_gather.p, f.w_elim.p + f.elim_base[l], L.n_elim, s);
+    launch_gather(v, L.d_kept_gather.p, active, L.n_kept, s);
+  }
+  if (f.tail_dim > 0) {
+    launch_dense_trmv(f.d_tail_Linv.p, active, v, f.tail_dim, 0, s);
+    launch_dense_trmv(f.d_tail_Linv.p, v, active, f.tail_dim, 1, s);
+  }
+  for (size_t l = f.levels.size(); l-- > 0;) {
+    const LevelFactor& L = f.levels[l];
+    CE_CUDA(cudaMemsetAsync(v, 0, static_cast<size_t>(L.dim) * sizeof(double), s));
+    launch_scatter(active, L.d_kept_gather.p, v, L.n_kept, s);
+    launch_scatter(f.w_elim.p + f.elim_base[l], L.d_elim_gather.p, v, L.n_elim, s);
+    ApplyLevelArgs a = level_args(f, L, v);
+    CE_CUDA(cudaMemsetAsync(f.w_flags.p, 0, static_cast<size_t>(L.M) * sizeof(int), s));
+    CE_CUDA(cudaMemsetAsync(f.w_ticket.p, 0, sizeof(unsigned long long), s));
+    launch_backward_sweep(a, static_cast<int>(std::min<int64_t>(grid, L.M)), s);
+    launch_basis_apply(a, 0, s);
+    CE_CUDA(cudaMemcpyAsync(active, v, static_cast<size_t>(L.dim) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  CE_CUDA(cudaMemcpyAsync(d_x, active, static_cast<size_t>(f.n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  CE_CUDA(cudaGetLastError());
+}
+
+// Validation tools (factorization.cpp:170-257) on the device.
+void apply_tool_device(const Factor& f, int which, const double* d_x, double* d_y, cudaStream_t s) {
+  double* active = f.w_active.p;
+  double* v = f.w_v.p;
+  CE_CUDA(cudaMemcpyAsync(active, d_x, static_cast<size_t>(f.n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (which == 2) {  // apply_q_transpose: y = [elim_1 | ... | tail]
+    int64_t at = 0;
+    for (const auto& L : f.levels) at += L.n_elim;
+    CE_CUDA(cudaMemcpyAsync(v, d_x + at, static_cast<size_t>(f.n - at) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CE_CUDA(cudaMemcpyAsync(active, v, static_cast<size_t>(f.n - at) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    for (size_t l = f.levels.size(); l-- > 0;) {
+      const LevelFactor& L = f.levels[l];
+      CE_CUDA(cudaMemsetAsync(v, 0, static_cast<size_t>(L.dim) * sizeof(double), s));
+      launch_scatter(active, L.d_kept_gather.p, v, L.n_kept, s);
+      launch_scatter(d_x + f.elim_base[l], L.d_elim_gather.p, v, L.n_elim, s);
+      ApplyLevelArgs a = level_args(f, L, v);
+      launch_basis_apply(a, 0, s);
+      CE_CUDA(cudaMemcpyAsync(active, v, static_cast<size_t>(L.dim) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    CE_CUDA(cudaMemcpyAsync(d_y, active, static_cast<size_t>(f.n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  std::vector<DevArray<int64_t>> eoffs;
+  std::vector<DevArray<double>> cvals;
+  for (size_t l = 0; l < f.levels.size(); ++l) {
+    const LevelFactor& L = f.levels[l];
+    CE_CUDA(cudaMemcpyAsync(v, active, static_cast<size_t>(L.dim) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    ApplyLevelArgs a = level_args(f, L, v);
+    launch_basis_apply(a, 1, s);
+    if (which == 1) {
+      launch_gather(v, L.d_elim_gather.p, d_y + f.elim_base[l], L.n_elim, s);
+    } else {
+      std::vector<int64_t> eo(static_cast<size_t>(L.M));
+      int64_t at = 0;
+      for (int64_t b = 0; b < L.M; ++b) {
+        eo[static_cast<size_t>(b)] = at;
+        at += L.width[static_cast<size_t>(b)];
+      }
+      eoffs.emplace_back();
+      eoffs.back().upload(eo, s);
+      cvals.emplace_back(static_cast<size_t>(std::max<int64_t>(at, 1)));
+      launch_operator_forward(a, eoffs.back().p, cvals.back().p, s);
+    }
+    launch_gather(v, L.d_kept_gather.p, active, L.n_kept, s);
+  }
+  if (which == 1) {
+    int64_t at = 0;
+    for (const auto& L : f.levels) at += L.n_elim;
+    CE_CUDA(cudaMemcpyAsync(d_y + at, active, static_cast<size_t>(f.n - at) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  if (f.tail_dim > 0) {
+    launch_dense_trmv(f.d_tail_L.p, active, v, f.tail_dim, 1, s);
+    launch_dense_trmv(f.d_tail_L.p, v, active, f.tail_dim, 0, s);
+  }
+  for (size_t l = f.levels.size(); l-- > 0;) {
+    const LevelFactor& L = f.levels[l];
+    CE_CUDA(cudaMemsetAsync(v, 0, static_cast<size_t>(L.dim) * sizeof(double), s));
+    launch_scatter(active, L.d_kept_gather.p, v, L.n_kept, s);
+    ApplyLevelArgs a = level_args(f, L, v);
+    launch_operator_backward(a, eoffs[l].p, cvals[l].p, s);
+    launch_basis_apply(a, 0, s);
+    CE_CUDA(cudaMemcpyAsync(active, v, static_cast<size_t>(L.dim) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  CE_CUDA(cudaMemcpyAsync(d_y, active, static_cast<size_t>(f.n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  CE_CUDA(cudaStreamSynchronize(s));
+}
+
+void matvec_device(const Matrix& A, const double* d_x, double* d_y, cudaStream_t s) {
+  launch_bsr_matvec(A.n, A.d_row_of.p, A.d_offsets.p, A.d_bsz.p, A.d_row_ptr.p, A.d_col_idx.p, A.d_val_ptr.p,
+                    A.d_values.p, d_x, d_y, s);
+}
+
+// ---------------------------------------------------------------- PCG
+SolveOut pcg_device(const Matrix& A, const Factor* M, const double* d_b, double* d_x, double tol, int64_t maxit,
+                    bool track_true) {
+  cudaStream_t s = A.ctx->stream;
+  const int64_t n = A.n;
+  SolveOut out;
+  const double t0 = now_s();
+  DevArray<double> r(static_cast<size_t>(n)), z(static_cast<size_t>(n)), p(static_cast<size_t>(n)), q(static_cast<size_t>(n));
+  DevArray<double> part(static_cast<size_t>(dot_partials_capacity())), sc(8);
+  auto dot = [&](const double* x, const double* y, int slot) {
+    const int np = launch_dot(x, y, n, part.p, s);
+    launch_sum_partials(part.p, np, sc.p + slot, s);
+  };
+  auto fetch = [&](double* h, int slot, int cnt) {
+    CE_CUDA(cudaMemcpyAsync(h, sc.p + slot, static_cast<size_t>(cnt) * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CE_CUDA(cudaStreamSynchronize(s));
+  };
+  auto precond = [&](const double* in, double* o) {
+    if (M) apply_device(*M, in, o, s);
+    else launch_copy(o, in, n, s);
+  };
+  const double one = 1.0;
+  CE_CUDA(cudaMemcpyAsync(sc.p + 7, &one, sizeof(double), cudaMemcpyHostToDevice, s));
+  auto true_resid = [&](double bnorm) {
+    matvec_device(A, d_x, q.p, s);
+    launch_copy(z.p, d_b, n, s);
+    launch_axpy(z.p, q.p, sc.p + 7, sc.p + 7, -1.0, n, s);  // z = b - A x
+    dot(z.p, z.p, 5);
+    double h = 0.0;
+    fetch(&h, 5, 1);
+    return std::sqrt(h) / bnorm;
+  };
+  CE_CUDA(cudaMemsetAsync(d_x, 0, static_cast<size_t>(n) * sizeof(double), s));
+  dot(d_b, d_b, 4);
+  double hb = 0.0;
+  fetch(&hb, 4, 1);
+  const double bnorm = std::sqrt(hb);
+  if (bnorm == 0.0) {
+    out.converged = true;
+    out.seconds = now_s() - t0;
+    return out;
+  }
+  launch_copy(r.p, d_b, n, s);
+  precond(r.p, z.p);
+  dot(r.p, z.p, 0);
+  double h[4];
+  fetch(h, 0, 1);
+  if (!std::isfinite(h[0])) throw std::runtime_error("preconditioner produced non-finite values");
+  if (h[0] < 0.0) throw std::runtime_error("preconditioner is not positive definite: r' M^-1 r < 0");
+  launch_copy(p.p, z.p, n, s);
+  double rel = 1.0;
+  for (int64_t itn = 1; itn <= maxit; ++itn) {
+    matvec_device(A, p.p, q.p, s);
+    dot(p.p, q.p, 2);
+    launch_axpy(d_x, p.p, sc.p + 0, sc.p + 2, 1.0, n, s);
+    launch_axpy(r.p, q.p, sc.p + 0, sc.p + 2, -1.0, n, s);
+    dot(r.p, r.p, 3);
+    fetch(h, 0, 4);
+    if (!std::isfinite(h[2]) || h[2] <= 0.0) throw std::runtime_error("operator is not positive definite: p' A p <= 0");
+    rel = std::sqrt(h[3]) / bnorm;
+    out.iterations = itn;
+    if (track_true) out.trace_true.push_back(true_resid(bnorm));
+    out.trace_rec.push_back(rel);
+    if (rel <= tol) {
+      out.converged = true;
+      break;
+    }
+    precond(r.p, z.p);
+    dot(r.p, z.p, 1);
+    launch_pcg_update_p(p.p, z.p, sc.p + 1, sc.p + 0, n, s);
+    CE_CUDA(cudaMemcpyAsync(sc.p + 0, sc.p + 1, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    double rzn = 0.0;
+    fetch(&rzn, 1, 1);
+    if (!std::isfinite(rzn)) throw std::runtime_error("preconditioner produced non-finite values");
+    if (rzn < 0.0) throw std::runtime_error("preconditioner is not positive definite: r' M^-1 r < 0");
+  }
+  out.final_rec = rel;
+  out.final_true = true_resid(bnorm);
+  CE_CUDA(cudaGetLastError());
+  out.seconds = now_s() - t0;
+  return out;
+}
+
+// ---------------------------------------------------------------- dump
+void dump_factor(const Factor& f, const std::string& path) {
+  std::FILE* fp = std::fopen(path.c_str(), "wb");
+  if (!fp) throw std::runtime_error("cannot open " + path);
+  auto i64 = [&](int64_t v) { std::fwrite(&v, sizeof v, 1, fp); };
+  auto f64 = [&](const double* p, size_t k) {
+    if (k) std::fwrite(p, sizeof(double), k, fp);
+  };
+  cudaStream_t s = f.ctx->stream;
+  std::fwrite("CEFD", 1, 4, fp);
+  i64(1);
+  i64(f.n);
+  i64(static_cast<int64_t>(f.levels.size()));
+  i64(f.tail_dim);
+  for (const LevelFactor& L : f.levels) {
+    std::vector<double> basis, sigma, fac;
+    L.d_basis.download(basis, s);
+    L.d_sigma.download(sigma, s);
+    L.d_fac.download(fac, s);
+    CE_CUDA(cudaStreamSynchronize(s));
+    i64(L.M);
+    for (int64_t v : L.offsets) i64(v);
+    for (int v : L.rank) i64(v);
+    for (unsigned char v : L.has_basis) i64(v);
+    for (int64_t b = 0; b < L.M; ++b)
+      if (L.has_basis[static_cast<size_t>(b)]) {
+        const int64_t bs = L.bsz[static_cast<size_t>(b)];
+        f64(basis.data() + L.basis_off[static_cast<size_t>(b)], static_cast<size_t>(bs * bs));
+      }
+    for (int v : L.fcols) i64(v);
+    for (int v : L.nsig) i64(v);
+    for (int64_t b = 0; b < L.M; ++b) f64(sigma.data() + L.sigma_off[static_cast<size_t>(b)], static_cast<size_t>(L.nsig[static_cast<size_t>(b)]));
+    for (int64_t b = 0; b < L.M; ++b) {
+      const int64_t w = L.width[static_cast<size_t>(b)], r = L.rank[static_cast<size_t>(b)];
+      i64(w);
+      if (w == 0) continue;
+      f64(fac.data() + L.chol_off[static_cast<size_t>(b)], static_cast<size_t>(w * w));
+      const double* G = fac.data() + L.g_off[static_cast<size_t>(b)];
+      f64(G, static_cast<size_t>(r * w));
+      const int64_t c0 = L.cptr[static_cast<size_t>(b)], c1 = L.cptr[static_cast<size_t>(b + 1)];
+      i64(c1 - c0);
+      for (int64_t e = c0; e < c1; ++e) {
+        const int t = L.ccol[static_cast<size_t>(e)];
+        i64(t);
+        f64(G + (r + L.croff[static_cast<size_t>(e)]) * w, static_cast<size_t>(L.bsz[static_cast<size_t>(t)] * w));
+      }
+    }
+    i64(static_cast<int64_t>(L.groups.size()));
+    for (const auto& g : L.groups) {
+      i64(static_cast<int64_t>(g.size()));
+      for (int64_t b : g) i64(b);
+    }
+  }
+  if (f.tail_dim > 0) {
+    std::vector<double> t;
+    f.d_tail_L.download(t, s);
+    CE_CUDA(cudaStreamSynchronize(s));
+    f64(t.data(), t.size());
+  }
+  std::fclose(fp);
+}
+
+}  // namespace ceg

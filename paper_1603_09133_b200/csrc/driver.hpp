@@ -1,0 +1,32 @@
+// Host driver entry points (internal).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "../../include/ce_gpu.h"
+#include "host_api.hpp"
+
+namespace ceg {
+
+LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vector<int> bcol);
+
+Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan, const ce_strategy* st,
+                  const ce_factor_opts* opts, int64_t* shift_total);
+
+void apply_device(const Factor& f, const double* d_b, double* d_x, cudaStream_t s);
+void apply_tool_device(const Factor& f, int which, const double* d_x, double* d_y, cudaStream_t s);
+void matvec_device(const Matrix& A, const double* d_x, double* d_y, cudaStream_t s);
+
+struct SolveOut {
+  bool converged = false;
+  int64_t iterations = 0;
+  double final_rec = 0.0, final_true = 0.0, seconds = 0.0;
+  std::vector<double> trace_rec, trace_true;
+};
+SolveOut pcg_device(const Matrix& A, const Factor* M, const double* d_b, double* d_x, double tol, int64_t maxit,
+                    bool track_true);
+
+void dump_factor(const Factor& f, const std::string& path);
+
+}  // namespace ceg

@@ -1,0 +1,166 @@
+// Internal host-side structures of the CE B200 library (not part of the C ABI).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace ceg {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// BreakdownError{level, block} of the reference (proj/include/ce/types.hpp:26-36).
+struct Breakdown : std::runtime_error {
+  Breakdown(int lvl, int64_t blk, const std::string& w) : std::runtime_error(w), level(lvl), block(blk) {}
+  int level;
+  int64_t block;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define CE_CUDA(x) ::ceg::cuda_check((x), #x)
+
+// Owning device array.
+template <class T>
+struct DevArray {
+  T* p = nullptr;
+  size_t n = 0;
+  DevArray() = default;
+  explicit DevArray(size_t count) { alloc(count); }
+  DevArray(const DevArray&) = delete;
+  DevArray& operator=(const DevArray&) = delete;
+  DevArray(DevArray&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevArray& operator=(DevArray&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DevArray() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) CE_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void upload(const std::vector<T>& h, cudaStream_t s) {
+    alloc(h.size());
+    if (!h.empty()) CE_CUDA(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void download(std::vector<T>& h, cudaStream_t s) const {
+    h.resize(n);
+    if (n) CE_CUDA(cudaMemcpyAsync(h.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  }
+  void zero(cudaStream_t s) {
+    if (n) CE_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+};
+
+// BASELINE problem (host CSB, plan, rhs).
+struct Problem {
+  int cfg = 0;
+  int64_t nx = 0, ny = 0, nz = 1, block = 8;
+  double eps = 1e-6, tol = 1e-8;
+  int64_t n = 0, m = 0;
+  std::vector<int64_t> offsets, row_ptr, col_idx, val_ptr, perm;
+  std::vector<double> values, rhs;
+  int64_t join = 2;
+  std::vector<int64_t> plan_level_blocks, plan_assign;
+  void build(int cfg_id, int64_t nx, int64_t ny, int64_t nz);
+};
+
+struct Context {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+};
+
+// Device-resident operator A (both triangles, BSR) + host copy of its structure.
+struct Matrix {
+  Context* ctx = nullptr;
+  int64_t n = 0, m = 0, nnzb = 0;
+  std::vector<int64_t> offsets, row_ptr, col_idx, val_ptr;
+  DevArray<int64_t> d_offsets, d_row_ptr, d_val_ptr;
+  DevArray<int> d_col_idx, d_bsz;
+  DevArray<double> d_values;
+  DevArray<int64_t> d_row_of;  // scalar row -> block row
+};
+
+// Symbolic plan of one level (host) — SURVEY.md §8a a3/a7: squared pattern,
+// half-symmetric slot layout, close/far split, factor layout, schedule.
+struct LevelPlan {
+  int64_t M = 0, dim = 0;
+  std::vector<int> bsz;
+  std::vector<int64_t> offsets;
+  std::vector<int64_t> bptr;  // base pattern CSR (both triangles, sorted, with diagonal)
+  std::vector<int> bcol;
+  std::vector<int64_t> sptr;  // squared pattern CSR
+  std::vector<int> scol;
+  std::vector<unsigned char> skind;  // 0 diag, 1 close, 2 far
+  std::vector<int64_t> sslot;        // stored (lower) slot of (i, j)
+  int64_t nslots = 0;
+  std::vector<int64_t> slot_off;     // value offset (doubles) of each stored slot
+  int64_t store_doubles = 0;
+  std::vector<int64_t> cptr;         // close lists (base minus diagonal)
+  std::vector<int> ccol, croff;
+  std::vector<int64_t> csum;         // sum of close block sizes per row
+  std::vector<int64_t> fsum;         // far columns per row
+  std::vector<int64_t> chol_off, g_off, basis_off, sigma_off;
+  int64_t fac_doubles = 0, basis_doubles = 0, sigma_doubles = 0;
+  std::vector<int64_t> item_start;
+  int64_t n_items = 0;
+  int bmax = 0;
+  int64_t fmax = 0, cmax = 0;
+  int64_t lower_blocks = 0;          // of the base pattern (LevelStats.pattern_blocks)
+};
+
+// Persistent device data of one completed level (FactorLevel, factorization.hpp:19-36).
+struct LevelFactor {
+  int64_t M = 0, dim = 0, n_elim = 0, n_kept = 0;
+  std::vector<int> bsz, rank, width;
+  std::vector<int64_t> offsets;
+  std::vector<unsigned char> has_basis;
+  std::vector<int64_t> cptr, chol_off, g_off, basis_off, sigma_off;
+  std::vector<int> ccol, croff, fcols, nsig;
+  std::vector<std::vector<int64_t>> groups;
+  DevArray<int> d_bsz, d_rank, d_width, d_ccol, d_croff, d_nsig, d_fcols;
+  DevArray<int64_t> d_offsets, d_cptr, d_chol_off, d_g_off, d_basis_off, d_sigma_off;
+  DevArray<unsigned char> d_has_basis;
+  DevArray<double> d_fac, d_basis, d_sigma;
+  DevArray<int64_t> d_elim_gather, d_kept_gather;
+  // stats
+  int64_t pattern_blocks = 0, shift_retries = 0, max_far = 0, max_close = 0;
+  double seconds = 0.0, sweep_seconds = 0.0, alg_bytes = 0.0, alg_flops = 0.0;
+};
+
+struct Factor {
+  Context* ctx = nullptr;
+  int64_t n = 0;
+  std::vector<LevelFactor> levels;
+  int64_t tail_dim = 0;
+  DevArray<double> d_tail_L, d_tail_Linv;
+  int64_t shift_retries = 0;
+  double total_seconds = 0.0, device_seconds = 0.0, sweep_seconds = 0.0;
+  double factor_blocks = 0.0, predicted_factor_blocks = 0.0;
+  int64_t l_scalar_nnz = 0, l_payload_bytes = 0, q_payload_bytes = 0, tail_bytes = 0;
+  // apply workspaces (sized to the level dims)
+  mutable DevArray<double> w_v, w_active, w_elim;
+  mutable std::vector<int64_t> elim_base;
+  mutable DevArray<int> w_flags;
+  mutable DevArray<unsigned long long> w_ticket;
+  mutable DevArray<double> w_host_stage;
+};
+
+}  // namespace ceg

@@ -1,0 +1,159 @@
+// Kernel argument blocks and launchers shared by the .cu files and the host driver.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace ceg {
+
+constexpr int kSweepThreads = 256;
+constexpr int kApplyThreads = 128;
+
+enum : int { kErrNone = 0, kErrBreakdown = 2, kErrPattern = 5, kErrInternal = 6 };
+
+// Launch accounting (every launcher calls note_launch once per kernel launch).
+void note_launch(int64_t n = 1);
+int64_t launch_count();
+
+// One level sweep: rows are compressed and
+// eliminated by a persistent kernel that walks the plan's ascending order as
+// a dependency DAG (row j waits for every i < j in sq(j), A.2).
+struct SweepArgs {
+  int64_t M;
+  int level;
+  const int* bsz;
+  const int64_t* sq_ptr;
+  const int* sq_col;
+  const int64_t* sq_slot;
+  const unsigned char* sq_kind;
+  const int64_t* slot_off;
+  double* store;
+  const int64_t* cl_ptr;
+  const int* cl_col;
+  const int* cl_roff;
+  const int64_t* cl_slot;  // stored slot of (i, t) per close entry
+  int* rank;
+  int* width;
+  unsigned char* has_basis;
+  int* fcols;
+  int* nsig;
+  double* basis;
+  const int64_t* basis_off;
+  double* sigma;
+  const int64_t* sigma_off;
+  double* fac;
+  const int64_t* chol_off;
+  const int64_t* g_off;
+  const int64_t* item_start;
+  int* done;
+  unsigned long long* ticket;
+  int64_t n_items;
+  const int* forced;  // nullptr or M entries (-1 = free)
+  int mode;           // 0 eps, 1 fixed rank
+  int absolute;
+  double eps;
+  int fixed_rank;
+  int* err;           // [0] code, [1] level, [2] row (low), [3] row (high)
+  int* shifts;
+  int bmax;
+  int kcap;
+  double* scratch;    // per-CTA global scratch when the tiles do not fit shared memory
+  int64_t scratch_per_cta;
+  int use_global_scratch;
+};
+
+// smem doubles needed by one sweep CTA for a level
+int64_t sweep_smem_doubles(int bmax, int kcap);
+void launch_sweep(const SweepArgs& a, int grid, size_t smem_bytes, cudaStream_t s);
+int sweep_max_ctas_per_sm(size_t smem_bytes);
+
+// Deferred pending-factor rotations g <- U_t^T g (level_matrix.cpp:66-69 deferred, A.2).
+void launch_pending_rotation(const SweepArgs& a, cudaStream_t s);
+
+// Level-1 store initialisation: scatter the lower blocks of A into the squared-pattern store.
+void launch_init_store_from_matrix(int64_t M, const int* bsz, const int64_t* a_row_ptr, const int* a_col,
+                                   const int64_t* a_val_ptr, const double* a_values, const int64_t* sq_ptr,
+                                   const int* sq_col, const int64_t* sq_slot, const int64_t* slot_off,
+                                   double* store, cudaStream_t s);
+
+// Remainder extraction straight into the next level's store (level_matrix.cpp:185-248).
+struct RemainderArgs {
+  int64_t M;
+  const int* bsz;
+  const int* rank;
+  const int64_t* sq_ptr;
+  const int* sq_col;
+  const int64_t* sq_slot;
+  const int64_t* slot_off;
+  const double* store;
+  const int* next_block;  // current block -> next block (-1 if dead)
+  const int* next_loc;    // local offset inside the super block
+  const int* nbsz;        // next block sizes
+  const int64_t* nsq_ptr;
+  const int* nsq_col;
+  const int64_t* nsq_slot;
+  const int64_t* nslot_off;
+  double* nstore;
+  int* err;
+};
+void launch_remainder(const RemainderArgs& a, cudaStream_t s);
+
+// Dense tail (factorization.cpp:419-436): densify the last store, Cholesky, inverse.
+void launch_densify(int64_t M, const int* bsz, const int64_t* offsets, const int64_t* sq_ptr, const int* sq_col,
+                    const int64_t* sq_slot, const int64_t* slot_off, const double* store, double* dense, int64_t n,
+                    cudaStream_t s);
+// In-place blocked lower Cholesky of the n x n row-major matrix; *fail set to 1 on a non-positive pivot.
+void dense_cholesky(double* a, int64_t n, int* d_fail, cudaStream_t s);
+void dense_add_shift(double* a, int64_t n, double shift, cudaStream_t s);
+void dense_trace(const double* a, int64_t n, double* d_out, cudaStream_t s);
+// Linv = L^{-1} (lower), row-major n x n.
+void dense_tri_inverse(const double* L, double* Linv, int64_t n, cudaStream_t s);
+
+// ---- apply (CEFactorization::solve, factorization.cpp:140-168) ----
+struct ApplyLevelArgs {
+  int64_t M;
+  const int* bsz;
+  const int64_t* offsets;
+  const int* rank;
+  const int* width;
+  const unsigned char* has_basis;
+  const double* basis;
+  const int64_t* basis_off;
+  const double* fac;
+  const int64_t* chol_off;
+  const int64_t* g_off;
+  const int64_t* cl_ptr;
+  const int* cl_col;
+  const int* cl_roff;
+  double* v;
+  int* flags;
+  unsigned long long* ticket;
+};
+void launch_basis_apply(const ApplyLevelArgs& a, int transpose, cudaStream_t s);
+void launch_forward_sweep(const ApplyLevelArgs& a, int grid, cudaStream_t s);
+void launch_forward_retained(const ApplyLevelArgs& a, cudaStream_t s);
+void launch_backward_sweep(const ApplyLevelArgs& a, int grid, cudaStream_t s);
+// operator tool (apply_operator) pieces
+void launch_operator_forward(const ApplyLevelArgs& a, const int64_t* elim_off, double* c, cudaStream_t s);
+void launch_operator_backward(const ApplyLevelArgs& a, const int64_t* elim_off, const double* c, cudaStream_t s);
+void launch_gather(const double* src, const int64_t* idx, double* dst, int64_t n, cudaStream_t s);
+void launch_scatter(const double* src, const int64_t* idx, double* dst, int64_t n, cudaStream_t s);
+// y = op(L) x with the dense lower matrix: trans 0 -> y = L x, 1 -> y = L^T x
+void launch_dense_trmv(const double* L, const double* x, double* y, int64_t n, int trans, cudaStream_t s);
+
+// ---- Krylov helpers ----
+void launch_bsr_matvec(int64_t n, const int64_t* row_of, const int64_t* offsets, const int* bsz,
+                       const int64_t* row_ptr, const int* col_idx, const int64_t* val_ptr, const double* values,
+                       const double* x, double* y, cudaStream_t s);
+// partial dot products -> d_partial[nblocks]; returns nblocks used
+int launch_dot(const double* x, const double* y, int64_t n, double* d_partial, cudaStream_t s);
+int dot_partials_capacity();
+void launch_sum_partials(const double* partial, int np, double* out, cudaStream_t s);
+void launch_axpy(double* y, const double* x, const double* alpha_num, const double* alpha_den, double sign,
+                 int64_t n, cudaStream_t s);
+void launch_pcg_update_p(double* p, const double* z, const double* rz_new, const double* rz_old, int64_t n,
+                         cudaStream_t s);
+void launch_copy(double* dst, const double* src, int64_t n, cudaStream_t s);
+
+}  // namespace ceg
