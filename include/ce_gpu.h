@@ -123,6 +123,8 @@ typedef struct {
   int64_t max_block, max_far_cols, max_close;
   double sweep_seconds;        /* CUDA-event time of the sweep kernel alone */
   double algorithmic_bytes, algorithmic_flops;
+  int64_t n_waves;             /* depth of the row dependency DAG */
+  int64_t n_items;             /* work items of the persistent sweep (rows + Schur tiles) */
 } ce_level_stats;
 
 /* ---- context / device ---- */

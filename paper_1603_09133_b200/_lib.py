@@ -68,7 +68,8 @@ class LevelStats(C.Structure):
                 ("retained", i64), ("max_rank", i64), ("mean_rank", C.c_double), ("seconds", C.c_double),
                 ("l_bytes", i64), ("q_bytes", i64), ("shift_retries", i64), ("max_block", i64),
                 ("max_far_cols", i64), ("max_close", i64), ("sweep_seconds", C.c_double),
-                ("algorithmic_bytes", C.c_double), ("algorithmic_flops", C.c_double)]
+                ("algorithmic_bytes", C.c_double), ("algorithmic_flops", C.c_double), ("n_waves", i64),
+                ("n_items", i64)]
 
 
 # name -> (restype, argtypes); every symbol include/ce_gpu.h declares

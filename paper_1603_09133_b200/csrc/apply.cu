@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(T) forward_kernel(ApplyLevelArgs A) {
     __syncthreads();
     const long long jl = s_row;
     if (jl >= A.M) break;
-    const int j = static_cast<int>(jl);
+    const int j = A.order[jl];
     const int64_t c0 = A.cl_ptr[j], c1 = A.cl_ptr[j + 1];
     if (threadIdx.x == 0) {
       for (int64_t e = c0; e < c1; ++e) {
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(T) backward_kernel(ApplyLevelArgs A) {
     __syncthreads();
     const long long tk = s_t;
     if (tk >= A.M) break;
-    const int j = static_cast<int>(A.M - 1 - tk);
+    const int j = A.order[tk];
     const int64_t c0 = A.cl_ptr[j], c1 = A.cl_ptr[j + 1];
     if (threadIdx.x == 0) {
       for (int64_t e = c1 - 1; e >= c0; --e) {

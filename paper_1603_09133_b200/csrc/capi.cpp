@@ -392,6 +392,8 @@ int ce_factor_get_level_stats(const ce_factor* fh, int64_t level, ce_level_stats
     out->max_close = L.max_close;
     out->algorithmic_bytes = L.alg_bytes;
     out->algorithmic_flops = L.alg_flops;
+    out->n_waves = L.n_waves;
+    out->n_items = L.n_items;
   });
 }
 

@@ -190,8 +190,8 @@ __global__ void tri_inverse_kernel(const double* L, double* X, int64_t n) {
 void launch_densify(int64_t M, const int* bsz, const int64_t* offsets, const int64_t* sq_ptr, const int* sq_col,
                     const int64_t* sq_slot, const int64_t* slot_off, const double* store, double* dense, int64_t n,
                     cudaStream_t s) {
-  if (M > 0)
-    note_launch();
+  if (M <= 0) return;
+  note_launch();
     densify_kernel<<<static_cast<unsigned>(M < 65535 ? M : 65535), 128, 0, s>>>(M, bsz, offsets, sq_ptr, sq_col, sq_slot,
                                                                               slot_off, store, dense, n);
 }

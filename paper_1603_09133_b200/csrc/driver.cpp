@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -26,8 +27,36 @@ void cuda_check(cudaError_t e, const char* what) {
 
 namespace {
 
-constexpr int64_t kPairInlineWork = int64_t{1} << 19;  // FMA below which a row's Schur pairs stay in phase A
-constexpr int64_t kPairTileWork = int64_t{1} << 19;    // FMA per phase-B tile
+// Task-splitting thresholds of the sweep task graph.  CE_FORCE_TASKS=1 (tests) drops them so
+// that small problems exercise the multi-task path of fat rows.
+struct Thresholds {
+  int64_t pair_inline = int64_t{1} << 19;  // FMA below which a row's Schur pairs stay in A2
+  int64_t leaf_work = int64_t{1} << 20;    // far gather f*b^2 above which TSQR leaves are split off
+  int64_t leaf_cols = 512;                 // far columns per TSQR leaf
+  int64_t strip_work = int64_t{1} << 20;   // strip rotation S*b^2 above which the strip is split off
+  int64_t strip_cols = 256;                // strip columns per task
+  bool small_panels = false;               // one close neighbour per Schur panel
+  Thresholds() {
+    const char* f = std::getenv("CE_FORCE_TASKS");  // bitmask: 1 leaves, 2 strip tasks, 4 Schur panels
+    const int m = f ? std::atoi(f) : 0;
+    if (m & 1) {
+      leaf_work = 0;
+      leaf_cols = 16;
+    }
+    if (m & 2) {
+      strip_work = 0;
+      strip_cols = 16;
+    }
+    if (m & 4) {
+      pair_inline = 0;
+      small_panels = true;
+    }
+  }
+};
+const Thresholds& thresholds() {
+  static const Thresholds t;
+  return t;
+}
 
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -160,34 +189,107 @@ LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vecto
   P.basis_off.resize(static_cast<size_t>(M));
   P.sigma_off.resize(static_cast<size_t>(M));
   P.item_start.assign(static_cast<size_t>(M + 1), 0);
-  int64_t fo = 0, bo = 0, so = 0, it = 0;
+  P.nA1.assign(static_cast<size_t>(M), 0);
+  P.nA3.assign(static_cast<size_t>(M), 0);
+  P.nB.assign(static_cast<size_t>(M), 0);
+  P.rs_off.assign(static_cast<size_t>(M), 0);
+  P.pan_ptr.assign(static_cast<size_t>(M + 1), 0);
+  // Schur panel height: both panels' g rows (<= cap x w doubles each) must fit the CTA buffer.
+  const int64_t bmax = std::max(P.bmax, 1);
+  const int64_t buf = sweep_smem_doubles(static_cast<int>(bmax), static_cast<int>(std::max<int64_t>(bmax, 128)));
+  const int64_t cap = thresholds().small_panels ? bmax : std::max<int64_t>(bmax, std::min<int64_t>(256, buf / (2 * bmax)));
+  int64_t fo = 0, bo = 0, so = 0, ro = 0;
   for (int64_t i = 0; i < M; ++i) {
-    const int64_t b = P.bsz[static_cast<size_t>(i)];
-    P.chol_off[static_cast<size_t>(i)] = fo;
+    const size_t iu = static_cast<size_t>(i);
+    const int64_t b = P.bsz[iu];
+    P.chol_off[iu] = fo;
     fo += b * b;
-    P.g_off[static_cast<size_t>(i)] = fo;
-    fo += (b + P.csum[static_cast<size_t>(i)]) * b;
-    P.basis_off[static_cast<size_t>(i)] = bo;
+    P.g_off[iu] = fo;
+    fo += (b + P.csum[iu]) * b;
+    P.basis_off[iu] = bo;
     bo += b * b;
-    P.sigma_off[static_cast<size_t>(i)] = so;
-    so += std::min<int64_t>(b, P.fsum[static_cast<size_t>(i)]);
+    P.sigma_off[iu] = so;
+    so += std::min<int64_t>(b, P.fsum[iu]);
+    // A1: TSQR leaves when the far gather is large (work ~ f b^2)
+    int64_t nfar = 0, nstrip = 0, strip_cols = 0;
+    for (int64_t e = P.sptr[iu]; e < P.sptr[iu + 1]; ++e) {
+      if (P.skind[static_cast<size_t>(e)] == 2) ++nfar;
+      if (P.skind[static_cast<size_t>(e)] != 0) {
+        ++nstrip;
+        strip_cols += P.bsz[static_cast<size_t>(P.scol[static_cast<size_t>(e)])];
+      }
+    }
+    const Thresholds& th = thresholds();
+    if (P.fsum[iu] * b * b > th.leaf_work) {
+      const int64_t leaves = std::min<int64_t>(nfar, (P.fsum[iu] + th.leaf_cols - 1) / th.leaf_cols);
+      if (leaves >= 2) {
+        P.nA1[iu] = static_cast<int>(leaves);
+        P.rs_off[iu] = ro;
+        ro += leaves * b * b;
+      }
+    }
+    // A3: strip tasks when rotating the strip is large (work ~ S b^2)
+    if (strip_cols * b * b > th.strip_work) {
+      const int64_t tasks = std::min<int64_t>(nstrip, (strip_cols + th.strip_cols - 1) / th.strip_cols);
+      if (tasks >= 2) P.nA3[iu] = static_cast<int>(tasks);
+    }
+    // B: Schur panels of the close list (greedy, <= cap rows each)
+    int64_t np = 0;
+    {
+      int64_t rows = 0;
+      for (int64_t k = P.cptr[iu]; k < P.cptr[iu + 1]; ++k) {
+        const int64_t bt = P.bsz[static_cast<size_t>(P.ccol[static_cast<size_t>(k)])];
+        if (np == 0 || rows + bt > cap) {
+          P.pan_start.push_back(static_cast<int>(k - P.cptr[iu]));
+          ++np;
+          rows = 0;
+        }
+        rows += bt;
+      }
+      P.pan_start.push_back(static_cast<int>(P.cptr[iu + 1] - P.cptr[iu]));
+      P.pan_ptr[iu + 1] = static_cast<int64_t>(P.pan_start.size());
+    }
     // Schur pair work: sum_{s<=t in close} b_s b_t * w, with w <= b
     int64_t sq2 = 0;
-    for (int64_t k = P.cptr[static_cast<size_t>(i)]; k < P.cptr[static_cast<size_t>(i + 1)]; ++k) {
+    for (int64_t k = P.cptr[iu]; k < P.cptr[iu + 1]; ++k) {
       const int64_t bt = P.bsz[static_cast<size_t>(P.ccol[static_cast<size_t>(k)])];
       sq2 += bt * bt;
     }
-    const int64_t cs = P.csum[static_cast<size_t>(i)];
+    const int64_t cs = P.csum[iu];
     const int64_t work = (cs * cs + sq2) / 2 * b;
-    const int64_t nc = P.cptr[static_cast<size_t>(i + 1)] - P.cptr[static_cast<size_t>(i)];
-    const int64_t pairs = nc * (nc + 1) / 2;
-    int64_t tiles = 0;
-    if (work > kPairInlineWork && pairs > 1) tiles = std::min<int64_t>(pairs, (work + kPairTileWork - 1) / kPairTileWork);
-    P.item_start[static_cast<size_t>(i)] = it;
-    it += 1 + tiles;
+    if (work > th.pair_inline && np * (np + 1) / 2 > 1) P.nB[iu] = static_cast<int>(np * (np + 1) / 2);
+    // with strip tasks the Schur update must follow all of them: one task runs every panel pair
+    if (P.nA3[iu] > 0 && P.nB[iu] == 0 && np > 0) P.nB[iu] = 1;
   }
-  P.item_start[static_cast<size_t>(M)] = it;
-  P.n_items = it;
+  P.rscratch_doubles = ro;
+  // Wave (topological) order of the dependency DAG: row j depends on every i < j in sq(j)
+  // (SURVEY.md A.2).  Items are issued in this order, so the ticket window always holds
+  // the current wavefront instead of a run of consecutive (mutually dependent) rows.
+  {
+    std::vector<int64_t> wave(static_cast<size_t>(M), 0);
+    for (int64_t j = 0; j < M; ++j) {
+      int64_t w = 0;
+      for (int64_t e = P.sptr[static_cast<size_t>(j)]; e < P.sptr[static_cast<size_t>(j + 1)]; ++e) {
+        const int i = P.scol[static_cast<size_t>(e)];
+        if (i >= j) break;
+        w = std::max(w, wave[static_cast<size_t>(i)] + 1);
+      }
+      wave[static_cast<size_t>(j)] = w;
+      P.n_waves = std::max(P.n_waves, w + 1);
+    }
+    P.order.resize(static_cast<size_t>(M));
+    std::iota(P.order.begin(), P.order.end(), 0);
+    std::stable_sort(P.order.begin(), P.order.end(),
+                     [&](int x, int y) { return wave[static_cast<size_t>(x)] < wave[static_cast<size_t>(y)]; });
+    int64_t it = 0;
+    for (int64_t k = 0; k < M; ++k) {
+      P.item_start[static_cast<size_t>(k)] = it;
+      const size_t r = static_cast<size_t>(P.order[static_cast<size_t>(k)]);
+      it += 1 + P.nA1[r] + P.nA3[r] + P.nB[r];
+    }
+    P.item_start[static_cast<size_t>(M)] = it;
+    P.n_items = it;
+  }
   P.fac_doubles = fo;
   P.basis_doubles = bo;
   P.sigma_doubles = so;
@@ -198,10 +300,19 @@ namespace {
 
 // Device copy of a plan's symbolic arrays (freed after the level).
 struct DevPlan {
-  DevArray<int> bsz, scol, ccol, croff;
-  DevArray<int64_t> sptr, sslot, slot_off, cptr, chol_off, g_off, basis_off, sigma_off, item_start, offsets, cl_slot;
+  DevArray<int> bsz, scol, ccol, croff, order, nA1, nA3, nB, pan_start;
+  DevArray<int64_t> sptr, sslot, slot_off, cptr, chol_off, g_off, basis_off, sigma_off, item_start, offsets, cl_slot,
+      fsum, rs_off, pan_ptr;
   DevArray<unsigned char> skind;
   void upload(const LevelPlan& P, cudaStream_t s) {
+    order.upload(P.order, s);
+    nA1.upload(P.nA1, s);
+    nA3.upload(P.nA3, s);
+    nB.upload(P.nB, s);
+    pan_start.upload(P.pan_start, s);
+    fsum.upload(P.fsum, s);
+    rs_off.upload(P.rs_off, s);
+    pan_ptr.upload(P.pan_ptr, s);
     bsz.upload(P.bsz, s);
     scol.upload(P.scol, s);
     ccol.upload(P.ccol, s);
@@ -360,6 +471,8 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     LF.pattern_blocks = cur.lower_blocks;
     LF.max_far = cur.fmax;
     LF.max_close = cur.cmax;
+    LF.n_waves = cur.n_waves;
+    LF.n_items = cur.n_items;
     LF.d_rank.alloc(static_cast<size_t>(cur.M));
     LF.d_width.alloc(static_cast<size_t>(cur.M));
     LF.d_has_basis.alloc(static_cast<size_t>(cur.M));
@@ -407,6 +520,19 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     a.chol_off = dcur.chol_off.p;
     a.g_off = dcur.g_off.p;
     a.item_start = dcur.item_start.p;
+    a.order = dcur.order.p;
+    a.nA1 = dcur.nA1.p;
+    a.nA3 = dcur.nA3.p;
+    a.nB = dcur.nB.p;
+    a.fsum = dcur.fsum.p;
+    a.rs_off = dcur.rs_off.p;
+    a.pan_ptr = dcur.pan_ptr.p;
+    a.pan_start = dcur.pan_start.p;
+    DevArray<double> d_rscratch(static_cast<size_t>(std::max<int64_t>(cur.rscratch_doubles, 1)));
+    DevArray<int> d_nz(static_cast<size_t>(cur.M));
+    d_nz.zero(s);
+    a.rscratch = d_rscratch.p;
+    a.nzflag = d_nz.p;
     a.done = d_done.p;
     a.ticket = d_ticket.p;
     a.n_items = cur.n_items;
@@ -593,6 +719,29 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     LF.d_g_off = std::move(dcur.g_off);
     LF.d_basis_off = std::move(dcur.basis_off);
     LF.d_sigma_off = std::move(dcur.sigma_off);
+    {
+      // wave orders of the apply's forward (deps: close i < j) and backward (deps: close t > j) sweeps
+      std::vector<int64_t> wf(static_cast<size_t>(cur.M), 0), wb(static_cast<size_t>(cur.M), 0);
+      for (int64_t j = 0; j < cur.M; ++j)
+        for (int64_t e = cur.cptr[static_cast<size_t>(j)]; e < cur.cptr[static_cast<size_t>(j + 1)]; ++e) {
+          const int i = cur.ccol[static_cast<size_t>(e)];
+          if (i < j) wf[static_cast<size_t>(j)] = std::max(wf[static_cast<size_t>(j)], wf[static_cast<size_t>(i)] + 1);
+        }
+      for (int64_t j = cur.M - 1; j >= 0; --j)
+        for (int64_t e = cur.cptr[static_cast<size_t>(j)]; e < cur.cptr[static_cast<size_t>(j + 1)]; ++e) {
+          const int t = cur.ccol[static_cast<size_t>(e)];
+          if (t > j) wb[static_cast<size_t>(j)] = std::max(wb[static_cast<size_t>(j)], wb[static_cast<size_t>(t)] + 1);
+        }
+      std::vector<int> of(static_cast<size_t>(cur.M)), ob(static_cast<size_t>(cur.M));
+      std::iota(of.begin(), of.end(), 0);
+      std::iota(ob.begin(), ob.end(), 0);
+      std::stable_sort(of.begin(), of.end(), [&](int x, int y) { return wf[static_cast<size_t>(x)] < wf[static_cast<size_t>(y)]; });
+      std::stable_sort(ob.begin(), ob.end(), [&](int x, int y) {
+        return wb[static_cast<size_t>(x)] < wb[static_cast<size_t>(y)] || (wb[static_cast<size_t>(x)] == wb[static_cast<size_t>(y)] && x > y);
+      });
+      LF.d_fwd_order.upload(of, s);
+      LF.d_bwd_order.upload(ob, s);
+    }
 
     // stats (factorization.cpp:376-405) + §8d algorithmic counts
     {
@@ -752,6 +901,7 @@ void apply_device(const Factor& f, const double* d_b, double* d_x, cudaStream_t 
     launch_basis_apply(a, 1, s);
     CE_CUDA(cudaMemsetAsync(f.w_flags.p, 0, static_cast<size_t>(L.M) * sizeof(int), s));
     CE_CUDA(cudaMemsetAsync(f.w_ticket.p, 0, sizeof(unsigned long long), s));
+    a.order = L.d_fwd_order.p;
     launch_forward_sweep(a, static_cast<int>(std::min<int64_t>(grid, L.M)), s);
     launch_forward_retained(a, s);
     launch_gather(v, L.d_elim_gather.p, f.w_elim.p + f.elim_base[l], L.n_elim, s);
@@ -769,6 +919,7 @@ void apply_device(const Factor& f, const double* d_b, double* d_x, cudaStream_t 
     ApplyLevelArgs a = level_args(f, L, v);
     CE_CUDA(cudaMemsetAsync(f.w_flags.p, 0, static_cast<size_t>(L.M) * sizeof(int), s));
     CE_CUDA(cudaMemsetAsync(f.w_ticket.p, 0, sizeof(unsigned long long), s));
+    a.order = L.d_bwd_order.p;
     launch_backward_sweep(a, static_cast<int>(std::min<int64_t>(grid, L.M)), s);
     launch_basis_apply(a, 0, s);
     CE_CUDA(cudaMemcpyAsync(active, v, static_cast<size_t>(L.dim) * sizeof(double), cudaMemcpyDeviceToDevice, s));

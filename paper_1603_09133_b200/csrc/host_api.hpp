@@ -119,8 +119,13 @@ struct LevelPlan {
   std::vector<int64_t> fsum;         // far columns per row
   std::vector<int64_t> chol_off, g_off, basis_off, sigma_off;
   int64_t fac_doubles = 0, basis_doubles = 0, sigma_doubles = 0;
-  std::vector<int64_t> item_start;
-  int64_t n_items = 0;
+  std::vector<int64_t> item_start;   // by position in `order`
+  std::vector<int> order;            // rows in wave (topological) order of the sq-DAG
+  std::vector<int> nA1, nA3, nB;     // per-row task counts (sweep.cu header)
+  std::vector<int64_t> pan_ptr, rs_off;
+  std::vector<int> pan_start;
+  int64_t rscratch_doubles = 0;
+  int64_t n_items = 0, n_waves = 0;
   int bmax = 0;
   int64_t fmax = 0, cmax = 0;
   int64_t lower_blocks = 0;          // of the base pattern (LevelStats.pattern_blocks)
@@ -140,8 +145,9 @@ struct LevelFactor {
   DevArray<unsigned char> d_has_basis;
   DevArray<double> d_fac, d_basis, d_sigma;
   DevArray<int64_t> d_elim_gather, d_kept_gather;
+  DevArray<int> d_fwd_order, d_bwd_order;
   // stats
-  int64_t pattern_blocks = 0, shift_retries = 0, max_far = 0, max_close = 0;
+  int64_t pattern_blocks = 0, shift_retries = 0, max_far = 0, max_close = 0, n_waves = 0, n_items = 0;
   double seconds = 0.0, sweep_seconds = 0.0, alg_bytes = 0.0, alg_flops = 0.0;
 };
 

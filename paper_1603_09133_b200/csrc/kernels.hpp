@@ -45,7 +45,17 @@ struct SweepArgs {
   double* fac;
   const int64_t* chol_off;
   const int64_t* g_off;
-  const int64_t* item_start;
+  const int64_t* item_start;  // first item of the row at each position of `order`
+  const int* order;           // rows in wave order
+  const int* nA1;             // TSQR leaf tasks per row (0 = gather inside A2)
+  const int* nA3;             // strip tasks per row (0 = strip inside A2)
+  const int* nB;              // Schur panel-pair tasks per row (0 = inline)
+  const int64_t* fsum;        // far columns per row
+  const int64_t* rs_off;      // per-row offset of the TSQR leaf triangles in rscratch
+  double* rscratch;
+  int* nzflag;                // per-row "far fill nonzero" flag from the leaves
+  const int64_t* pan_ptr;     // per-row offset into pan_start (np + 1 entries per row)
+  const int* pan_start;       // close-list index where each Schur panel starts
   int* done;
   unsigned long long* ticket;
   int64_t n_items;
@@ -128,6 +138,7 @@ struct ApplyLevelArgs {
   const int* cl_roff;
   double* v;
   int* flags;
+  const int* order;  // sweep order (wave order of the forward / backward DAG)
   unsigned long long* ticket;
 };
 void launch_basis_apply(const ApplyLevelArgs& a, int transpose, cudaStream_t s);

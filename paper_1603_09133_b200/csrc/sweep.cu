@@ -6,17 +6,18 @@
 //   LevelMatrix::eliminate_subrow  proj/src/level_matrix.cpp:84-178
 //   level_sweep hot loop           proj/src/factorization.cpp:56-59
 //
-// B200 design: one persistent kernel per level.  Work items are taken from a
-// global ticket in plan order; item 0 of row i compresses and eliminates the
-// row (phase A, one CTA), items 1..T_i apply its Schur pair updates
-// X_st -= g_s g_t^T in tiles spread over other CTAs (phase B, fat rows only).
-// Row j's phase A waits until every row i < j of sq(j) has finished all its
-// items (rows at block-graph distance >= 3 commute), so every
-// block receives its updates in the reference order and no atomics touch data.
-// The far-block concatenation F_i is never materialised: its transpose is
-// streamed through shared memory in chunks into a Householder TSQR, the b x b
-// triangle is diagonalised by parallel one-sided Jacobi (round-robin pairs, one
-// warp per pair), and U is emitted in the canonical gauge (oracle/dense.hpp).
+// B200 design: one persistent kernel per level walks a task graph.  Rows are
+// issued in wave (topological) order of the squared-pattern DAG; row j's first
+// task waits until every row i < j of sq(j) has finished all its tasks (rows at
+// block-graph distance >= 3 commute), so every block receives
+// its updates in the reference order without atomics on data.  A row is
+//   [A1 x nA1]  far-block gather + Householder TSQR leaves (fat rows only)
+//   [A2]        TSQR combine, one-sided Jacobi SVD, rank rule, canonical U,
+//               rotated diagonal, pivot Cholesky (+ shift retry), coupling
+//   [A3 x nA3]  rotation / truncation / TRSM / retained Schur / zeroing of the
+//               row's strip blocks (fat rows only; thin rows do it in A2)
+//   [B  x nB ]  Schur panel-pair updates X_st -= g_s g_t^T from smem tiles
+// Thin rows (level 1) are a single task done by one CTA.
 #include <cfloat>
 #include <cstdio>
 
@@ -27,6 +28,7 @@ namespace {
 
 constexpr int T = kSweepThreads;
 constexpr int NW = T / 32;
+constexpr double kClusterTol = 1e-9;  // oracle/dense.hpp
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldcg(p); }
 
@@ -42,22 +44,12 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__device__ __forceinline__ double gauge_weight(int k) {
-  const double x = __dmul_rn(static_cast<double>(k + 1), 0.6180339887498949);
+__device__ __forceinline__ double gauge_weight2(int k, int j) {
+  const double cj = __dadd_rn(0.6180339887498949, __dmul_rn(0.2071067811865475, static_cast<double>(j)));
+  const double x = __dmul_rn(static_cast<double>(k + 1), cj);
   return 1.0 + 0.5 * (x - floor(x));
 }
-
-// Deterministic block-wide sum; every thread receives the same value.
-__device__ double block_sum(double v, double* red) {
-  v = warp_sum(v);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double s = 0.0;
-#pragma unroll
-  for (int k = 0; k < NW; ++k) s += red[k];
-  return s;
-}
+__device__ __forceinline__ double gauge_weight(int k) { return gauge_weight2(k, 0); }
 
 __device__ __forceinline__ int rr_player(int k, int round, int nb) {
   return k == 0 ? 0 : 1 + (k - 1 + round) % (nb - 1);
@@ -70,6 +62,19 @@ __device__ int64_t find_slot(const int64_t* sq_ptr, const int* sq_col, const int
     const int c = sq_col[mid];
     if (c == col) return sq_slot[mid];
     if (c < col) lo = mid + 1;
+    else hi = mid;
+  }
+  return -1;
+}
+
+// index of neighbour t in row i's close list (or -1)
+__device__ int64_t close_index(const SweepArgs& A, int i, int t) {
+  int64_t lo = A.cl_ptr[i], hi = A.cl_ptr[i + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const int c = A.cl_col[mid];
+    if (c == t) return mid;
+    if (c < t) lo = mid + 1;
     else hi = mid;
   }
   return -1;
@@ -101,6 +106,11 @@ __device__ void set_error(int* err, int code, int level, int64_t row) {
     err[2] = static_cast<int>(row & 0x7fffffff);
     err[3] = static_cast<int>(row >> 31);
   }
+}
+
+// Element (a, c) of X_ij (b_i x b_j) in the half-symmetric store.
+__device__ __forceinline__ int64_t xidx(int a, int c, int bi, int bj, bool trans) {
+  return trans ? static_cast<int64_t>(c) * bi + a : static_cast<int64_t>(a) * bj + c;
 }
 
 // Structured Householder QR update [R; C] -> [R'; 0].  R: b x b column-major
@@ -206,23 +216,16 @@ __device__ void jacobi(double* R, double* V, int b, int meff, int* any) {
   }
 }
 
-// Canonical gauge (oracle/dense.cpp canonical_basis): U1 = sign-fixed leading
-// singular vectors, U2 = trailing columns of the Householder QR of U1.
+// Canonical gauge (oracle/dense.cpp canonical_basis): U1 = leading singular
+// vectors (clusters of equal singular values -> orth(U_c U_c^T G_c), singletons
+// sign-fixed), U2 = trailing columns of the Householder QR of U1.
 // V: column-major right singular vectors of R (unsorted), perm: sorted order.
 // Writes U row-major into s.U.  Uses s.C (A, then Q) and s.R (reflectors).
-__device__ __forceinline__ double gauge_weight2(int k, int j) {
-  const double cj = __dadd_rn(0.6180339887498949, __dmul_rn(0.2071067811865475, static_cast<double>(j)));
-  const double x = __dmul_rn(static_cast<double>(k + 1), cj);
-  return 1.0 + 0.5 * (x - floor(x));
-}
-
-constexpr double kClusterTol = 1e-9;  // oracle/dense.hpp
-
-__device__ void canonical_basis(const Buf& s, int b, int r, int nsig, double* shr) {
+__device__ void canonical_basis(const Buf& s, int b, int r, int nsig) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* A = s.C;   // b x r column-major
   double* Vh = s.R;  // reflectors, column-major
-  __shared__ int cstart[512];  // cstart[k] = first index of k's cluster
+  __shared__ int cstart[512];
   if (threadIdx.x == 0) {
     int k0 = 0;
     while (k0 < r) {
@@ -233,7 +236,6 @@ __device__ void canonical_basis(const Buf& s, int b, int r, int nsig, double* sh
     }
   }
   __syncthreads();
-  // one warp per cluster: singletons get the sign fix, clusters orth(U_c U_c^T G_c)
   int nclus = 0;
   for (int k0 = 0; k0 < r; ++k0) {
     if (cstart[k0] != k0) continue;
@@ -326,7 +328,6 @@ __device__ void canonical_basis(const Buf& s, int b, int r, int nsig, double* sh
     }
     __syncthreads();
   }
-  // Q[:, r:] = H_0 ... H_{r-1} E_{r:} (column-major in C)
   double* Q = s.C;
   const int nq = b - r;
   for (int idx = threadIdx.x; idx < nq * b; idx += T) {
@@ -352,76 +353,19 @@ __device__ void canonical_basis(const Buf& s, int b, int r, int nsig, double* sh
     s.U[a * b + r + jj] = Q[idx];
   }
   __syncthreads();
-  (void)shr;
 }
 
-// Element (a, c) of X_ij (b_i x b_j) in the half-symmetric store.
-__device__ __forceinline__ int64_t xidx(int a, int c, int bi, int bj, bool trans) {
-  return trans ? static_cast<int64_t>(c) * bi + a : static_cast<int64_t>(a) * bj + c;
-}
-
-// Schur pair updates of row i for pairs [p_begin, p_end) of close(i) x close(i), ks <= kt.
-__device__ void pair_updates(const SweepArgs& A, int i, int r, int w, int64_t p_begin, int64_t p_end) {
-  const int64_t c0 = A.cl_ptr[i];
-  const int nc = static_cast<int>(A.cl_ptr[i + 1] - c0);
-  const double* G = A.fac + A.g_off[i];
-  int ks = 0;
-  int64_t idx = p_begin;
-  while (ks < nc && idx >= nc - ks) {
-    idx -= nc - ks;
-    ++ks;
-  }
-  int kt = ks + static_cast<int>(idx);
-  for (int64_t p = p_begin; p < p_end; ++p) {
-    const int s = A.cl_col[c0 + ks], t = A.cl_col[c0 + kt];  // s <= t
-    const int bs_ = A.bsz[s], bt = A.bsz[t];
-    const int64_t slot = find_slot(A.sq_ptr, A.sq_col, A.sq_slot, t, s);
-    if (slot < 0) {
-      if (threadIdx.x == 0) set_error(A.err, kErrPattern, A.level, i);
-      return;
-    }
-    double* X = A.store + A.slot_off[slot];  // stored (t, s): bt x bs
-    const double* gs = G + static_cast<int64_t>(r + A.cl_roff[c0 + ks]) * w;
-    const double* gt = G + static_cast<int64_t>(r + A.cl_roff[c0 + kt]) * w;
-    for (int e = threadIdx.x; e < bt * bs_; e += T) {
-      const int x = e / bs_, y = e % bs_;
-      double acc = 0.0;
-      for (int q = 0; q < w; ++q) acc += ldg(gt + static_cast<int64_t>(x) * w + q) * ldg(gs + static_cast<int64_t>(y) * w + q);
-      X[e] = ldg(X + e) - acc;
-    }
-    if (++kt == nc) {
-      ++ks;
-      kt = ks;
-    }
-  }
-}
-
-// Phase A: compress_row(i) + eliminate_subrow(i) (+ inline pairs when the row has no tiles).
-__device__ void phase_a(const SweepArgs& A, int i, const Buf& s, int ntiles) {
-  __shared__ double shr[4];
-  __shared__ double red[NW];
-  __shared__ int sflag[4];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int b = A.bsz[i];
-  const int64_t p0 = A.sq_ptr[i], p1 = A.sq_ptr[i + 1];
-  int64_t dslot = -1;
-  for (int64_t e = p0; e < p1; ++e)
-    if (A.sq_col[e] == i) {
-      dslot = A.sq_slot[e];
-      break;
-    }
-  double* Dg = A.store + A.slot_off[dslot];
-  for (int idx = tid; idx < b * b; idx += T) {
-    s.D[idx] = ldg(Dg + idx);
-    s.R[idx] = 0.0;
-  }
-  if (tid == 0) sflag[0] = 0;
-  __syncthreads();
-
-  // ---- gather F^T chunk by chunk into the TSQR (compression.cpp:38-48) ----
-  int fcols = 0, kfill = 0;
-  for (int64_t e = p0; e < p1; ++e) {
+// Gather the far blocks with far-ordinal in [fb, fe) of row i into F^T chunks
+// and fold them into the TSQR triangle s.R.  Returns far columns seen.
+__device__ int gather_tsqr(const SweepArgs& A, int i, int b, const Buf& s, int fb, int fe, int* nzflag,
+                           double* shr) {
+  const int tid = threadIdx.x;
+  int fcols = 0, kfill = 0, ord = 0;
+  for (int64_t e = A.sq_ptr[i]; e < A.sq_ptr[i + 1]; ++e) {
     if (A.sq_kind[e] != 2) continue;
+    const int o = ord++;
+    if (o < fb) continue;
+    if (o >= fe) break;
     const int j = A.sq_col[e];
     const int bj = A.bsz[j];
     const bool tr = j > i;
@@ -441,7 +385,7 @@ __device__ void phase_a(const SweepArgs& A, int i, const Buf& s, int ntiles) {
       }
       const double v = ldg(X + xidx(a, c, b, bj, tr));
       s.C[(kfill + c) * b + a] = v;
-      if (v != 0.0) sflag[0] = 1;
+      if (v != 0.0) *nzflag = 1;
     }
     __syncthreads();
     kfill += bj;
@@ -449,13 +393,190 @@ __device__ void phase_a(const SweepArgs& A, int i, const Buf& s, int ntiles) {
   }
   if (kfill > 0) tsqr_update(s.R, s.C, kfill, b, shr);
   __syncthreads();
+  return fcols;
+}
+
+// Strip block e of row i: rotate by U (basis) or keep, truncate far rows >= r,
+// then for close blocks g_t = (L^{-1} X[r:, :])^T and X[:r, :] -= C g_t^T, and
+// finally zero rows >= r (level_matrix.cpp:51-65, 125-171).
+// s.U = U (row-major), s.R = L (w x w), s.V = C (r x w); s.C, s.D scratch.
+__device__ void strip_block(const SweepArgs& A, int i, int b, int r, int w, bool basis, int64_t e, const Buf& s) {
+  const int tid = threadIdx.x;
+  const int j = A.sq_col[e];
+  const int bj = A.bsz[j];
+  const bool tr = j > i;
+  const int kind = A.sq_kind[e];
+  double* X = A.store + A.slot_off[A.sq_slot[e]];
+  const int n = b * bj;
+  if (basis) {
+    for (int idx = tid; idx < n; idx += T) {
+      int a, c;
+      if (tr) {
+        c = idx / b;
+        a = idx % b;
+      } else {
+        a = idx / bj;
+        c = idx % bj;
+      }
+      s.C[a * bj + c] = ldg(X + xidx(a, c, b, bj, tr));
+    }
+    __syncthreads();
+    for (int idx = tid; idx < n; idx += T) {
+      const int a = idx / bj, c = idx % bj;
+      double acc = 0.0;
+      if (!(kind == 2 && a >= r))
+        for (int k = 0; k < b; ++k) acc += s.U[k * b + a] * s.C[k * bj + c];
+      s.D[idx] = acc;
+    }
+  } else {
+    for (int idx = tid; idx < n; idx += T) {
+      int a, c;
+      if (tr) {
+        c = idx / b;
+        a = idx % b;
+      } else {
+        a = idx / bj;
+        c = idx % bj;
+      }
+      s.D[a * bj + c] = (kind == 2 && a >= r) ? 0.0 : ldg(X + xidx(a, c, b, bj, tr));
+    }
+  }
+  __syncthreads();
+  if (kind == 1 && w > 0) {
+    const int64_t ci = close_index(A, i, j);
+    const int roff = A.cl_roff[ci];
+    double* G = A.fac + A.g_off[i];
+    for (int c = tid; c < bj; c += T) {
+      double* gc = G + static_cast<int64_t>(r + roff + c) * w;
+      for (int q = 0; q < w; ++q) {
+        double acc = s.D[(r + q) * bj + c];
+        for (int p = 0; p < q; ++p) acc -= s.R[q * w + p] * s.D[(r + p) * bj + c];
+        acc /= s.R[q * w + q];
+        s.D[(r + q) * bj + c] = acc;
+        gc[q] = acc;
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < r * bj; idx += T) {
+      const int a = idx / bj, c = idx % bj;
+      double acc = 0.0;
+      for (int q = 0; q < w; ++q) acc += s.V[a * w + q] * s.D[(r + q) * bj + c];
+      s.D[idx] -= acc;
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < n; idx += T) {
+    int a, c;
+    if (tr) {
+      c = idx / b;
+      a = idx % b;
+    } else {
+      a = idx / bj;
+      c = idx % bj;
+    }
+    X[xidx(a, c, b, bj, tr)] = (w > 0 && a >= r) ? 0.0 : s.D[a * bj + c];
+  }
+  __syncthreads();
+}
+
+// Schur update of one panel pair (P, Q), P <= Q, of row i's close list:
+// X_ts -= g_t g_s^T for s in panel P, t in panel Q, s <= t (level_matrix.cpp:148-162).
+// g rows of both panels are staged in shared memory.
+__device__ void panel_update(const SweepArgs& A, int i, int r, int w, int P, int Q, double* sm) {
+  const int tid = threadIdx.x;
+  const int64_t c0 = A.cl_ptr[i];
+  const int* ps = A.pan_start + A.pan_ptr[i];
+  const int s0 = ps[P], s1 = ps[P + 1], t0 = ps[Q], t1 = ps[Q + 1];
+  const int rs0 = A.cl_roff[c0 + s0];
+  const int rsn = A.cl_roff[c0 + s1 - 1] + A.bsz[A.cl_col[c0 + s1 - 1]] - rs0;
+  const int rt0 = A.cl_roff[c0 + t0];
+  const int rtn = A.cl_roff[c0 + t1 - 1] + A.bsz[A.cl_col[c0 + t1 - 1]] - rt0;
+  const double* G = A.fac + A.g_off[i];
+  double* Gs = sm;
+  double* Gt = P == Q ? sm : sm + static_cast<int64_t>(rsn) * w;
+  for (int idx = tid; idx < rsn * w; idx += T) Gs[idx] = ldg(G + static_cast<int64_t>(r + rs0) * w + idx);
+  if (P != Q)
+    for (int idx = tid; idx < rtn * w; idx += T) Gt[idx] = ldg(G + static_cast<int64_t>(r + rt0) * w + idx);
+  __syncthreads();
+  for (int ks = s0; ks < s1; ++ks) {
+    const int s = A.cl_col[c0 + ks];
+    const int bs_ = A.bsz[s];
+    const double* gs = Gs + static_cast<int64_t>(A.cl_roff[c0 + ks] - rs0) * w;
+    for (int kt = (P == Q ? ks : t0); kt < t1; ++kt) {
+      const int t = A.cl_col[c0 + kt];
+      const int bt = A.bsz[t];
+      const double* gt = Gt + static_cast<int64_t>(A.cl_roff[c0 + kt] - rt0) * w;
+      const int64_t slot = find_slot(A.sq_ptr, A.sq_col, A.sq_slot, t, s);
+      if (slot < 0) {
+        if (tid == 0) set_error(A.err, kErrPattern, A.level, i);
+        continue;
+      }
+      double* X = A.store + A.slot_off[slot];  // stored (t, s): bt x bs
+      for (int e = tid; e < bt * bs_; e += T) {
+        const int x = e / bs_, y = e % bs_;
+        const double* a = gt + x * w;
+        const double* c = gs + y * w;
+        double acc = 0.0;
+        for (int q = 0; q < w; ++q) acc += a[q] * c[q];
+        X[e] = ldg(X + e) - acc;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ void all_panels(const SweepArgs& A, int i, int r, int w, double* sm) {
+  const int np = static_cast<int>(A.pan_ptr[i + 1] - A.pan_ptr[i]) - 1;
+  for (int P = 0; P < np; ++P)
+    for (int Q = P; Q < np; ++Q) panel_update(A, i, r, w, P, Q, sm);
+}
+
+// A2: compression decision + basis + pivot factorisation; with nA3 == 0 also the strip,
+// with nB == 0 also the Schur panels.
+__device__ void task_a2(const SweepArgs& A, int i, const Buf& s, int nA1, int nA3, int nB) {
+  __shared__ double shr[4];
+  __shared__ int sflag[4];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = A.bsz[i];
+  const int64_t p0 = A.sq_ptr[i], p1 = A.sq_ptr[i + 1];
+  int64_t dslot = -1;
+  for (int64_t e = p0; e < p1; ++e)
+    if (A.sq_col[e] == i) {
+      dslot = A.sq_slot[e];
+      break;
+    }
+  double* Dg = A.store + A.slot_off[dslot];
+  for (int idx = tid; idx < b * b; idx += T) {
+    s.D[idx] = ldg(Dg + idx);
+    s.R[idx] = 0.0;
+  }
+  if (tid == 0) sflag[0] = 0;
+  __syncthreads();
+
+  // ---- far-block triangle (compression.cpp:38-48) ----
+  int fcols;
+  if (nA1 == 0) {
+    fcols = gather_tsqr(A, i, b, s, 0, 1 << 30, &sflag[0], shr);
+  } else {
+    fcols = static_cast<int>(A.fsum[i]);
+    for (int k = 0; k < nA1; ++k) {
+      const double* Rk = A.rscratch + A.rs_off[i] + static_cast<int64_t>(k) * b * b;
+      for (int idx = tid; idx < b * b; idx += T) {
+        const int m = idx / b, j = idx % b;  // chunk row m = row m of R_k
+        s.C[idx] = ldg(Rk + j * b + m);
+      }
+      __syncthreads();
+      tsqr_update(s.R, s.C, b, b, shr);
+    }
+    if (tid == 0) sflag[0] = ld_acquire(A.nzflag + i);
+    __syncthreads();
+  }
   const bool nonzero = sflag[0] != 0;
   const int meff = fcols < b ? fcols : b;
 
   // ---- rank decision + basis (compression.cpp:20-61) ----
-  int r = 0;
+  int r = 0, nsig = 0;
   bool basis = false;
-  int nsig = 0;
   if (fcols > 0) {
     bool need_svd;
     if (A.mode == 1) {
@@ -499,17 +620,16 @@ __device__ void phase_a(const SweepArgs& A, int i, const Buf& s, int ntiles) {
       }
       basis = r < b;
     } else if (A.mode == 0) {
-      r = 0;  // all-zero fill (compression.cpp:44-47)
+      r = 0;
     }
   }
-  // (fcols == 0: r = 0, identity basis, compression.cpp:26-30)
+  const int w = b - r;
 
-  // ---- rotate the row (level_matrix.cpp:51-76) ----
+  // ---- basis and rotated diagonal (level_matrix.cpp:51-54) ----
   if (basis) {
-    canonical_basis(s, b, r, nsig, shr);
+    canonical_basis(s, b, r, nsig);
     double* Ug = A.basis + A.basis_off[i];
     for (int idx = tid; idx < b * b; idx += T) Ug[idx] = s.U[idx];
-    // D <- sym(U^T (D U))
     for (int idx = tid; idx < b * b; idx += T) {
       const int a = idx / b, c = idx % b;
       double acc = 0.0;
@@ -529,54 +649,12 @@ __device__ void phase_a(const SweepArgs& A, int i, const Buf& s, int ntiles) {
       s.D[idx] = 0.5 * (s.R[a * b + c] + s.R[c * b + a]);
     }
     __syncthreads();
-    for (int64_t e = p0; e < p1; ++e) {
-      const int kind = A.sq_kind[e];
-      if (kind == 0) continue;
-      const int j = A.sq_col[e];
-      const int bj = A.bsz[j];
-      const bool tr = j > i;
-      double* X = A.store + A.slot_off[A.sq_slot[e]];
-      for (int idx = tid; idx < b * bj; idx += T) {
-        const int a = idx / bj, c = idx % bj;
-        s.C[idx] = ldg(X + xidx(a, c, b, bj, tr));
-      }
-      __syncthreads();
-      for (int idx = tid; idx < b * bj; idx += T) {
-        int a, c;
-        if (tr) {
-          c = idx / b;
-          a = idx % b;
-        } else {
-          a = idx / bj;
-          c = idx % bj;
-        }
-        double acc = 0.0;
-        if (!(kind == 2 && a >= r))
-          for (int k = 0; k < b; ++k) acc += s.U[k * b + a] * s.C[k * bj + c];
-        X[xidx(a, c, b, bj, tr)] = acc;
-      }
-      __syncthreads();
-    }
-  } else if (r < b) {
-    for (int64_t e = p0; e < p1; ++e) {
-      if (A.sq_kind[e] != 2) continue;
-      const int j = A.sq_col[e];
-      const int bj = A.bsz[j];
-      const bool tr = j > i;
-      double* X = A.store + A.slot_off[A.sq_slot[e]];
-      for (int idx = tid; idx < (b - r) * bj; idx += T) {
-        const int a = r + idx / bj, c = idx % bj;
-        X[xidx(a, c, b, bj, tr)] = 0.0;
-      }
-    }
-    __syncthreads();
   }
 
-  // ---- eliminate_subrow (level_matrix.cpp:84-178) ----
-  const int w = b - r;
+  // ---- pivot factorisation (level_matrix.cpp:104-138) ----
   if (w > 0) {
-    double* P = s.R;      // w x w row-major
-    double* Pbak = s.V;   // backup for the shift retry
+    double* P = s.R;     // w x w
+    double* Pbak = s.V;  // shift-retry backup, then the coupling C (r x w)
     for (int idx = tid; idx < w * w; idx += T) {
       const int q = idx / w, p = idx % w;
       P[idx] = s.D[(r + q) * b + r + p];
@@ -634,96 +712,27 @@ __device__ void phase_a(const SweepArgs& A, int i, const Buf& s, int ntiles) {
       L[idx] = v;
     }
     __syncthreads();
-    // TRSM: coupling and neighbor blocks, one right-hand side column per thread
-    const int64_t c0 = A.cl_ptr[i];
-    const int nc = static_cast<int>(A.cl_ptr[i + 1] - c0);
-    const int csum = nc > 0 ? A.cl_roff[c0 + nc - 1] + A.bsz[A.cl_col[c0 + nc - 1]] : 0;
+    // coupling C = (L^{-1} D[r:, :r])^T -> G rows [0, r) and s.V
     double* G = A.fac + A.g_off[i];
-    for (int rho = tid; rho < r + csum; rho += T) {
-      double* y = G + static_cast<int64_t>(rho) * w;
-      if (rho < r) {
-        for (int q = 0; q < w; ++q) {
-          double acc = s.D[(r + q) * b + rho];
-          for (int p = 0; p < q; ++p) acc -= P[q * w + p] * y[p];
-          y[q] = acc / P[q * w + q];
-        }
-      } else {
-        const int off = rho - r;
-        int lo = 0, hi = nc - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (A.cl_roff[c0 + mid] <= off) lo = mid;
-          else hi = mid - 1;
-        }
-        const int t = A.cl_col[c0 + lo];
-        const int bt = A.bsz[t];
-        const int c = off - A.cl_roff[c0 + lo];
-        const bool tr = t > i;
-        const double* X = A.store + A.slot_off[A.cl_slot[c0 + lo]];
-        for (int q = 0; q < w; ++q) {
-          double acc = ldg(X + xidx(r + q, c, b, bt, tr));
-          for (int p = 0; p < q; ++p) acc -= P[q * w + p] * y[p];
-          y[q] = acc / P[q * w + q];
-        }
+    for (int rho = tid; rho < r; rho += T) {
+      double* y = s.V + rho * w;
+      for (int q = 0; q < w; ++q) {
+        double acc = s.D[(r + q) * b + rho];
+        for (int p = 0; p < q; ++p) acc -= P[q * w + p] * y[p];
+        y[q] = acc / P[q * w + q];
       }
+      for (int q = 0; q < w; ++q) G[static_cast<int64_t>(rho) * w + q] = y[q];
     }
     __syncthreads();
-    // Schur update of the retained part (level_matrix.cpp:140-147)
-    if (r > 0) {
-      for (int idx = tid; idx < r * r; idx += T) {
-        const int a = idx / r, c = idx % r;
-        double acc = 0.0;
-        for (int q = 0; q < w; ++q) acc += ldg(G + a * w + q) * ldg(G + c * w + q);
-        s.D[a * b + c] -= acc;
-      }
-      for (int64_t idx = tid; idx < static_cast<int64_t>(r) * csum; idx += T) {
-        const int a = static_cast<int>(idx / csum);
-        const int off = static_cast<int>(idx % csum);
-        int lo = 0, hi = nc - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (A.cl_roff[c0 + mid] <= off) lo = mid;
-          else hi = mid - 1;
-        }
-        const int t = A.cl_col[c0 + lo];
-        const int bt = A.bsz[t];
-        const int c = off - A.cl_roff[c0 + lo];
-        const bool tr = t > i;
-        double* X = A.store + A.slot_off[A.cl_slot[c0 + lo]];
-        const double* ga = G + static_cast<int64_t>(a) * w;
-        const double* gt = G + static_cast<int64_t>(r + off) * w;
-        double acc = 0.0;
-        for (int q = 0; q < w; ++q) acc += ldg(ga + q) * ldg(gt + q);
-        const int64_t xi = xidx(a, c, b, bt, tr);
-        X[xi] = ldg(X + xi) - acc;
-      }
-    }
-    __syncthreads();
-    if (ntiles == 0) {
-      pair_updates(A, i, r, w, 0, static_cast<int64_t>(nc) * (nc + 1) / 2);
-      __syncthreads();
-    }
-    // eliminated rows/cols leave the level (level_matrix.cpp:165-171)
+    // D[:r, :r] -= C C^T; eliminated rows/cols of D leave the level
     for (int idx = tid; idx < b * b; idx += T) {
       const int a = idx / b, c = idx % b;
-      if (a >= r || c >= r) s.D[idx] = 0.0;
-    }
-    for (int64_t e = p0; e < p1; ++e) {
-      if (A.sq_kind[e] == 0) continue;
-      const int j = A.sq_col[e];
-      const int bj = A.bsz[j];
-      const bool tr = j > i;
-      double* X = A.store + A.slot_off[A.sq_slot[e]];
-      for (int idx = tid; idx < w * bj; idx += T) {
-        int a, c;
-        if (tr) {
-          c = idx / w;
-          a = r + idx % w;
-        } else {
-          a = r + idx / bj;
-          c = idx % bj;
-        }
-        X[xidx(a, c, b, bj, tr)] = 0.0;
+      if (a >= r || c >= r) {
+        s.D[idx] = 0.0;
+      } else {
+        double acc = 0.0;
+        for (int q = 0; q < w; ++q) acc += s.V[a * w + q] * s.V[c * w + q];
+        s.D[idx] -= acc;
       }
     }
     __syncthreads();
@@ -736,6 +745,43 @@ __device__ void phase_a(const SweepArgs& A, int i, const Buf& s, int ntiles) {
     A.fcols[i] = fcols;
     A.nsig[i] = nsig;
   }
+  __syncthreads();
+
+  // ---- strip (thin rows) ----
+  if (nA3 == 0 && (basis || w > 0)) {
+    for (int64_t e = p0; e < p1; ++e)
+      if (A.sq_kind[e] != 0) strip_block(A, i, b, r, w, basis, e, s);
+    if (nB == 0 && w > 0) all_panels(A, i, r, w, s.R);
+  }
+}
+
+// A3 tile k: strip entries with strip-ordinal in [k*ns/nA3, (k+1)*ns/nA3).
+__device__ void task_a3(const SweepArgs& A, int i, const Buf& s, int k, int nA3, int nB) {
+  const int tid = threadIdx.x;
+  const int b = A.bsz[i];
+  const int r = __ldcg(A.rank + i), w = __ldcg(A.width + i);
+  const bool basis = __ldcg(reinterpret_cast<const unsigned char*>(A.has_basis) + i) != 0;
+  if (!basis && w == 0) return;
+  if (basis)
+    for (int idx = tid; idx < b * b; idx += T) s.U[idx] = ldg(A.basis + A.basis_off[i] + idx);
+  if (w > 0) {
+    for (int idx = tid; idx < w * w; idx += T) s.R[idx] = ldg(A.fac + A.chol_off[i] + idx);
+    for (int idx = tid; idx < r * w; idx += T) s.V[idx] = ldg(A.fac + A.g_off[i] + idx);
+  }
+  __syncthreads();
+  const int64_t p0 = A.sq_ptr[i], p1 = A.sq_ptr[i + 1];
+  const int ns = static_cast<int>(p1 - p0) - 1;
+  const int ob = static_cast<int>(static_cast<int64_t>(ns) * k / nA3);
+  const int oe = static_cast<int>(static_cast<int64_t>(ns) * (k + 1) / nA3);
+  int ord = 0;
+  for (int64_t e = p0; e < p1; ++e) {
+    if (A.sq_kind[e] == 0) continue;
+    const int o = ord++;
+    if (o < ob) continue;
+    if (o >= oe) break;
+    strip_block(A, i, b, r, w, basis, e, s);
+  }
+  (void)nB;
 }
 
 __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
@@ -744,6 +790,8 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
   const Buf s = carve(base, A.bmax, A.kcap);
   __shared__ long long s_item;
   __shared__ int s_stop;
+  __shared__ double shr[4];
+  __shared__ int nz;
   for (;;) {
     if (threadIdx.x == 0) {
       s_stop = *reinterpret_cast<volatile int*>(A.err) != 0;
@@ -753,22 +801,39 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
     if (s_stop) break;
     const long long item = s_item;
     if (item >= A.n_items) break;
-    // row owning the item: largest i with item_start[i] <= item
     int64_t lo = 0, hi = A.M - 1;
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) >> 1;
       if (A.item_start[mid] <= item) lo = mid;
       else hi = mid - 1;
     }
-    const int i = static_cast<int>(lo);
-    const int part = static_cast<int>(item - A.item_start[i]);
-    const int ntiles = static_cast<int>(A.item_start[i + 1] - A.item_start[i]) - 1;
+    const int i = A.order[lo];
+    const int part = static_cast<int>(item - A.item_start[lo]);
+    const int nA1 = A.nA1[i], nA3 = A.nA3[i], nB = A.nB[i];
+    // stage of the item and the number of this row's items it must wait for
+    int stage, k = 0, need = 0;
+    if (part < nA1) {
+      stage = 1;
+      k = part;
+    } else if (part == nA1) {
+      stage = 2;
+      need = nA1;
+    } else if (part <= nA1 + nA3) {
+      stage = 3;
+      k = part - nA1 - 1;
+      need = nA1 + 1;
+    } else {
+      stage = 4;
+      k = part - nA1 - 1 - nA3;
+      need = nA1 + 1 + nA3;
+    }
+    const bool first = (stage == 1) || (stage == 2 && nA1 == 0);
     if (threadIdx.x == 0) {
-      if (part == 0) {
+      if (first) {
         for (int64_t e = A.sq_ptr[i]; e < A.sq_ptr[i + 1]; ++e) {
           const int j = A.sq_col[e];
           if (j >= i) break;
-          const int target = static_cast<int>(A.item_start[j + 1] - A.item_start[j]);
+          const int target = 1 + A.nA1[j] + A.nA3[j] + A.nB[j];
           while (ld_acquire(A.done + j) < target) {
             if (*reinterpret_cast<volatile int*>(A.err) != 0) {
               s_stop = 1;
@@ -779,7 +844,7 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
           if (s_stop) break;
         }
       } else {
-        while (ld_acquire(A.done + i) < 1) {
+        while (ld_acquire(A.done + i) < need) {
           if (*reinterpret_cast<volatile int*>(A.err) != 0) {
             s_stop = 1;
             break;
@@ -788,18 +853,43 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
         }
       }
       __threadfence();
+      nz = 0;
     }
     __syncthreads();
     if (s_stop) break;
-    if (part == 0) {
-      phase_a(A, i, s, ntiles);
+    if (stage == 1) {
+      const int b = A.bsz[i];
+      for (int idx = threadIdx.x; idx < b * b; idx += T) s.R[idx] = 0.0;
+      __syncthreads();
+      // far-ordinal range of this leaf
+      int nf = 0;
+      for (int64_t e = A.sq_ptr[i]; e < A.sq_ptr[i + 1]; ++e) nf += A.sq_kind[e] == 2;
+      const int fb = static_cast<int>(static_cast<int64_t>(nf) * k / nA1);
+      const int fe = static_cast<int>(static_cast<int64_t>(nf) * (k + 1) / nA1);
+      gather_tsqr(A, i, b, s, fb, fe, &nz, shr);
+      double* Rk = A.rscratch + A.rs_off[i] + static_cast<int64_t>(k) * b * b;
+      for (int idx = threadIdx.x; idx < b * b; idx += T) Rk[idx] = s.R[idx];
+      if (threadIdx.x == 0 && nz) atomicOr(A.nzflag + i, 1);
+    } else if (stage == 2) {
+      task_a2(A, i, s, nA1, nA3, nB);
+    } else if (stage == 3) {
+      task_a3(A, i, s, k, nA3, nB);
     } else {
-      const int r = __ldcg(A.rank + i), w = __ldcg(A.width + i);
+      const int w = __ldcg(A.width + i);
       if (w > 0) {
-        const int nc = static_cast<int>(A.cl_ptr[i + 1] - A.cl_ptr[i]);
-        const int64_t P = static_cast<int64_t>(nc) * (nc + 1) / 2;
-        const int64_t pb = P * (part - 1) / ntiles, pe = P * part / ntiles;
-        pair_updates(A, i, r, w, pb, pe);
+        const int r = __ldcg(A.rank + i);
+        const int np = static_cast<int>(A.pan_ptr[i + 1] - A.pan_ptr[i]) - 1;
+        if (nB == 1) {
+          all_panels(A, i, r, w, s.R);
+        } else {
+          // tile k -> panel pair (P, Q), P <= Q
+          int P = 0, kk = k;
+          while (kk >= np - P) {
+            kk -= np - P;
+            ++P;
+          }
+          panel_update(A, i, r, w, P, P + kk, s.R);
+        }
       }
     }
     __syncthreads();
@@ -858,7 +948,6 @@ __global__ void remainder_kernel(RemainderArgs A) {
   for (int64_t s = blockIdx.x; s < A.M; s += gridDim.x) {
     const int rs = A.rank[s];
     if (rs == 0) continue;
-    const int bs_ = A.bsz[s];
     const int ga = A.next_block[s], ls = A.next_loc[s];
     for (int64_t e = A.sq_ptr[s]; e < A.sq_ptr[s + 1]; ++e) {
       const int t = A.sq_col[e];
@@ -912,31 +1001,29 @@ void launch_sweep(const SweepArgs& a, int grid, size_t smem_bytes, cudaStream_t 
 }
 
 void launch_pending_rotation(const SweepArgs& a, cudaStream_t s) {
+  if (a.M <= 0) return;
   const size_t smem = static_cast<size_t>(a.bmax) * a.bmax * sizeof(double);
   cudaFuncSetAttribute(pending_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (a.M > 0) {
-    note_launch();
-    pending_kernel<<<static_cast<unsigned>(a.M), T, smem, s>>>(a);
-  }
+  note_launch();
+  pending_kernel<<<static_cast<unsigned>(a.M), T, smem, s>>>(a);
 }
 
 void launch_init_store_from_matrix(int64_t M, const int* bsz, const int64_t* a_row_ptr, const int* a_col,
                                    const int64_t* a_val_ptr, const double* a_values, const int64_t* sq_ptr,
                                    const int* sq_col, const int64_t* sq_slot, const int64_t* slot_off,
                                    double* store, cudaStream_t s) {
+  if (M <= 0) return;
   const unsigned grid = static_cast<unsigned>(M < 65535 * 8 ? M : 65535 * 8);
-  if (M > 0)
-    note_launch();
-    init_store_kernel<<<grid, 128, 0, s>>>(M, bsz, a_row_ptr, a_col, a_val_ptr, a_values, sq_ptr, sq_col, sq_slot,
-                                           slot_off, store);
+  note_launch();
+  init_store_kernel<<<grid, 128, 0, s>>>(M, bsz, a_row_ptr, a_col, a_val_ptr, a_values, sq_ptr, sq_col, sq_slot,
+                                         slot_off, store);
 }
 
 void launch_remainder(const RemainderArgs& a, cudaStream_t s) {
+  if (a.M <= 0) return;
   const unsigned grid = static_cast<unsigned>(a.M < 65535 * 8 ? a.M : 65535 * 8);
-  if (a.M > 0) {
-    note_launch();
-    remainder_kernel<<<grid, 128, 0, s>>>(a);
-  }
+  note_launch();
+  remainder_kernel<<<grid, 128, 0, s>>>(a);
 }
 
 }  // namespace ceg
