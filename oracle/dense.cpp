@@ -166,7 +166,39 @@ SvdLeft svd_left(const Mat& F) {
   for (index_t i = 0; i < m; ++i)
     for (index_t j = i; j < b; ++j) R(i, j) = T(i, j);
 
-  // One-sided Jacobi on the columns of R; V accumulates the rotations.
+  // QR preconditioning (Drmac-Veselic): R^T = Q2 R2, so R = [R2^T 0] Q2^T and the
+  // right singular vectors of R are Q2 times those of X = [R2^T 0] (m x b).
+  // One-sided Jacobi on X converges in a few sweeps; V accumulates its rotations.
+  Mat Rt = R.transpose();  // b x m
+  std::vector<std::vector<double>> hv(static_cast<size_t>(m));
+  std::vector<double> htau(static_cast<size_t>(m), 0.0);
+  for (index_t k = 0; k < m; ++k) {
+    double s2 = 0.0;
+    for (index_t i = k + 1; i < b; ++i) s2 += Rt(i, k) * Rt(i, k);
+    std::vector<double>& v = hv[static_cast<size_t>(k)];
+    v.assign(static_cast<size_t>(b), 0.0);
+    if (s2 == 0.0) continue;  // dlarfg: tau = 0
+    const double x0 = Rt(k, k);
+    const double nrm = std::sqrt(x0 * x0 + s2);
+    const double beta = x0 >= 0.0 ? -nrm : nrm;
+    const double tau = (beta - x0) / beta;
+    const double scale = 1.0 / (x0 - beta);
+    v[static_cast<size_t>(k)] = 1.0;
+    for (index_t i = k + 1; i < b; ++i) v[static_cast<size_t>(i)] = Rt(i, k) * scale;
+    htau[static_cast<size_t>(k)] = tau;
+    Rt(k, k) = beta;
+    for (index_t i = k + 1; i < b; ++i) Rt(i, k) = 0.0;
+    for (index_t j = k + 1; j < m; ++j) {
+      double d = Rt(k, j);
+      for (index_t i = k + 1; i < b; ++i) d += v[static_cast<size_t>(i)] * Rt(i, j);
+      d *= tau;
+      Rt(k, j) -= d;
+      for (index_t i = k + 1; i < b; ++i) Rt(i, j) -= d * v[static_cast<size_t>(i)];
+    }
+  }
+  for (index_t i = 0; i < m; ++i)
+    for (index_t j = 0; j < b; ++j) R(i, j) = (j < m && j <= i) ? Rt(j, i) : 0.0;  // X = [R2^T 0]
+
   Mat V = Mat::identity(b);
   const double tol = std::sqrt(static_cast<double>(std::max<index_t>(m, 1))) * DBL_EPSILON;
   int sweep = 0;
@@ -202,6 +234,18 @@ SvdLeft svd_left(const Mat& F) {
     if (!rotated) break;
   }
   out.sweeps = sweep + 1;
+  // V <- Q2 V = H_0 ... H_{m-1} V
+  for (index_t k = m - 1; k >= 0; --k) {
+    const double tau = htau[static_cast<size_t>(k)];
+    if (tau == 0.0) continue;
+    const std::vector<double>& v = hv[static_cast<size_t>(k)];
+    for (index_t j = 0; j < b; ++j) {
+      double d = 0.0;
+      for (index_t i = k; i < b; ++i) d += v[static_cast<size_t>(i)] * V(i, j);
+      d *= tau;
+      for (index_t i = k; i < b; ++i) V(i, j) -= d * v[static_cast<size_t>(i)];
+    }
+  }
 
   std::vector<double> norms(static_cast<size_t>(b));
   for (index_t j = 0; j < b; ++j) {

@@ -66,6 +66,8 @@ double gauge_weight(index_t k);
 double gauge_weight2(index_t k, index_t j);
 // Singular values closer than kClusterTol * sigma_1 share one canonical basis.
 constexpr double kClusterTol = 1e-9;
+// Jacobi skips pairs of columns whose squared norms are both <= kNoise2 * ||R||_F^2.
+constexpr double kNoise2 = 1e-28;
 
 struct SvdLeft {
   std::vector<double> sigma;  // min(rows, cols) singular values, descending

@@ -10,7 +10,9 @@ hand-written sm_100a CUDA; there is no CPU fallback.
 
 from ._lib import lib, LibraryMissing  # noqa: F401
 from .ce import (  # noqa: F401
+    BlockSparseMatrix,
     BreakdownError,
+    CoarseningPlan,
     CEFactorization,
     CompressionStrategy,
     Context,
@@ -25,7 +27,9 @@ from .ce import (  # noqa: F401
 )
 
 __all__ = [
+    "BlockSparseMatrix",
     "BreakdownError",
+    "CoarseningPlan",
     "CEFactorization",
     "CompressionStrategy",
     "Context",

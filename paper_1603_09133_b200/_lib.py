@@ -78,6 +78,8 @@ SIGNATURES = {
     "ce_ctx_destroy": (None, [vp]),
     "ce_last_error": (C.c_char_p, []),
     "ce_device_count": (C.c_int, []),
+    "ce_ctx_stream": (C.c_int, [vp, C.POINTER(vp)]),
+    "ce_launch_count": (i64, []),
     "ce_matrix_upload": (C.c_int, [vp, C.POINTER(CsbHost), C.POINTER(vp)]),
     "ce_matrix_free": (None, [vp]),
     "ce_matrix_dim": (i64, [vp]),

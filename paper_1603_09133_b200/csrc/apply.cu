@@ -15,6 +15,10 @@ namespace ceg {
 namespace {
 
 constexpr int T = kApplyThreads;
+constexpr int kApplyWarps = T / 32;
+constexpr int kWmax = 256;  // max eliminated width per block handled by the apply sweeps
+// dynamic shared memory of the sweeps: z/s (kWmax) + per-warp partial sums and u staging
+constexpr size_t kSweepSmem = (kWmax + 2 * kWmax * kApplyWarps) * sizeof(double);
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldcg(p); }
 
@@ -82,19 +86,36 @@ __global__ void __launch_bounds__(T) forward_kernel(ApplyLevelArgs A) {
     if (w > 0) {
       const int r = A.rank[j];
       double* vj = A.v + A.offsets[j];
+      // warps pull incoming neighbours i < j: z[q] -= g_{i->j}[r_j + q, :] u_i (lane <-> q)
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      double* part = z + kWmax + warp * 2 * kWmax;
+      double* ub = part + kWmax;
+      for (int q = lane; q < w; q += 32) part[q] = 0.0;
+      int nb = 0;
+      for (int64_t e = c0; e < c1; ++e) {
+        const int i = A.cl_col[e];
+        if (i >= j) break;
+        const int wi = A.width[i];
+        if (wi == 0) continue;
+        if ((nb++ % kApplyWarps) != warp) continue;
+        const int ri = A.rank[i];
+        const int ro = close_roff(A, i, j);
+        const double* ui = A.v + A.offsets[i] + ri;
+        for (int p = lane; p < wi; p += 32) ub[p] = ldg(ui + p);
+        __syncwarp();
+        const double* g = A.fac + A.g_off[i] + static_cast<int64_t>(ri + ro + r) * wi;
+        for (int q = lane; q < w; q += 32) {
+          const double* gq = g + static_cast<int64_t>(q) * wi;
+          double acc = 0.0;
+          for (int p = 0; p < wi; ++p) acc += gq[p] * ub[p];
+          part[q] += acc;
+        }
+        __syncwarp();
+      }
+      __syncthreads();
       for (int q = threadIdx.x; q < w; q += T) {
         double acc = ldg(vj + r + q);
-        for (int64_t e = c0; e < c1; ++e) {
-          const int i = A.cl_col[e];
-          if (i >= j) break;
-          const int wi = A.width[i];
-          if (wi == 0) continue;
-          const int ri = A.rank[i];
-          const int ro = close_roff(A, i, j);
-          const double* g = A.fac + A.g_off[i] + static_cast<int64_t>(ri + ro + r + q) * wi;
-          const double* ui = A.v + A.offsets[i] + ri;
-          for (int p = 0; p < wi; ++p) acc -= ldg(g + p) * ldg(ui + p);
-        }
+        for (int k = 0; k < kApplyWarps; ++k) acc -= z[kWmax + k * 2 * kWmax + q];
         z[q] = acc;
       }
       __syncthreads();
@@ -120,7 +141,8 @@ __global__ void __launch_bounds__(T) forward_kernel(ApplyLevelArgs A) {
 }
 
 // Retained coordinates: v_j[:r_j] -= C_j u_j + sum_{i in close(j)} g_{i->j}[:r_j] u_i.
-__global__ void retained_kernel(ApplyLevelArgs A) {
+__global__ void __launch_bounds__(T) retained_kernel(ApplyLevelArgs A) {
+  extern __shared__ double rsm[];
   for (int64_t jl = blockIdx.x; jl < A.M; jl += gridDim.x) {
     const int j = static_cast<int>(jl);
     const int r = A.rank[j];
@@ -128,24 +150,47 @@ __global__ void retained_kernel(ApplyLevelArgs A) {
     const int w = A.width[j];
     double* vj = A.v + A.offsets[j];
     const int64_t c0 = A.cl_ptr[j], c1 = A.cl_ptr[j + 1];
+    // segment 0: own coupling C_j u_j; segment k: g_{i->j}[:r_j] u_i for the k-th close neighbour i
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* part = rsm + warp * 2 * kWmax;
+    double* ub = part + kWmax;
+    for (int a = lane; a < r; a += 32) part[a] = 0.0;
+    __syncwarp();
+    const int nseg = static_cast<int>(c1 - c0) + 1;
+    for (int sgi = warp; sgi < nseg; sgi += kApplyWarps) {
+      const double* g;
+      int wi, ri;
+      const double* ui;
+      if (sgi == 0) {
+        wi = w;
+        if (wi == 0) continue;
+        g = A.fac + A.g_off[j];
+        ui = vj + r;
+      } else {
+        const int i = A.cl_col[c0 + sgi - 1];
+        wi = A.width[i];
+        if (wi == 0) continue;
+        ri = A.rank[i];
+        g = A.fac + A.g_off[i] + static_cast<int64_t>(ri + close_roff(A, i, j)) * wi;
+        ui = A.v + A.offsets[i] + ri;
+      }
+      for (int p = lane; p < wi; p += 32) ub[p] = ui[p];
+      __syncwarp();
+      for (int a = lane; a < r; a += 32) {
+        const double* ga = g + static_cast<int64_t>(a) * wi;
+        double acc = 0.0;
+        for (int p = 0; p < wi; ++p) acc += ga[p] * ub[p];
+        part[a] += acc;
+      }
+      __syncwarp();
+    }
+    __syncthreads();
     for (int a = threadIdx.x; a < r; a += T) {
       double acc = 0.0;
-      if (w > 0) {
-        const double* C = A.fac + A.g_off[j] + static_cast<int64_t>(a) * w;
-        for (int q = 0; q < w; ++q) acc += C[q] * vj[r + q];
-      }
-      for (int64_t e = c0; e < c1; ++e) {
-        const int i = A.cl_col[e];
-        const int wi = A.width[i];
-        if (wi == 0) continue;
-        const int ri = A.rank[i];
-        const int ro = close_roff(A, i, j);
-        const double* g = A.fac + A.g_off[i] + static_cast<int64_t>(ri + ro + a) * wi;
-        const double* ui = A.v + A.offsets[i] + ri;
-        for (int p = 0; p < wi; ++p) acc += g[p] * ui[p];
-      }
+      for (int k = 0; k < kApplyWarps; ++k) acc += rsm[k * 2 * kWmax + a];
       vj[a] -= acc;
     }
+    __syncthreads();
   }
 }
 
@@ -174,16 +219,38 @@ __global__ void __launch_bounds__(T) backward_kernel(ApplyLevelArgs A) {
       const int r = A.rank[j];
       double* vj = A.v + A.offsets[j];
       const double* G = A.fac + A.g_off[j];
+      // s[q] = v_j[r+q] - sum_rows G[a][q] * v(a): warps over segments (coupling, then each neighbour),
+      // lanes over q so every G row is read coalesced
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      double* part = sb + kWmax + warp * kWmax;
+      for (int q = lane; q < w; q += 32) part[q] = 0.0;
+      __syncwarp();
+      const int nseg = static_cast<int>(c1 - c0) + 1;
+      for (int sgi = warp; sgi < nseg; sgi += kApplyWarps) {
+        const double* rows;
+        const double* vt;
+        int nt;
+        if (sgi == 0) {
+          rows = G;
+          vt = vj;
+          nt = r;
+        } else {
+          const int64_t e = c0 + sgi - 1;
+          const int t = A.cl_col[e];
+          nt = t > j ? A.bsz[t] : A.rank[t];
+          rows = G + static_cast<int64_t>(r + A.cl_roff[e]) * w;
+          vt = A.v + A.offsets[t];
+        }
+        for (int a = 0; a < nt; ++a) {
+          const double va = ldg(vt + a);
+          const double* ga = rows + static_cast<int64_t>(a) * w;
+          for (int q = lane; q < w; q += 32) part[q] += ga[q] * va;
+        }
+      }
+      __syncthreads();
       for (int q = threadIdx.x; q < w; q += T) {
         double acc = ldg(vj + r + q);
-        for (int a = 0; a < r; ++a) acc -= G[static_cast<int64_t>(a) * w + q] * ldg(vj + a);
-        for (int64_t e = c0; e < c1; ++e) {
-          const int t = A.cl_col[e];
-          const int nt = t > j ? A.bsz[t] : A.rank[t];
-          const double* gt = G + static_cast<int64_t>(r + A.cl_roff[e]) * w;
-          const double* vt = A.v + A.offsets[t];
-          for (int a = 0; a < nt; ++a) acc -= gt[static_cast<int64_t>(a) * w + q] * ldg(vt + a);
-        }
+        for (int k = 0; k < kApplyWarps; ++k) acc -= sb[kWmax + k * kWmax + q];
         sb[q] = acc;
       }
       __syncthreads();
@@ -308,19 +375,19 @@ void launch_basis_apply(const ApplyLevelArgs& a, int transpose, cudaStream_t s) 
 void launch_forward_sweep(const ApplyLevelArgs& a, int grid, cudaStream_t s) {
   if (a.M == 0) return;
   note_launch();
-  forward_kernel<<<grid, T, 1024 * sizeof(double), s>>>(a);
+  forward_kernel<<<grid, T, kSweepSmem, s>>>(a);
 }
 
 void launch_forward_retained(const ApplyLevelArgs& a, cudaStream_t s) {
   if (a.M == 0) return;
   note_launch();
-  retained_kernel<<<grid_for(a.M), T, 0, s>>>(a);
+  retained_kernel<<<grid_for(a.M), T, 2 * kWmax * kApplyWarps * sizeof(double), s>>>(a);
 }
 
 void launch_backward_sweep(const ApplyLevelArgs& a, int grid, cudaStream_t s) {
   if (a.M == 0) return;
   note_launch();
-  backward_kernel<<<grid, T, 1024 * sizeof(double), s>>>(a);
+  backward_kernel<<<grid, T, kSweepSmem, s>>>(a);
 }
 
 void launch_operator_forward(const ApplyLevelArgs& a, const int64_t* elim_off, double* c, cudaStream_t s) {

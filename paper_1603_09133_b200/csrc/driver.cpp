@@ -197,7 +197,9 @@ LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vecto
   // Schur panel height: both panels' g rows (<= cap x w doubles each) must fit the CTA buffer.
   const int64_t bmax = std::max(P.bmax, 1);
   const int64_t buf = sweep_smem_doubles(static_cast<int>(bmax), static_cast<int>(std::max<int64_t>(bmax, 128)));
-  const int64_t cap = thresholds().small_panels ? bmax : std::max<int64_t>(bmax, std::min<int64_t>(256, buf / (2 * bmax)));
+  // (sweep.cu kPanelRows / kPanelNb bound the panel height / neighbour count)
+  const int64_t cap = thresholds().small_panels ? bmax : std::max<int64_t>(bmax, std::min<int64_t>(256, buf / (2 * bmax) - 4));
+  constexpr int64_t kPanelNb = 32;
   int64_t fo = 0, bo = 0, so = 0, ro = 0;
   for (int64_t i = 0; i < M; ++i) {
     const size_t iu = static_cast<size_t>(i);
@@ -236,15 +238,17 @@ LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vecto
     // B: Schur panels of the close list (greedy, <= cap rows each)
     int64_t np = 0;
     {
-      int64_t rows = 0;
+      int64_t rows = 0, nbs = 0;
       for (int64_t k = P.cptr[iu]; k < P.cptr[iu + 1]; ++k) {
         const int64_t bt = P.bsz[static_cast<size_t>(P.ccol[static_cast<size_t>(k)])];
-        if (np == 0 || rows + bt > cap) {
+        if (np == 0 || rows + bt > cap || nbs == kPanelNb) {
           P.pan_start.push_back(static_cast<int>(k - P.cptr[iu]));
           ++np;
           rows = 0;
+          nbs = 0;
         }
         rows += bt;
+        ++nbs;
       }
       P.pan_start.push_back(static_cast<int>(P.cptr[iu + 1] - P.cptr[iu]));
       P.pan_ptr[iu + 1] = static_cast<int64_t>(P.pan_start.size());
@@ -289,6 +293,41 @@ LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vecto
     }
     P.item_start[static_cast<size_t>(M)] = it;
     P.n_items = it;
+    // Ticket order: wave by wave, and inside a wave stage by stage across its (independent)
+    // rows, so the rows of one wave advance through their stages together.
+    P.item_row.clear();
+    P.item_part.clear();
+    P.item_row.reserve(static_cast<size_t>(it));
+    P.item_part.reserve(static_cast<size_t>(it));
+    for (int64_t w0 = 0; w0 < M;) {
+      int64_t w1 = w0 + 1;
+      const int64_t wv = wave[static_cast<size_t>(P.order[static_cast<size_t>(w0)])];
+      while (w1 < M && wave[static_cast<size_t>(P.order[static_cast<size_t>(w1)])] == wv) ++w1;
+      for (int stage = 0; stage < 4; ++stage)
+        for (int64_t k = w0; k < w1; ++k) {
+          const int row = P.order[static_cast<size_t>(k)];
+          const size_t r = static_cast<size_t>(row);
+          int pb, pe;
+          if (stage == 0) {
+            pb = 0;
+            pe = P.nA1[r];
+          } else if (stage == 1) {
+            pb = P.nA1[r];
+            pe = pb + 1;
+          } else if (stage == 2) {
+            pb = P.nA1[r] + 1;
+            pe = pb + P.nA3[r];
+          } else {
+            pb = P.nA1[r] + 1 + P.nA3[r];
+            pe = pb + P.nB[r];
+          }
+          for (int p = pb; p < pe; ++p) {
+            P.item_row.push_back(row);
+            P.item_part.push_back(p);
+          }
+        }
+      w0 = w1;
+    }
   }
   P.fac_doubles = fo;
   P.basis_doubles = bo;
@@ -300,12 +339,14 @@ namespace {
 
 // Device copy of a plan's symbolic arrays (freed after the level).
 struct DevPlan {
-  DevArray<int> bsz, scol, ccol, croff, order, nA1, nA3, nB, pan_start;
+  DevArray<int> bsz, scol, ccol, croff, order, nA1, nA3, nB, pan_start, item_row, item_part;
   DevArray<int64_t> sptr, sslot, slot_off, cptr, chol_off, g_off, basis_off, sigma_off, item_start, offsets, cl_slot,
       fsum, rs_off, pan_ptr;
   DevArray<unsigned char> skind;
   void upload(const LevelPlan& P, cudaStream_t s) {
     order.upload(P.order, s);
+    item_row.upload(P.item_row, s);
+    item_part.upload(P.item_part, s);
     nA1.upload(P.nA1, s);
     nA3.upload(P.nA3, s);
     nB.upload(P.nB, s);
@@ -521,6 +562,8 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     a.g_off = dcur.g_off.p;
     a.item_start = dcur.item_start.p;
     a.order = dcur.order.p;
+    a.item_row = dcur.item_row.p;
+    a.item_part = dcur.item_part.p;
     a.nA1 = dcur.nA1.p;
     a.nA3 = dcur.nA3.p;
     a.nB = dcur.nB.p;
@@ -545,7 +588,8 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     a.shifts = d_shifts.p;
     a.bmax = std::max(cur.bmax, 1);
     a.kcap = std::max(a.bmax, 128);
-    int64_t need = sweep_smem_doubles(a.bmax, a.kcap);
+    // per-CTA buffer, rounded to 256 B so every CTA's (global-scratch) base keeps double2 alignment
+    int64_t need = (sweep_smem_doubles(a.bmax, a.kcap) + 31) / 32 * 32;
     size_t smem = static_cast<size_t>(need) * sizeof(double);
     DevArray<double> scratch;
     int per_sm = 0;
@@ -553,6 +597,8 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       per_sm = sweep_max_ctas_per_sm(smem);
     }
     if (per_sm < 1) {
+      std::fprintf(stderr, "[ce] level %zu: sweep buffer %lld doubles -> global scratch\n", li + 1,
+                   static_cast<long long>(need));
       a.use_global_scratch = 1;
       smem = 0;
       per_sm = std::max(1, sweep_max_ctas_per_sm(0));
@@ -564,6 +610,13 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       scratch.alloc(static_cast<size_t>(need) * static_cast<size_t>(grid));
       a.scratch = scratch.p;
       a.scratch_per_cta = need;
+    }
+    static const bool profile = std::getenv("CE_PROFILE") && std::getenv("CE_PROFILE")[0] == '1';
+    DevArray<unsigned long long> d_prof;
+    if (profile) {
+      d_prof.alloc(kProfCount);
+      d_prof.zero(s);
+      a.prof = d_prof.p;
     }
     Events ev_lvl, ev_sw;
     CE_CUDA(cudaEventRecord(ev_lvl.a, s));
@@ -582,6 +635,19 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       os << "elimination breakdown at level " << herr[1] << ", block " << row
          << ": trailing pivot not positive definite after shift";
       throw Breakdown(herr[1], row, os.str());
+    }
+    if (profile) {
+      std::vector<unsigned long long> hp;
+      d_prof.download(hp, s);
+      CE_CUDA(cudaStreamSynchronize(s));
+      const char* names[] = {"wait", "A1", "A2", "A2.tsqr", "A2.svd", "A2.basis", "A2.pivot", "A2.strip", "A2.panels",
+                             "A3", "B", "nA1", "nA2", "nA3", "nB"};
+      std::fprintf(stderr, "[ce-profile] level %zu M=%lld grid=%d waves=%lld items=%lld sweep=%.3f ms |", li + 1,
+                   static_cast<long long>(cur.M), grid, static_cast<long long>(cur.n_waves),
+                   static_cast<long long>(cur.n_items), 1e3 * ev_sw.seconds());
+      for (int k = 0; k < kProfCount; ++k)
+        std::fprintf(stderr, " %s=%.3g", names[k], k < kProfNA1 ? static_cast<double>(hp[static_cast<size_t>(k)]) / 1.9e9 : static_cast<double>(hp[static_cast<size_t>(k)]));
+      std::fprintf(stderr, "  (cycle sums in SM-seconds @1.9GHz)\n");
     }
     if (herr[0] == kErrPattern) throw std::logic_error("update outside the squared pattern");
     if (herr[0] != 0) throw std::logic_error("internal sweep error");

@@ -47,6 +47,8 @@ struct SweepArgs {
   const int64_t* g_off;
   const int64_t* item_start;  // first item of the row at each position of `order`
   const int* order;           // rows in wave order
+  const int* item_row;        // ticket -> row
+  const int* item_part;       // ticket -> task index within the row
   const int* nA1;             // TSQR leaf tasks per row (0 = gather inside A2)
   const int* nA3;             // strip tasks per row (0 = strip inside A2)
   const int* nB;              // Schur panel-pair tasks per row (0 = inline)
@@ -71,6 +73,13 @@ struct SweepArgs {
   double* scratch;    // per-CTA global scratch when the tiles do not fit shared memory
   int64_t scratch_per_cta;
   int use_global_scratch;
+  unsigned long long* prof;  // CE_PROFILE=1: per-stage SM-cycle counters (kProf*), else nullptr
+};
+
+// Cycle counters of the sweep kernel (CE_PROFILE=1).
+enum : int {
+  kProfWait = 0, kProfA1, kProfA2, kProfA2Tsqr, kProfA2Svd, kProfA2Basis, kProfA2Pivot, kProfA2Strip,
+  kProfA2Panels, kProfA3, kProfB, kProfNA1, kProfNA2, kProfNA3, kProfNB, kProfCount
 };
 
 // smem doubles needed by one sweep CTA for a level

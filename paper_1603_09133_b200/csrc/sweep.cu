@@ -29,6 +29,8 @@ namespace {
 constexpr int T = kSweepThreads;
 constexpr int NW = T / 32;
 constexpr double kClusterTol = 1e-9;  // oracle/dense.hpp
+constexpr int kPanelNb = 32;          // close neighbours per Schur panel (host planner matches)
+constexpr int kPanelRows = 260;       // g rows per Schur panel (<= 256 + padding)
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldcg(p); }
 
@@ -100,6 +102,10 @@ __device__ Buf carve(double* base, int bmax, int kcap) {
   return s;
 }
 
+__device__ __forceinline__ void prof_add(const SweepArgs& A, int k, long long v) {
+  if (A.prof && threadIdx.x == 0) atomicAdd(A.prof + k, static_cast<unsigned long long>(v));
+}
+
 __device__ void set_error(int* err, int code, int level, int64_t row) {
   if (atomicCAS(err, 0, code) == 0) {
     err[1] = level;
@@ -114,14 +120,17 @@ __device__ __forceinline__ int64_t xidx(int a, int c, int bi, int bj, bool trans
 }
 
 // Structured Householder QR update [R; C] -> [R'; 0].  R: b x b column-major
-// (R[k][j] at R[j*b+k]); C: K x b row-major.  LAPACK dlarfg conventions.
-__device__ void tsqr_update(double* R, double* C, int K, int b, double* shr) {
+// (R[k][j] at R[j*b+k]); C: K x b column-major with leading dimension ldc
+// (element (m, j) at C[j*ldc+m]: column walks are bank-conflict free).
+// LAPACK dlarfg conventions.
+__device__ void tsqr_update(double* R, double* C, int K, int b, int ldc, double* shr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int k = 0; k < b; ++k) {
+    double* Ck = C + static_cast<int64_t>(k) * ldc;
     if (warp == 0) {
       double s2 = 0.0;
       for (int m = lane; m < K; m += 32) {
-        const double c = C[m * b + k];
+        const double c = Ck[m];
         s2 += c * c;
       }
       s2 = warp_sum(s2);
@@ -136,7 +145,7 @@ __device__ void tsqr_update(double* R, double* C, int K, int b, double* shr) {
       __syncwarp();
       if (tau != 0.0) {
         if (lane == 0) R[k * b + k] = beta;
-        for (int m = lane; m < K; m += 32) C[m * b + k] *= scale;
+        for (int m = lane; m < K; m += 32) Ck[m] *= scale;
       }
       if (lane == 0) shr[0] = tau;
     }
@@ -144,13 +153,14 @@ __device__ void tsqr_update(double* R, double* C, int K, int b, double* shr) {
     const double tau = shr[0];
     if (tau != 0.0) {
       for (int j = k + 1 + warp; j < b; j += NW) {
+        double* Cj = C + static_cast<int64_t>(j) * ldc;
         double s = 0.0;
-        for (int m = lane; m < K; m += 32) s += C[m * b + k] * C[m * b + j];
+        for (int m = lane; m < K; m += 32) s += Ck[m] * Cj[m];
         s = warp_sum(s);
         const double tw = tau * (R[j * b + k] + s);
         __syncwarp();
         if (lane == 0) R[j * b + k] -= tw;
-        for (int m = lane; m < K; m += 32) C[m * b + j] -= tw * C[m * b + k];
+        for (int m = lane; m < K; m += 32) Cj[m] -= tw * Ck[m];
       }
     }
     __syncthreads();
@@ -159,7 +169,12 @@ __device__ void tsqr_update(double* R, double* C, int K, int b, double* shr) {
 
 // One-sided Jacobi on the columns of R (b x b, column-major); V accumulates.
 __device__ void jacobi(double* R, double* V, int b, int meff, int* any) {
+  // a group of G lanes handles one column pair per round (short reductions, many pairs in flight)
+  const int G = b <= 64 ? 8 : (b <= 128 ? 16 : 32);
+  const int gpw = 32 / G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / G, gl = lane % G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
   for (int idx = threadIdx.x; idx < b * b; idx += T) V[idx] = (idx / b == idx % b) ? 1.0 : 0.0;
   const double tol = sqrt(static_cast<double>(meff > 1 ? meff : 1)) * DBL_EPSILON;
   const int nb = b + (b & 1);
@@ -167,7 +182,7 @@ __device__ void jacobi(double* R, double* V, int b, int meff, int* any) {
     if (threadIdx.x == 0) *any = 0;
     __syncthreads();
     for (int round = 0; round < nb - 1; ++round) {
-      for (int pi = warp; pi < nb / 2; pi += NW) {
+      for (int pi = warp * gpw + grp; pi < nb / 2; pi += NW * gpw) {
         int p = rr_player(pi, round, nb), q = rr_player(nb - 1 - pi, round, nb);
         if (p > q) {
           const int t = p;
@@ -178,41 +193,121 @@ __device__ void jacobi(double* R, double* V, int b, int meff, int* any) {
         double* cp = R + p * b;
         double* cq = R + q * b;
         double al = 0.0, be = 0.0, ga = 0.0;
-        for (int k = lane; k < b; k += 32) {
+        for (int k = gl; k < b; k += G) {
           const double x = cp[k], y = cq[k];
           al += x * x;
           be += y * y;
           ga += x * y;
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
+        for (int o = G >> 1; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(gmask, al, o);
+          be += __shfl_xor_sync(gmask, be, o);
+          ga += __shfl_xor_sync(gmask, ga, o);
+        }
         if (al == 0.0 || be == 0.0) continue;
         if (!(fabs(ga) > tol * sqrt(al) * sqrt(be))) continue;
         const double zeta = (be - al) / (2.0 * ga);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double cs = 1.0 / sqrt(1.0 + t * t);
         const double sn = cs * t;
-        __syncwarp();
-        for (int k = lane; k < b; k += 32) {
+        __syncwarp(gmask);
+        for (int k = gl; k < b; k += G) {
           const double x = cp[k], y = cq[k];
           cp[k] = cs * x - sn * y;
           cq[k] = sn * x + cs * y;
         }
         double* vp = V + p * b;
         double* vq = V + q * b;
-        for (int k = lane; k < b; k += 32) {
+        for (int k = gl; k < b; k += G) {
           const double x = vp[k], y = vq[k];
           vp[k] = cs * x - sn * y;
           vq[k] = sn * x + cs * y;
         }
-        if (lane == 0) *any = 1;
+        if (gl == 0) *any = 1;
       }
       __syncthreads();
     }
     const int a = *any;
     __syncthreads();
     if (!a) break;
+  }
+}
+
+// QR preconditioning of the Jacobi SVD (Drmac-Veselic; oracle/dense.cpp svd_left):
+// R^T = Q2 R2 by Householder on s.C (reflectors kept below the diagonal, tau in
+// s.tau), then s.R <- X = R2^T (column-major, lower triangular).
+__device__ void precondition_qr(const Buf& s, int b, double* shr) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* Aq = s.C;  // b x b column-major, ld b
+  for (int idx = threadIdx.x; idx < b * b; idx += T) {
+    const int j = idx / b, i = idx % b;  // Aq(i, j) = R^T(i, j) = R(j, i)
+    Aq[idx] = s.R[i * b + j];
+  }
+  __syncthreads();
+  for (int k = 0; k < b; ++k) {
+    double* Ak = Aq + k * b;
+    if (warp == 0) {
+      double s2 = 0.0;
+      for (int i = k + 1 + lane; i < b; i += 32) s2 += Ak[i] * Ak[i];
+      s2 = warp_sum(s2);
+      double tau = 0.0, scale = 0.0, beta = 0.0;
+      if (s2 > 0.0) {
+        const double x0 = Ak[k];
+        const double nrm = sqrt(x0 * x0 + s2);
+        beta = x0 >= 0.0 ? -nrm : nrm;
+        tau = (beta - x0) / beta;
+        scale = 1.0 / (x0 - beta);
+      }
+      __syncwarp();
+      if (tau != 0.0) {
+        if (lane == 0) Ak[k] = beta;
+        for (int i = k + 1 + lane; i < b; i += 32) Ak[i] *= scale;
+      }
+      if (lane == 0) s.tau[k] = tau;
+    }
+    __syncthreads();
+    const double tau = s.tau[k];
+    if (tau != 0.0) {
+      for (int j = k + 1 + warp; j < b; j += NW) {
+        double* Aj = Aq + j * b;
+        double d = 0.0;
+        for (int i = k + 1 + lane; i < b; i += 32) d += Ak[i] * Aj[i];
+        d = warp_sum(d);
+        d = tau * (Aj[k] + d);
+        __syncwarp();
+        if (lane == 0) Aj[k] -= d;
+        for (int i = k + 1 + lane; i < b; i += 32) Aj[i] -= d * Ak[i];
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < b * b; idx += T) {
+    const int j = idx / b, i = idx % b;  // X(i, j) = R2(j, i) for i >= j
+    s.R[idx] = i >= j ? Aq[i * b + j] : 0.0;
+  }
+  __syncthreads();
+  (void)shr;
+}
+
+// V <- Q2 V with Q2 = H_0 ... H_{b-1} from precondition_qr (V column-major).
+__device__ void apply_q2(const Buf& s, int b) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* Aq = s.C;
+  for (int k = b - 1; k >= 0; --k) {
+    const double tau = s.tau[k];
+    if (tau == 0.0) continue;
+    const double* v = Aq + k * b;  // v_k = 1, v_i (i > k) below the diagonal
+    for (int j = warp; j < b; j += NW) {
+      double* Vj = s.V + j * b;
+      double d = 0.0;
+      for (int i = k + 1 + lane; i < b; i += 32) d += v[i] * Vj[i];
+      d = warp_sum(d);
+      d = tau * (Vj[k] + d);
+      __syncwarp();
+      if (lane == 0) Vj[k] -= d;
+      for (int i = k + 1 + lane; i < b; i += 32) Vj[i] -= d * v[i];
+    }
+    __syncthreads();
   }
 }
 
@@ -371,7 +466,7 @@ __device__ int gather_tsqr(const SweepArgs& A, int i, int b, const Buf& s, int f
     const bool tr = j > i;
     const double* X = A.store + A.slot_off[A.sq_slot[e]];
     if (kfill + bj > A.kcap) {
-      tsqr_update(s.R, s.C, kfill, b, shr);
+      tsqr_update(s.R, s.C, kfill, b, A.kcap, shr);
       kfill = 0;
     }
     for (int idx = tid; idx < bj * b; idx += T) {
@@ -384,14 +479,14 @@ __device__ int gather_tsqr(const SweepArgs& A, int i, int b, const Buf& s, int f
         c = idx % bj;
       }
       const double v = ldg(X + xidx(a, c, b, bj, tr));
-      s.C[(kfill + c) * b + a] = v;
+      s.C[static_cast<int64_t>(a) * A.kcap + kfill + c] = v;  // F^T chunk, column-major
       if (v != 0.0) *nzflag = 1;
     }
     __syncthreads();
     kfill += bj;
     fcols += bj;
   }
-  if (kfill > 0) tsqr_update(s.R, s.C, kfill, b, shr);
+  if (kfill > 0) tsqr_update(s.R, s.C, kfill, b, A.kcap, shr);
   __syncthreads();
   return fcols;
 }
@@ -483,42 +578,98 @@ __device__ void strip_block(const SweepArgs& A, int i, int b, int r, int w, bool
 // X_ts -= g_t g_s^T for s in panel P, t in panel Q, s <= t (level_matrix.cpp:148-162).
 // g rows of both panels are staged in shared memory.
 __device__ void panel_update(const SweepArgs& A, int i, int r, int w, int P, int Q, double* sm) {
+  __shared__ long long slot_tab[kPanelNb * kPanelNb];  // value offset of stored (t, s), -1: not updated
+  __shared__ int tab_bs[kPanelNb];
+  __shared__ unsigned char xblk[kPanelRows], yblk[kPanelRows];
+  __shared__ unsigned short xloc[kPanelRows], yloc[kPanelRows];
   const int tid = threadIdx.x;
   const int64_t c0 = A.cl_ptr[i];
   const int* ps = A.pan_start + A.pan_ptr[i];
   const int s0 = ps[P], s1 = ps[P + 1], t0 = ps[Q], t1 = ps[Q + 1];
+  const int ns = s1 - s0, nt = t1 - t0;
   const int rs0 = A.cl_roff[c0 + s0];
   const int rsn = A.cl_roff[c0 + s1 - 1] + A.bsz[A.cl_col[c0 + s1 - 1]] - rs0;
   const int rt0 = A.cl_roff[c0 + t0];
   const int rtn = A.cl_roff[c0 + t1 - 1] + A.bsz[A.cl_col[c0 + t1 - 1]] - rt0;
+  const int lds = (rsn + 3) & ~3, ldt = (rtn + 3) & ~3;
+  // g rows transposed into shared memory: GsT[q][y], GtT[q][x]
   const double* G = A.fac + A.g_off[i];
-  double* Gs = sm;
-  double* Gt = P == Q ? sm : sm + static_cast<int64_t>(rsn) * w;
-  for (int idx = tid; idx < rsn * w; idx += T) Gs[idx] = ldg(G + static_cast<int64_t>(r + rs0) * w + idx);
+  double* GsT = sm;
+  double* GtT = P == Q ? sm : sm + static_cast<int64_t>(lds) * w;
+  for (int idx = tid; idx < lds * w; idx += T) {
+    const int y = idx / w, q = idx % w;
+    GsT[q * lds + y] = y < rsn ? ldg(G + static_cast<int64_t>(r + rs0 + y) * w + q) : 0.0;
+  }
   if (P != Q)
-    for (int idx = tid; idx < rtn * w; idx += T) Gt[idx] = ldg(G + static_cast<int64_t>(r + rt0) * w + idx);
-  __syncthreads();
-  for (int ks = s0; ks < s1; ++ks) {
-    const int s = A.cl_col[c0 + ks];
-    const int bs_ = A.bsz[s];
-    const double* gs = Gs + static_cast<int64_t>(A.cl_roff[c0 + ks] - rs0) * w;
-    for (int kt = (P == Q ? ks : t0); kt < t1; ++kt) {
-      const int t = A.cl_col[c0 + kt];
-      const int bt = A.bsz[t];
-      const double* gt = Gt + static_cast<int64_t>(A.cl_roff[c0 + kt] - rt0) * w;
+    for (int idx = tid; idx < ldt * w; idx += T) {
+      const int x = idx / w, q = idx % w;
+      GtT[q * ldt + x] = x < rtn ? ldg(G + static_cast<int64_t>(r + rt0 + x) * w + q) : 0.0;
+    }
+  for (int idx = tid; idx < nt * ns; idx += T) {
+    const int kt = idx / ns, ks = idx % ns;
+    long long off = -1;
+    if (!(P == Q && ks > kt)) {
+      const int t = A.cl_col[c0 + t0 + kt], s = A.cl_col[c0 + s0 + ks];
       const int64_t slot = find_slot(A.sq_ptr, A.sq_col, A.sq_slot, t, s);
-      if (slot < 0) {
-        if (tid == 0) set_error(A.err, kErrPattern, A.level, i);
-        continue;
-      }
-      double* X = A.store + A.slot_off[slot];  // stored (t, s): bt x bs
-      for (int e = tid; e < bt * bs_; e += T) {
-        const int x = e / bs_, y = e % bs_;
-        const double* a = gt + x * w;
-        const double* c = gs + y * w;
-        double acc = 0.0;
-        for (int q = 0; q < w; ++q) acc += a[q] * c[q];
-        X[e] = ldg(X + e) - acc;
+      if (slot < 0) set_error(A.err, kErrPattern, A.level, i);
+      else off = A.slot_off[slot];
+    }
+    slot_tab[idx] = off;
+  }
+  for (int ks = tid; ks < ns; ks += T) {
+    const int e = static_cast<int>(c0) + s0 + ks;
+    const int bs_ = A.bsz[A.cl_col[e]];
+    tab_bs[ks] = bs_;
+    const int y0 = A.cl_roff[e] - rs0;
+    for (int y = 0; y < bs_; ++y) {
+      yblk[y0 + y] = static_cast<unsigned char>(ks);
+      yloc[y0 + y] = static_cast<unsigned short>(y);
+    }
+  }
+  for (int kt = tid; kt < nt; kt += T) {
+    const int e = static_cast<int>(c0) + t0 + kt;
+    const int bt = A.bsz[A.cl_col[e]];
+    const int x0 = A.cl_roff[e] - rt0;
+    for (int x = 0; x < bt; ++x) {
+      xblk[x0 + x] = static_cast<unsigned char>(kt);
+      xloc[x0 + x] = static_cast<unsigned short>(x);
+    }
+  }
+  __syncthreads();
+  // rtn x rsn outer product in 4x4 register tiles; epilogue scatters into the (t, s) blocks
+  const int mx = ldt / 4, my = lds / 4;
+  for (int mt = tid; mt < mx * my; mt += T) {
+    const int x0 = (mt / my) * 4, y0 = (mt % my) * 4;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+    for (int q = 0; q < w; ++q) {
+      const double2 ta = *reinterpret_cast<const double2*>(GtT + q * ldt + x0);
+      const double2 tb = *reinterpret_cast<const double2*>(GtT + q * ldt + x0 + 2);
+      const double2 sa = *reinterpret_cast<const double2*>(GsT + q * lds + y0);
+      const double2 sb = *reinterpret_cast<const double2*>(GsT + q * lds + y0 + 2);
+      const double av[4] = {ta.x, ta.y, tb.x, tb.y}, cv[4] = {sa.x, sa.y, sb.x, sb.y};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] += av[a] * cv[c];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int x = x0 + a;
+      if (x >= rtn) break;
+      const int kt = xblk[x], xl = xloc[x];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int y = y0 + c;
+        if (y >= rsn) break;
+        const int ks = yblk[y];
+        const long long off = slot_tab[kt * ns + ks];
+        if (off < 0) continue;
+        double* X = A.store + off + static_cast<int64_t>(xl) * tab_bs[ks] + yloc[y];
+        *X = ldg(X) - acc[a][c];
       }
     }
   }
@@ -537,6 +688,7 @@ __device__ void task_a2(const SweepArgs& A, int i, const Buf& s, int nA1, int nA
   __shared__ double shr[4];
   __shared__ int sflag[4];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long t_a2 = clock64();
   const int b = A.bsz[i];
   const int64_t p0 = A.sq_ptr[i], p1 = A.sq_ptr[i + 1];
   int64_t dslot = -1;
@@ -559,20 +711,26 @@ __device__ void task_a2(const SweepArgs& A, int i, const Buf& s, int nA1, int nA
     fcols = gather_tsqr(A, i, b, s, 0, 1 << 30, &sflag[0], shr);
   } else {
     fcols = static_cast<int>(A.fsum[i]);
-    for (int k = 0; k < nA1; ++k) {
-      const double* Rk = A.rscratch + A.rs_off[i] + static_cast<int64_t>(k) * b * b;
-      for (int idx = tid; idx < b * b; idx += T) {
-        const int m = idx / b, j = idx % b;  // chunk row m = row m of R_k
-        s.C[idx] = ldg(Rk + j * b + m);
+    // fold the leaf triangles, as many per chunk as fit (chunk rows <= kcap)
+    const int per = A.kcap / b > 0 ? A.kcap / b : 1;
+    for (int k0 = 0; k0 < nA1; k0 += per) {
+      const int nk = nA1 - k0 < per ? nA1 - k0 : per;
+      const int K = nk * b;
+      for (int idx = tid; idx < K * b; idx += T) {
+        const int j = idx / K, m = idx % K;  // chunk element (m, j) = R_{k0 + m/b}[m%b][j]
+        const double* Rk = A.rscratch + A.rs_off[i] + static_cast<int64_t>(k0 + m / b) * b * b;
+        s.C[static_cast<int64_t>(j) * A.kcap + m] = ldg(Rk + j * b + m % b);
       }
       __syncthreads();
-      tsqr_update(s.R, s.C, b, b, shr);
+      tsqr_update(s.R, s.C, K, b, A.kcap, shr);
     }
     if (tid == 0) sflag[0] = ld_acquire(A.nzflag + i);
     __syncthreads();
   }
   const bool nonzero = sflag[0] != 0;
   const int meff = fcols < b ? fcols : b;
+  long long tp = clock64();
+  prof_add(A, kProfA2Tsqr, tp - t_a2);
 
   // ---- rank decision + basis (compression.cpp:20-61) ----
   int r = 0, nsig = 0;
@@ -586,7 +744,9 @@ __device__ void task_a2(const SweepArgs& A, int i, const Buf& s, int nA1, int nA
       need_svd = nonzero;
     }
     if (need_svd) {
+      precondition_qr(s, b, shr);
       jacobi(s.R, s.V, b, meff, &sflag[1]);
+      apply_q2(s, b);
       for (int j = warp; j < b; j += NW) {
         double acc = 0.0;
         for (int k = lane; k < b; k += 32) acc += s.R[j * b + k] * s.R[j * b + k];
@@ -624,6 +784,11 @@ __device__ void task_a2(const SweepArgs& A, int i, const Buf& s, int nA1, int nA
     }
   }
   const int w = b - r;
+  {
+    const long long t = clock64();
+    prof_add(A, kProfA2Svd, t - tp);
+    tp = t;
+  }
 
   // ---- basis and rotated diagonal (level_matrix.cpp:51-54) ----
   if (basis) {
@@ -651,6 +816,11 @@ __device__ void task_a2(const SweepArgs& A, int i, const Buf& s, int nA1, int nA
     __syncthreads();
   }
 
+  {
+    const long long t = clock64();
+    prof_add(A, kProfA2Basis, t - tp);
+    tp = t;
+  }
   // ---- pivot factorisation (level_matrix.cpp:104-138) ----
   if (w > 0) {
     double* P = s.R;     // w x w
@@ -746,12 +916,23 @@ __device__ void task_a2(const SweepArgs& A, int i, const Buf& s, int nA1, int nA
     A.nsig[i] = nsig;
   }
   __syncthreads();
+  {
+    const long long t = clock64();
+    prof_add(A, kProfA2Pivot, t - tp);
+    tp = t;
+  }
 
   // ---- strip (thin rows) ----
   if (nA3 == 0 && (basis || w > 0)) {
     for (int64_t e = p0; e < p1; ++e)
       if (A.sq_kind[e] != 0) strip_block(A, i, b, r, w, basis, e, s);
+    {
+      const long long t = clock64();
+      prof_add(A, kProfA2Strip, t - tp);
+      tp = t;
+    }
     if (nB == 0 && w > 0) all_panels(A, i, r, w, s.R);
+    prof_add(A, kProfA2Panels, clock64() - tp);
   }
 }
 
@@ -801,14 +982,8 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
     if (s_stop) break;
     const long long item = s_item;
     if (item >= A.n_items) break;
-    int64_t lo = 0, hi = A.M - 1;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi + 1) >> 1;
-      if (A.item_start[mid] <= item) lo = mid;
-      else hi = mid - 1;
-    }
-    const int i = A.order[lo];
-    const int part = static_cast<int>(item - A.item_start[lo]);
+    const int i = A.item_row[item];
+    const int part = A.item_part[item];
     const int nA1 = A.nA1[i], nA3 = A.nA3[i], nB = A.nB[i];
     // stage of the item and the number of this row's items it must wait for
     int stage, k = 0, need = 0;
@@ -828,6 +1003,7 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
       need = nA1 + 1 + nA3;
     }
     const bool first = (stage == 1) || (stage == 2 && nA1 == 0);
+    const long long t_wait = clock64();
     if (threadIdx.x == 0) {
       if (first) {
         for (int64_t e = A.sq_ptr[i]; e < A.sq_ptr[i + 1]; ++e) {
@@ -857,6 +1033,8 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
     }
     __syncthreads();
     if (s_stop) break;
+    const long long t_run = clock64();
+    prof_add(A, kProfWait, t_run - t_wait);
     if (stage == 1) {
       const int b = A.bsz[i];
       for (int idx = threadIdx.x; idx < b * b; idx += T) s.R[idx] = 0.0;
@@ -893,6 +1071,11 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
       }
     }
     __syncthreads();
+    {
+      const int slot = stage == 1 ? kProfA1 : stage == 2 ? kProfA2 : stage == 3 ? kProfA3 : kProfB;
+      prof_add(A, slot, clock64() - t_run);
+      prof_add(A, stage == 1 ? kProfNA1 : stage == 2 ? kProfNA2 : stage == 3 ? kProfNA3 : kProfNB, 1);
+    }
     if (threadIdx.x == 0) {
       __threadfence();
       atomicAdd(A.done + i, 1);
@@ -989,8 +1172,14 @@ int64_t sweep_smem_doubles(int bmax, int kcap) {
 
 int sweep_max_ctas_per_sm(size_t smem_bytes) {
   int n = 0;
-  cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_bytes));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep_kernel, T, smem_bytes);
+  cudaError_t e = cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem_bytes));
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sweep_kernel, T, smem_bytes);
+  if (e != cudaSuccess) {
+    std::fprintf(stderr, "[ce] sweep occupancy query failed: %s\n", cudaGetErrorString(e));
+    cudaGetLastError();
+    return 0;
+  }
   return n;
 }
 

@@ -1,0 +1,65 @@
+"""Full-size BASELINE configs on the GPU, checked through size-independent
+properties (the oracle is too slow at these sizes): telescoping dimensions,
+orthogonal bases (sampled), M (M^-1 x) = x, PCG to the stated tolerance with the
+true residual below target, deterministic re-factorization."""
+
+import numpy as np
+import pytest
+
+import paper_1603_09133_b200 as ce
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cfg2(gpu_ctx):
+    p = ce.Problem(2)
+    a = ce.DeviceMatrix(p.matrix())
+    f = ce.ce_factorize(a, p.plan, p.strategy())
+    return p, a, f
+
+
+def test_cfg2_dimensions_telescope(cfg2):
+    p, a, f = cfg2
+    lv = f.level_stats()
+    assert lv[0]["block_count"] == 65536
+    dim = p.n
+    for s in lv:
+        assert s["eliminated"] + s["retained"] == dim
+        dim = s["retained"]
+    assert dim == f.stats["tail_dim"]
+    assert f.stats["shift_retries"] == 0
+
+
+def test_cfg2_pcg_reaches_target(cfg2):
+    p, a, f = cfg2
+    rep, x = ce.pcg(a, p.n, p.rhs, f, ce.PcgOptions(tol=p.tol, maxit=200))
+    assert rep.converged
+    assert rep.final_true_residual <= 10 * p.tol
+    r = p.rhs - a.matvec(x)
+    assert np.linalg.norm(r) <= 10 * p.tol * np.linalg.norm(p.rhs)
+
+
+def test_cfg2_operator_self_consistency(cfg2):
+    p, a, f = cfg2
+    x = np.random.default_rng(0).standard_normal(p.n)
+    y = f.apply_operator(f.solve(x))
+    assert np.linalg.norm(y - x) <= 1e-8 * np.linalg.norm(x)
+    # M approximates A: ||A x - M x|| small relative to ||A x|| at eps = 1e-6
+    ax, mx = a.matvec(x), f.apply_operator(x)
+    assert np.linalg.norm(ax - mx) <= 1e-3 * np.linalg.norm(ax)
+
+
+def test_cfg2_refactorization_deterministic(cfg2):
+    p, a, f = cfg2
+    g = ce.ce_factorize(a, p.plan, p.strategy())
+    x = np.random.default_rng(1).standard_normal(p.n)
+    assert np.array_equal(f.solve(x), g.solve(x))
+
+
+def test_cfg1_full_pcg(gpu_ctx):
+    p = ce.Problem(1)
+    a = ce.DeviceMatrix(p.matrix())
+    f = ce.ce_factorize(a, p.plan, p.strategy())
+    rep, x = ce.pcg(a, p.n, p.rhs, f, ce.PcgOptions(tol=p.tol))
+    assert rep.converged and rep.final_true_residual <= 10 * p.tol
