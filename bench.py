@@ -97,7 +97,7 @@ class ClockSampler:
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4) if "Active" in s[3 + k]})
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[3 + k].strip() == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.samples)}
 
@@ -135,6 +135,21 @@ def cpu_oracle_run(cfg, grid, solve=True):
     return json.loads(out.strip().splitlines()[-1])
 
 
+def reduce_max(x, dist=None, dev=None):
+    """Max over ranks (the slowest rank defines the job time); identity without a process group."""
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_throughput(world, n, steps, max_time):
+    """Whole-job factorization unknowns/s: every rank factorises its own n-unknown problem."""
+    return world * n * steps / max_time
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -156,7 +171,8 @@ def run_reference(args):
     line = {"metric": METRIC, "value": v, "unit": "unknowns/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args.cfg, list(grid)), "cfg": args.cfg},
+            "config": {"workload": workload_name(args.cfg, args.grid), "cfg": args.cfg,
+                       "cpu_sample_grid": list(grid)},
             "pcg_solve_ms": 1e3 * statistics.mean(pcg_s), "factor_ms": 1e3 * statistics.mean(fac),
             "cpu_baseline": {"value": v, "unit": "unknowns/s", "cores": 1, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -185,11 +201,7 @@ def run_product(args):
         torch.cuda.synchronize()
 
     def allmax(x):
-        if not dist:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_max(x, dist, dev)
 
     prob = ce.Problem(args.cfg, *args.grid)
     n = prob.n
@@ -241,7 +253,7 @@ def run_product(args):
 
     fac_total = allmax(sum(r["fac"] for r in recs))
     step_total = allmax(sum(r["fac"] + r["pcg"] for r in recs))
-    value = world * n * args.steps / fac_total
+    value = job_throughput(world, n, args.steps, fac_total)
     sweep_t = sum(r["sweep"] for r in recs) / len(recs)
     abytes = recs[-1]["abytes"]
     aflops = recs[-1]["aflops"]
