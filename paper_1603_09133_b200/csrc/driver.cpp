@@ -535,6 +535,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     }
 
     SweepArgs a{};
+    a.dbg = std::getenv("CE_DBG") ? std::atoi(std::getenv("CE_DBG")) : 0;
     a.M = cur.M;
     a.level = static_cast<int>(li) + 1;
     a.bsz = dcur.bsz.p;
@@ -641,12 +642,12 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       d_prof.download(hp, s);
       CE_CUDA(cudaStreamSynchronize(s));
       const char* names[] = {"wait", "A1", "A2", "A2.tsqr", "A2.svd", "A2.basis", "A2.pivot", "A2.strip", "A2.panels",
-                             "A3", "B", "nA1", "nA2", "nA3", "nB"};
+                             "A3", "B", "nA1", "nA2", "nA3", "nB", "svd.pre", "svd.jac", "svd.post", "sweeps", "svds"};
       std::fprintf(stderr, "[ce-profile] level %zu M=%lld grid=%d waves=%lld items=%lld sweep=%.3f ms |", li + 1,
                    static_cast<long long>(cur.M), grid, static_cast<long long>(cur.n_waves),
                    static_cast<long long>(cur.n_items), 1e3 * ev_sw.seconds());
       for (int k = 0; k < kProfCount; ++k)
-        std::fprintf(stderr, " %s=%.3g", names[k], k < kProfNA1 ? static_cast<double>(hp[static_cast<size_t>(k)]) / 1.9e9 : static_cast<double>(hp[static_cast<size_t>(k)]));
+        std::fprintf(stderr, " %s=%.3g", names[k], (k < kProfNA1 || (k >= kProfSvdPre && k <= kProfSvdPost)) ? static_cast<double>(hp[static_cast<size_t>(k)]) / 1.9e9 : static_cast<double>(hp[static_cast<size_t>(k)]));
       std::fprintf(stderr, "  (cycle sums in SM-seconds @1.9GHz)\n");
     }
     if (herr[0] == kErrPattern) throw std::logic_error("update outside the squared pattern");

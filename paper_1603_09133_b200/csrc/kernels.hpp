@@ -73,13 +73,15 @@ struct SweepArgs {
   double* scratch;    // per-CTA global scratch when the tiles do not fit shared memory
   int64_t scratch_per_cta;
   int use_global_scratch;
+  int dbg;  // CE_DBG bitmask (development): 1 generic TSQR, 2 generic Jacobi
   unsigned long long* prof;  // CE_PROFILE=1: per-stage SM-cycle counters (kProf*), else nullptr
 };
 
 // Cycle counters of the sweep kernel (CE_PROFILE=1).
 enum : int {
   kProfWait = 0, kProfA1, kProfA2, kProfA2Tsqr, kProfA2Svd, kProfA2Basis, kProfA2Pivot, kProfA2Strip,
-  kProfA2Panels, kProfA3, kProfB, kProfNA1, kProfNA2, kProfNA3, kProfNB, kProfCount
+  kProfA2Panels, kProfA3, kProfB, kProfNA1, kProfNA2, kProfNA3, kProfNB, kProfSvdPre, kProfSvdJac, kProfSvdPost,
+  kProfSweeps, kProfSvds, kProfCount
 };
 
 // smem doubles needed by one sweep CTA for a level

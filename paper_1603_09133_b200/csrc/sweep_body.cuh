@@ -1,0 +1,1390 @@
+// Level-sweep kernel body (included twice by sweep.cu, see there): task graph
+// walker, TSQR / Jacobi SVD / canonical basis / pivot Cholesky / strip / Schur
+// panels.  CE_SMEM_BUFFER selects where the per-CTA work buffer lives.
+#if CE_SMEM_BUFFER
+#define CE_SHARED(p) __builtin_assume(__isShared(p))
+#else
+#define CE_SHARED(p) ((void)0)
+#endif
+// all tiles of a (local copy of a) Buf
+#define CE_SHARED_BUF(s)                                                                             \
+  do {                                                                                               \
+    CE_SHARED(s.R); CE_SHARED(s.V); CE_SHARED(s.U); CE_SHARED(s.D); CE_SHARED(s.C);               \
+    CE_SHARED(s.sig); CE_SHARED(s.tau); CE_SHARED(s.nrm); CE_SHARED(s.perm);                       \
+  } while (0)
+
+struct Buf {
+  double *R, *V, *U, *D, *C, *sig, *tau, *nrm;
+  int* perm;
+};
+
+__device__ Buf carve(double* base, int bmax, int kcap) {
+  Buf s;
+  const Layout L = sweep_layout(bmax, kcap);
+  s.R = base;
+  s.V = s.R + L.bb;
+  s.U = s.V + L.bb;
+  s.D = s.U + L.bb;
+  s.C = s.D + L.bb;
+  s.sig = s.C + L.creg + L.extra;
+  s.tau = s.sig + bmax;
+  s.nrm = s.tau + bmax;
+  s.perm = reinterpret_cast<int*>(s.nrm + bmax);
+  return s;
+}
+
+// Structured Householder QR update [R; C] -> [R'; 0].  R: b x b column-major
+// (R[k][j] at R[j*b+k]); C: K x b column-major with odd leading dimension ldc
+// (element (m, j) at C[j*ldc+m]).  One thread per column: step k applies reflector
+// k to every column j > k, and the owner of column k+1 prepares reflector k+1 right
+// after its own update, so each step costs a single barrier.  LAPACK dlarfg conventions.
+__device__ void tsqr_update(double* R, double* C, int K, int b, int ldc, double* shr) {
+  if (threadIdx.x == 0 && b > 0) {
+    double beta;
+    const double tau = house_prep(R[0], C, K, &beta);
+    if (tau != 0.0) R[0] = beta;
+    shr[0] = tau;
+  }
+  __syncthreads();
+  for (int k = 0; k + 1 < b; ++k) {
+    const double tau = shr[k & 1];
+    for (int j = k + 1 + threadIdx.x; j < b; j += T) {
+      double* Cj = C + static_cast<int64_t>(j) * ldc;
+      if (tau != 0.0) {
+        const double* Ck = C + static_cast<int64_t>(k) * ldc;
+        const double d = tau * dot4(R[j * b + k], Ck, Cj, K);
+        R[j * b + k] -= d;
+        for (int m = 0; m < K; ++m) Cj[m] -= d * Ck[m];
+      }
+      if (j == k + 1) {
+        double beta;
+        const double t1 = house_prep(R[j * b + j], Cj, K, &beta);
+        if (t1 != 0.0) R[j * b + j] = beta;
+        shr[(k + 1) & 1] = t1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Group variant of tsqr_update: G lanes per column (partial dots combined with xor
+// shuffles inside the group), T / G columns per pass, one barrier per step; the group
+// owning column k + 1 prepares reflector k + 1 after its update.
+template <int G>
+__device__ void tsqr_group_t(double* R, double* C, int K, int b, int ldc, double* shr) {
+  constexpr int NG = T / G;
+  const int tid = threadIdx.x, grp = tid / G, gl = tid % G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((tid & 31) / G * G));
+  auto prep = [&](int j) {
+    double* Cj = C + static_cast<int64_t>(j) * ldc;
+    double s0 = 0.0, s1 = 0.0;
+    int m = gl;
+    for (; m + G < K; m += 2 * G) {
+      s0 += Cj[m] * Cj[m];
+      s1 += Cj[m + G] * Cj[m + G];
+    }
+    if (m < K) s0 += Cj[m] * Cj[m];
+    const double ss = group_sum<G>(s0 + s1, gmask);
+    const double x0 = R[j * b + j];
+    double tau = 0.0;
+    if (ss > 0.0) {
+      const double nrm = sqrt(x0 * x0 + ss);
+      const double beta = x0 >= 0.0 ? -nrm : nrm;
+      const double scale = 1.0 / (x0 - beta);
+      for (int q = gl; q < K; q += G) Cj[q] *= scale;
+      tau = (beta - x0) / beta;
+      __syncwarp(gmask);
+      if (gl == 0) R[j * b + j] = beta;
+    }
+    if (gl == 0) shr[j & 1] = tau;
+  };
+  if (grp == 0 && b > 0) prep(0);
+  __syncthreads();
+  for (int k = 0; k + 1 < b; ++k) {
+    const double tau = shr[k & 1];
+    const double* Ck = C + static_cast<int64_t>(k) * ldc;
+    for (int j = k + 1 + grp; j < b; j += NG) {
+      double* Cj = C + static_cast<int64_t>(j) * ldc;
+      if (tau != 0.0) {
+        const double rkj = R[j * b + k];
+        double s0 = 0.0, s1 = 0.0;
+        int m = gl;
+        for (; m + G < K; m += 2 * G) {
+          s0 += Ck[m] * Cj[m];
+          s1 += Ck[m + G] * Cj[m + G];
+        }
+        if (m < K) s0 += Ck[m] * Cj[m];
+        const double d = tau * (rkj + group_sum<G>(s0 + s1, gmask));
+        for (int q = gl; q < K; q += G) Cj[q] -= d * Ck[q];
+        if (gl == 0) R[j * b + k] = rkj - d;
+      }
+      if (j == k + 1) {
+        __syncwarp(gmask);
+        prep(j);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__device__ void tsqr_group(double* R, double* C, int K, int b, int ldc, double* shr) {
+  if (b <= 16) tsqr_group_t<16>(R, C, K, b, ldc, shr);
+  else if (b <= 32) tsqr_group_t<8>(R, C, K, b, ldc, shr);
+  else tsqr_group_t<8>(R, C, K, b, ldc, shr);
+}
+
+// Register-resident Householder QR update [R; C] -> [R'; 0] (same contract as
+// tsqr_update).  A group of G lanes keeps NC columns of the chunk in registers
+// (E = K / G elements per lane, K <= G * E); per step only the reflector is read
+// from shared memory (the owner writes it back into its chunk column), so shared
+// traffic per step is one K-vector per warp instead of five per column.
+template <int G, int E, int NC>
+__device__ __noinline__ void tsqr_reg_t(double* R, double* C, int K, int b, int ldc, double* shr) {
+  CE_SHARED(R);
+  CE_SHARED(C);
+  constexpr int NG = T / G;
+  const int tid = threadIdx.x, grp = tid / G, gl = tid % G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((tid & 31) / G * G));
+  double x[NC][E];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = grp + c * NG;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int m = gl + e * G;
+      x[c][e] = (j < b && m < K) ? C[static_cast<int64_t>(j) * ldc + m] : 0.0;
+    }
+  }
+  // reflector of column j (= grp + c * NG): scale the registers, publish v and tau
+  auto prep = [&](double* xc, int j) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+      s0 = fma(xc[e], xc[e], s0);
+      if (e + 1 < E) s1 = fma(xc[e + 1], xc[e + 1], s1);
+    }
+    const double x0 = R[j * b + j];  // read before the group shuffle (lane 0 overwrites it)
+    const double ss = group_sum<G>(s0 + s1, gmask);
+    double tau = 0.0;
+    if (ss > 0.0) {
+      const double n2 = fma(x0, x0, ss);
+      const bool fast = n2 > 1e-290 && n2 < 1e290;  // SFU + Newton only away from under/overflow
+      const double nrm = fast ? n2 * rsqrt_nr(n2) : sqrt(n2);
+      const double beta = x0 >= 0.0 ? -nrm : nrm;
+      const double den = x0 - beta;
+      const double scale = fast ? rcp_nr(den) : 1.0 / den;
+      tau = fast ? -den * rcp_nr(beta) : (beta - x0) / beta;
+      double* Cj = C + static_cast<int64_t>(j) * ldc;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int m = gl + e * G;
+        xc[e] *= scale;
+        if (m < K) Cj[m] = xc[e];
+      }
+      if (gl == 0) R[j * b + j] = beta;
+    }
+    if (gl == 0) shr[j & 1] = tau;
+  };
+  if (grp == 0 && b > 0) prep(x[0], 0);
+  __syncthreads();
+  for (int k = 0; k + 1 < b; ++k) {
+    const double tau = shr[k & 1];
+    if (tau != 0.0) {
+      const double* Ck = C + static_cast<int64_t>(k) * ldc;
+      // partial dots of every owned column against v_k (v read once), then the update
+      // (v re-read: keeping it in registers as well would spill for NC > 1)
+      double sd[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) sd[c] = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int m = gl + e * G;
+        const double ve = m < K ? Ck[m] : 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sd[c] = fma(ve, x[c][e], sd[c]);
+      }
+      double dd[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int j = grp + c * NG;
+        dd[c] = 0.0;
+        if (j > k && j < b) {
+          const double rkj = R[j * b + k];
+          dd[c] = tau * (rkj + group_sum<G>(sd[c], gmask));
+          if (gl == 0) R[j * b + k] = rkj - dd[c];
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int m = gl + e * G;
+        const double ve = m < K ? Ck[m] : 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) x[c][e] = fma(-dd[c], ve, x[c][e]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (grp + c * NG == k + 1) prep(x[c], k + 1);
+    __syncthreads();
+  }
+}
+
+// Dispatch: register-resident variants for b <= 64 and K <= 128, else the generic one.
+__device__ void tsqr_fast(double* R, double* C, int K, int b, int ldc, double* shr) {
+  if (K <= 128 && b <= 16) tsqr_reg_t<16, 8, 1>(R, C, K, b, ldc, shr);
+  else if (K <= 128 && b <= 32) tsqr_reg_t<8, 16, 1>(R, C, K, b, ldc, shr);
+  else if (K <= 128 && b <= 64) tsqr_reg_t<8, 16, 2>(R, C, K, b, ldc, shr);
+  else tsqr_group(R, C, K, b, ldc, shr);
+}
+
+// One-sided Jacobi (Hestenes) on the columns of X (b x b, column-major, odd leading
+// dimension ld); V (same layout) accumulates the rotations.  Round-robin rounds of
+// disjoint column pairs; a group of G lanes owns one pair, partial dots are combined
+// with xor shuffles inside the group.  Small blocks (all pairs fit one warp) run on
+// warp 0 with no CTA barrier; larger ones use the whole CTA with one barrier per round.
+// Rotation test |gamma| > tol sqrt(alpha beta), tol = sqrt(m) eps (oracle/dense.cpp svd_left).
+__device__ int jacobi(double* X, double* V, int b, int ld, int meff) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int idx = tid; idx < b * ld; idx += T) V[idx] = (idx / ld == idx % ld) ? 1.0 : 0.0;
+  __syncthreads();
+  const double tol = sqrt(static_cast<double>(meff > 1 ? meff : 1)) * DBL_EPSILON;
+  const double tol2 = tol * tol;
+  const int nb = b + (b & 1);
+  const int np = nb / 2;
+  int G = 1;
+  while (G < 16 && np * G * 2 <= T) G *= 2;
+  const bool one_warp = np * 4 <= 32;
+  if (one_warp) G = 32 / np >= 8 ? 8 : (32 / np >= 4 ? 4 : 2);
+  const int pi = tid / G, gl = tid % G;
+  __shared__ int s_sweeps;
+  if (one_warp && tid >= 32) {
+    __syncthreads();
+    return s_sweeps;
+  }
+  int nsw = 100;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    int rotated = 0;
+    for (int round = 0; round < nb - 1; ++round) {
+      for (int base = 0; base < np; base += T / G) {
+        int p = 0, q = b;
+        if (base + pi < np) {
+          p = rr_player(base + pi, round, nb);
+          q = rr_player(nb - 1 - base - pi, round, nb);
+          if (p > q) {
+            const int t = p;
+            p = q;
+            q = t;
+          }
+        }
+        const bool valid = q < b;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        double* cp = X + p * ld;
+        double* cq = X + q * ld;
+        if (valid) {
+          for (int k = gl; k < b; k += G) {
+            const double x = cp[k], y = cq[k];
+            al += x * x;
+            be += y * y;
+            ga += x * y;
+          }
+        }
+        for (int o = G >> 1; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (valid && al != 0.0 && be != 0.0 && ga * ga > tol2 * al * be) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = rsqrt(1.0 + t * t);
+          const double sn = cs * t;
+          for (int k = gl; k < b; k += G) {
+            const double x = cp[k], y = cq[k];
+            cp[k] = cs * x - sn * y;
+            cq[k] = sn * x + cs * y;
+          }
+          double* vp = V + p * ld;
+          double* vq = V + q * ld;
+          for (int k = gl; k < b; k += G) {
+            const double x = vp[k], y = vq[k];
+            vp[k] = cs * x - sn * y;
+            vq[k] = sn * x + cs * y;
+          }
+          rotated = 1;
+        }
+      }
+      if (one_warp) __syncwarp();
+      else if (round < nb - 2) __syncthreads();
+    }
+    const int any = one_warp ? __any_sync(0xffffffffu, rotated) : __syncthreads_or(rotated);
+    if (!any) {
+      nsw = sweep + 1;
+      break;
+    }
+  }
+  if (one_warp) {
+    if (tid == 0) s_sweeps = nsw;
+    __syncthreads();
+  }
+  return nsw;
+}
+
+// Unrolled one-sided Jacobi for b <= G * E: G lanes per column pair, the pair's two
+// columns held in registers for the round (E elements per lane); only the first
+// roundup(np * G, 32) threads take part (warp-synchronous when that is one warp).
+// Angle: t = sign(d) 2g / (|d| + sqrt(d^2 + 4g^2)) with d = beta - alpha, the same
+// root as oracle/dense.cpp (zeta = d / 2g), from SFU approximations + Newton steps.
+template <int G, int E>
+__device__ __noinline__ int jacobi_t(double* X, double* V, int b, int ld, int meff) {
+  CE_SHARED(X);
+  CE_SHARED(V);
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < b * ld; idx += T) V[idx] = (idx / ld == idx % ld) ? 1.0 : 0.0;
+  const int nb = b + (b & 1), np = nb / 2, nr = nb - 1;
+  const int nact = (np * G + 31) & ~31;
+  __shared__ int s_sweeps;
+  __syncthreads();
+  if (tid >= nact) {
+    __syncthreads();
+    return s_sweeps;
+  }
+  const double tol = sqrt(static_cast<double>(meff > 1 ? meff : 1)) * DBL_EPSILON;
+  const double tol2 = tol * tol;
+  const int pi = tid / G, gl = tid % G;
+  int nsw = 100;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    int rotated = 0;
+    for (int round = 0; round < nr; ++round) {
+      // round-robin players of pair pi: 0 and nb-1-pi rotate through 1..nb-1
+      int p = 0, q = b;
+      if (pi < np) {
+        int a = pi - 1 + round;
+        a = pi == 0 ? -1 : (a >= nr ? a - nr : a);
+        int c = nb - 2 - pi + round;
+        c = c >= nr ? c - nr : c;
+        p = a + 1;
+        q = c + 1;
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+      }
+      const bool valid = q < b;
+      double* cp = X + p * ld;
+      double* cq = X + (valid ? q : p) * ld;
+      double x[E], y[E];
+      double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int k = gl + e * G;
+        const bool in = valid && k < b;
+        x[e] = in ? cp[k] : 0.0;
+        y[e] = in ? cq[k] : 0.0;
+        al = fma(x[e], x[e], al);
+        be = fma(y[e], y[e], be);
+        ga = fma(x[e], y[e], ga);
+      }
+#pragma unroll
+      for (int o = G >> 1; o > 0; o >>= 1) {
+        al += __shfl_xor_sync(0xffffffffu, al, o);
+        be += __shfl_xor_sync(0xffffffffu, be, o);
+        ga += __shfl_xor_sync(0xffffffffu, ga, o);
+      }
+      // rotation test |gamma| > tol sqrt(alpha) sqrt(beta), squared unless alpha beta underflows
+      const double ab = al * be;
+      const bool rot = valid && al != 0.0 && be != 0.0 &&
+                       (ab > 1e-290 ? ga * ga > tol2 * ab : fabs(ga) > tol * sqrt(al) * sqrt(be));
+      if (rot) {
+        const double d = be - al;
+        const double g2 = ga + ga;
+        const double hh = fma(d, d, g2 * g2);
+        double t;
+        if (hh > 1e-290 && hh < 1e290) {
+          const double h = hh * rsqrt_nr(hh);
+          t = (d >= 0.0 ? g2 : -g2) * rcp_nr(fabs(d) + h);
+        } else {  // extreme magnitudes: the oracle's IEEE formula
+          const double zeta = d / g2;
+          t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        }
+        const double cs = rsqrt_nr(fma(t, t, 1.0));
+        const double sn = cs * t;
+        double* vp = V + p * ld;
+        double* vq = V + q * ld;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int k = gl + e * G;
+          if (k < b) {
+            cp[k] = cs * x[e] - sn * y[e];
+            cq[k] = sn * x[e] + cs * y[e];
+            const double u = vp[k], w = vq[k];
+            vp[k] = cs * u - sn * w;
+            vq[k] = sn * u + cs * w;
+          }
+        }
+        rotated = 1;
+      }
+      if (nact == 32) __syncwarp();
+      else if (round + 1 < nr) bar_n(nact);
+    }
+    const int any = nact == 32 ? __any_sync(0xffffffffu, rotated) : bar_or(nact, rotated);
+    if (!any) {
+      nsw = sweep + 1;
+      break;
+    }
+  }
+  if (tid == 0) s_sweeps = nsw;
+  __syncthreads();
+  return nsw;
+}
+
+__device__ int jacobi_fast(double* X, double* V, int b, int ld, int meff) {
+  if (b <= 16) return jacobi_t<4, 4>(X, V, b, ld, meff);
+  if (b <= 32) return jacobi_t<8, 4>(X, V, b, ld, meff);
+  if (b <= 64) return jacobi_t<8, 8>(X, V, b, ld, meff);
+  return jacobi(X, V, b, ld, meff);
+}
+
+// QR preconditioning of the Jacobi SVD (Drmac-Veselic; oracle/dense.cpp svd_left):
+// R^T = Q2 R2 by Householder on s.C (b x b column-major, leading dimension pad_ld(b);
+// reflectors kept below the diagonal, tau in s.tau), then s.R <- X = R2^T
+// (column-major, leading dimension pad_ld(b), lower triangular).  One thread per column,
+// the owner of column k + 1 prepares reflector k + 1 right after its own update.
+__device__ __noinline__ void precondition_qr(const Buf& s_, int b) {
+  const Buf s = s_;
+  CE_SHARED_BUF(s);
+  const int ld = pad_ld(b);
+  double* Aq = s.C;
+  for (int idx = threadIdx.x; idx < b * b; idx += T) {
+    const int j = idx / b, i = idx % b;  // Aq(i, j) = R^T(i, j) = R(j, i)
+    Aq[j * ld + i] = s.R[i * b + j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && b > 0) {
+    double beta;
+    const double tau = house_prep(Aq[0], Aq + 1, b - 1, &beta);
+    if (tau != 0.0) Aq[0] = beta;
+    s.tau[0] = tau;
+  }
+  __syncthreads();
+  for (int k = 0; k + 1 < b; ++k) {
+    const double tau = s.tau[k];
+    const double* Ak = Aq + k * ld;
+    for (int j = k + 1 + threadIdx.x; j < b; j += T) {
+      double* Aj = Aq + j * ld;
+      if (tau != 0.0) {
+        const double d = tau * dot4(Aj[k], Ak + k + 1, Aj + k + 1, b - k - 1);
+        Aj[k] -= d;
+        for (int i = k + 1; i < b; ++i) Aj[i] -= d * Ak[i];
+      }
+      if (j == k + 1) {
+        double beta;
+        const double t1 = house_prep(Aj[j], Aj + j + 1, b - j - 1, &beta);
+        if (t1 != 0.0) Aj[j] = beta;
+        s.tau[j] = t1;
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < b * b; idx += T) {
+    const int j = idx / b, i = idx % b;  // X(i, j) = R2(j, i) for i >= j
+    s.R[j * ld + i] = i >= j ? Aq[i * ld + j] : 0.0;
+  }
+  __syncthreads();
+}
+
+// V <- Q2 V with Q2 = H_0 ... H_{b-1} from precondition_qr (V column-major, ld pad_ld(b)).
+// One thread per column of V, one barrier per reflector.
+__device__ __noinline__ void apply_q2(const Buf& s_, int b) {
+  const Buf s = s_;
+  CE_SHARED_BUF(s);
+  const int ld = pad_ld(b);
+  const double* Aq = s.C;
+  for (int k = b - 2; k >= 0; --k) {
+    const double tau = s.tau[k];
+    if (tau == 0.0) continue;
+    const double* v = Aq + k * ld;  // v_k = 1, v_i (i > k) below the diagonal
+    for (int j = threadIdx.x; j < b; j += T) {
+      double* Vj = s.V + j * ld;
+      const double d = tau * dot4(Vj[k], v + k + 1, Vj + k + 1, b - k - 1);
+      Vj[k] -= d;
+      for (int i = k + 1; i < b; ++i) Vj[i] -= d * v[i];
+    }
+    __syncthreads();
+  }
+}
+
+// Canonical gauge (oracle/dense.cpp canonical_basis): U1 = leading singular
+// vectors (clusters of equal singular values -> orth(U_c U_c^T G_c), singletons
+// sign-fixed), U2 = trailing columns of the Householder QR of U1.
+// V: column-major right singular vectors of R (unsorted), perm: sorted order.
+// Writes U row-major into s.U.  Uses s.C (A, then Q) and s.R (reflectors).
+__device__ __noinline__ void canonical_basis(const Buf& s_, int b, int r, int nsig) {
+  const Buf s = s_;
+  CE_SHARED_BUF(s);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* A = s.C;   // b x r column-major
+  double* Vh = s.R;  // reflectors, column-major
+  __shared__ int cstart[512];
+  if (threadIdx.x == 0) {
+    int k0 = 0;
+    while (k0 < r) {
+      int k1 = k0 + 1;
+      while (k1 < r && k1 < nsig && s.sig[k1 - 1] - s.sig[k1] <= kClusterTol * s.sig[0]) ++k1;
+      for (int k = k0; k < k1; ++k) cstart[k] = k0;
+      k0 = k1;
+    }
+  }
+  __syncthreads();
+  int nclus = 0;
+  for (int k0 = 0; k0 < r; ++k0) {
+    if (cstart[k0] != k0) continue;
+    int k1 = k0 + 1;
+    while (k1 < r && cstart[k1] == k0) ++k1;
+    const int c = k1 - k0;
+    if ((nclus++ % NW) != warp) continue;
+    if (c == 1) {
+      const double* v = s.V + static_cast<int64_t>(s.perm[k0]) * pad_ld(b);
+      double g = 0.0;
+      for (int a = lane; a < b; a += 32) g += gauge_weight(a) * v[a];
+      g = warp_sum(g);
+      const double sg = g >= 0.0 ? 1.0 : -1.0;
+      for (int a = lane; a < b; a += 32) A[k0 * b + a] = sg * v[a];
+    } else {
+      for (int j = 0; j < c; ++j) {
+        double* z = A + (k0 + j) * b;
+        for (int a = lane; a < b; a += 32) z[a] = 0.0;
+        for (int q = 0; q < c; ++q) {
+          const double* v = s.V + static_cast<int64_t>(s.perm[k0 + q]) * pad_ld(b);
+          double m = 0.0;
+          for (int a = lane; a < b; a += 32) m += v[a] * gauge_weight2(a, j);
+          m = warp_sum(m);
+          for (int a = lane; a < b; a += 32) z[a] += v[a] * m;
+        }
+      }
+      __syncwarp();
+      for (int j = 0; j < c; ++j) {
+        double* z = A + (k0 + j) * b;
+        for (int pass = 0; pass < 2; ++pass)
+          for (int q = 0; q < j; ++q) {
+            const double* y = A + (k0 + q) * b;
+            double d = 0.0;
+            for (int a = lane; a < b; a += 32) d += y[a] * z[a];
+            d = warp_sum(d);
+            for (int a = lane; a < b; a += 32) z[a] -= d * y[a];
+            __syncwarp();
+          }
+        double n2 = 0.0;
+        for (int a = lane; a < b; a += 32) n2 += z[a] * z[a];
+        const double nrm = sqrt(warp_sum(n2));
+        for (int a = lane; a < b; a += 32) z[a] /= nrm;
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < b * r; idx += T) {
+    const int k = idx / b, a = idx % b;
+    s.U[a * b + k] = A[idx];
+  }
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    if (warp == 0) {
+      double n2 = 0.0, rest = 0.0, g = 0.0;
+      for (int a = k + lane; a < b; a += 32) {
+        const double x = A[k * b + a];
+        n2 += x * x;
+        if (a > k) rest += x * x;
+        g += gauge_weight(a) * x;
+      }
+      n2 = warp_sum(n2);
+      rest = warp_sum(rest);
+      g = warp_sum(g);
+      const double nrm = sqrt(n2);
+      double tau = 0.0;
+      if (nrm != 0.0) {
+        const double sg = g >= 0.0 ? 1.0 : -1.0;
+        const double xk = A[k * b + k];
+        const double beta = -sg * nrm;
+        double vk;
+        if (xk == 0.0 || (xk > 0.0) == (sg > 0.0)) vk = xk - beta;
+        else vk = -rest / (xk + beta);
+        const double vtv = vk * vk + rest;
+        tau = vtv > 0.0 ? 2.0 / vtv : 0.0;
+        for (int a = k + lane; a < b; a += 32) Vh[k * b + a] = (a == k) ? vk : A[k * b + a];
+      }
+      if (lane == 0) s.tau[k] = tau;
+    }
+    __syncthreads();
+    const double tau = s.tau[k];
+    if (tau != 0.0) {
+      for (int j = k + 1 + warp; j < r; j += NW) {
+        double d = 0.0;
+        for (int a = k + lane; a < b; a += 32) d += Vh[k * b + a] * A[j * b + a];
+        d = warp_sum(d) * tau;
+        __syncwarp();
+        for (int a = k + lane; a < b; a += 32) A[j * b + a] -= d * Vh[k * b + a];
+      }
+    }
+    __syncthreads();
+  }
+  double* Q = s.C;
+  const int nq = b - r;
+  for (int idx = threadIdx.x; idx < nq * b; idx += T) {
+    const int jj = idx / b, a = idx % b;
+    Q[idx] = (a == r + jj) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int k = r - 1; k >= 0; --k) {
+    const double tau = s.tau[k];
+    if (tau != 0.0) {
+      for (int jj = warp; jj < nq; jj += NW) {
+        double d = 0.0;
+        for (int a = k + lane; a < b; a += 32) d += Vh[k * b + a] * Q[jj * b + a];
+        d = warp_sum(d) * tau;
+        __syncwarp();
+        for (int a = k + lane; a < b; a += 32) Q[jj * b + a] -= d * Vh[k * b + a];
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < nq * b; idx += T) {
+    const int jj = idx / b, a = idx % b;
+    s.U[a * b + r + jj] = Q[idx];
+  }
+  __syncthreads();
+}
+
+__device__ void tsqr_sel(const SweepArgs& A, double* R, double* C, int K, int b, int ldc, double* shr) {
+  if (A.dbg & 1) tsqr_group(R, C, K, b, ldc, shr);
+  else tsqr_fast(R, C, K, b, ldc, shr);
+}
+
+// Gather the far blocks with far-ordinal in [fb, fe) of row i into F^T chunks
+// and fold them into the TSQR triangle s.R.  Returns far columns seen.
+__device__ int gather_tsqr(const SweepArgs& A, int i, int b, const Buf& s_, int fb, int fe, int* nzflag,
+                           double* shr) {
+  const Buf s = s_;
+  CE_SHARED_BUF(s);
+  const int tid = threadIdx.x;
+  int fcols = 0, kfill = 0, ord = 0;
+  for (int64_t e = A.sq_ptr[i]; e < A.sq_ptr[i + 1]; ++e) {
+    if (A.sq_kind[e] != 2) continue;
+    const int o = ord++;
+    if (o < fb) continue;
+    if (o >= fe) break;
+    const int j = A.sq_col[e];
+    const int bj = A.bsz[j];
+    const bool tr = j > i;
+    const double* X = A.store + A.slot_off[A.sq_slot[e]];
+    if (kfill + bj > A.kcap) {
+      tsqr_sel(A, s.R, s.C, kfill, b, chunk_ld(A.kcap), shr);
+      kfill = 0;
+    }
+    for (int idx = tid; idx < bj * b; idx += T) {
+      int a, c;
+      if (tr) {
+        c = idx / b;
+        a = idx % b;
+      } else {
+        a = idx / bj;
+        c = idx % bj;
+      }
+      const double v = ldg(X + xidx(a, c, b, bj, tr));
+      s.C[static_cast<int64_t>(a) * chunk_ld(A.kcap) + kfill + c] = v;  // F^T chunk, column-major
+      if (v != 0.0) *nzflag = 1;
+    }
+    __syncthreads();
+    kfill += bj;
+    fcols += bj;
+  }
+  if (kfill > 0) tsqr_sel(A, s.R, s.C, kfill, b, chunk_ld(A.kcap), shr);
+  __syncthreads();
+  return fcols;
+}
+
+// Strip entries of row i with strip-ordinal in [ob, oe), in column chunks of up to
+// cw columns (the blocks' columns side by side, one thread per column):
+//   rotate by U (basis rows) or keep; far blocks keep rows < r only;
+//   close blocks: g_t = (L^{-1} X[r:, :])^T -> G rows, X[:r, :] -= C g_t^T;
+//   rows >= r are zeroed on write-back (level_matrix.cpp:51-65, 125-171).
+// s.U = U (row-major), s.R = L (w x w), s.V = C (r x w); [s.D, s.sig) holds the chunks.
+__device__ __noinline__ void strip_range(const SweepArgs& A, int i, int b, int r, int w, bool basis, int ob, int oe,
+                            const Buf& s_) {
+  const Buf s = s_;
+  CE_SHARED_BUF(s);
+  constexpr int kMaxBlk = 64;
+  __shared__ long long ch_e[kMaxBlk];
+  __shared__ int ch_c0[kMaxBlk + 1];
+  __shared__ int ch_roff[kMaxBlk];
+  __shared__ int ch_n, ch_ord;
+  __shared__ long long ch_next;
+  const int tid = threadIdx.x;
+  const int cw = sweep_layout(A.bmax, A.kcap).cw;
+  double* IN = s.D;
+  double* OUT = basis ? s.D + static_cast<int64_t>(b) * cw : s.D;
+  for (int q = tid; q < w; q += T) s.tau[q] = 1.0 / s.R[q * w + q];
+  const int64_t p0 = A.sq_ptr[i], p1 = A.sq_ptr[i + 1];
+  if (tid == 0) {
+    ch_next = p0;
+    ch_ord = 0;
+  }
+  __syncthreads();
+  for (;;) {
+    if (tid == 0) {
+      int64_t e = ch_next;
+      int ord = ch_ord, n = 0, cols = 0;
+      for (; e < p1; ++e) {
+        const int kind = A.sq_kind[e];
+        if (kind == 0) continue;
+        if (ord >= oe) {
+          e = p1;
+          break;
+        }
+        if (ord < ob) {
+          ++ord;
+          continue;
+        }
+        const int j = A.sq_col[e];
+        const int bj = A.bsz[j];
+        if (n == kMaxBlk || cols + bj > cw) break;
+        ch_e[n] = e;
+        ch_c0[n] = cols;
+        ch_roff[n] = kind == 1 ? A.cl_roff[close_index(A, i, j)] : -1;
+        ++n;
+        cols += bj;
+        ++ord;
+      }
+      ch_c0[n] = cols;
+      ch_n = n;
+      ch_next = e;
+      ch_ord = ord;
+    }
+    __syncthreads();
+    const int n = ch_n;
+    if (n == 0) break;
+    const int ncol = ch_c0[n];
+    for (int k = 0; k < n; ++k) {
+      const int64_t ek = ch_e[k];
+      const int j = A.sq_col[ek], bj = A.bsz[j];
+      const bool tr = j > i, far = ch_roff[k] < 0;
+      const double* X = A.store + A.slot_off[A.sq_slot[ek]];
+      double* dst = IN + ch_c0[k];
+      for (int idx = tid; idx < b * bj; idx += T) {
+        int a, c;
+        if (tr) {
+          c = idx / b;
+          a = idx % b;
+        } else {
+          a = idx / bj;
+          c = idx % bj;
+        }
+        dst[a * cw + c] = (!basis && far && a >= r) ? 0.0 : ldg(X + xidx(a, c, b, bj, tr));
+      }
+    }
+    __syncthreads();
+    for (int c = tid; c < ncol; c += T) {
+      int k = 0;
+      while (ch_c0[k + 1] <= c) ++k;
+      const bool far = ch_roff[k] < 0;
+      if (basis) {
+        const int na = far ? r : b;
+        for (int a0 = 0; a0 < na; a0 += 8) {
+          double acc[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+          for (int kk = 0; kk < b; ++kk) {
+            const double x = IN[kk * cw + c];
+            const double* Ur = s.U + kk * b + a0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[u] = fma(Ur[u], x, acc[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (a0 + u < na) OUT[(a0 + u) * cw + c] = acc[u];
+        }
+      }
+      if (!far && w > 0) {
+        double* G = A.fac + A.g_off[i] + static_cast<int64_t>(r + ch_roff[k] + c - ch_c0[k]) * w;
+        double* y = OUT + static_cast<int64_t>(r) * cw + c;
+        for (int q = 0; q < w; ++q) {
+          const double* Lq = s.R + q * w;
+          double a0 = y[q * cw], a1 = 0.0;
+          int p = 0;
+          for (; p + 1 < q; p += 2) {
+            a0 = fma(-Lq[p], y[p * cw], a0);
+            a1 = fma(-Lq[p + 1], y[(p + 1) * cw], a1);
+          }
+          if (p < q) a0 = fma(-Lq[p], y[p * cw], a0);
+          const double v = (a0 + a1) * s.tau[q];
+          y[q * cw] = v;
+          G[q] = v;
+        }
+        int a = 0;
+        for (; a + 3 < r; a += 4) {
+          double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+          for (int q = 0; q < w; ++q) {
+            const double yq = y[q * cw];
+            c0 = fma(s.V[a * w + q], yq, c0);
+            c1 = fma(s.V[(a + 1) * w + q], yq, c1);
+            c2 = fma(s.V[(a + 2) * w + q], yq, c2);
+            c3 = fma(s.V[(a + 3) * w + q], yq, c3);
+          }
+          OUT[a * cw + c] -= c0;
+          OUT[(a + 1) * cw + c] -= c1;
+          OUT[(a + 2) * cw + c] -= c2;
+          OUT[(a + 3) * cw + c] -= c3;
+        }
+        for (; a < r; ++a) {
+          double c0 = 0.0;
+          for (int q = 0; q < w; ++q) c0 = fma(s.V[a * w + q], y[q * cw], c0);
+          OUT[a * cw + c] -= c0;
+        }
+      }
+    }
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+      const int64_t ek = ch_e[k];
+      const int j = A.sq_col[ek], bj = A.bsz[j];
+      const bool tr = j > i;
+      double* X = A.store + A.slot_off[A.sq_slot[ek]];
+      const double* src = OUT + ch_c0[k];
+      for (int idx = tid; idx < b * bj; idx += T) {
+        int a, c;
+        if (tr) {
+          c = idx / b;
+          a = idx % b;
+        } else {
+          a = idx / bj;
+          c = idx % bj;
+        }
+        X[xidx(a, c, b, bj, tr)] = (w > 0 && a >= r) ? 0.0 : src[a * cw + c];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Schur update of one panel pair (P, Q), P <= Q, of row i's close list:
+// X_ts -= g_t g_s^T for s in panel P, t in panel Q, s <= t (level_matrix.cpp:148-162).
+// g rows of both panels are staged in shared memory.
+__device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int w, int P, int Q, double* sm) {
+  CE_SHARED(sm);
+  __shared__ long long slot_tab[kPanelNb * kPanelNb];  // value offset of stored (t, s), -1: not updated
+  __shared__ int tab_bs[kPanelNb];
+  __shared__ unsigned char xblk[kPanelRows], yblk[kPanelRows];
+  __shared__ unsigned short xloc[kPanelRows], yloc[kPanelRows];
+  const int tid = threadIdx.x;
+  const int64_t c0 = A.cl_ptr[i];
+  const int* ps = A.pan_start + A.pan_ptr[i];
+  const int s0 = ps[P], s1 = ps[P + 1], t0 = ps[Q], t1 = ps[Q + 1];
+  const int ns = s1 - s0, nt = t1 - t0;
+  const int rs0 = A.cl_roff[c0 + s0];
+  const int rsn = A.cl_roff[c0 + s1 - 1] + A.bsz[A.cl_col[c0 + s1 - 1]] - rs0;
+  const int rt0 = A.cl_roff[c0 + t0];
+  const int rtn = A.cl_roff[c0 + t1 - 1] + A.bsz[A.cl_col[c0 + t1 - 1]] - rt0;
+  const int lds = (rsn + 3) & ~3, ldt = (rtn + 3) & ~3;
+  // g rows transposed into shared memory: GsT[q][y], GtT[q][x]
+  const double* G = A.fac + A.g_off[i];
+  double* GsT = sm;
+  double* GtT = P == Q ? sm : sm + static_cast<int64_t>(lds) * w;
+  for (int idx = tid; idx < lds * w; idx += T) {
+    const int y = idx / w, q = idx % w;
+    GsT[q * lds + y] = y < rsn ? ldg(G + static_cast<int64_t>(r + rs0 + y) * w + q) : 0.0;
+  }
+  if (P != Q)
+    for (int idx = tid; idx < ldt * w; idx += T) {
+      const int x = idx / w, q = idx % w;
+      GtT[q * ldt + x] = x < rtn ? ldg(G + static_cast<int64_t>(r + rt0 + x) * w + q) : 0.0;
+    }
+  for (int idx = tid; idx < nt * ns; idx += T) {
+    const int kt = idx / ns, ks = idx % ns;
+    long long off = -1;
+    if (!(P == Q && ks > kt)) {
+      const int t = A.cl_col[c0 + t0 + kt], s = A.cl_col[c0 + s0 + ks];
+      const int64_t slot = find_slot(A.sq_ptr, A.sq_col, A.sq_slot, t, s);
+      if (slot < 0) set_error(A.err, kErrPattern, A.level, i);
+      else off = A.slot_off[slot];
+    }
+    slot_tab[idx] = off;
+  }
+  for (int ks = tid; ks < ns; ks += T) {
+    const int e = static_cast<int>(c0) + s0 + ks;
+    const int bs_ = A.bsz[A.cl_col[e]];
+    tab_bs[ks] = bs_;
+    const int y0 = A.cl_roff[e] - rs0;
+    for (int y = 0; y < bs_; ++y) {
+      yblk[y0 + y] = static_cast<unsigned char>(ks);
+      yloc[y0 + y] = static_cast<unsigned short>(y);
+    }
+  }
+  for (int kt = tid; kt < nt; kt += T) {
+    const int e = static_cast<int>(c0) + t0 + kt;
+    const int bt = A.bsz[A.cl_col[e]];
+    const int x0 = A.cl_roff[e] - rt0;
+    for (int x = 0; x < bt; ++x) {
+      xblk[x0 + x] = static_cast<unsigned char>(kt);
+      xloc[x0 + x] = static_cast<unsigned short>(x);
+    }
+  }
+  __syncthreads();
+  // rtn x rsn outer product in 4x4 register tiles; epilogue scatters into the (t, s) blocks
+  const int mx = ldt / 4, my = lds / 4;
+  for (int mt = tid; mt < mx * my; mt += T) {
+    const int x0 = (mt / my) * 4, y0 = (mt % my) * 4;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+    for (int q = 0; q < w; ++q) {
+      const double2 ta = *reinterpret_cast<const double2*>(GtT + q * ldt + x0);
+      const double2 tb = *reinterpret_cast<const double2*>(GtT + q * ldt + x0 + 2);
+      const double2 sa = *reinterpret_cast<const double2*>(GsT + q * lds + y0);
+      const double2 sb = *reinterpret_cast<const double2*>(GsT + q * lds + y0 + 2);
+      const double av[4] = {ta.x, ta.y, tb.x, tb.y}, cv[4] = {sa.x, sa.y, sb.x, sb.y};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] += av[a] * cv[c];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int x = x0 + a;
+      if (x >= rtn) break;
+      const int kt = xblk[x], xl = xloc[x];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int y = y0 + c;
+        if (y >= rsn) break;
+        const int ks = yblk[y];
+        const long long off = slot_tab[kt * ns + ks];
+        if (off < 0) continue;
+        double* X = A.store + off + static_cast<int64_t>(xl) * tab_bs[ks] + yloc[y];
+        *X = ldg(X) - acc[a][c];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ void all_panels(const SweepArgs& A, int i, int r, int w, double* sm) {
+  const int np = static_cast<int>(A.pan_ptr[i + 1] - A.pan_ptr[i]) - 1;
+  for (int P = 0; P < np; ++P)
+    for (int Q = P; Q < np; ++Q) panel_update(A, i, r, w, P, Q, sm);
+}
+
+// A2: compression decision + basis + pivot factorisation; with nA3 == 0 also the strip,
+// with nB == 0 also the Schur panels.
+__device__ void task_a2(const SweepArgs& A, int i, const Buf& s_, int nA1, int nA3, int nB) {
+  const Buf s = s_;
+  CE_SHARED_BUF(s);
+  __shared__ double shr[4];
+  __shared__ int sflag[4];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long t_a2 = clock64();
+  const int b = A.bsz[i];
+  const int64_t p0 = A.sq_ptr[i], p1 = A.sq_ptr[i + 1];
+  int64_t dslot = -1;
+  for (int64_t e = p0; e < p1; ++e)
+    if (A.sq_col[e] == i) {
+      dslot = A.sq_slot[e];
+      break;
+    }
+  double* Dg = A.store + A.slot_off[dslot];
+  for (int idx = tid; idx < b * b; idx += T) {
+    s.D[idx] = ldg(Dg + idx);
+    s.R[idx] = 0.0;
+  }
+  if (tid == 0) sflag[0] = 0;
+  __syncthreads();
+
+  // ---- far-block triangle (compression.cpp:38-48) ----
+  int fcols;
+  if (nA1 == 0) {
+    fcols = gather_tsqr(A, i, b, s, 0, 1 << 30, &sflag[0], shr);
+  } else {
+    fcols = static_cast<int>(A.fsum[i]);
+    // fold the leaf triangles, as many per chunk as fit (chunk rows <= kcap)
+    const int per = A.kcap / b > 0 ? A.kcap / b : 1;
+    for (int k0 = 0; k0 < nA1; k0 += per) {
+      const int nk = nA1 - k0 < per ? nA1 - k0 : per;
+      const int K = nk * b;
+      for (int idx = tid; idx < K * b; idx += T) {
+        const int j = idx / K, m = idx % K;  // chunk element (m, j) = R_{k0 + m/b}[m%b][j]
+        const double* Rk = A.rscratch + A.rs_off[i] + static_cast<int64_t>(k0 + m / b) * b * b;
+        s.C[static_cast<int64_t>(j) * chunk_ld(A.kcap) + m] = ldg(Rk + j * b + m % b);
+      }
+      __syncthreads();
+      tsqr_sel(A, s.R, s.C, K, b, chunk_ld(A.kcap), shr);
+    }
+    if (tid == 0) sflag[0] = ld_acquire(A.nzflag + i);
+    __syncthreads();
+  }
+  const bool nonzero = sflag[0] != 0;
+  const int meff = fcols < b ? fcols : b;
+  long long tp = clock64();
+  prof_add(A, kProfA2Tsqr, tp - t_a2);
+
+  // ---- rank decision + basis (compression.cpp:20-61) ----
+  int r = 0, nsig = 0;
+  bool basis = false;
+  if (fcols > 0) {
+    bool need_svd;
+    if (A.mode == 1) {
+      r = A.fixed_rank < b ? A.fixed_rank : b;
+      need_svd = nonzero && r < b;
+    } else {
+      need_svd = nonzero;
+    }
+    if (need_svd) {
+      long long t0 = clock64();
+      precondition_qr(s, b);
+      long long t1 = clock64();
+      const int nsw = (A.dbg & 2) ? jacobi(s.R, s.V, b, pad_ld(b), meff) : jacobi_fast(s.R, s.V, b, pad_ld(b), meff);
+      long long t2 = clock64();
+      apply_q2(s, b);
+      prof_add(A, kProfSvdPre, t1 - t0);
+      prof_add(A, kProfSvdJac, t2 - t1);
+      prof_add(A, kProfSvdPost, clock64() - t2);
+      prof_add(A, kProfSweeps, nsw);
+      prof_add(A, kProfSvds, 1);
+      for (int j = warp; j < b; j += NW) {
+        double acc = 0.0;
+        for (int k = lane; k < b; k += 32) acc += s.R[j * pad_ld(b) + k] * s.R[j * pad_ld(b) + k];
+        acc = warp_sum(acc);
+        if (lane == 0) s.nrm[j] = sqrt(acc);
+      }
+      __syncthreads();
+      for (int j = tid; j < b; j += T) {
+        const double sj = s.nrm[j];
+        if (!isfinite(sj)) set_error(A.err, kErrInternal, A.level, i);  // never rank a NaN
+        int rank = 0;
+        for (int k = 0; k < b; ++k) {
+          const double sk = s.nrm[k];
+          if (sk > sj || (sk == sj && k < j)) ++rank;
+        }
+        s.perm[rank] = j;
+        s.sig[rank] = sj;
+      }
+      __syncthreads();
+      nsig = meff;
+      for (int k = tid; k < nsig; k += T) A.sigma[A.sigma_off[i] + k] = s.sig[k];
+      if (A.mode == 0) {
+        const double thr = A.absolute ? A.eps : A.eps * s.sig[0];
+        r = nsig;
+        for (int k = 0; k < nsig; ++k)
+          if (s.sig[k] <= thr) {
+            r = k;
+            break;
+          }
+        if (A.forced && A.forced[i] >= 0) r = A.forced[i];
+        if (r > b) r = b;
+      }
+      basis = r < b;
+    } else if (A.mode == 0) {
+      r = 0;
+    }
+  }
+  const int w = b - r;
+  {
+    const long long t = clock64();
+    prof_add(A, kProfA2Svd, t - tp);
+    tp = t;
+  }
+
+  // ---- basis and rotated diagonal (level_matrix.cpp:51-54) ----
+  if (basis) {
+    canonical_basis(s, b, r, nsig);
+    double* Ug = A.basis + A.basis_off[i];
+    for (int idx = tid; idx < b * b; idx += T) Ug[idx] = s.U[idx];
+    for (int idx = tid; idx < b * b; idx += T) {
+      const int a = idx / b, c = idx % b;
+      double acc = 0.0;
+      for (int k = 0; k < b; ++k) acc += s.D[a * b + k] * s.U[k * b + c];
+      s.C[idx] = acc;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < b * b; idx += T) {
+      const int a = idx / b, c = idx % b;
+      double acc = 0.0;
+      for (int k = 0; k < b; ++k) acc += s.U[k * b + a] * s.C[k * b + c];
+      s.R[idx] = acc;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < b * b; idx += T) {
+      const int a = idx / b, c = idx % b;
+      s.D[idx] = 0.5 * (s.R[a * b + c] + s.R[c * b + a]);
+    }
+    __syncthreads();
+  }
+
+  {
+    const long long t = clock64();
+    prof_add(A, kProfA2Basis, t - tp);
+    tp = t;
+  }
+  // ---- pivot factorisation (level_matrix.cpp:104-138) ----
+  if (w > 0) {
+    double* P = s.R;     // w x w
+    double* Pbak = s.V;  // shift-retry backup, then the coupling C (r x w)
+    for (int idx = tid; idx < w * w; idx += T) {
+      const int q = idx / w, p = idx % w;
+      P[idx] = s.D[(r + q) * b + r + p];
+      Pbak[idx] = P[idx];
+    }
+    __syncthreads();
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      if (attempt == 1) {
+        if (tid == 0) {
+          double tr = 0.0;
+          for (int q = 0; q < w; ++q) tr += Pbak[q * w + q];
+          shr[1] = 1e-12 * tr / static_cast<double>(w);
+        }
+        __syncthreads();
+        for (int idx = tid; idx < w * w; idx += T) {
+          const int q = idx / w, p = idx % w;
+          P[idx] = Pbak[idx] + (q == p ? shr[1] : 0.0);
+        }
+        __syncthreads();
+      }
+      if (tid == 0) sflag[2] = 0;
+      __syncthreads();
+      for (int k = 0; k < w; ++k) {
+        if (tid == 0) {
+          const double d = P[k * w + k];
+          if (!(d > 0.0)) sflag[2] = 1;
+          else P[k * w + k] = sqrt(d);
+        }
+        __syncthreads();
+        if (sflag[2]) break;
+        const double dk = P[k * w + k];
+        for (int q = k + 1 + tid; q < w; q += T) P[q * w + k] /= dk;
+        __syncthreads();
+        const int m = w - k - 1;
+        for (int idx = tid; idx < m * m; idx += T) {
+          const int q = k + 1 + idx / m, p = k + 1 + idx % m;
+          if (p <= q) P[q * w + p] -= P[q * w + k] * P[p * w + k];
+        }
+        __syncthreads();
+      }
+      if (!sflag[2]) {
+        if (attempt == 1 && tid == 0) atomicAdd(A.shifts, 1);
+        break;
+      }
+      if (attempt == 1) {
+        if (tid == 0) set_error(A.err, kErrBreakdown, A.level, i);
+        return;
+      }
+    }
+    double* L = A.fac + A.chol_off[i];
+    for (int idx = tid; idx < w * w; idx += T) {
+      const int q = idx / w, p = idx % w;
+      const double v = p <= q ? P[idx] : 0.0;
+      P[idx] = v;
+      L[idx] = v;
+    }
+    __syncthreads();
+    // coupling C = (L^{-1} D[r:, :r])^T -> G rows [0, r) and s.V
+    double* G = A.fac + A.g_off[i];
+    for (int rho = tid; rho < r; rho += T) {
+      double* y = s.V + rho * w;
+      for (int q = 0; q < w; ++q) {
+        double acc = s.D[(r + q) * b + rho];
+        for (int p = 0; p < q; ++p) acc -= P[q * w + p] * y[p];
+        y[q] = acc / P[q * w + q];
+      }
+      for (int q = 0; q < w; ++q) G[static_cast<int64_t>(rho) * w + q] = y[q];
+    }
+    __syncthreads();
+    // D[:r, :r] -= C C^T; eliminated rows/cols of D leave the level
+    for (int idx = tid; idx < b * b; idx += T) {
+      const int a = idx / b, c = idx % b;
+      if (a >= r || c >= r) {
+        s.D[idx] = 0.0;
+      } else {
+        double acc = 0.0;
+        for (int q = 0; q < w; ++q) acc += s.V[a * w + q] * s.V[c * w + q];
+        s.D[idx] -= acc;
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < b * b; idx += T) Dg[idx] = s.D[idx];
+  if (tid == 0) {
+    A.rank[i] = r;
+    A.width[i] = w;
+    A.has_basis[i] = basis ? 1 : 0;
+    A.fcols[i] = fcols;
+    A.nsig[i] = nsig;
+  }
+  __syncthreads();
+  {
+    const long long t = clock64();
+    prof_add(A, kProfA2Pivot, t - tp);
+    tp = t;
+  }
+
+  // ---- strip (thin rows) ----
+  if (nA3 == 0 && (basis || w > 0)) {
+    strip_range(A, i, b, r, w, basis, 0, 1 << 30, s);
+    {
+      const long long t = clock64();
+      prof_add(A, kProfA2Strip, t - tp);
+      tp = t;
+    }
+    if (nB == 0 && w > 0) all_panels(A, i, r, w, s.R);
+    prof_add(A, kProfA2Panels, clock64() - tp);
+  }
+}
+
+// A3 tile k: strip entries with strip-ordinal in [k*ns/nA3, (k+1)*ns/nA3).
+__device__ void task_a3(const SweepArgs& A, int i, const Buf& s_, int k, int nA3, int nB) {
+  const Buf s = s_;
+  CE_SHARED_BUF(s);
+  const int tid = threadIdx.x;
+  const int b = A.bsz[i];
+  const int r = __ldcg(A.rank + i), w = __ldcg(A.width + i);
+  const bool basis = __ldcg(reinterpret_cast<const unsigned char*>(A.has_basis) + i) != 0;
+  if (!basis && w == 0) return;
+  if (basis)
+    for (int idx = tid; idx < b * b; idx += T) s.U[idx] = ldg(A.basis + A.basis_off[i] + idx);
+  if (w > 0) {
+    for (int idx = tid; idx < w * w; idx += T) s.R[idx] = ldg(A.fac + A.chol_off[i] + idx);
+    for (int idx = tid; idx < r * w; idx += T) s.V[idx] = ldg(A.fac + A.g_off[i] + idx);
+  }
+  __syncthreads();
+  const int64_t p0 = A.sq_ptr[i], p1 = A.sq_ptr[i + 1];
+  const int ns = static_cast<int>(p1 - p0) - 1;
+  const int ob = static_cast<int>(static_cast<int64_t>(ns) * k / nA3);
+  const int oe = static_cast<int>(static_cast<int64_t>(ns) * (k + 1) / nA3);
+  strip_range(A, i, b, r, w, basis, ob, oe, s);
+  (void)nB;
+}
+
+__global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
+  extern __shared__ double smem_dyn[];
+#if CE_SMEM_BUFFER
+  double* base = smem_dyn;
+#else
+  double* base = A.scratch + static_cast<int64_t>(blockIdx.x) * A.scratch_per_cta;
+#endif
+  const Buf s = carve(base, A.bmax, A.kcap);
+  CE_SHARED_BUF(s);
+  __shared__ long long s_item;
+  __shared__ int s_stop;
+  __shared__ double shr[4];
+  __shared__ int nz;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      s_stop = *reinterpret_cast<volatile int*>(A.err) != 0;
+      s_item = s_stop ? 0 : static_cast<long long>(atomicAdd(A.ticket, 1ULL));
+    }
+    __syncthreads();
+    if (s_stop) break;
+    const long long item = s_item;
+    if (item >= A.n_items) break;
+    const int i = A.item_row[item];
+    const int part = A.item_part[item];
+    const int nA1 = A.nA1[i], nA3 = A.nA3[i], nB = A.nB[i];
+    // stage of the item and the number of this row's items it must wait for
+    int stage, k = 0, need = 0;
+    if (part < nA1) {
+      stage = 1;
+      k = part;
+    } else if (part == nA1) {
+      stage = 2;
+      need = nA1;
+    } else if (part <= nA1 + nA3) {
+      stage = 3;
+      k = part - nA1 - 1;
+      need = nA1 + 1;
+    } else {
+      stage = 4;
+      k = part - nA1 - 1 - nA3;
+      need = nA1 + 1 + nA3;
+    }
+    const bool first = (stage == 1) || (stage == 2 && nA1 == 0);
+    const long long t_wait = clock64();
+    if (threadIdx.x == 0) {
+      if (first) {
+        for (int64_t e = A.sq_ptr[i]; e < A.sq_ptr[i + 1]; ++e) {
+          const int j = A.sq_col[e];
+          if (j >= i) break;
+          const int target = 1 + A.nA1[j] + A.nA3[j] + A.nB[j];
+          while (ld_acquire(A.done + j) < target) {
+            if (*reinterpret_cast<volatile int*>(A.err) != 0) {
+              s_stop = 1;
+              break;
+            }
+            __nanosleep(64);
+          }
+          if (s_stop) break;
+        }
+      } else {
+        while (ld_acquire(A.done + i) < need) {
+          if (*reinterpret_cast<volatile int*>(A.err) != 0) {
+            s_stop = 1;
+            break;
+          }
+          __nanosleep(64);
+        }
+      }
+      __threadfence();
+      nz = 0;
+    }
+    __syncthreads();
+    if (s_stop) break;
+    const long long t_run = clock64();
+    prof_add(A, kProfWait, t_run - t_wait);
+    if (stage == 1) {
+      const int b = A.bsz[i];
+      for (int idx = threadIdx.x; idx < b * b; idx += T) s.R[idx] = 0.0;
+      __syncthreads();
+      // far-ordinal range of this leaf
+      int nf = 0;
+      for (int64_t e = A.sq_ptr[i]; e < A.sq_ptr[i + 1]; ++e) nf += A.sq_kind[e] == 2;
+      const int fb = static_cast<int>(static_cast<int64_t>(nf) * k / nA1);
+      const int fe = static_cast<int>(static_cast<int64_t>(nf) * (k + 1) / nA1);
+      gather_tsqr(A, i, b, s, fb, fe, &nz, shr);
+      double* Rk = A.rscratch + A.rs_off[i] + static_cast<int64_t>(k) * b * b;
+      for (int idx = threadIdx.x; idx < b * b; idx += T) Rk[idx] = s.R[idx];
+      if (threadIdx.x == 0 && nz) atomicOr(A.nzflag + i, 1);
+    } else if (stage == 2) {
+      task_a2(A, i, s, nA1, nA3, nB);
+    } else if (stage == 3) {
+      task_a3(A, i, s, k, nA3, nB);
+    } else {
+      const int w = __ldcg(A.width + i);
+      if (w > 0) {
+        const int r = __ldcg(A.rank + i);
+        const int np = static_cast<int>(A.pan_ptr[i + 1] - A.pan_ptr[i]) - 1;
+        if (nB == 1) {
+          all_panels(A, i, r, w, s.R);
+        } else {
+          // tile k -> panel pair (P, Q), P <= Q
+          int P = 0, kk = k;
+          while (kk >= np - P) {
+            kk -= np - P;
+            ++P;
+          }
+          panel_update(A, i, r, w, P, P + kk, s.R);
+        }
+      }
+    }
+    __syncthreads();
+    {
+      const int slot = stage == 1 ? kProfA1 : stage == 2 ? kProfA2 : stage == 3 ? kProfA3 : kProfB;
+      prof_add(A, slot, clock64() - t_run);
+      prof_add(A, stage == 1 ? kProfNA1 : stage == 2 ? kProfNA2 : stage == 3 ? kProfNA3 : kProfNB, 1);
+    }
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(A.done + i, 1);
+    }
+  }
+}
+
+
+#undef CE_SHARED_BUF
+#undef CE_SHARED
