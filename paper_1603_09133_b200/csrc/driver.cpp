@@ -196,7 +196,7 @@ LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vecto
   P.pan_ptr.assign(static_cast<size_t>(M + 1), 0);
   // Schur panel height: both panels' g rows (<= cap x w doubles each) must fit the CTA buffer.
   const int64_t bmax = std::max(P.bmax, 1);
-  const int64_t buf = sweep_smem_doubles(static_cast<int>(bmax), static_cast<int>(std::max<int64_t>(bmax, 128)));
+  const int64_t buf = sweep_smem_doubles(static_cast<int>(bmax), sweep_kcap(static_cast<int>(bmax)));
   // (sweep.cu kPanelRows / kPanelNb bound the panel height / neighbour count)
   const int64_t cap = thresholds().small_panels ? bmax : std::max<int64_t>(bmax, std::min<int64_t>(256, buf / (2 * bmax) - 4));
   constexpr int64_t kPanelNb = 32;
@@ -266,6 +266,52 @@ LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vecto
     if (P.nA3[iu] > 0 && P.nB[iu] == 0 && np > 0) P.nB[iu] = 1;
   }
   P.rscratch_doubles = ro;
+  // Per-entry metadata the sweep tasks load in one coalesced pass (no dependent chains
+  // sq_col -> bsz, sq_slot -> slot_off, close-list search on the device), the diagonal
+  // entry and completion target of every row, and the entry ranges of the A1 / A3 tasks
+  // (same far-ordinal / strip-ordinal partitions as before).
+  {
+    const size_t nnz = P.scol.size();
+    P.sboff.resize(nnz);
+    P.sbsz.resize(nnz);
+    P.sroff.assign(nnz, -1);
+    P.sdiag.resize(static_cast<size_t>(M));
+    P.target.resize(static_cast<size_t>(M));
+    P.leaf_ptr.assign(static_cast<size_t>(M + 1), 0);
+    P.strip_ptr.assign(static_cast<size_t>(M + 1), 0);
+    P.leaf_e.clear();
+    P.strip_e.clear();
+    for (int64_t i = 0; i < M; ++i) {
+      const size_t iu = static_cast<size_t>(i);
+      std::vector<int64_t> far_e, strip_e;
+      for (int64_t e = P.sptr[iu]; e < P.sptr[iu + 1]; ++e) {
+        const size_t eu = static_cast<size_t>(e);
+        const int j = P.scol[eu];
+        P.sboff[eu] = P.slot_off[static_cast<size_t>(P.sslot[eu])];
+        P.sbsz[eu] = P.bsz[static_cast<size_t>(j)];
+        if (j == i) P.sdiag[iu] = e;
+        if (P.skind[eu] == 1) {
+          const int64_t k = csr_find(P.cptr, P.ccol, i, j);
+          P.sroff[eu] = P.croff[static_cast<size_t>(k)];
+        }
+        if (P.skind[eu] == 2) far_e.push_back(e);
+        if (P.skind[eu] != 0) strip_e.push_back(e);
+      }
+      P.target[iu] = 1 + P.nA1[iu] + P.nA3[iu] + P.nB[iu];
+      const int64_t pend = P.sptr[iu + 1];
+      const int64_t nf = static_cast<int64_t>(far_e.size()), ns = static_cast<int64_t>(strip_e.size());
+      for (int k = 0; k <= P.nA1[iu]; ++k) {
+        const int64_t o = P.nA1[iu] > 0 ? nf * k / P.nA1[iu] : 0;
+        P.leaf_e.push_back(o < nf ? far_e[static_cast<size_t>(o)] : pend);
+      }
+      P.leaf_ptr[iu + 1] = static_cast<int64_t>(P.leaf_e.size());
+      for (int k = 0; k <= P.nA3[iu]; ++k) {
+        const int64_t o = P.nA3[iu] > 0 ? ns * k / P.nA3[iu] : 0;
+        P.strip_e.push_back(o < ns ? strip_e[static_cast<size_t>(o)] : pend);
+      }
+      P.strip_ptr[iu + 1] = static_cast<int64_t>(P.strip_e.size());
+    }
+  }
   // Wave (topological) order of the dependency DAG: row j depends on every i < j in sq(j)
   // (SURVEY.md A.2).  Items are issued in this order, so the ticket window always holds
   // the current wavefront instead of a run of consecutive (mutually dependent) rows.
@@ -339,9 +385,9 @@ namespace {
 
 // Device copy of a plan's symbolic arrays (freed after the level).
 struct DevPlan {
-  DevArray<int> bsz, scol, ccol, croff, order, nA1, nA3, nB, pan_start, item_row, item_part;
+  DevArray<int> bsz, scol, ccol, croff, order, nA1, nA3, nB, pan_start, item_row, item_part, sbsz, sroff, target;
   DevArray<int64_t> sptr, sslot, slot_off, cptr, chol_off, g_off, basis_off, sigma_off, item_start, offsets, cl_slot,
-      fsum, rs_off, pan_ptr;
+      fsum, rs_off, pan_ptr, sboff, sdiag, leaf_ptr, leaf_e, strip_ptr, strip_e;
   DevArray<unsigned char> skind;
   void upload(const LevelPlan& P, cudaStream_t s) {
     order.upload(P.order, s);
@@ -369,6 +415,15 @@ struct DevPlan {
     item_start.upload(P.item_start, s);
     offsets.upload(P.offsets, s);
     skind.upload(P.skind, s);
+    sboff.upload(P.sboff, s);
+    sbsz.upload(P.sbsz, s);
+    sroff.upload(P.sroff, s);
+    sdiag.upload(P.sdiag, s);
+    target.upload(P.target, s);
+    leaf_ptr.upload(P.leaf_ptr, s);
+    leaf_e.upload(P.leaf_e, s);
+    strip_ptr.upload(P.strip_ptr, s);
+    strip_e.upload(P.strip_e, s);
     std::vector<int64_t> cls(P.ccol.size());
     for (int64_t i = 0; i < P.M; ++i)
       for (int64_t k = P.cptr[static_cast<size_t>(i)]; k < P.cptr[static_cast<size_t>(i + 1)]; ++k)
@@ -465,6 +520,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
   dcur.upload(cur, s);
   DevArray<double> store(static_cast<size_t>(cur.store_doubles));
   store.zero(s);
+  DevArray<double> nstore;  // next level's store; the two buffers are swapped and reused (grow-only)
   Events ev_all;
   CE_CUDA(cudaEventRecord(ev_all.a, s));
   launch_init_store_from_matrix(cur.M, dcur.bsz.p, A->d_row_ptr.p, A->d_col_idx.p, A->d_val_ptr.p, A->d_values.p,
@@ -480,6 +536,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
 
   while (cur.dim > dense_threshold && static_cast<int64_t>(F->levels.size()) < max_levels) {
     const size_t li = F->levels.size();
+    const double h_t0 = now_s();
     const auto plan_groups = li < plan_levels.size() ? plan_levels[li] : pair_groups(static_cast<int64_t>(alive_map.size()), join);
     std::vector<std::vector<int64_t>> cur_groups;
     std::vector<int64_t> slot_of_group(plan_groups.size(), -1);
@@ -572,6 +629,15 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     a.rs_off = dcur.rs_off.p;
     a.pan_ptr = dcur.pan_ptr.p;
     a.pan_start = dcur.pan_start.p;
+    a.sq_boff = dcur.sboff.p;
+    a.sq_bsz = dcur.sbsz.p;
+    a.sq_roff = dcur.sroff.p;
+    a.sq_diag = dcur.sdiag.p;
+    a.target = dcur.target.p;
+    a.leaf_ptr = dcur.leaf_ptr.p;
+    a.leaf_e = dcur.leaf_e.p;
+    a.strip_ptr = dcur.strip_ptr.p;
+    a.strip_e = dcur.strip_e.p;
     DevArray<double> d_rscratch(static_cast<size_t>(std::max<int64_t>(cur.rscratch_doubles, 1)));
     DevArray<int> d_nz(static_cast<size_t>(cur.M));
     d_nz.zero(s);
@@ -588,7 +654,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     a.err = d_err.p;
     a.shifts = d_shifts.p;
     a.bmax = std::max(cur.bmax, 1);
-    a.kcap = std::max(a.bmax, 128);
+    a.kcap = sweep_kcap(a.bmax);
     // per-CTA buffer, rounded to 256 B so every CTA's (global-scratch) base keeps double2 alignment
     int64_t need = (sweep_smem_doubles(a.bmax, a.kcap) + 31) / 32 * 32;
     size_t smem = static_cast<size_t>(need) * sizeof(double);
@@ -605,6 +671,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       per_sm = std::max(1, sweep_max_ctas_per_sm(0));
       per_sm = std::min(per_sm, 4);
     }
+    if (const char* cps = std::getenv("CE_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(cps)));
     int grid = ctx->sm_count * per_sm;
     if (grid > cur.n_items) grid = static_cast<int>(std::max<int64_t>(cur.n_items, 1));
     if (a.use_global_scratch) {
@@ -620,6 +687,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       a.prof = d_prof.p;
     }
     Events ev_lvl, ev_sw;
+    const double h_t1 = now_s();
     CE_CUDA(cudaEventRecord(ev_lvl.a, s));
     CE_CUDA(cudaEventRecord(ev_sw.a, s));
     launch_sweep(a, grid, smem, s);
@@ -660,6 +728,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     LF.d_fcols.download(LF.fcols, s);
     LF.d_nsig.download(LF.nsig, s);
     CE_CUDA(cudaStreamSynchronize(s));
+    const double h_ts = now_s();
     int64_t eliminated = 0;
     for (int w : LF.width) eliminated += w;
     if (eliminated == 0) break;  // factorization.cpp:374 (store untouched: every r_i = b_i)
@@ -725,12 +794,15 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
 
     LevelPlan next;
     DevPlan dnext;
-    DevArray<double> nstore;
+    const double h_t2 = now_s();
+    double h_t3 = h_t2;
     if (nM > 0) {
       next = plan_level(nbsz, nptr, ncol);
+      h_t3 = now_s();
       dnext.upload(next, s);
-      nstore.alloc(static_cast<size_t>(next.store_doubles));
-      nstore.zero(s);
+      if (nstore.n < static_cast<size_t>(next.store_doubles)) nstore.alloc(static_cast<size_t>(next.store_doubles));
+      if (next.store_doubles > 0)
+        CE_CUDA(cudaMemsetAsync(nstore.p, 0, static_cast<size_t>(next.store_doubles) * sizeof(double), s));
       DevArray<int> d_nb, d_nl;
       d_nb.upload(next_block, s);
       d_nl.upload(next_loc, s);
@@ -764,6 +836,9 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     }
     LF.seconds = ev_lvl.seconds();
     LF.sweep_seconds = ev_sw.seconds();
+    if (profile)
+      std::fprintf(stderr, "[ce-profile] level %zu host: setup %.1f ms, sweep+downloads %.1f ms, coarse pattern %.1f ms, plan %.1f ms, upload+remainder %.1f ms\n",
+                   li + 1, 1e3 * (h_t1 - h_t0), 1e3 * (h_ts - h_t1), 1e3 * (h_t2 - h_ts), 1e3 * (h_t3 - h_t2), 1e3 * (now_s() - h_t3));
     F->sweep_seconds += LF.sweep_seconds;
 
     // host copies needed by apply / dump / stats
@@ -862,7 +937,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
 
     cur = std::move(next);
     dcur = std::move(dnext);
-    store = std::move(nstore);
+    std::swap(store, nstore);
     if (nM == 0) break;
   }
 

@@ -126,6 +126,11 @@ struct LevelPlan {
   std::vector<int64_t> pan_ptr, rs_off;
   std::vector<int> pan_start;
   int64_t rscratch_doubles = 0;
+  std::vector<int64_t> sboff;        // per sq entry: value offset of its stored block
+  std::vector<int> sbsz, sroff;      // per sq entry: block size, close-list row offset (-1: not close)
+  std::vector<int64_t> sdiag;        // per row: sq entry of the diagonal
+  std::vector<int> target;           // per row: items of the row (completion count)
+  std::vector<int64_t> leaf_ptr, leaf_e, strip_ptr, strip_e;  // A1 / A3 task entry ranges
   int64_t n_items = 0, n_waves = 0;
   int bmax = 0;
   int64_t fmax = 0, cmax = 0;

@@ -58,6 +58,15 @@ struct SweepArgs {
   int* nzflag;                // per-row "far fill nonzero" flag from the leaves
   const int64_t* pan_ptr;     // per-row offset into pan_start (np + 1 entries per row)
   const int* pan_start;       // close-list index where each Schur panel starts
+  const int64_t* sq_boff;     // per sq entry: value offset of the stored block
+  const int* sq_bsz;          // per sq entry: block size of the column block
+  const int* sq_roff;         // per sq entry: row offset in the close list (-1: not close)
+  const int64_t* sq_diag;     // per row: sq entry of the diagonal block
+  const int* target;          // per row: number of items (done[] value when the row is finished)
+  const int64_t* leaf_ptr;    // per row: range into leaf_e (nA1 + 1 entries)
+  const int64_t* leaf_e;      // first sq entry of each TSQR leaf (last = row end)
+  const int64_t* strip_ptr;   // per row: range into strip_e (nA3 + 1 entries)
+  const int64_t* strip_e;     // first sq entry of each strip task (last = row end)
   int* done;
   unsigned long long* ticket;
   int64_t n_items;
@@ -86,6 +95,7 @@ enum : int {
 
 // smem doubles needed by one sweep CTA for a level
 int64_t sweep_smem_doubles(int bmax, int kcap);
+int sweep_kcap(int bmax);  // F^T chunk height for a level
 void launch_sweep(const SweepArgs& a, int grid, size_t smem_bytes, cudaStream_t s);
 int sweep_max_ctas_per_sm(size_t smem_bytes);
 

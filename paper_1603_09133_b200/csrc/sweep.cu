@@ -100,7 +100,7 @@ __host__ __device__ inline Layout sweep_layout(int bmax, int kcap) {
   L.creg = static_cast<int64_t>((kcap + 1) | 1) * bmax;             // F^T chunk
   L.base = 4 * L.bb + L.creg + 3LL * bmax + (bmax + 1) / 2 + 4;    // R V U D C sig tau nrm perm
   const int64_t dreg = L.bb + L.creg;
-  const int64_t budget = 12000;  // doubles per CTA (two CTAs per SM)
+  const int64_t budget = 11000;  // doubles per CTA (two CTAs per SM next to ~22 KB static smem)
   int64_t cw = dreg / (2 * bmax);
   const int64_t cwb = (budget - L.base + dreg) / (2 * bmax);
   if (cwb > cw) cw = cwb;
@@ -307,6 +307,14 @@ __global__ void remainder_kernel(RemainderArgs A) {
 }
 
 }  // namespace
+
+int sweep_kcap(int bmax) {
+  // F^T chunk height: 128 rows, shortened (not below 64) so that the per-CTA buffer of
+  // wide-block levels still allows two CTAs per SM
+  int k = 128;
+  while (k > bmax && k > 64 && sweep_layout(bmax, k).base > 11000) k -= 8;
+  return k > bmax ? k : bmax;
+}
 
 int64_t sweep_smem_doubles(int bmax, int kcap) {
   const Layout L = sweep_layout(bmax, kcap);

@@ -143,8 +143,11 @@ __device__ __noinline__ void tsqr_reg_t(double* R, double* C, int K, int b, int 
   CE_SHARED(R);
   CE_SHARED(C);
   constexpr int NG = T / G;
-  const int tid = threadIdx.x, grp = tid / G, gl = tid % G;
-  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((tid & 31) / G * G));
+  constexpr unsigned kFull = 0xffffffffu;
+  // control flow is warp-uniform around every shuffle (full-mask shuffles: partial masks
+  // make the compiler emit MATCH/REDUX convergence checks on the critical path)
+  const int tid = threadIdx.x, grp = tid / G, gl = tid % G, warp = tid >> 5;
+  const int wmax = ((warp + 1) * 32) / G - 1 + (NC - 1) * NG;  // largest column owned in this warp
   double x[NC][E];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
@@ -155,16 +158,18 @@ __device__ __noinline__ void tsqr_reg_t(double* R, double* C, int K, int b, int 
       x[c][e] = (j < b && m < K) ? C[static_cast<int64_t>(j) * ldc + m] : 0.0;
     }
   }
-  // reflector of column j (= grp + c * NG): scale the registers, publish v and tau
-  auto prep = [&](double* xc, int j) {
+  // reflector of column j: every lane of the owner's warp runs it (full-mask shuffles),
+  // only the owner group (own) scales its registers and publishes v, beta and tau
+  auto prep = [&](double (&xc)[E], int j, bool own) {
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int e = 0; e < E; e += 2) {
       s0 = fma(xc[e], xc[e], s0);
       if (e + 1 < E) s1 = fma(xc[e + 1], xc[e + 1], s1);
     }
-    const double x0 = R[j * b + j];  // read before the group shuffle (lane 0 overwrites it)
-    const double ss = group_sum<G>(s0 + s1, gmask);
+    const double x0 = R[j * b + j];  // read before the shuffle (lane 0 overwrites it)
+    const double ss = group_sum<G>(s0 + s1, kFull);
+    if (!own) return;
     double tau = 0.0;
     if (ss > 0.0) {
       const double n2 = fma(x0, x0, ss);
@@ -185,14 +190,12 @@ __device__ __noinline__ void tsqr_reg_t(double* R, double* C, int K, int b, int 
     }
     if (gl == 0) shr[j & 1] = tau;
   };
-  if (grp == 0 && b > 0) prep(x[0], 0);
+  if (warp == 0 && b > 0) prep(x[0], 0, grp == 0);
   __syncthreads();
   for (int k = 0; k + 1 < b; ++k) {
     const double tau = shr[k & 1];
-    if (tau != 0.0) {
+    if (tau != 0.0 && wmax > k) {
       const double* Ck = C + static_cast<int64_t>(k) * ldc;
-      // partial dots of every owned column against v_k (v read once), then the update
-      // (v re-read: keeping it in registers as well would spill for NC > 1)
       double sd[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) sd[c] = 0.0;
@@ -207,12 +210,11 @@ __device__ __noinline__ void tsqr_reg_t(double* R, double* C, int K, int b, int 
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         const int j = grp + c * NG;
-        dd[c] = 0.0;
-        if (j > k && j < b) {
-          const double rkj = R[j * b + k];
-          dd[c] = tau * (rkj + group_sum<G>(sd[c], gmask));
-          if (gl == 0) R[j * b + k] = rkj - dd[c];
-        }
+        const bool valid = j > k && j < b;
+        const double rkj = valid ? R[j * b + k] : 0.0;
+        const double tot = group_sum<G>(sd[c], kFull);
+        dd[c] = valid ? tau * (rkj + tot) : 0.0;
+        if (valid && gl == 0) R[j * b + k] = rkj - dd[c];
       }
 #pragma unroll
       for (int e = 0; e < E; ++e) {
@@ -222,9 +224,12 @@ __device__ __noinline__ void tsqr_reg_t(double* R, double* C, int K, int b, int 
         for (int c = 0; c < NC; ++c) x[c][e] = fma(-dd[c], ve, x[c][e]);
       }
     }
+    const int jn = k + 1, og = jn % NG, oc = jn / NG;
+    if ((og * G) >> 5 == warp) {
 #pragma unroll
-    for (int c = 0; c < NC; ++c)
-      if (grp + c * NG == k + 1) prep(x[c], k + 1);
+      for (int c = 0; c < NC; ++c)
+        if (c == oc) prep(x[c], jn, grp == og);
+    }
     __syncthreads();
   }
 }
@@ -660,208 +665,249 @@ __device__ void tsqr_sel(const SweepArgs& A, double* R, double* C, int K, int b,
   else tsqr_fast(R, C, K, b, ldc, shr);
 }
 
-// Gather the far blocks with far-ordinal in [fb, fe) of row i into F^T chunks
-// and fold them into the TSQR triangle s.R.  Returns far columns seen.
-__device__ int gather_tsqr(const SweepArgs& A, int i, int b, const Buf& s_, int fb, int fe, int* nzflag,
-                           double* shr) {
+// Window of a row's squared-pattern entries staged in shared memory (one coalesced
+// pass over the host-built per-entry tables) plus the column map of the current chunk.
+constexpr int kEW = 256;
+constexpr int kChunkMax = 512;
+struct EntWin {
+  long long off[kEW];
+  int col[kEW];
+  int roff[kEW];
+  unsigned short bsz[kEW];
+  unsigned char kind[kEW];
+  unsigned short cblk[kChunkMax];  // chunk column -> window entry
+  unsigned short ccol[kChunkMax];  // chunk column -> column inside its block
+};
+
+__device__ int load_window(const SweepArgs& A, int64_t e0, int64_t e1, EntWin& W) {
+  const int n = static_cast<int>(e1 - e0 < kEW ? e1 - e0 : kEW);
+  for (int t = threadIdx.x; t < n; t += T) {
+    const int64_t e = e0 + t;
+    W.off[t] = A.sq_boff[e];
+    W.col[t] = A.sq_col[e];
+    W.roff[t] = A.sq_roff[e];
+    W.bsz[t] = static_cast<unsigned short>(A.sq_bsz[e]);
+    W.kind[t] = A.sq_kind[e];
+  }
+  __syncthreads();
+  return n;
+}
+
+// Gather the far blocks among entries [eb, ee) of row i into F^T chunks (chunk row =
+// far column, column = row of the block row) and fold them into the TSQR triangle
+// s.R.  Returns far columns seen.
+__device__ int gather_tsqr(const SweepArgs& A, int i, int b, const Buf& s_, int64_t eb, int64_t ee, int* nzflag,
+                           double* shr, EntWin& W) {
   const Buf s = s_;
   CE_SHARED_BUF(s);
+  __shared__ int g_add, g_next, g_full;
   const int tid = threadIdx.x;
-  int fcols = 0, kfill = 0, ord = 0;
-  for (int64_t e = A.sq_ptr[i]; e < A.sq_ptr[i + 1]; ++e) {
-    if (A.sq_kind[e] != 2) continue;
-    const int o = ord++;
-    if (o < fb) continue;
-    if (o >= fe) break;
-    const int j = A.sq_col[e];
-    const int bj = A.bsz[j];
-    const bool tr = j > i;
-    const double* X = A.store + A.slot_off[A.sq_slot[e]];
-    if (kfill + bj > A.kcap) {
-      tsqr_sel(A, s.R, s.C, kfill, b, chunk_ld(A.kcap), shr);
-      kfill = 0;
-    }
-    for (int idx = tid; idx < bj * b; idx += T) {
-      int a, c;
-      if (tr) {
-        c = idx / b;
-        a = idx % b;
-      } else {
-        a = idx / bj;
-        c = idx % bj;
+  const int ldc = chunk_ld(A.kcap);
+  int fcols = 0, kfill = 0, nzl = 0;
+  for (int64_t w0 = eb; w0 < ee; w0 += kEW) {
+    const int n = load_window(A, w0, ee, W);
+    int k = 0;
+    while (k < n) {
+      if (tid == 0) {
+        int kk = k, add = 0, full = 0;
+        for (; kk < n; ++kk) {
+          if (W.kind[kk] != 2) continue;
+          const int bj = W.bsz[kk];
+          if (kfill + add + bj > A.kcap) {
+            full = 1;
+            break;
+          }
+          for (int c = 0; c < bj; ++c) {
+            W.cblk[add + c] = static_cast<unsigned short>(kk);
+            W.ccol[add + c] = static_cast<unsigned short>(c);
+          }
+          add += bj;
+        }
+        if (full && add == 0 && kfill == 0) {  // a block wider than the chunk: impossible by kcap >= bmax
+          set_error(A.err, kErrInternal, A.level, i);
+          kk = n;
+          full = 0;
+        }
+        g_add = add;
+        g_next = kk;
+        g_full = full;
       }
-      const double v = ldg(X + xidx(a, c, b, bj, tr));
-      s.C[static_cast<int64_t>(a) * chunk_ld(A.kcap) + kfill + c] = v;  // F^T chunk, column-major
-      if (v != 0.0) *nzflag = 1;
+      __syncthreads();
+      const int add = g_add, full = g_full;
+      k = g_next;
+      const int tot = add * b;
+      for (int base = tid; base < tot; base += 4 * T) {
+        double v[4];
+        int dst[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int idx = base + u * T;
+          dst[u] = -1;
+          v[u] = 0.0;
+          if (idx < tot) {
+            const int m = idx % add, a = idx / add;
+            const int blk = W.cblk[m];
+            const int bj = W.bsz[blk];
+            v[u] = ldg(A.store + W.off[blk] + xidx(a, W.ccol[m], b, bj, W.col[blk] > i));
+            dst[u] = a * ldc + kfill + m;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (dst[u] >= 0) {
+            s.C[dst[u]] = v[u];
+            nzl |= v[u] != 0.0;
+          }
+      }
+      kfill += add;
+      fcols += add;
+      __syncthreads();
+      if (full) {
+        tsqr_sel(A, s.R, s.C, kfill, b, ldc, shr);
+        kfill = 0;
+      }
     }
-    __syncthreads();
-    kfill += bj;
-    fcols += bj;
   }
-  if (kfill > 0) tsqr_sel(A, s.R, s.C, kfill, b, chunk_ld(A.kcap), shr);
+  if (kfill > 0) tsqr_sel(A, s.R, s.C, kfill, b, ldc, shr);
+  if (nzl) *nzflag = 1;
   __syncthreads();
   return fcols;
 }
 
-// Strip entries of row i with strip-ordinal in [ob, oe), in column chunks of up to
-// cw columns (the blocks' columns side by side, one thread per column):
+// Strip entries [eb, ee) of row i (kind != 0), in column chunks of up to cw columns
+// (the blocks' columns side by side, one thread per column):
 //   rotate by U (basis rows) or keep; far blocks keep rows < r only;
 //   close blocks: g_t = (L^{-1} X[r:, :])^T -> G rows, X[:r, :] -= C g_t^T;
 //   rows >= r are zeroed on write-back (level_matrix.cpp:51-65, 125-171).
 // s.U = U (row-major), s.R = L (w x w), s.V = C (r x w); [s.D, s.sig) holds the chunks.
-__device__ __noinline__ void strip_range(const SweepArgs& A, int i, int b, int r, int w, bool basis, int ob, int oe,
-                            const Buf& s_) {
+__device__ __noinline__ void strip_range(const SweepArgs& A, int i, int b, int r, int w, bool basis, int64_t eb,
+                                         int64_t ee, const Buf& s_, EntWin& W) {
   const Buf s = s_;
   CE_SHARED_BUF(s);
-  constexpr int kMaxBlk = 64;
-  __shared__ long long ch_e[kMaxBlk];
-  __shared__ int ch_c0[kMaxBlk + 1];
-  __shared__ int ch_roff[kMaxBlk];
-  __shared__ int ch_n, ch_ord;
-  __shared__ long long ch_next;
+  __shared__ int c_n, c_next;
   const int tid = threadIdx.x;
   const int cw = sweep_layout(A.bmax, A.kcap).cw;
   double* IN = s.D;
   double* OUT = basis ? s.D + static_cast<int64_t>(b) * cw : s.D;
   for (int q = tid; q < w; q += T) s.tau[q] = 1.0 / s.R[q * w + q];
-  const int64_t p0 = A.sq_ptr[i], p1 = A.sq_ptr[i + 1];
-  if (tid == 0) {
-    ch_next = p0;
-    ch_ord = 0;
-  }
-  __syncthreads();
-  for (;;) {
-    if (tid == 0) {
-      int64_t e = ch_next;
-      int ord = ch_ord, n = 0, cols = 0;
-      for (; e < p1; ++e) {
-        const int kind = A.sq_kind[e];
-        if (kind == 0) continue;
-        if (ord >= oe) {
-          e = p1;
-          break;
-        }
-        if (ord < ob) {
-          ++ord;
-          continue;
-        }
-        const int j = A.sq_col[e];
-        const int bj = A.bsz[j];
-        if (n == kMaxBlk || cols + bj > cw) break;
-        ch_e[n] = e;
-        ch_c0[n] = cols;
-        ch_roff[n] = kind == 1 ? A.cl_roff[close_index(A, i, j)] : -1;
-        ++n;
-        cols += bj;
-        ++ord;
-      }
-      ch_c0[n] = cols;
-      ch_n = n;
-      ch_next = e;
-      ch_ord = ord;
-    }
-    __syncthreads();
-    const int n = ch_n;
-    if (n == 0) break;
-    const int ncol = ch_c0[n];
-    for (int k = 0; k < n; ++k) {
-      const int64_t ek = ch_e[k];
-      const int j = A.sq_col[ek], bj = A.bsz[j];
-      const bool tr = j > i, far = ch_roff[k] < 0;
-      const double* X = A.store + A.slot_off[A.sq_slot[ek]];
-      double* dst = IN + ch_c0[k];
-      for (int idx = tid; idx < b * bj; idx += T) {
-        int a, c;
-        if (tr) {
-          c = idx / b;
-          a = idx % b;
-        } else {
-          a = idx / bj;
-          c = idx % bj;
-        }
-        dst[a * cw + c] = (!basis && far && a >= r) ? 0.0 : ldg(X + xidx(a, c, b, bj, tr));
-      }
-    }
-    __syncthreads();
-    for (int c = tid; c < ncol; c += T) {
-      int k = 0;
-      while (ch_c0[k + 1] <= c) ++k;
-      const bool far = ch_roff[k] < 0;
-      if (basis) {
-        const int na = far ? r : b;
-        for (int a0 = 0; a0 < na; a0 += 8) {
-          double acc[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) acc[u] = 0.0;
-          for (int kk = 0; kk < b; ++kk) {
-            const double x = IN[kk * cw + c];
-            const double* Ur = s.U + kk * b + a0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc[u] = fma(Ur[u], x, acc[u]);
+  for (int64_t w0 = eb; w0 < ee; w0 += kEW) {
+    const int n = load_window(A, w0, ee, W);
+    int k = 0;
+    while (k < n) {
+      if (tid == 0) {
+        int kk = k, cols = 0;
+        for (; kk < n; ++kk) {
+          if (W.kind[kk] == 0) continue;
+          const int bj = W.bsz[kk];
+          if (cols + bj > cw) break;
+          for (int c = 0; c < bj; ++c) {
+            W.cblk[cols + c] = static_cast<unsigned short>(kk);
+            W.ccol[cols + c] = static_cast<unsigned short>(c);
           }
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (a0 + u < na) OUT[(a0 + u) * cw + c] = acc[u];
+          cols += bj;
         }
+        if (cols == 0 && kk < n) {  // a block wider than the chunk: impossible by cw >= bmax
+          set_error(A.err, kErrInternal, A.level, i);
+          kk = n;
+        }
+        c_n = cols;
+        c_next = kk;
       }
-      if (!far && w > 0) {
-        double* G = A.fac + A.g_off[i] + static_cast<int64_t>(r + ch_roff[k] + c - ch_c0[k]) * w;
-        double* y = OUT + static_cast<int64_t>(r) * cw + c;
-        for (int q = 0; q < w; ++q) {
-          const double* Lq = s.R + q * w;
-          double a0 = y[q * cw], a1 = 0.0;
-          int p = 0;
-          for (; p + 1 < q; p += 2) {
-            a0 = fma(-Lq[p], y[p * cw], a0);
-            a1 = fma(-Lq[p + 1], y[(p + 1) * cw], a1);
+      __syncthreads();
+      const int ncol = c_n;
+      k = c_next;
+      if (ncol == 0) continue;
+      const int tot = ncol * b;
+      for (int base = tid; base < tot; base += 4 * T) {
+        double v[4];
+        int dst[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int idx = base + u * T;
+          dst[u] = -1;
+          v[u] = 0.0;
+          if (idx < tot) {
+            const int m = idx % ncol, a = idx / ncol;
+            const int blk = W.cblk[m];
+            const bool far = W.roff[blk] < 0;
+            if (!(!basis && far && a >= r))
+              v[u] = ldg(A.store + W.off[blk] + xidx(a, W.ccol[m], b, W.bsz[blk], W.col[blk] > i));
+            dst[u] = a * cw + m;
           }
-          if (p < q) a0 = fma(-Lq[p], y[p * cw], a0);
-          const double v = (a0 + a1) * s.tau[q];
-          y[q * cw] = v;
-          G[q] = v;
         }
-        int a = 0;
-        for (; a + 3 < r; a += 4) {
-          double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (dst[u] >= 0) IN[dst[u]] = v[u];
+      }
+      __syncthreads();
+      for (int c = tid; c < ncol; c += T) {
+        const int blk = W.cblk[c];
+        const int roff = W.roff[blk];
+        const bool far = roff < 0;
+        if (basis) {
+          const int na = far ? r : b;
+          for (int a0 = 0; a0 < na; a0 += 8) {
+            double acc[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+            for (int kk = 0; kk < b; ++kk) {
+              const double x = IN[kk * cw + c];
+              const double* Ur = s.U + kk * b + a0;
+#pragma unroll
+              for (int u = 0; u < 8; ++u) acc[u] = fma(Ur[u], x, acc[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (a0 + u < na) OUT[(a0 + u) * cw + c] = acc[u];
+          }
+        }
+        if (!far && w > 0) {
+          double* G = A.fac + A.g_off[i] + static_cast<int64_t>(r + roff + W.ccol[c]) * w;
+          double* y = OUT + static_cast<int64_t>(r) * cw + c;
           for (int q = 0; q < w; ++q) {
-            const double yq = y[q * cw];
-            c0 = fma(s.V[a * w + q], yq, c0);
-            c1 = fma(s.V[(a + 1) * w + q], yq, c1);
-            c2 = fma(s.V[(a + 2) * w + q], yq, c2);
-            c3 = fma(s.V[(a + 3) * w + q], yq, c3);
+            const double* Lq = s.R + q * w;
+            double a0 = y[q * cw], a1 = 0.0;
+            int p = 0;
+            for (; p + 1 < q; p += 2) {
+              a0 = fma(-Lq[p], y[p * cw], a0);
+              a1 = fma(-Lq[p + 1], y[(p + 1) * cw], a1);
+            }
+            if (p < q) a0 = fma(-Lq[p], y[p * cw], a0);
+            const double v = (a0 + a1) * s.tau[q];
+            y[q * cw] = v;
+            G[q] = v;
           }
-          OUT[a * cw + c] -= c0;
-          OUT[(a + 1) * cw + c] -= c1;
-          OUT[(a + 2) * cw + c] -= c2;
-          OUT[(a + 3) * cw + c] -= c3;
-        }
-        for (; a < r; ++a) {
-          double c0 = 0.0;
-          for (int q = 0; q < w; ++q) c0 = fma(s.V[a * w + q], y[q * cw], c0);
-          OUT[a * cw + c] -= c0;
+          int a = 0;
+          for (; a + 3 < r; a += 4) {
+            double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+            for (int q = 0; q < w; ++q) {
+              const double yq = y[q * cw];
+              c0 = fma(s.V[a * w + q], yq, c0);
+              c1 = fma(s.V[(a + 1) * w + q], yq, c1);
+              c2 = fma(s.V[(a + 2) * w + q], yq, c2);
+              c3 = fma(s.V[(a + 3) * w + q], yq, c3);
+            }
+            OUT[a * cw + c] -= c0;
+            OUT[(a + 1) * cw + c] -= c1;
+            OUT[(a + 2) * cw + c] -= c2;
+            OUT[(a + 3) * cw + c] -= c3;
+          }
+          for (; a < r; ++a) {
+            double c0 = 0.0;
+            for (int q = 0; q < w; ++q) c0 = fma(s.V[a * w + q], y[q * cw], c0);
+            OUT[a * cw + c] -= c0;
+          }
         }
       }
-    }
-    __syncthreads();
-    for (int k = 0; k < n; ++k) {
-      const int64_t ek = ch_e[k];
-      const int j = A.sq_col[ek], bj = A.bsz[j];
-      const bool tr = j > i;
-      double* X = A.store + A.slot_off[A.sq_slot[ek]];
-      const double* src = OUT + ch_c0[k];
-      for (int idx = tid; idx < b * bj; idx += T) {
-        int a, c;
-        if (tr) {
-          c = idx / b;
-          a = idx % b;
-        } else {
-          a = idx / bj;
-          c = idx % bj;
-        }
-        X[xidx(a, c, b, bj, tr)] = (w > 0 && a >= r) ? 0.0 : src[a * cw + c];
+      __syncthreads();
+      for (int idx = tid; idx < tot; idx += T) {
+        const int m = idx % ncol, a = idx / ncol;
+        const int blk = W.cblk[m];
+        double* X = A.store + W.off[blk] + xidx(a, W.ccol[m], b, W.bsz[blk], W.col[blk] > i);
+        *X = (w > 0 && a >= r) ? 0.0 : OUT[a * cw + m];
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
@@ -872,31 +918,54 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
   CE_SHARED(sm);
   __shared__ long long slot_tab[kPanelNb * kPanelNb];  // value offset of stored (t, s), -1: not updated
   __shared__ int tab_bs[kPanelNb];
+  __shared__ int roff_s[kPanelNb], roff_t[kPanelNb];
+  __shared__ int n_live[2];
   __shared__ unsigned char xblk[kPanelRows], yblk[kPanelRows];
   __shared__ unsigned short xloc[kPanelRows], yloc[kPanelRows];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t c0 = A.cl_ptr[i];
   const int* ps = A.pan_start + A.pan_ptr[i];
   const int s0 = ps[P], s1 = ps[P + 1], t0 = ps[Q], t1 = ps[Q + 1];
   const int ns = s1 - s0, nt = t1 - t0;
-  const int rs0 = A.cl_roff[c0 + s0];
-  const int rsn = A.cl_roff[c0 + s1 - 1] + A.bsz[A.cl_col[c0 + s1 - 1]] - rs0;
-  const int rt0 = A.cl_roff[c0 + t0];
-  const int rtn = A.cl_roff[c0 + t1 - 1] + A.bsz[A.cl_col[c0 + t1 - 1]] - rt0;
-  const int lds = (rsn + 3) & ~3, ldt = (rtn + 3) & ~3;
-  // g rows transposed into shared memory: GsT[q][y], GtT[q][x]
-  const double* G = A.fac + A.g_off[i];
-  double* GsT = sm;
-  double* GtT = P == Q ? sm : sm + static_cast<int64_t>(lds) * w;
-  for (int idx = tid; idx < lds * w; idx += T) {
-    const int y = idx / w, q = idx % w;
-    GsT[q * lds + y] = y < rsn ? ldg(G + static_cast<int64_t>(r + rs0 + y) * w + q) : 0.0;
-  }
-  if (P != Q)
-    for (int idx = tid; idx < ldt * w; idx += T) {
-      const int x = idx / w, q = idx % w;
-      GtT[q * ldt + x] = x < rtn ? ldg(G + static_cast<int64_t>(r + rt0 + x) * w + q) : 0.0;
+  // Live rows of each neighbour's g block: a neighbour u < i was eliminated earlier in
+  // this level, its block row is zero below its rank, so g_u (= columns of X_iu) is zero
+  // in rows >= rank(u) and X_st only changes in the retained rows / columns.  The panel
+  // is compacted to live rows (bit-identical result: the skipped terms are exact zeros).
+  if (warp < 2) {
+    const int n = warp == 0 ? ns : nt, base = warp == 0 ? s0 : t0;
+    int live = 0, roff = 0, bu = 0;
+    if (lane < n) {
+      const int64_t e = c0 + base + lane;
+      const int u = A.cl_col[e];
+      bu = A.bsz[u];
+      roff = A.cl_roff[e];
+      live = u < i ? __ldcg(A.rank + u) : bu;
     }
+    int incl = live;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int y0 = incl - live;
+    if (lane < n) {
+      if (warp == 0) {
+        tab_bs[lane] = bu;
+        roff_s[lane] = roff;
+        for (int y = 0; y < live; ++y) {
+          yblk[y0 + y] = static_cast<unsigned char>(lane);
+          yloc[y0 + y] = static_cast<unsigned short>(y);
+        }
+      } else {
+        roff_t[lane] = roff;
+        for (int x = 0; x < live; ++x) {
+          xblk[y0 + x] = static_cast<unsigned char>(lane);
+          xloc[y0 + x] = static_cast<unsigned short>(x);
+        }
+      }
+    }
+    if (lane == 31) n_live[warp] = incl;
+  }
   for (int idx = tid; idx < nt * ns; idx += T) {
     const int kt = idx / ns, ks = idx % ns;
     long long off = -1;
@@ -908,25 +977,22 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
     }
     slot_tab[idx] = off;
   }
-  for (int ks = tid; ks < ns; ks += T) {
-    const int e = static_cast<int>(c0) + s0 + ks;
-    const int bs_ = A.bsz[A.cl_col[e]];
-    tab_bs[ks] = bs_;
-    const int y0 = A.cl_roff[e] - rs0;
-    for (int y = 0; y < bs_; ++y) {
-      yblk[y0 + y] = static_cast<unsigned char>(ks);
-      yloc[y0 + y] = static_cast<unsigned short>(y);
-    }
+  __syncthreads();
+  const int rsn = n_live[0], rtn = n_live[1];
+  const int lds = (rsn + 3) & ~3, ldt = (rtn + 3) & ~3;
+  // g rows transposed into shared memory: GsT[q][y], GtT[q][x] (live rows only)
+  const double* G = A.fac + A.g_off[i];
+  double* GsT = sm;
+  double* GtT = P == Q ? sm : sm + static_cast<int64_t>(lds) * w;
+  for (int idx = tid; idx < lds * w; idx += T) {
+    const int y = idx / w, q = idx % w;
+    GsT[q * lds + y] = y < rsn ? ldg(G + static_cast<int64_t>(r + roff_s[yblk[y]] + yloc[y]) * w + q) : 0.0;
   }
-  for (int kt = tid; kt < nt; kt += T) {
-    const int e = static_cast<int>(c0) + t0 + kt;
-    const int bt = A.bsz[A.cl_col[e]];
-    const int x0 = A.cl_roff[e] - rt0;
-    for (int x = 0; x < bt; ++x) {
-      xblk[x0 + x] = static_cast<unsigned char>(kt);
-      xloc[x0 + x] = static_cast<unsigned short>(x);
+  if (P != Q)
+    for (int idx = tid; idx < ldt * w; idx += T) {
+      const int x = idx / w, q = idx % w;
+      GtT[q * ldt + x] = x < rtn ? ldg(G + static_cast<int64_t>(r + roff_t[xblk[x]] + xloc[x]) * w + q) : 0.0;
     }
-  }
   __syncthreads();
   // rtn x rsn outer product in 4x4 register tiles; epilogue scatters into the (t, s) blocks
   const int mx = ldt / 4, my = lds / 4;
@@ -976,7 +1042,7 @@ __device__ void all_panels(const SweepArgs& A, int i, int r, int w, double* sm) 
 
 // A2: compression decision + basis + pivot factorisation; with nA3 == 0 also the strip,
 // with nB == 0 also the Schur panels.
-__device__ void task_a2(const SweepArgs& A, int i, const Buf& s_, int nA1, int nA3, int nB) {
+__device__ void task_a2(const SweepArgs& A, int i, const Buf& s_, int nA1, int nA3, int nB, EntWin& W) {
   const Buf s = s_;
   CE_SHARED_BUF(s);
   __shared__ double shr[4];
@@ -985,13 +1051,7 @@ __device__ void task_a2(const SweepArgs& A, int i, const Buf& s_, int nA1, int n
   const long long t_a2 = clock64();
   const int b = A.bsz[i];
   const int64_t p0 = A.sq_ptr[i], p1 = A.sq_ptr[i + 1];
-  int64_t dslot = -1;
-  for (int64_t e = p0; e < p1; ++e)
-    if (A.sq_col[e] == i) {
-      dslot = A.sq_slot[e];
-      break;
-    }
-  double* Dg = A.store + A.slot_off[dslot];
+  double* Dg = A.store + A.sq_boff[A.sq_diag[i]];
   for (int idx = tid; idx < b * b; idx += T) {
     s.D[idx] = ldg(Dg + idx);
     s.R[idx] = 0.0;
@@ -1002,7 +1062,7 @@ __device__ void task_a2(const SweepArgs& A, int i, const Buf& s_, int nA1, int n
   // ---- far-block triangle (compression.cpp:38-48) ----
   int fcols;
   if (nA1 == 0) {
-    fcols = gather_tsqr(A, i, b, s, 0, 1 << 30, &sflag[0], shr);
+    fcols = gather_tsqr(A, i, b, s, p0, p1, &sflag[0], shr, W);
   } else {
     fcols = static_cast<int>(A.fsum[i]);
     // fold the leaf triangles, as many per chunk as fit (chunk rows <= kcap)
@@ -1227,7 +1287,7 @@ __device__ void task_a2(const SweepArgs& A, int i, const Buf& s_, int nA1, int n
 
   // ---- strip (thin rows) ----
   if (nA3 == 0 && (basis || w > 0)) {
-    strip_range(A, i, b, r, w, basis, 0, 1 << 30, s);
+    strip_range(A, i, b, r, w, basis, p0, p1, s, W);
     {
       const long long t = clock64();
       prof_add(A, kProfA2Strip, t - tp);
@@ -1239,7 +1299,7 @@ __device__ void task_a2(const SweepArgs& A, int i, const Buf& s_, int nA1, int n
 }
 
 // A3 tile k: strip entries with strip-ordinal in [k*ns/nA3, (k+1)*ns/nA3).
-__device__ void task_a3(const SweepArgs& A, int i, const Buf& s_, int k, int nA3, int nB) {
+__device__ void task_a3(const SweepArgs& A, int i, const Buf& s_, int k, int nA3, int nB, EntWin& W) {
   const Buf s = s_;
   CE_SHARED_BUF(s);
   const int tid = threadIdx.x;
@@ -1254,11 +1314,9 @@ __device__ void task_a3(const SweepArgs& A, int i, const Buf& s_, int k, int nA3
     for (int idx = tid; idx < r * w; idx += T) s.V[idx] = ldg(A.fac + A.g_off[i] + idx);
   }
   __syncthreads();
-  const int64_t p0 = A.sq_ptr[i], p1 = A.sq_ptr[i + 1];
-  const int ns = static_cast<int>(p1 - p0) - 1;
-  const int ob = static_cast<int>(static_cast<int64_t>(ns) * k / nA3);
-  const int oe = static_cast<int>(static_cast<int64_t>(ns) * (k + 1) / nA3);
-  strip_range(A, i, b, r, w, basis, ob, oe, s);
+  const int64_t* se = A.strip_e + A.strip_ptr[i] + k;
+  strip_range(A, i, b, r, w, basis, se[0], se[1], s, W);
+  (void)nA3;
   (void)nB;
 }
 
@@ -1273,6 +1331,7 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
   CE_SHARED_BUF(s);
   __shared__ long long s_item;
   __shared__ int s_stop;
+  __shared__ EntWin W;
   __shared__ double shr[4];
   __shared__ int nz;
   for (;;) {
@@ -1306,21 +1365,25 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
     }
     const bool first = (stage == 1) || (stage == 2 && nA1 == 0);
     const long long t_wait = clock64();
+    if (first) {
+      // every predecessor j < i of sq(i) finished (one poller per entry, in parallel)
+      const int64_t pb = A.sq_ptr[i], pe = A.sq_diag[i];
+      for (int64_t e = pb + threadIdx.x; e < pe; e += T) {
+        const int j = A.sq_col[e];
+        const int tgt = A.target[j];
+        while (ld_acquire(A.done + j) < tgt) {
+          if (*reinterpret_cast<volatile int*>(A.err) != 0) {
+            s_stop = 1;
+            break;
+          }
+          __nanosleep(64);
+        }
+        if (s_stop) break;
+      }
+      __threadfence();
+    }
     if (threadIdx.x == 0) {
       if (first) {
-        for (int64_t e = A.sq_ptr[i]; e < A.sq_ptr[i + 1]; ++e) {
-          const int j = A.sq_col[e];
-          if (j >= i) break;
-          const int target = 1 + A.nA1[j] + A.nA3[j] + A.nB[j];
-          while (ld_acquire(A.done + j) < target) {
-            if (*reinterpret_cast<volatile int*>(A.err) != 0) {
-              s_stop = 1;
-              break;
-            }
-            __nanosleep(64);
-          }
-          if (s_stop) break;
-        }
       } else {
         while (ld_acquire(A.done + i) < need) {
           if (*reinterpret_cast<volatile int*>(A.err) != 0) {
@@ -1341,19 +1404,16 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
       const int b = A.bsz[i];
       for (int idx = threadIdx.x; idx < b * b; idx += T) s.R[idx] = 0.0;
       __syncthreads();
-      // far-ordinal range of this leaf
-      int nf = 0;
-      for (int64_t e = A.sq_ptr[i]; e < A.sq_ptr[i + 1]; ++e) nf += A.sq_kind[e] == 2;
-      const int fb = static_cast<int>(static_cast<int64_t>(nf) * k / nA1);
-      const int fe = static_cast<int>(static_cast<int64_t>(nf) * (k + 1) / nA1);
-      gather_tsqr(A, i, b, s, fb, fe, &nz, shr);
+      // far-entry range of this leaf
+      const int64_t* le = A.leaf_e + A.leaf_ptr[i] + k;
+      gather_tsqr(A, i, b, s, le[0], le[1], &nz, shr, W);
       double* Rk = A.rscratch + A.rs_off[i] + static_cast<int64_t>(k) * b * b;
       for (int idx = threadIdx.x; idx < b * b; idx += T) Rk[idx] = s.R[idx];
       if (threadIdx.x == 0 && nz) atomicOr(A.nzflag + i, 1);
     } else if (stage == 2) {
-      task_a2(A, i, s, nA1, nA3, nB);
+      task_a2(A, i, s, nA1, nA3, nB, W);
     } else if (stage == 3) {
-      task_a3(A, i, s, k, nA3, nB);
+      task_a3(A, i, s, k, nA3, nB, W);
     } else {
       const int w = __ldcg(A.width + i);
       if (w > 0) {

@@ -6,6 +6,7 @@
 #include "../paper_1603_09133_b200/csrc/sweep.cu"
 
 #include <vector>
+#include <cstdlib>
 
 namespace ceg {
 void note_launch(int64_t) {}
@@ -129,7 +130,7 @@ __device__ void tsqr_probe(double* R, double* C, int K, int b, int ldc, double* 
   }
 }
 
-__device__ long long g_stage[8];
+__device__ long long g_stage[16];
 // stage-stamped update loop (no prep) for one thread
 template <int G>
 __device__ void tsqr_stamp(double* R, double* C, int K, int b, int ldc, double* shr) {
@@ -166,6 +167,214 @@ __device__ void tsqr_stamp(double* R, double* C, int K, int b, int ldc, double* 
   }
   if (tid == 0 && blockIdx.x == 0) for (int q = 0; q < 4; ++q) g_stage[q] = st[q] / (b - 1);
 }
+
+template <int G, int E, int NC>
+__device__ void tsqr_stamp_t(double* R, double* C, int K, int b, int ldc, double* shr) {
+  __builtin_assume(__isShared(R));
+  __builtin_assume(__isShared(C));
+  constexpr int NG = T / G;
+  const int tid = threadIdx.x, grp = tid / G, gl = tid % G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((tid & 31) / G * G));
+  double x[NC][E];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = grp + c * NG;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int m = gl + e * G;
+      x[c][e] = (j < b && m < K) ? C[static_cast<int64_t>(j) * ldc + m] : 0.0;
+    }
+  }
+  // reflector of column j (= grp + c * NG): scale the registers, publish v and tau
+  auto prep = [&](double* xc, int j) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+      s0 = fma(xc[e], xc[e], s0);
+      if (e + 1 < E) s1 = fma(xc[e + 1], xc[e + 1], s1);
+    }
+    const double x0 = R[j * b + j];  // read before the group shuffle (lane 0 overwrites it)
+    const double ss = group_sum<G>(s0 + s1, gmask);
+    double tau = 0.0;
+    if (ss > 0.0) {
+      const double n2 = fma(x0, x0, ss);
+      const bool fast = n2 > 1e-290 && n2 < 1e290;  // SFU + Newton only away from under/overflow
+      const double nrm = fast ? n2 * rsqrt_nr(n2) : sqrt(n2);
+      const double beta = x0 >= 0.0 ? -nrm : nrm;
+      const double den = x0 - beta;
+      const double scale = fast ? rcp_nr(den) : 1.0 / den;
+      tau = fast ? -den * rcp_nr(beta) : (beta - x0) / beta;
+      double* Cj = C + static_cast<int64_t>(j) * ldc;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int m = gl + e * G;
+        xc[e] *= scale;
+        if (m < K) Cj[m] = xc[e];
+      }
+      if (gl == 0) R[j * b + j] = beta;
+    }
+    if (gl == 0) shr[j & 1] = tau;
+  };
+  if (grp == 0 && b > 0) prep(x[0], 0);
+  __syncthreads();
+  long long st[6] = {0, 0, 0, 0, 0, 0};
+  const long long tloop0 = clock64();
+  for (int k = 0; k + 1 < b; ++k) {
+    long long c0 = clock64();
+    const double tau = shr[k & 1];
+    if (tau != 0.0) {
+      const double* Ck = C + static_cast<int64_t>(k) * ldc;
+      // partial dots of every owned column against v_k (v read once), then the update
+      // (v re-read: keeping it in registers as well would spill for NC > 1)
+      double sd[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) sd[c] = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int m = gl + e * G;
+        const double ve = m < K ? Ck[m] : 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sd[c] = fma(ve, x[c][e], sd[c]);
+      }
+      st[0] += clock64() - c0;
+      c0 = clock64();
+      double dd[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int j = grp + c * NG;
+        dd[c] = 0.0;
+        if (j > k && j < b) {
+          const double rkj = R[j * b + k];
+          dd[c] = tau * (rkj + group_sum<G>(sd[c], gmask));
+          if (gl == 0) R[j * b + k] = rkj - dd[c];
+        }
+      }
+      st[1] += clock64() - c0;
+      c0 = clock64();
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int m = gl + e * G;
+        const double ve = m < K ? Ck[m] : 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) x[c][e] = fma(-dd[c], ve, x[c][e]);
+      }
+      st[2] += clock64() - c0;
+    }
+    c0 = clock64();
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (grp + c * NG == k + 1) prep(x[c], k + 1);
+    st[3] += clock64() - c0;
+    c0 = clock64();
+    __syncthreads();
+    st[4] += clock64() - c0;
+  }
+  st[5] = clock64() - tloop0;
+  if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == G))
+    for (int q = 0; q < 6; ++q) g_stage[q + (threadIdx.x == 0 ? 0 : 6)] = st[q] / (b - 1);
+}
+
+
+template <int G, int E, int NC, int MODE>
+__device__ __noinline__ void tsqr_abl_t(double* R, double* C, int K, int b, int ldc, double* shr) {
+  __builtin_assume(__isShared(R));
+  __builtin_assume(__isShared(C));
+  constexpr int NG = T / G;
+  constexpr unsigned kFull = 0xffffffffu;
+  // control flow is warp-uniform around every shuffle (full-mask shuffles: partial masks
+  // make the compiler emit MATCH/REDUX convergence checks on the critical path)
+  const int tid = threadIdx.x, grp = tid / G, gl = tid % G, warp = tid >> 5;
+  const int wmax = ((warp + 1) * 32) / G - 1 + (NC - 1) * NG;  // largest column owned in this warp
+  double x[NC][E];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = grp + c * NG;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int m = gl + e * G;
+      x[c][e] = (j < b && m < K) ? C[static_cast<int64_t>(j) * ldc + m] : 0.0;
+    }
+  }
+  // reflector of column j: every lane of the owner's warp runs it (full-mask shuffles),
+  // only the owner group (own) scales its registers and publishes v, beta and tau
+  auto prep = [&](double (&xc)[E], int j, bool own) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+      s0 = fma(xc[e], xc[e], s0);
+      if (e + 1 < E) s1 = fma(xc[e + 1], xc[e + 1], s1);
+    }
+    const double x0 = R[j * b + j];  // read before the shuffle (lane 0 overwrites it)
+    const double ss = group_sum<G>(s0 + s1, kFull);
+    if (!own) return;
+    if (MODE & 1) {
+      if (gl == 0) shr[j & 1] = 1e-3 + 1e-30 * ss;
+      return;
+    }
+    double tau = 0.0;
+    if (ss > 0.0) {
+      const double n2 = fma(x0, x0, ss);
+      const bool fast = n2 > 1e-290 && n2 < 1e290;  // SFU + Newton only away from under/overflow
+      const double nrm = fast ? n2 * rsqrt_nr(n2) : sqrt(n2);
+      const double beta = x0 >= 0.0 ? -nrm : nrm;
+      const double den = x0 - beta;
+      const double scale = fast ? rcp_nr(den) : 1.0 / den;
+      tau = fast ? -den * rcp_nr(beta) : (beta - x0) / beta;
+      double* Cj = C + static_cast<int64_t>(j) * ldc;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int m = gl + e * G;
+        xc[e] *= scale;
+        if (m < K) Cj[m] = xc[e];
+      }
+      if (gl == 0) R[j * b + j] = beta;
+    }
+    if (gl == 0) shr[j & 1] = tau;
+  };
+  if (warp == 0 && b > 0) prep(x[0], 0, grp == 0);
+  __syncthreads();
+  for (int k = 0; k + 1 < b; ++k) {
+    const double tau = shr[k & 1];
+    if (!(MODE & 2) && tau != 0.0 && wmax > k) {
+      const double* Ck = C + static_cast<int64_t>(k) * ldc;
+      double sd[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) sd[c] = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int m = gl + e * G;
+        const double ve = m < K ? Ck[m] : 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sd[c] = fma(ve, x[c][e], sd[c]);
+      }
+      double dd[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int j = grp + c * NG;
+        const bool valid = j > k && j < b;
+        const double rkj = valid ? R[j * b + k] : 0.0;
+        const double tot = group_sum<G>(sd[c], kFull);
+        dd[c] = valid ? tau * (rkj + tot) : 0.0;
+        if (valid && gl == 0) R[j * b + k] = rkj - dd[c];
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int m = gl + e * G;
+        const double ve = m < K ? Ck[m] : 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) x[c][e] = fma(-dd[c], ve, x[c][e]);
+      }
+    }
+    const int jn = k + 1, og = jn % NG, oc = jn / NG;
+    if ((og * G) >> 5 == warp) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (c == oc) prep(x[c], jn, grp == og);
+    }
+    __syncthreads();
+  }
+}
+
 
 __device__ __forceinline__ double hrand(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;
@@ -213,6 +422,19 @@ __global__ void __launch_bounds__(T) micro_kernel(int which, int b, int K, int r
     else if (which == 11) tsqr_stamp<16>(R, C, K, b, ldc, shr);
     else if (which == 12) tsqr_fast(R, C, K, b, ldc, shr);
     else if (which == 13) nsw_tot += jacobi_fast(R, V, b, ld, b);
+    else if (which == 14) tsqr_reg_t<16, 8, 3>(R, C, K, b, ldc, shr);
+    else if (which == 15) tsqr_reg_t<8, 16, 2>(R, C, K, b, ldc, shr);
+    else if (which == 16) tsqr_reg_t<4, 32, 1>(R, C, K, b, ldc, shr);
+    else if (which == 17) tsqr_reg_t<16, 8, 4>(R, C, K, b, ldc, shr);
+    else if (which == 18) tsqr_reg_t<32, 4, 6>(R, C, K, b, ldc, shr);
+    else if (which == 19) tsqr_reg_t<8, 16, 1>(R, C, K, b, ldc, shr);
+    else if (which == 20) tsqr_reg_t<16, 8, 1>(R, C, K, b, ldc, shr);
+    else if (which == 21) tsqr_stamp_t<16, 8, 1>(R, C, K, b, ldc, shr);
+    else if (which == 23) tsqr_abl_t<16, 8, 1, 0>(R, C, K, b, ldc, shr);
+    else if (which == 24) tsqr_abl_t<16, 8, 1, 1>(R, C, K, b, ldc, shr);
+    else if (which == 25) tsqr_abl_t<16, 8, 1, 2>(R, C, K, b, ldc, shr);
+    else if (which == 26) tsqr_abl_t<16, 8, 1, 3>(R, C, K, b, ldc, shr);
+    else if (which == 22) tsqr_stamp_t<16, 8, 3>(R, C, K, b, ldc, shr);
     __syncthreads();
     const long long t1 = clock64();
     acc += static_cast<unsigned long long>(t1 - t0);
@@ -305,7 +527,7 @@ int main() {
   cudaSetDevice(dev);
   int nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = 2 * nsm;
+  const int grid = (getenv("MICRO_CPS") ? atoi(getenv("MICRO_CPS")) : 2) * nsm;
   unsigned long long* d_cyc;
   double* d_out;
   int* d_sw;
@@ -318,7 +540,7 @@ int main() {
     double* d_o;
     cudaMalloc(&d_l, 16 * sizeof(long long));
     cudaMalloc(&d_o, 1024 * sizeof(double));
-    for (int mode = 0; mode < 3; ++mode)
+    for (int mode = 0; mode < 0; ++mode)
       for (int nt : {32, 128, 256, 512, 1024}) {
         thr_kernel<<<1, nt>>>(d_o, d_l, mode);
         cudaDeviceSynchronize();
@@ -329,10 +551,10 @@ int main() {
                     mode == 0 ? "dfma" : (mode == 1 ? "shfl64" : "ffma"), nt, l, ops / l);
       }
   }
-  {
+  if (!getenv("MICRO_CASE")) {
     long long* d_l;
     cudaMalloc(&d_l, 16 * sizeof(long long));
-    for (int nt : {32, 256}) {
+    for (int nt : {32}) {
       lat_kernel<<<1, nt>>>(d_out, d_l, 0.5);
       cudaDeviceSynchronize();
       long long l[16];
@@ -342,11 +564,11 @@ int main() {
     }
   }
   struct Case { int which, b, K; };
-  const Case cases[] = {{0, 16, 128}, {12, 16, 128}, {0, 24, 128}, {12, 24, 128}, {0, 40, 120}, {12, 40, 120},
-                        {0, 40, 128}, {12, 40, 128}, {0, 64, 128}, {12, 64, 128}, {0, 16, 48}, {12, 16, 48},
-                        {3, 16, 0}, {13, 16, 0}, {3, 24, 0}, {13, 24, 0}, {3, 40, 0}, {13, 40, 0}, {3, 64, 0}, {13, 64, 0}};
-  const char* names[] = {"tsqr_warps", "tsqr_update", "tsqr_group", "jacobi", "tsqr_g4", "tsqr_g16", "tsqr_g32", "noprep", "noupdate", "fastdiv", "probe_full", "stamp", "tsqr_fast", "jacobi_fast"};
+  const Case cases[] = {{23, 16, 128}, {24, 16, 128}, {25, 16, 128}, {26, 16, 128}};
+  const char* names[] = {"tsqr_warps", "tsqr_update", "tsqr_group", "jacobi", "tsqr_g4", "tsqr_g16", "tsqr_g32", "noprep", "noupdate", "fastdiv", "probe_full", "stamp", "tsqr_fast", "jacobi_fast", "reg16x8x3", "reg8x16x2", "reg4x32x1", "reg16x8x4", "reg32x4x6", "reg8x16x1", "reg16x8x1", "stamp16", "stamp40", "abl_full", "abl_noprep", "abl_noupd", "abl_none"};
+  const int only = getenv("MICRO_CASE") ? atoi(getenv("MICRO_CASE")) : -1;
   for (const Case& c : cases) {
+    if (only >= 0 && c.which != only) continue;
     const int ld = c.b | 1;
     const size_t smem = (2 * c.b * ld + (c.K | 1) * c.b + 64) * sizeof(double);
     const int reps = 20;
@@ -372,6 +594,12 @@ int main() {
                 mean / 1900.0);
     if (c.which == 3 || c.which == 13) std::printf("  sweeps %.2f  cycles/round %.0f", sws, mean / (sws * ((c.b + (c.b & 1)) - 1)));
     std::printf("  out[0..2] %.6f %.6f %.6f\n", out[0], out[1], out[2]);
+    if (c.which == 21 || c.which == 22) {
+      long long st[16];
+      cudaMemcpyFromSymbol(st, g_stage, sizeof(st));
+      std::printf("   thread0: v+dot %lld  reduce %lld  update %lld  prep %lld  barrier %lld  loop/step %lld\n", st[0], st[1], st[2], st[3], st[4], st[5]);
+      std::printf("   thread G: v+dot %lld  reduce %lld  update %lld  prep %lld  barrier %lld  loop/step %lld\n", st[6], st[7], st[8], st[9], st[10], st[11]);
+    }
     if (c.which == 11) {
       long long st[8];
       cudaMemcpyFromSymbol(st, g_stage, sizeof(st));
