@@ -28,19 +28,6 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
-// Row offset of neighbour `j` inside row i's close list, or -1.
-__device__ int close_roff(const ApplyLevelArgs& A, int i, int j) {
-  int64_t lo = A.cl_ptr[i], hi = A.cl_ptr[i + 1];
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    const int c = A.cl_col[mid];
-    if (c == j) return A.cl_roff[mid];
-    if (c < j) lo = mid + 1;
-    else hi = mid;
-  }
-  return -1;
-}
-
 __global__ void basis_kernel(ApplyLevelArgs A, int transpose) {
   extern __shared__ double seg[];
   for (int64_t b = blockIdx.x; b < A.M; b += gridDim.x) {
@@ -62,53 +49,49 @@ __global__ void basis_kernel(ApplyLevelArgs A, int transpose) {
   }
 }
 
-// Forward sweep, rows in ascending order.
+// Forward sweep, rows in wave order.  Row j: wait for its contributing neighbours
+// i < j (polled in parallel), pull z = v_j[r:] - sum_i g_{i->j}[r_j:, :] u_i (a warp
+// per neighbour, lanes over the rows of g), then u_j = L_j^{-1} z.
 __global__ void __launch_bounds__(T) forward_kernel(ApplyLevelArgs A) {
   extern __shared__ double z[];
   __shared__ long long s_row;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (;;) {
     if (threadIdx.x == 0) s_row = static_cast<long long>(atomicAdd(A.ticket, 1ULL));
     __syncthreads();
     const long long jl = s_row;
     if (jl >= A.M) break;
     const int j = A.order[jl];
-    const int64_t c0 = A.cl_ptr[j], c1 = A.cl_ptr[j + 1];
-    if (threadIdx.x == 0) {
-      for (int64_t e = c0; e < c1; ++e) {
-        const int i = A.cl_col[e];
-        if (i >= j) break;
-        while (ld_acquire(A.flags + i) == 0) __nanosleep(32);
-      }
-      __threadfence();
-    }
+    const int64_t k0 = A.in_ptr[j], k1 = k0 + A.in_split[j];
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += T)
+      while (ld_acquire(A.flags + A.in_src[k]) == 0) __nanosleep(32);
+    __threadfence();
     __syncthreads();
     const int w = A.width[j];
     if (w > 0) {
       const int r = A.rank[j];
       double* vj = A.v + A.offsets[j];
-      // warps pull incoming neighbours i < j: z[q] -= g_{i->j}[r_j + q, :] u_i (lane <-> q)
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
       double* part = z + kWmax + warp * 2 * kWmax;
       double* ub = part + kWmax;
       for (int q = lane; q < w; q += 32) part[q] = 0.0;
-      int nb = 0;
-      for (int64_t e = c0; e < c1; ++e) {
-        const int i = A.cl_col[e];
-        if (i >= j) break;
-        const int wi = A.width[i];
-        if (wi == 0) continue;
-        if ((nb++ % kApplyWarps) != warp) continue;
-        const int ri = A.rank[i];
-        const int ro = close_roff(A, i, j);
-        const double* ui = A.v + A.offsets[i] + ri;
+      for (int64_t k = k0 + warp; k < k1; k += kApplyWarps) {
+        const int wi = A.in_w[k];
+        const double* ui = A.v + A.in_uoff[k];
         for (int p = lane; p < wi; p += 32) ub[p] = ldg(ui + p);
         __syncwarp();
-        const double* g = A.fac + A.g_off[i] + static_cast<int64_t>(ri + ro + r) * wi;
+        const double* g = A.fac + A.in_goff[k] + static_cast<int64_t>(r) * wi;
         for (int q = lane; q < w; q += 32) {
           const double* gq = g + static_cast<int64_t>(q) * wi;
-          double acc = 0.0;
-          for (int p = 0; p < wi; ++p) acc += gq[p] * ub[p];
-          part[q] += acc;
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int p = 0;
+          for (; p + 3 < wi; p += 4) {
+            a0 = fma(__ldg(gq + p), ub[p], a0);
+            a1 = fma(__ldg(gq + p + 1), ub[p + 1], a1);
+            a2 = fma(__ldg(gq + p + 2), ub[p + 2], a2);
+            a3 = fma(__ldg(gq + p + 3), ub[p + 3], a3);
+          }
+          for (; p < wi; ++p) a0 = fma(__ldg(gq + p), ub[p], a0);
+          part[q] += (a0 + a1) + (a2 + a3);
         }
         __syncwarp();
       }
@@ -119,18 +102,18 @@ __global__ void __launch_bounds__(T) forward_kernel(ApplyLevelArgs A) {
         z[q] = acc;
       }
       __syncthreads();
-      if (threadIdx.x < 32) {
-        const double* L = A.fac + A.chol_off[j];
-        for (int p = 0; p < w; ++p) {
-          const double up = z[p] / L[p * w + p];
-          __syncwarp();
-          for (int q = p + 1 + threadIdx.x; q < w; q += 32) z[q] -= L[q * w + p] * up;
-          if (threadIdx.x == 0) z[p] = up;
-          __syncwarp();
+      const double* Li = A.linv + A.linv_off[j];
+      for (int q = threadIdx.x; q < w; q += T) {
+        const double* lq = Li + static_cast<int64_t>(q) * w;
+        double a0 = 0.0, a1 = 0.0;
+        int p = 0;
+        for (; p + 1 <= q; p += 2) {
+          a0 = fma(__ldg(lq + p), z[p], a0);
+          a1 = fma(__ldg(lq + p + 1), z[p + 1], a1);
         }
+        if (p <= q) a0 = fma(__ldg(lq + p), z[p], a0);
+        vj[r + q] = a0 + a1;
       }
-      __syncthreads();
-      for (int q = threadIdx.x; q < w; q += T) vj[r + q] = z[q];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -149,17 +132,17 @@ __global__ void __launch_bounds__(T) retained_kernel(ApplyLevelArgs A) {
     if (r == 0) continue;
     const int w = A.width[j];
     double* vj = A.v + A.offsets[j];
-    const int64_t c0 = A.cl_ptr[j], c1 = A.cl_ptr[j + 1];
-    // segment 0: own coupling C_j u_j; segment k: g_{i->j}[:r_j] u_i for the k-th close neighbour i
+    const int64_t k0 = A.in_ptr[j], k1 = A.in_ptr[j + 1];
+    // segment 0: own coupling C_j u_j; segment s > 0: the (s-1)-th contributing neighbour
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* part = rsm + warp * 2 * kWmax;
     double* ub = part + kWmax;
     for (int a = lane; a < r; a += 32) part[a] = 0.0;
     __syncwarp();
-    const int nseg = static_cast<int>(c1 - c0) + 1;
+    const int nseg = static_cast<int>(k1 - k0) + 1;
     for (int sgi = warp; sgi < nseg; sgi += kApplyWarps) {
       const double* g;
-      int wi, ri;
+      int wi;
       const double* ui;
       if (sgi == 0) {
         wi = w;
@@ -167,20 +150,23 @@ __global__ void __launch_bounds__(T) retained_kernel(ApplyLevelArgs A) {
         g = A.fac + A.g_off[j];
         ui = vj + r;
       } else {
-        const int i = A.cl_col[c0 + sgi - 1];
-        wi = A.width[i];
-        if (wi == 0) continue;
-        ri = A.rank[i];
-        g = A.fac + A.g_off[i] + static_cast<int64_t>(ri + close_roff(A, i, j)) * wi;
-        ui = A.v + A.offsets[i] + ri;
+        const int64_t k = k0 + sgi - 1;
+        wi = A.in_w[k];
+        g = A.fac + A.in_goff[k];
+        ui = A.v + A.in_uoff[k];
       }
       for (int p = lane; p < wi; p += 32) ub[p] = ui[p];
       __syncwarp();
       for (int a = lane; a < r; a += 32) {
         const double* ga = g + static_cast<int64_t>(a) * wi;
-        double acc = 0.0;
-        for (int p = 0; p < wi; ++p) acc += ga[p] * ub[p];
-        part[a] += acc;
+        double a0 = 0.0, a1 = 0.0;
+        int p = 0;
+        for (; p + 1 < wi; p += 2) {
+          a0 = fma(__ldg(ga + p), ub[p], a0);
+          a1 = fma(__ldg(ga + p + 1), ub[p + 1], a1);
+        }
+        if (p < wi) a0 = fma(__ldg(ga + p), ub[p], a0);
+        part[a] += a0 + a1;
       }
       __syncwarp();
     }
@@ -194,35 +180,31 @@ __global__ void __launch_bounds__(T) retained_kernel(ApplyLevelArgs A) {
   }
 }
 
-// Backward sweep, rows in descending order.
+// Backward sweep, rows in wave order.  Row j: wait for its dependencies t > j (w_t > 0),
+// s = v_j[r:] - G_j^T v (coupling rows against v_j[:r], neighbour rows against v_t), then
+// u_j = L_j^{-T} s.
 __global__ void __launch_bounds__(T) backward_kernel(ApplyLevelArgs A) {
   extern __shared__ double sb[];
   __shared__ long long s_t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (;;) {
     if (threadIdx.x == 0) s_t = static_cast<long long>(atomicAdd(A.ticket, 1ULL));
     __syncthreads();
     const long long tk = s_t;
     if (tk >= A.M) break;
     const int j = A.order[tk];
-    const int64_t c0 = A.cl_ptr[j], c1 = A.cl_ptr[j + 1];
-    if (threadIdx.x == 0) {
-      for (int64_t e = c1 - 1; e >= c0; --e) {
-        const int t = A.cl_col[e];
-        if (t <= j) break;
-        while (ld_acquire(A.flags + t) == 0) __nanosleep(32);
-      }
-      __threadfence();
-    }
+    for (int64_t k = A.dep_ptr[j] + threadIdx.x; k < A.dep_ptr[j + 1]; k += T)
+      while (ld_acquire(A.flags + A.dep_t[k]) == 0) __nanosleep(32);
+    __threadfence();
     __syncthreads();
     const int w = A.width[j];
     if (w > 0) {
       const int r = A.rank[j];
+      const int64_t c0 = A.cl_ptr[j], c1 = A.cl_ptr[j + 1];
       double* vj = A.v + A.offsets[j];
       const double* G = A.fac + A.g_off[j];
-      // s[q] = v_j[r+q] - sum_rows G[a][q] * v(a): warps over segments (coupling, then each neighbour),
-      // lanes over q so every G row is read coalesced
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      double* part = sb + kWmax + warp * kWmax;
+      double* part = sb + kWmax + warp * 2 * kWmax;
+      double* vbuf = part + kWmax;
       for (int q = lane; q < w; q += 32) part[q] = 0.0;
       __syncwarp();
       const int nseg = static_cast<int>(c1 - c0) + 1;
@@ -236,41 +218,303 @@ __global__ void __launch_bounds__(T) backward_kernel(ApplyLevelArgs A) {
           nt = r;
         } else {
           const int64_t e = c0 + sgi - 1;
-          const int t = A.cl_col[e];
-          nt = t > j ? A.bsz[t] : A.rank[t];
+          nt = A.cl_nt[e];
           rows = G + static_cast<int64_t>(r + A.cl_roff[e]) * w;
-          vt = A.v + A.offsets[t];
+          vt = A.v + A.offsets[A.cl_col[e]];
         }
-        for (int a = 0; a < nt; ++a) {
-          const double va = ldg(vt + a);
-          const double* ga = rows + static_cast<int64_t>(a) * w;
-          for (int q = lane; q < w; q += 32) part[q] += ga[q] * va;
+        // v_t staged with one coalesced load; rows of G read coalesced, 4 in flight per lane
+        for (int a = lane; a < nt; a += 32) vbuf[a] = ldg(vt + a);
+        __syncwarp();
+        for (int q = lane; q < w; q += 32) {
+          const double* gq = rows + q;
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int a = 0;
+          for (; a + 3 < nt; a += 4) {
+            a0 = fma(__ldg(gq + static_cast<int64_t>(a) * w), vbuf[a], a0);
+            a1 = fma(__ldg(gq + static_cast<int64_t>(a + 1) * w), vbuf[a + 1], a1);
+            a2 = fma(__ldg(gq + static_cast<int64_t>(a + 2) * w), vbuf[a + 2], a2);
+            a3 = fma(__ldg(gq + static_cast<int64_t>(a + 3) * w), vbuf[a + 3], a3);
+          }
+          for (; a < nt; ++a) a0 = fma(__ldg(gq + static_cast<int64_t>(a) * w), vbuf[a], a0);
+          part[q] += (a0 + a1) + (a2 + a3);
         }
+        __syncwarp();
       }
       __syncthreads();
       for (int q = threadIdx.x; q < w; q += T) {
         double acc = ldg(vj + r + q);
-        for (int k = 0; k < kApplyWarps; ++k) acc -= sb[kWmax + k * kWmax + q];
+        for (int k = 0; k < kApplyWarps; ++k) acc -= sb[kWmax + k * 2 * kWmax + q];
         sb[q] = acc;
       }
       __syncthreads();
-      if (threadIdx.x < 32) {
-        const double* L = A.fac + A.chol_off[j];
-        for (int q = w - 1; q >= 0; --q) {
-          const double uq = sb[q] / L[q * w + q];
-          __syncwarp();
-          for (int p = threadIdx.x; p < q; p += 32) sb[p] -= L[q * w + p] * uq;
-          if (threadIdx.x == 0) sb[q] = uq;
-          __syncwarp();
+      const double* Li = A.linv + A.linv_off[j];
+      for (int p = threadIdx.x; p < w; p += T) {
+        double a0 = 0.0, a1 = 0.0;
+        int q = p;
+        for (; q + 1 < w; q += 2) {
+          a0 = fma(__ldg(Li + static_cast<int64_t>(q) * w + p), sb[q], a0);
+          a1 = fma(__ldg(Li + static_cast<int64_t>(q + 1) * w + p), sb[q + 1], a1);
         }
+        if (q < w) a0 = fma(__ldg(Li + static_cast<int64_t>(q) * w + p), sb[q], a0);
+        vj[r + p] = a0 + a1;
       }
-      __syncthreads();
-      for (int q = threadIdx.x; q < w; q += T) vj[r + q] = sb[q];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
       atomicExch(A.flags + j, 1);
+    }
+  }
+}
+
+// ---- split-row sweeps (item = (row, part)) ----
+// Forward partial: sum over incoming entries [k0, k1) of g_{i->j}[r_j:, :] u_i -> scratch.
+// Forward finalize: z = v_j[r:] - sum of the row's partials (fixed order), u_j = L^{-1} z.
+__global__ void __launch_bounds__(T) forward_task_kernel(ApplyLevelArgs A) {
+  extern __shared__ double z[];
+  __shared__ long long s_item;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = static_cast<long long>(atomicAdd(A.ticket, 1ULL));
+    __syncthreads();
+    const long long it = s_item;
+    if (it >= A.n_items) break;
+    const int j = A.item_row[it], part0 = A.item_part[it];
+    const int64_t pp = A.part_ptr[j];
+    const int P = static_cast<int>(A.part_ptr[j + 1] - pp) - 1;
+    const int w = A.width[j], r = A.rank[j];
+    double* scr = A.scratch + A.scr_off[j];
+    const bool fused = part0 < 0;  // single-slice row: pull and finalize in one item
+    const int part = fused ? 0 : part0;
+    if (part < P) {
+      const int64_t k0 = A.part_b[pp + part], k1 = A.part_b[pp + part + 1];
+      for (int64_t k = k0 + threadIdx.x; k < k1; k += T)
+        while (ld_acquire(A.flags + A.in_src[k]) == 0) __nanosleep(32);
+      __threadfence();
+      __syncthreads();
+      double* pw = z + kWmax + warp * 2 * kWmax;
+      double* ub = pw + kWmax;
+      for (int q = lane; q < w; q += 32) pw[q] = 0.0;
+      for (int64_t k = k0 + warp; k < k1; k += kApplyWarps) {
+        const int wi = A.in_w[k];
+        const double* ui = A.v + A.in_uoff[k];
+        for (int p = lane; p < wi; p += 32) ub[p] = ldg(ui + p);
+        __syncwarp();
+        const double* g = A.fac + A.in_goff[k] + static_cast<int64_t>(r) * wi;
+        for (int q = lane; q < w; q += 32) {
+          const double* gq = g + static_cast<int64_t>(q) * wi;
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int p = 0;
+          for (; p + 3 < wi; p += 4) {
+            a0 = fma(__ldg(gq + p), ub[p], a0);
+            a1 = fma(__ldg(gq + p + 1), ub[p + 1], a1);
+            a2 = fma(__ldg(gq + p + 2), ub[p + 2], a2);
+            a3 = fma(__ldg(gq + p + 3), ub[p + 3], a3);
+          }
+          for (; p < wi; ++p) a0 = fma(__ldg(gq + p), ub[p], a0);
+          pw[q] += (a0 + a1) + (a2 + a3);
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      if (fused) {
+        double* vj = A.v + A.offsets[j];
+        for (int q = threadIdx.x; q < w; q += T) {
+          double acc = 0.0;
+          for (int k = 0; k < kApplyWarps; ++k) acc += z[kWmax + k * 2 * kWmax + q];
+          z[q] = ldg(vj + r + q) - acc;
+        }
+        __syncthreads();
+      } else {
+        for (int q = threadIdx.x; q < w; q += T) {
+          double acc = 0.0;
+          for (int k = 0; k < kApplyWarps; ++k) acc += z[kWmax + k * 2 * kWmax + q];
+          scr[static_cast<int64_t>(part) * w + q] = acc;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(A.parts_done + j, 1);
+        }
+        continue;
+      }
+    }
+    {
+      if (!fused) {
+        if (threadIdx.x == 0) {
+          while (ld_acquire(A.parts_done + j) < P) __nanosleep(32);
+          __threadfence();
+        }
+        __syncthreads();
+        double* vj = A.v + A.offsets[j];
+        for (int q = threadIdx.x; q < w; q += T) {
+          double acc = ldg(vj + r + q);
+          for (int k = 0; k < P; ++k) acc -= ldg(scr + static_cast<int64_t>(k) * w + q);
+          z[q] = acc;
+        }
+        __syncthreads();
+      }
+      double* vj = A.v + A.offsets[j];
+      const double* Li = A.linv + A.linv_off[j];
+      for (int q = threadIdx.x; q < w; q += T) {
+        const double* lq = Li + static_cast<int64_t>(q) * w;
+        double a0 = 0.0, a1 = 0.0;
+        int p = 0;
+        for (; p + 1 <= q; p += 2) {
+          a0 = fma(__ldg(lq + p), z[p], a0);
+          a1 = fma(__ldg(lq + p + 1), z[p + 1], a1);
+        }
+        if (p <= q) a0 = fma(__ldg(lq + p), z[p], a0);
+        vj[r + q] = a0 + a1;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicExch(A.flags + j, 1);
+      }
+    }
+  }
+}
+
+// Backward partial: segments [s0, s1) of row j (segment 0 = coupling rows against
+// v_j[:r], segment e > 0 = close entry e-1 rows against v_t) -> scratch.
+// Backward finalize: s = v_j[r:] - sum of partials, u_j = L^{-T} s.
+__global__ void __launch_bounds__(T) backward_task_kernel(ApplyLevelArgs A) {
+  extern __shared__ double sb[];
+  __shared__ long long s_item;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = static_cast<long long>(atomicAdd(A.ticket, 1ULL));
+    __syncthreads();
+    const long long it = s_item;
+    if (it >= A.n_items) break;
+    const int j = A.item_row[it], part0 = A.item_part[it];
+    const int64_t pp = A.part_ptr[j];
+    const int P = static_cast<int>(A.part_ptr[j + 1] - pp) - 1;
+    const int w = A.width[j], r = A.rank[j];
+    double* scr = A.scratch + A.scr_off[j];
+    const int64_t c0 = A.cl_ptr[j];
+    const bool fused = part0 < 0;  // single-slice row: pull and finalize in one item
+    const int part = fused ? 0 : part0;
+    if (part < P) {
+      const int s0 = static_cast<int>(A.part_b[pp + part]), s1 = static_cast<int>(A.part_b[pp + part + 1]);
+      for (int sgi = s0 + threadIdx.x; sgi < s1; sgi += T) {
+        if (sgi == 0) continue;
+        const int t = A.cl_col[c0 + sgi - 1];
+        if (t > j && A.width[t] > 0)
+          while (ld_acquire(A.flags + t) == 0) __nanosleep(32);
+      }
+      __threadfence();
+      __syncthreads();
+      double* vj = A.v + A.offsets[j];
+      const double* G = A.fac + A.g_off[j];
+      double* pw = sb + kWmax + warp * 2 * kWmax;
+      double* vbuf = pw + kWmax;
+      for (int q = lane; q < w; q += 32) pw[q] = 0.0;
+      __syncwarp();
+      for (int sgi = s0 + warp; sgi < s1; sgi += kApplyWarps) {
+        const double* rows;
+        const double* vt;
+        int nt;
+        if (sgi == 0) {
+          rows = G;
+          vt = vj;
+          nt = r;
+        } else {
+          const int64_t e = c0 + sgi - 1;
+          nt = A.cl_nt[e];
+          rows = G + static_cast<int64_t>(r + A.cl_roff[e]) * w;
+          vt = A.v + A.offsets[A.cl_col[e]];
+        }
+        for (int a = lane; a < nt; a += 32) vbuf[a] = ldg(vt + a);
+        __syncwarp();
+        for (int q = lane; q < w; q += 32) {
+          const double* gq = rows + q;
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int a = 0;
+          for (; a + 3 < nt; a += 4) {
+            a0 = fma(__ldg(gq + static_cast<int64_t>(a) * w), vbuf[a], a0);
+            a1 = fma(__ldg(gq + static_cast<int64_t>(a + 1) * w), vbuf[a + 1], a1);
+            a2 = fma(__ldg(gq + static_cast<int64_t>(a + 2) * w), vbuf[a + 2], a2);
+            a3 = fma(__ldg(gq + static_cast<int64_t>(a + 3) * w), vbuf[a + 3], a3);
+          }
+          for (; a < nt; ++a) a0 = fma(__ldg(gq + static_cast<int64_t>(a) * w), vbuf[a], a0);
+          pw[q] += (a0 + a1) + (a2 + a3);
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+      if (fused) {
+        for (int q = threadIdx.x; q < w; q += T) {
+          double acc = 0.0;
+          for (int k = 0; k < kApplyWarps; ++k) acc += sb[kWmax + k * 2 * kWmax + q];
+          sb[q] = ldg(vj + r + q) - acc;
+        }
+        __syncthreads();
+      } else {
+        for (int q = threadIdx.x; q < w; q += T) {
+          double acc = 0.0;
+          for (int k = 0; k < kApplyWarps; ++k) acc += sb[kWmax + k * 2 * kWmax + q];
+          scr[static_cast<int64_t>(part) * w + q] = acc;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(A.parts_done + j, 1);
+        }
+        continue;
+      }
+    }
+    {
+      double* vj = A.v + A.offsets[j];
+      if (!fused) {
+        if (threadIdx.x == 0) {
+          while (ld_acquire(A.parts_done + j) < P) __nanosleep(32);
+          __threadfence();
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < w; q += T) {
+          double acc = ldg(vj + r + q);
+          for (int k = 0; k < P; ++k) acc -= ldg(scr + static_cast<int64_t>(k) * w + q);
+          sb[q] = acc;
+        }
+        __syncthreads();
+      }
+      const double* Li = A.linv + A.linv_off[j];
+      for (int p = threadIdx.x; p < w; p += T) {
+        double a0 = 0.0, a1 = 0.0;
+        int q = p;
+        for (; q + 1 < w; q += 2) {
+          a0 = fma(__ldg(Li + static_cast<int64_t>(q) * w + p), sb[q], a0);
+          a1 = fma(__ldg(Li + static_cast<int64_t>(q + 1) * w + p), sb[q + 1], a1);
+        }
+        if (q < w) a0 = fma(__ldg(Li + static_cast<int64_t>(q) * w + p), sb[q], a0);
+        vj[r + p] = a0 + a1;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicExch(A.flags + j, 1);
+      }
+    }
+  }
+}
+
+// L^{-1} of each row's w x w pivot factor: thread per column, forward substitution.
+__global__ void pivot_inverse_kernel(int64_t M, const int* width, const double* fac, const int64_t* chol_off,
+                                     double* linv, const int64_t* linv_off) {
+  for (int64_t j = blockIdx.x; j < M; j += gridDim.x) {
+    const int w = width[j];
+    if (w == 0) continue;
+    const double* L = fac + chol_off[j];
+    double* X = linv + linv_off[j];
+    for (int c = threadIdx.x; c < w; c += blockDim.x) {
+      for (int q = 0; q < c; ++q) X[static_cast<int64_t>(q) * w + c] = 0.0;
+      for (int q = c; q < w; ++q) {
+        double acc = q == c ? 1.0 : 0.0;
+        for (int p = c; p < q; ++p) acc -= L[static_cast<int64_t>(q) * w + p] * X[static_cast<int64_t>(p) * w + c];
+        X[static_cast<int64_t>(q) * w + c] = acc / L[static_cast<int64_t>(q) * w + q];
+      }
     }
   }
 }
@@ -378,6 +622,18 @@ void launch_forward_sweep(const ApplyLevelArgs& a, int grid, cudaStream_t s) {
   forward_kernel<<<grid, T, kSweepSmem, s>>>(a);
 }
 
+void launch_forward_tasks(const ApplyLevelArgs& a, int grid, cudaStream_t s) {
+  if (a.n_items == 0) return;
+  note_launch();
+  forward_task_kernel<<<grid, T, kSweepSmem, s>>>(a);
+}
+
+void launch_backward_tasks(const ApplyLevelArgs& a, int grid, cudaStream_t s) {
+  if (a.n_items == 0) return;
+  note_launch();
+  backward_task_kernel<<<grid, T, kSweepSmem, s>>>(a);
+}
+
 void launch_forward_retained(const ApplyLevelArgs& a, cudaStream_t s) {
   if (a.M == 0) return;
   note_launch();
@@ -416,6 +672,13 @@ void launch_scatter(const double* src, const int64_t* idx, double* dst, int64_t 
     note_launch();
     scatter_kernel<<<static_cast<unsigned>((n + 255) / 256 < 65535 * 4 ? (n + 255) / 256 : 65535 * 4), 256, 0, s>>>(src, idx, dst, n);
   }
+}
+
+void launch_pivot_inverse(int64_t M, const int* width, const double* fac, const int64_t* chol_off, double* linv,
+                          const int64_t* linv_off, cudaStream_t s) {
+  if (M <= 0) return;
+  note_launch();
+  pivot_inverse_kernel<<<grid_for(M), 64, 0, s>>>(M, width, fac, chol_off, linv, linv_off);
 }
 
 void launch_dense_trmv(const double* L, const double* x, double* y, int64_t n, int trans, cudaStream_t s) {

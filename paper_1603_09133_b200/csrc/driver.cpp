@@ -862,19 +862,47 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     LF.d_basis_off = std::move(dcur.basis_off);
     LF.d_sigma_off = std::move(dcur.sigma_off);
     {
-      // wave orders of the apply's forward (deps: close i < j) and backward (deps: close t > j) sweeps
-      std::vector<int64_t> wf(static_cast<size_t>(cur.M), 0), wb(static_cast<size_t>(cur.M), 0);
-      for (int64_t j = 0; j < cur.M; ++j)
-        for (int64_t e = cur.cptr[static_cast<size_t>(j)]; e < cur.cptr[static_cast<size_t>(j + 1)]; ++e) {
-          const int i = cur.ccol[static_cast<size_t>(e)];
-          if (i < j) wf[static_cast<size_t>(j)] = std::max(wf[static_cast<size_t>(j)], wf[static_cast<size_t>(i)] + 1);
-        }
-      for (int64_t j = cur.M - 1; j >= 0; --j)
-        for (int64_t e = cur.cptr[static_cast<size_t>(j)]; e < cur.cptr[static_cast<size_t>(j + 1)]; ++e) {
+      // Apply pull lists: for row j every close neighbour i with w_i > 0 (ascending), the fac
+      // offset of g_{i->j} and of u_i in v; backward dependencies t > j with w_t > 0; rows of
+      // v_t read by the backward pull; pivot inverses.  Wave orders of both sweeps follow the
+      // same (refined) dependencies.
+      const int64_t M = cur.M;
+      std::vector<int64_t> in_ptr(static_cast<size_t>(M + 1), 0), in_goff, in_uoff, dep_ptr(static_cast<size_t>(M + 1), 0),
+          linv_off(static_cast<size_t>(M), 0);
+      std::vector<int> in_split(static_cast<size_t>(M), 0), in_src, in_w, dep_t, cl_nt(cur.ccol.size());
+      int64_t lo = 0;
+      for (int64_t j = 0; j < M; ++j) {
+        const size_t ju = static_cast<size_t>(j);
+        linv_off[ju] = lo;
+        lo += static_cast<int64_t>(LF.width[ju]) * LF.width[ju];
+        for (int64_t e = cur.cptr[ju]; e < cur.cptr[ju + 1]; ++e) {
           const int t = cur.ccol[static_cast<size_t>(e)];
-          if (t > j) wb[static_cast<size_t>(j)] = std::max(wb[static_cast<size_t>(j)], wb[static_cast<size_t>(t)] + 1);
+          const size_t tu = static_cast<size_t>(t);
+          cl_nt[static_cast<size_t>(e)] = t > j ? cur.bsz[tu] : LF.rank[tu];
+          if (LF.width[tu] == 0) continue;
+          const int64_t k = csr_find(cur.cptr, cur.ccol, t, static_cast<int>(j));
+          in_src.push_back(t);
+          in_goff.push_back(cur.g_off[tu] + static_cast<int64_t>(LF.rank[tu] + cur.croff[static_cast<size_t>(k)]) * LF.width[tu]);
+          in_w.push_back(LF.width[tu]);
+          in_uoff.push_back(cur.offsets[tu] + LF.rank[tu]);
+          if (t < j) ++in_split[ju];
+          if (t > j) dep_t.push_back(t);
         }
-      std::vector<int> of(static_cast<size_t>(cur.M)), ob(static_cast<size_t>(cur.M));
+        in_ptr[ju + 1] = static_cast<int64_t>(in_src.size());
+        dep_ptr[ju + 1] = static_cast<int64_t>(dep_t.size());
+      }
+      std::vector<int64_t> wf(static_cast<size_t>(M), 0), wb(static_cast<size_t>(M), 0);
+      for (int64_t j = 0; j < M; ++j)
+        for (int64_t k = in_ptr[static_cast<size_t>(j)]; k < in_ptr[static_cast<size_t>(j)] + in_split[static_cast<size_t>(j)]; ++k) {
+          const int i = in_src[static_cast<size_t>(k)];
+          wf[static_cast<size_t>(j)] = std::max(wf[static_cast<size_t>(j)], wf[static_cast<size_t>(i)] + 1);
+        }
+      for (int64_t j = M - 1; j >= 0; --j)
+        for (int64_t k = dep_ptr[static_cast<size_t>(j)]; k < dep_ptr[static_cast<size_t>(j + 1)]; ++k) {
+          const int t = dep_t[static_cast<size_t>(k)];
+          wb[static_cast<size_t>(j)] = std::max(wb[static_cast<size_t>(j)], wb[static_cast<size_t>(t)] + 1);
+        }
+      std::vector<int> of(static_cast<size_t>(M)), ob(static_cast<size_t>(M));
       std::iota(of.begin(), of.end(), 0);
       std::iota(ob.begin(), ob.end(), 0);
       std::stable_sort(of.begin(), of.end(), [&](int x, int y) { return wf[static_cast<size_t>(x)] < wf[static_cast<size_t>(y)]; });
@@ -883,6 +911,106 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       });
       LF.d_fwd_order.upload(of, s);
       LF.d_bwd_order.upload(ob, s);
+      LF.d_in_ptr.upload(in_ptr, s);
+      LF.d_in_split.upload(in_split, s);
+      LF.d_in_src.upload(in_src, s);
+      LF.d_in_goff.upload(in_goff, s);
+      LF.d_in_w.upload(in_w, s);
+      LF.d_in_uoff.upload(in_uoff, s);
+      LF.d_dep_ptr.upload(dep_ptr, s);
+      LF.d_dep_t.upload(dep_t, s);
+      LF.d_cl_nt.upload(cl_nt, s);
+      LF.d_linv_off.upload(linv_off, s);
+      // split-row task graphs: slices of ~kSlice doubles of factor data per partial task
+      {
+        constexpr int64_t kSlice = 4096;
+        auto build = [&](bool fwd, const std::vector<int64_t>& wave, DevArray<int64_t>& d_ptr, DevArray<int64_t>& d_b,
+                         DevArray<int64_t>& d_scr, DevArray<int>& d_irow, DevArray<int>& d_ipart, int64_t& n_items) {
+          std::vector<int64_t> ptr(static_cast<size_t>(M + 1), 0), bnd, scr(static_cast<size_t>(M), 0);
+          std::vector<int> P(static_cast<size_t>(M), 0);
+          int64_t so = 0;
+          for (int64_t j = 0; j < M; ++j) {
+            const size_t ju = static_cast<size_t>(j);
+            const int64_t w = LF.width[ju];
+            scr[ju] = so;
+            if (fwd) {
+              const int64_t k0 = in_ptr[ju], k1 = k0 + in_split[ju];
+              bnd.push_back(k0);
+              int64_t acc = 0;
+              for (int64_t k = k0; k < k1; ++k) {
+                acc += w * in_w[static_cast<size_t>(k)];
+                if (acc >= kSlice && k + 1 < k1) {
+                  bnd.push_back(k + 1);
+                  acc = 0;
+                }
+              }
+              if (k1 > k0) bnd.push_back(k1);
+            } else {
+              const int64_t nseg = 1 + cur.cptr[ju + 1] - cur.cptr[ju];
+              bnd.push_back(0);
+              int64_t acc = 0;
+              for (int64_t sg = 0; sg < nseg; ++sg) {
+                const int64_t rows = sg == 0 ? LF.rank[ju] : cl_nt[static_cast<size_t>(cur.cptr[ju] + sg - 1)];
+                acc += w * rows;
+                if (acc >= kSlice && sg + 1 < nseg) {
+                  bnd.push_back(sg + 1);
+                  acc = 0;
+                }
+              }
+              bnd.push_back(nseg);
+            }
+            ptr[ju + 1] = static_cast<int64_t>(bnd.size());
+            P[ju] = static_cast<int>(ptr[ju + 1] - ptr[ju]) - 1;
+            so += static_cast<int64_t>(P[ju]) * w;
+          }
+          // items in wave order: the wave's partial tasks, then its finalizes
+          std::vector<int> ord(static_cast<size_t>(M));
+          std::iota(ord.begin(), ord.end(), 0);
+          std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return wave[static_cast<size_t>(x)] < wave[static_cast<size_t>(y)]; });
+          std::vector<int> irow, ipart;
+          for (int64_t a0 = 0; a0 < M;) {
+            int64_t a1 = a0 + 1;
+            const int64_t wv = wave[static_cast<size_t>(ord[static_cast<size_t>(a0)])];
+            while (a1 < M && wave[static_cast<size_t>(ord[static_cast<size_t>(a1)])] == wv) ++a1;
+            // rows with a single slice are one fused item (part -1)
+            for (int pass = 0; pass < 2; ++pass)
+              for (int64_t a = a0; a < a1; ++a) {
+                const int j = ord[static_cast<size_t>(a)];
+                if (LF.width[static_cast<size_t>(j)] == 0) continue;
+                const bool fused = P[static_cast<size_t>(j)] == 1;
+                if (pass == 0) {
+                  if (fused) continue;
+                  for (int t = 0; t < P[static_cast<size_t>(j)]; ++t) {
+                    irow.push_back(j);
+                    ipart.push_back(t);
+                  }
+                } else {
+                  irow.push_back(j);
+                  ipart.push_back(fused ? -1 : P[static_cast<size_t>(j)]);
+                }
+              }
+            a0 = a1;
+          }
+          d_ptr.upload(ptr, s);
+          d_b.upload(bnd, s);
+          d_scr.upload(scr, s);
+          d_irow.upload(irow, s);
+          d_ipart.upload(ipart, s);
+          n_items = static_cast<int64_t>(irow.size());
+          LF.scratch_doubles = std::max(LF.scratch_doubles, so);
+        };
+        if (std::getenv("CE_PROFILE") && std::getenv("CE_PROFILE")[0] == '1') {
+          const int64_t nwf = M ? *std::max_element(wf.begin(), wf.end()) + 1 : 0;
+          const int64_t nwb = M ? *std::max_element(wb.begin(), wb.end()) + 1 : 0;
+          std::fprintf(stderr, "[ce-profile] level %zu apply waves: forward %lld backward %lld\n", li + 1,
+                       static_cast<long long>(nwf), static_cast<long long>(nwb));
+        }
+        build(true, wf, LF.d_fpart_ptr, LF.d_fpart_b, LF.d_fscr_off, LF.d_fitem_row, LF.d_fitem_part, LF.n_fitems);
+        build(false, wb, LF.d_bpart_ptr, LF.d_bpart_b, LF.d_bscr_off, LF.d_bitem_row, LF.d_bitem_part, LF.n_bitems);
+      }
+      LF.d_linv.alloc(static_cast<size_t>(std::max<int64_t>(lo, 1)));
+      launch_pivot_inverse(M, LF.d_width.p, LF.d_fac.p, LF.d_chol_off.p, LF.d_linv.p, LF.d_linv_off.p, s);
+      CE_CUDA(cudaGetLastError());
     }
 
     // stats (factorization.cpp:376-405) + §8d algorithmic counts
@@ -1001,7 +1129,11 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     eb += L.n_elim;
   }
   F->w_flags.alloc(static_cast<size_t>(mmax));
+  F->w_parts.alloc(static_cast<size_t>(mmax));
   F->w_ticket.alloc(1);
+  int64_t scr = 1;
+  for (const auto& L : F->levels) scr = std::max(scr, L.scratch_doubles);
+  F->w_scratch.alloc(static_cast<size_t>(scr));
   F->total_seconds = now_s() - t_start;
   return F.release();
 }
@@ -1027,12 +1159,27 @@ ApplyLevelArgs level_args(const Factor& f, const LevelFactor& L, double* v) {
   a.v = v;
   a.flags = f.w_flags.p;
   a.ticket = f.w_ticket.p;
+  a.in_ptr = L.d_in_ptr.p;
+  a.in_split = L.d_in_split.p;
+  a.in_src = L.d_in_src.p;
+  a.in_goff = L.d_in_goff.p;
+  a.in_w = L.d_in_w.p;
+  a.in_uoff = L.d_in_uoff.p;
+  a.dep_ptr = L.d_dep_ptr.p;
+  a.dep_t = L.d_dep_t.p;
+  a.cl_nt = L.d_cl_nt.p;
+  a.linv = L.d_linv.p;
+  a.linv_off = L.d_linv_off.p;
+  a.scratch = f.w_scratch.p;
+  a.parts_done = f.w_parts.p;
   return a;
 }
 }  // namespace
 
 void apply_device(const Factor& f, const double* d_b, double* d_x, cudaStream_t s) {
   const int grid = f.ctx->sm_count * 8;
+  static const bool aprof = std::getenv("CE_PROFILE") && std::getenv("CE_PROFILE")[0] == '1';
+  std::vector<Events> evs(aprof ? 2 * f.levels.size() : 0);
   double* active = f.w_active.p;
   double* v = f.w_v.p;
   CE_CUDA(cudaMemcpyAsync(active, d_b, static_cast<size_t>(f.n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -1043,8 +1190,16 @@ void apply_device(const Factor& f, const double* d_b, double* d_x, cudaStream_t 
     launch_basis_apply(a, 1, s);
     CE_CUDA(cudaMemsetAsync(f.w_flags.p, 0, static_cast<size_t>(L.M) * sizeof(int), s));
     CE_CUDA(cudaMemsetAsync(f.w_ticket.p, 0, sizeof(unsigned long long), s));
-    a.order = L.d_fwd_order.p;
-    launch_forward_sweep(a, static_cast<int>(std::min<int64_t>(grid, L.M)), s);
+    CE_CUDA(cudaMemsetAsync(f.w_parts.p, 0, static_cast<size_t>(L.M) * sizeof(int), s));
+    a.item_row = L.d_fitem_row.p;
+    a.item_part = L.d_fitem_part.p;
+    a.n_items = L.n_fitems;
+    a.part_ptr = L.d_fpart_ptr.p;
+    a.part_b = L.d_fpart_b.p;
+    a.scr_off = L.d_fscr_off.p;
+    if (aprof) CE_CUDA(cudaEventRecord(evs[2 * l].a, s));
+    launch_forward_tasks(a, static_cast<int>(std::min<int64_t>(grid, std::max<int64_t>(L.n_fitems, 1))), s);
+    if (aprof) CE_CUDA(cudaEventRecord(evs[2 * l].b, s));
     launch_forward_retained(a, s);
     launch_gather(v, L.d_elim_gather.p, f.w_elim.p + f.elim_base[l], L.n_elim, s);
     launch_gather(v, L.d_kept_gather.p, active, L.n_kept, s);
@@ -1061,13 +1216,27 @@ void apply_device(const Factor& f, const double* d_b, double* d_x, cudaStream_t 
     ApplyLevelArgs a = level_args(f, L, v);
     CE_CUDA(cudaMemsetAsync(f.w_flags.p, 0, static_cast<size_t>(L.M) * sizeof(int), s));
     CE_CUDA(cudaMemsetAsync(f.w_ticket.p, 0, sizeof(unsigned long long), s));
-    a.order = L.d_bwd_order.p;
-    launch_backward_sweep(a, static_cast<int>(std::min<int64_t>(grid, L.M)), s);
+    CE_CUDA(cudaMemsetAsync(f.w_parts.p, 0, static_cast<size_t>(L.M) * sizeof(int), s));
+    a.item_row = L.d_bitem_row.p;
+    a.item_part = L.d_bitem_part.p;
+    a.n_items = L.n_bitems;
+    a.part_ptr = L.d_bpart_ptr.p;
+    a.part_b = L.d_bpart_b.p;
+    a.scr_off = L.d_bscr_off.p;
+    if (aprof) CE_CUDA(cudaEventRecord(evs[2 * l + 1].a, s));
+    launch_backward_tasks(a, static_cast<int>(std::min<int64_t>(grid, std::max<int64_t>(L.n_bitems, 1))), s);
+    if (aprof) CE_CUDA(cudaEventRecord(evs[2 * l + 1].b, s));
     launch_basis_apply(a, 0, s);
     CE_CUDA(cudaMemcpyAsync(active, v, static_cast<size_t>(L.dim) * sizeof(double), cudaMemcpyDeviceToDevice, s));
   }
   CE_CUDA(cudaMemcpyAsync(d_x, active, static_cast<size_t>(f.n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
   CE_CUDA(cudaGetLastError());
+  if (aprof) {
+    CE_CUDA(cudaStreamSynchronize(s));
+    for (size_t l = 0; l < f.levels.size(); ++l)
+      std::fprintf(stderr, "[ce-profile] apply level %zu: forward %.3f ms, backward %.3f ms (M=%lld)\n", l + 1,
+                   1e3 * evs[2 * l].seconds(), 1e3 * evs[2 * l + 1].seconds(), static_cast<long long>(f.levels[l].M));
+  }
 }
 
 // Validation tools (factorization.cpp:170-257) on the device.

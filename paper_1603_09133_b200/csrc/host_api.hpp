@@ -152,6 +152,14 @@ struct LevelFactor {
   DevArray<double> d_fac, d_basis, d_sigma;
   DevArray<int64_t> d_elim_gather, d_kept_gather;
   DevArray<int> d_fwd_order, d_bwd_order;
+  // apply pull lists (apply.cu) and pivot inverses
+  DevArray<int64_t> d_in_ptr, d_in_goff, d_in_uoff, d_dep_ptr, d_linv_off;
+  DevArray<int> d_in_split, d_in_src, d_in_w, d_dep_t, d_cl_nt;
+  DevArray<double> d_linv;
+  // split-row task graphs of the apply sweeps (forward f / backward b)
+  DevArray<int64_t> d_fpart_ptr, d_fpart_b, d_fscr_off, d_bpart_ptr, d_bpart_b, d_bscr_off;
+  DevArray<int> d_fitem_row, d_fitem_part, d_bitem_row, d_bitem_part;
+  int64_t n_fitems = 0, n_bitems = 0, scratch_doubles = 0;
   // stats
   int64_t pattern_blocks = 0, shift_retries = 0, max_far = 0, max_close = 0, n_waves = 0, n_items = 0;
   double seconds = 0.0, sweep_seconds = 0.0, alg_bytes = 0.0, alg_flops = 0.0;
@@ -172,6 +180,8 @@ struct Factor {
   mutable std::vector<int64_t> elim_base;
   mutable DevArray<int> w_flags;
   mutable DevArray<unsigned long long> w_ticket;
+  mutable DevArray<double> w_scratch;  // apply partial sums
+  mutable DevArray<int> w_parts;       // apply per-row finished partial tasks
   mutable DevArray<double> w_host_stage;
 };
 

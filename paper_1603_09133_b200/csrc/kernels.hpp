@@ -161,9 +161,36 @@ struct ApplyLevelArgs {
   int* flags;
   const int* order;  // sweep order (wave order of the forward / backward DAG)
   unsigned long long* ticket;
+  // host-built pull lists (no close-list searches on the device)
+  const int64_t* in_ptr;    // per row j: range of its contributing close neighbours i (w_i > 0), ascending i
+  const int* in_split;      // per row j: number of those with i < j (the forward sweep's dependencies)
+  const int* in_src;        // i
+  const int64_t* in_goff;   // fac offset of g_{i->j} (b_j rows x w_i)
+  const int* in_w;          // w_i
+  const int64_t* in_uoff;   // v offset of u_i (offsets[i] + r_i)
+  const int64_t* dep_ptr;   // per row j: backward-sweep dependencies t > j (w_t > 0)
+  const int* dep_t;
+  const int* cl_nt;         // per close entry (j, t): rows of v_t read by the backward pull
+  const double* linv;       // per row: L^{-1} (w x w, row-major, lower)
+  const int64_t* linv_off;
+  // split-row task graph of the sweeps: items (row, part) in wave order; part < P_j is a
+  // partial pull over a slice of the row's inputs, part == P_j the row's finalize
+  const int* item_row;
+  const int* item_part;
+  int64_t n_items;
+  const int64_t* part_ptr;  // per row: range into part_b (P_j + 1 boundaries)
+  const int64_t* part_b;    // slice boundaries (forward: in_* entries; backward: segments)
+  const int64_t* scr_off;   // per row: offset of its P_j x w partial sums in scratch
+  double* scratch;
+  int* parts_done;          // per row: finished partial tasks
 };
+// L^{-1} of every row's pivot factor (apply sweeps multiply instead of substituting).
+void launch_pivot_inverse(int64_t M, const int* width, const double* fac, const int64_t* chol_off, double* linv,
+                          const int64_t* linv_off, cudaStream_t s);
 void launch_basis_apply(const ApplyLevelArgs& a, int transpose, cudaStream_t s);
 void launch_forward_sweep(const ApplyLevelArgs& a, int grid, cudaStream_t s);
+void launch_forward_tasks(const ApplyLevelArgs& a, int grid, cudaStream_t s);
+void launch_backward_tasks(const ApplyLevelArgs& a, int grid, cudaStream_t s);
 void launch_forward_retained(const ApplyLevelArgs& a, cudaStream_t s);
 void launch_backward_sweep(const ApplyLevelArgs& a, int grid, cudaStream_t s);
 // operator tool (apply_operator) pieces
