@@ -294,6 +294,8 @@ def run_product(args):
             "config": {"workload": workload_name(args.cfg, args.grid), "cfg": args.cfg, "n": n,
                        "parallelism": f"replicas x{world}", "l2": "inputs > L2 (A is %.2f GB)" % (host_a.values.nbytes / 1e9)},
             "factor_ms": 1e3 * fac_total / args.steps, "pcg_solve_ms": 1e3 * (step_total - fac_total) / args.steps,
+            "factor_ms_steps": [round(1e3 * r["fac"], 1) for r in recs],
+            "pcg_ms_steps": [round(1e3 * r["pcg"], 1) for r in recs],
             "pcg_iterations": recs[-1]["its"], "pcg_true_residual": recs[-1]["resid"], "pcg_converged": recs[-1]["conv"],
             "levels": recs[-1]["levels"], "tail_dim": recs[-1]["tail"],
             "roofline": {"bound": bound, "kernel": "level sweep (compress+eliminate), summed over levels",

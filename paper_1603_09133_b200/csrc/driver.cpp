@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <memory>
 #include <numeric>
 #include <sstream>
@@ -119,17 +120,15 @@ int64_t csr_find(const std::vector<int64_t>& ptr, const std::vector<int>& col, i
 }  // namespace
 
 // ---------------------------------------------------------------- planner
-LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vector<int> bcol) {
+// Symbolic part of a level plan (block sizes not needed): squared pattern, entry kinds,
+// stored-slot numbering, close lists and the wave order of the row DAG.  Runs on a host
+// thread for level l+1 while level l sweeps on the device (speculating that every group
+// of level l keeps a nonzero rank).
+LevelPlan plan_symbolic(int64_t M, std::vector<int64_t> bptr, std::vector<int> bcol) {
   LevelPlan P;
-  const int64_t M = static_cast<int64_t>(bsz.size());
   P.M = M;
-  P.bsz = std::move(bsz);
   P.bptr = std::move(bptr);
   P.bcol = std::move(bcol);
-  P.offsets.assign(static_cast<size_t>(M + 1), 0);
-  for (int64_t i = 0; i < M; ++i) P.offsets[static_cast<size_t>(i + 1)] = P.offsets[static_cast<size_t>(i)] + P.bsz[static_cast<size_t>(i)];
-  P.dim = P.offsets.back();
-  for (int b : P.bsz) P.bmax = std::max(P.bmax, b);
   for (int64_t i = 0; i < M; ++i)
     for (int64_t k = P.bptr[static_cast<size_t>(i)]; k < P.bptr[static_cast<size_t>(i + 1)]; ++k)
       if (P.bcol[static_cast<size_t>(k)] <= i) ++P.lower_blocks;
@@ -146,7 +145,56 @@ LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vecto
       if (j <= i) P.sslot[static_cast<size_t>(e)] = slot++;
     }
   P.nslots = slot;
-  P.slot_off.assign(static_cast<size_t>(slot), 0);
+  for (int64_t i = 0; i < M; ++i)
+    for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e) {
+      const int j = P.scol[static_cast<size_t>(e)];
+      if (j <= i) continue;
+      P.sslot[static_cast<size_t>(e)] = P.sslot[static_cast<size_t>(csr_find(P.sptr, P.scol, j, static_cast<int>(i)))];
+    }
+
+  P.cptr.assign(static_cast<size_t>(M + 1), 0);
+  for (int64_t i = 0; i < M; ++i) {
+    for (int64_t k = P.bptr[static_cast<size_t>(i)]; k < P.bptr[static_cast<size_t>(i + 1)]; ++k) {
+      const int t = P.bcol[static_cast<size_t>(k)];
+      if (t == i) continue;
+      P.ccol.push_back(t);
+    }
+    P.cptr[static_cast<size_t>(i + 1)] = static_cast<int64_t>(P.ccol.size());
+    P.cmax = std::max<int64_t>(P.cmax, static_cast<int64_t>(P.cptr[static_cast<size_t>(i + 1)] - P.cptr[static_cast<size_t>(i)]));
+  }
+  P.sdiag.resize(static_cast<size_t>(M));
+  for (int64_t i = 0; i < M; ++i) P.sdiag[static_cast<size_t>(i)] = csr_find(P.sptr, P.scol, i, static_cast<int>(i));
+  // Wave (topological) order of the dependency DAG: row j depends on every i < j in sq(j)
+  // (SURVEY.md A.2).  Items are issued in this order, so the ticket window always holds
+  // the current wavefront instead of a run of consecutive (mutually dependent) rows.
+  P.wave.assign(static_cast<size_t>(M), 0);
+  for (int64_t j = 0; j < M; ++j) {
+    int64_t w = 0;
+    for (int64_t e = P.sptr[static_cast<size_t>(j)]; e < P.sptr[static_cast<size_t>(j + 1)]; ++e) {
+      const int i = P.scol[static_cast<size_t>(e)];
+      if (i >= j) break;
+      w = std::max(w, P.wave[static_cast<size_t>(i)] + 1);
+    }
+    P.wave[static_cast<size_t>(j)] = w;
+    P.n_waves = std::max(P.n_waves, w + 1);
+  }
+  P.order.resize(static_cast<size_t>(M));
+  std::iota(P.order.begin(), P.order.end(), 0);
+  std::stable_sort(P.order.begin(), P.order.end(),
+                   [&](int x, int y) { return P.wave[static_cast<size_t>(x)] < P.wave[static_cast<size_t>(y)]; });
+  return P;
+}
+
+// Numeric part: everything that depends on the block sizes.
+void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
+  const int64_t M = P.M;
+  P.bsz = std::move(bsz);
+  P.offsets.assign(static_cast<size_t>(M + 1), 0);
+  for (int64_t i = 0; i < M; ++i) P.offsets[static_cast<size_t>(i + 1)] = P.offsets[static_cast<size_t>(i)] + P.bsz[static_cast<size_t>(i)];
+  P.dim = P.offsets.back();
+  P.bmax = 0;
+  for (int b : P.bsz) P.bmax = std::max(P.bmax, b);
+  P.slot_off.assign(static_cast<size_t>(P.nslots), 0);
   int64_t off = 0;
   for (int64_t i = 0; i < M; ++i)
     for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e) {
@@ -156,28 +204,17 @@ LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vecto
       off += static_cast<int64_t>(P.bsz[static_cast<size_t>(i)]) * P.bsz[static_cast<size_t>(j)];
     }
   P.store_doubles = off;
-  for (int64_t i = 0; i < M; ++i)
-    for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e) {
-      const int j = P.scol[static_cast<size_t>(e)];
-      if (j <= i) continue;
-      P.sslot[static_cast<size_t>(e)] = P.sslot[static_cast<size_t>(csr_find(P.sptr, P.scol, j, static_cast<int>(i)))];
-    }
-
-  P.cptr.assign(static_cast<size_t>(M + 1), 0);
   P.csum.assign(static_cast<size_t>(M), 0);
   P.fsum.assign(static_cast<size_t>(M), 0);
+  P.croff.assign(P.ccol.size(), 0);
+  P.fmax = 0;
   for (int64_t i = 0; i < M; ++i) {
     int64_t c = 0;
-    for (int64_t k = P.bptr[static_cast<size_t>(i)]; k < P.bptr[static_cast<size_t>(i + 1)]; ++k) {
-      const int t = P.bcol[static_cast<size_t>(k)];
-      if (t == i) continue;
-      P.ccol.push_back(t);
-      P.croff.push_back(static_cast<int>(c));
-      c += P.bsz[static_cast<size_t>(t)];
+    for (int64_t k = P.cptr[static_cast<size_t>(i)]; k < P.cptr[static_cast<size_t>(i + 1)]; ++k) {
+      P.croff[static_cast<size_t>(k)] = static_cast<int>(c);
+      c += P.bsz[static_cast<size_t>(P.ccol[static_cast<size_t>(k)])];
     }
     P.csum[static_cast<size_t>(i)] = c;
-    P.cptr[static_cast<size_t>(i + 1)] = static_cast<int64_t>(P.ccol.size());
-    P.cmax = std::max<int64_t>(P.cmax, static_cast<int64_t>(P.cptr[static_cast<size_t>(i + 1)] - P.cptr[static_cast<size_t>(i)]));
     int64_t f = 0;
     for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e)
       if (P.skind[static_cast<size_t>(e)] == 2) f += P.bsz[static_cast<size_t>(P.scol[static_cast<size_t>(e)])];
@@ -275,7 +312,6 @@ LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vecto
     P.sboff.resize(nnz);
     P.sbsz.resize(nnz);
     P.sroff.assign(nnz, -1);
-    P.sdiag.resize(static_cast<size_t>(M));
     P.target.resize(static_cast<size_t>(M));
     P.leaf_ptr.assign(static_cast<size_t>(M + 1), 0);
     P.strip_ptr.assign(static_cast<size_t>(M + 1), 0);
@@ -289,7 +325,6 @@ LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vecto
         const int j = P.scol[eu];
         P.sboff[eu] = P.slot_off[static_cast<size_t>(P.sslot[eu])];
         P.sbsz[eu] = P.bsz[static_cast<size_t>(j)];
-        if (j == i) P.sdiag[iu] = e;
         if (P.skind[eu] == 1) {
           const int64_t k = csr_find(P.cptr, P.ccol, i, j);
           P.sroff[eu] = P.croff[static_cast<size_t>(k)];
@@ -312,25 +347,9 @@ LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vecto
       P.strip_ptr[iu + 1] = static_cast<int64_t>(P.strip_e.size());
     }
   }
-  // Wave (topological) order of the dependency DAG: row j depends on every i < j in sq(j)
-  // (SURVEY.md A.2).  Items are issued in this order, so the ticket window always holds
-  // the current wavefront instead of a run of consecutive (mutually dependent) rows.
+  // ticket order of the row tasks (wave order from the symbolic plan)
   {
-    std::vector<int64_t> wave(static_cast<size_t>(M), 0);
-    for (int64_t j = 0; j < M; ++j) {
-      int64_t w = 0;
-      for (int64_t e = P.sptr[static_cast<size_t>(j)]; e < P.sptr[static_cast<size_t>(j + 1)]; ++e) {
-        const int i = P.scol[static_cast<size_t>(e)];
-        if (i >= j) break;
-        w = std::max(w, wave[static_cast<size_t>(i)] + 1);
-      }
-      wave[static_cast<size_t>(j)] = w;
-      P.n_waves = std::max(P.n_waves, w + 1);
-    }
-    P.order.resize(static_cast<size_t>(M));
-    std::iota(P.order.begin(), P.order.end(), 0);
-    std::stable_sort(P.order.begin(), P.order.end(),
-                     [&](int x, int y) { return wave[static_cast<size_t>(x)] < wave[static_cast<size_t>(y)]; });
+    const std::vector<int64_t>& wave = P.wave;
     int64_t it = 0;
     for (int64_t k = 0; k < M; ++k) {
       P.item_start[static_cast<size_t>(k)] = it;
@@ -378,6 +397,11 @@ LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vecto
   P.fac_doubles = fo;
   P.basis_doubles = bo;
   P.sigma_doubles = so;
+}
+
+LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vector<int> bcol) {
+  LevelPlan P = plan_symbolic(static_cast<int64_t>(bsz.size()), std::move(bptr), std::move(bcol));
+  plan_numeric(P, std::move(bsz));
   return P;
 }
 
@@ -591,6 +615,31 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       d_forced.upload(fr, s);
     }
 
+    // speculative symbolic plan of the next level on a host thread (assumes every group
+    // keeps a nonzero rank; checked after the sweep, recomputed if not)
+    std::future<LevelPlan> spec = std::async(std::launch::async, [&cur, &cur_groups]() {
+      const int64_t ng = static_cast<int64_t>(cur_groups.size());
+      std::vector<int64_t> gof(static_cast<size_t>(cur.M), 0);
+      for (int64_t g = 0; g < ng; ++g)
+        for (int64_t b : cur_groups[static_cast<size_t>(g)]) gof[static_cast<size_t>(b)] = g;
+      std::vector<int64_t> nptr(static_cast<size_t>(ng + 1), 0), mark(static_cast<size_t>(ng), -1);
+      std::vector<int> ncol, row;
+      for (int64_t g = 0; g < ng; ++g) {
+        row.clear();
+        for (int64_t b : cur_groups[static_cast<size_t>(g)])
+          for (int64_t e = cur.sptr[static_cast<size_t>(b)]; e < cur.sptr[static_cast<size_t>(b + 1)]; ++e) {
+            const int64_t h = gof[static_cast<size_t>(cur.scol[static_cast<size_t>(e)])];
+            if (mark[static_cast<size_t>(h)] == g) continue;
+            mark[static_cast<size_t>(h)] = g;
+            row.push_back(static_cast<int>(h));
+          }
+        std::sort(row.begin(), row.end());
+        ncol.insert(ncol.end(), row.begin(), row.end());
+        nptr[static_cast<size_t>(g + 1)] = static_cast<int64_t>(ncol.size());
+      }
+      return plan_symbolic(ng, std::move(nptr), std::move(ncol));
+    });
+
     SweepArgs a{};
     a.dbg = std::getenv("CE_DBG") ? std::atoi(std::getenv("CE_DBG")) : 0;
     a.M = cur.M;
@@ -753,7 +802,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     const int64_t nM = static_cast<int64_t>(nbsz.size());
     std::vector<int64_t> nptr(static_cast<size_t>(nM + 1), 0);
     std::vector<int> ncol;
-    {
+    if (nM != ng) {  // some group died: the speculative plan does not apply
       std::vector<int64_t> mark(static_cast<size_t>(ng), -1);
       std::vector<int> row;
       for (int64_t g = 0; g < ng; ++g) {
@@ -797,7 +846,13 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     const double h_t2 = now_s();
     double h_t3 = h_t2;
     if (nM > 0) {
-      next = plan_level(nbsz, nptr, ncol);
+      LevelPlan sp = spec.get();
+      if (nM == ng) {
+        next = std::move(sp);
+        plan_numeric(next, nbsz);
+      } else {
+        next = plan_level(nbsz, nptr, ncol);
+      }
       h_t3 = now_s();
       dnext.upload(next, s);
       if (nstore.n < static_cast<size_t>(next.store_doubles)) nstore.alloc(static_cast<size_t>(next.store_doubles));
@@ -861,6 +916,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     LF.d_g_off = std::move(dcur.g_off);
     LF.d_basis_off = std::move(dcur.basis_off);
     LF.d_sigma_off = std::move(dcur.sigma_off);
+    const double h_ta = now_s();
     {
       // Apply pull lists: for row j every close neighbour i with w_i > 0 (ascending), the fac
       // offset of g_{i->j} and of u_i in v; backward dependencies t > j with w_t > 0; rows of
@@ -1013,6 +1069,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       CE_CUDA(cudaGetLastError());
     }
 
+    const double h_tb = now_s();
     // stats (factorization.cpp:376-405) + §8d algorithmic counts
     {
       std::vector<int64_t> pend(static_cast<size_t>(cur.M), 0);
@@ -1062,7 +1119,11 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       if (slot_of_group[g] >= 0) next_alive[g] = alive[static_cast<size_t>(slot_of_group[g])];
     alive_map = std::move(next_alive);
     F->levels.push_back(std::move(LF));
+    if (std::getenv("CE_PROFILE") && std::getenv("CE_PROFILE")[0] == '1')
+      std::fprintf(stderr, "[ce-profile] level %zu host: apply lists %.1f ms, stats+rest %.1f ms, iteration %.1f ms\n", li + 1,
+                   1e3 * (h_tb - h_ta), 1e3 * (now_s() - h_tb), 1e3 * (now_s() - h_t0));
 
+    if (spec.valid()) spec.wait();  // the speculative planner reads `cur`
     cur = std::move(next);
     dcur = std::move(dnext);
     std::swap(store, nstore);

@@ -121,6 +121,7 @@ struct LevelPlan {
   int64_t fac_doubles = 0, basis_doubles = 0, sigma_doubles = 0;
   std::vector<int64_t> item_start;   // by position in `order`
   std::vector<int> order;            // rows in wave (topological) order of the sq-DAG
+  std::vector<int64_t> wave;         // wave index of every row
   std::vector<int> item_row, item_part;  // ticket -> (row, task index within the row)
   std::vector<int> nA1, nA3, nB;     // per-row task counts (sweep.cu header)
   std::vector<int64_t> pan_ptr, rs_off;
