@@ -185,8 +185,12 @@ int64_t ce_launch_count(void) { return ceg::launch_count(); }
 
 void ce_ctx_destroy(ce_ctx* ctx) {
   if (!ctx) return;
-  if (ctx->ctx.stream) cudaStreamDestroy(ctx->ctx.stream);
+  if (ctx->ctx.stream) {
+    cudaStreamSynchronize(ctx->ctx.stream);
+    cudaStreamDestroy(ctx->ctx.stream);
+  }
   delete ctx;
+  ceg::pool_trim();  // cached device blocks go back to the driver with the last context
 }
 
 int ce_matrix_upload(ce_ctx* ctx, const ce_csb_host* a, ce_matrix** out) {

@@ -10,6 +10,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <future>
+#include <map>
+#include <mutex>
 #include <memory>
 #include <numeric>
 #include <sstream>
@@ -58,6 +60,77 @@ const Thresholds& thresholds() {
   static const Thresholds t;
   return t;
 }
+
+}  // namespace
+
+// ---- caching device allocator (host_api.hpp) ----
+namespace {
+struct Pool {
+  std::mutex mu;
+  std::multimap<size_t, std::pair<int, void*>> free_blocks;  // rounded bytes -> (device, ptr)
+};
+Pool& pool() {
+  static Pool* p = new Pool();  // intentionally leaked: blocks may be released during static destruction
+  return *p;
+}
+size_t pool_round(size_t bytes) {
+  if (bytes <= 4096) return 4096;
+  size_t g = size_t{1} << (63 - __builtin_clzll(bytes));  // power of two <= bytes
+  g = std::max<size_t>(g / 8, 4096);                       // 12.5% granularity
+  return (bytes + g - 1) / g * g;
+}
+}  // namespace
+
+void* pool_alloc(size_t bytes) {
+  const size_t rb = pool_round(bytes);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    Pool& P = pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    for (auto it = P.free_blocks.lower_bound(rb); it != P.free_blocks.end() && it->first <= rb + rb / 4; ++it)
+      if (it->second.first == dev) {
+        void* p = it->second.second;
+        P.free_blocks.erase(it);
+        return p;
+      }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, rb);
+  if (e == cudaErrorMemoryAllocation) {  // drop the cache and retry once
+    cudaGetLastError();
+    pool_trim();
+    e = cudaMalloc(&p, rb);
+  }
+  CE_CUDA(e);
+  return p;
+}
+
+void pool_free(void* p, size_t bytes) {
+  if (!p) return;
+  int dev = 0;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) == cudaSuccess) dev = at.device;
+  else cudaGetLastError();
+  Pool& P = pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  P.free_blocks.emplace(pool_round(bytes), std::make_pair(dev, p));
+}
+
+void pool_trim() {
+  Pool& P = pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& kv : P.free_blocks) {
+    cudaSetDevice(kv.second.first);
+    cudaFree(kv.second.second);
+  }
+  P.free_blocks.clear();
+  cudaSetDevice(cur);
+}
+
+namespace {
 
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -405,6 +478,174 @@ LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vecto
   return P;
 }
 
+// Apply pull lists, task graphs and pivot inverses of one completed level (host loops +
+// uploads on the context stream).  Runs on a host thread while the next level sweeps.
+void build_apply_lists(LevelFactor& LF, size_t li, cudaStream_t main_stream) {
+  // own non-blocking stream: pageable uploads on the main stream would wait behind the
+  // next level's sweep kernel
+  (void)main_stream;
+  cudaStream_t s = nullptr;
+  CE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  } guard{s};
+  {
+    // Apply pull lists: for row j every close neighbour i with w_i > 0 (ascending), the fac
+    // offset of g_{i->j} and of u_i in v; backward dependencies t > j with w_t > 0; rows of
+    // v_t read by the backward pull; pivot inverses.  Wave orders of both sweeps follow the
+    // same (refined) dependencies.
+    const int64_t M = LF.M;
+    std::vector<int64_t> in_ptr(static_cast<size_t>(M + 1), 0), in_goff, in_uoff, dep_ptr(static_cast<size_t>(M + 1), 0),
+        linv_off(static_cast<size_t>(M), 0);
+    std::vector<int> in_split(static_cast<size_t>(M), 0), in_src, in_w, dep_t, cl_nt(LF.ccol.size());
+    int64_t lo = 0;
+    for (int64_t j = 0; j < M; ++j) {
+      const size_t ju = static_cast<size_t>(j);
+      linv_off[ju] = lo;
+      lo += static_cast<int64_t>(LF.width[ju]) * LF.width[ju];
+      for (int64_t e = LF.cptr[ju]; e < LF.cptr[ju + 1]; ++e) {
+        const int t = LF.ccol[static_cast<size_t>(e)];
+        const size_t tu = static_cast<size_t>(t);
+        cl_nt[static_cast<size_t>(e)] = t > j ? LF.bsz[tu] : LF.rank[tu];
+        if (LF.width[tu] == 0) continue;
+        const int64_t k = csr_find(LF.cptr, LF.ccol, t, static_cast<int>(j));
+        in_src.push_back(t);
+        in_goff.push_back(LF.g_off[tu] + static_cast<int64_t>(LF.rank[tu] + LF.croff[static_cast<size_t>(k)]) * LF.width[tu]);
+        in_w.push_back(LF.width[tu]);
+        in_uoff.push_back(LF.offsets[tu] + LF.rank[tu]);
+        if (t < j) ++in_split[ju];
+        if (t > j) dep_t.push_back(t);
+      }
+      in_ptr[ju + 1] = static_cast<int64_t>(in_src.size());
+      dep_ptr[ju + 1] = static_cast<int64_t>(dep_t.size());
+    }
+    std::vector<int64_t> wf(static_cast<size_t>(M), 0), wb(static_cast<size_t>(M), 0);
+    for (int64_t j = 0; j < M; ++j)
+      for (int64_t k = in_ptr[static_cast<size_t>(j)]; k < in_ptr[static_cast<size_t>(j)] + in_split[static_cast<size_t>(j)]; ++k) {
+        const int i = in_src[static_cast<size_t>(k)];
+        wf[static_cast<size_t>(j)] = std::max(wf[static_cast<size_t>(j)], wf[static_cast<size_t>(i)] + 1);
+      }
+    for (int64_t j = M - 1; j >= 0; --j)
+      for (int64_t k = dep_ptr[static_cast<size_t>(j)]; k < dep_ptr[static_cast<size_t>(j + 1)]; ++k) {
+        const int t = dep_t[static_cast<size_t>(k)];
+        wb[static_cast<size_t>(j)] = std::max(wb[static_cast<size_t>(j)], wb[static_cast<size_t>(t)] + 1);
+      }
+    std::vector<int> of(static_cast<size_t>(M)), ob(static_cast<size_t>(M));
+    std::iota(of.begin(), of.end(), 0);
+    std::iota(ob.begin(), ob.end(), 0);
+    std::stable_sort(of.begin(), of.end(), [&](int x, int y) { return wf[static_cast<size_t>(x)] < wf[static_cast<size_t>(y)]; });
+    std::stable_sort(ob.begin(), ob.end(), [&](int x, int y) {
+      return wb[static_cast<size_t>(x)] < wb[static_cast<size_t>(y)] || (wb[static_cast<size_t>(x)] == wb[static_cast<size_t>(y)] && x > y);
+    });
+    LF.d_fwd_order.upload(of, s);
+    LF.d_bwd_order.upload(ob, s);
+    LF.d_in_ptr.upload(in_ptr, s);
+    LF.d_in_split.upload(in_split, s);
+    LF.d_in_src.upload(in_src, s);
+    LF.d_in_goff.upload(in_goff, s);
+    LF.d_in_w.upload(in_w, s);
+    LF.d_in_uoff.upload(in_uoff, s);
+    LF.d_dep_ptr.upload(dep_ptr, s);
+    LF.d_dep_t.upload(dep_t, s);
+    LF.d_cl_nt.upload(cl_nt, s);
+    LF.d_linv_off.upload(linv_off, s);
+    // split-row task graphs: slices of ~kSlice doubles of factor data per partial task
+    {
+      constexpr int64_t kSlice = 4096;
+      auto build = [&](bool fwd, const std::vector<int64_t>& wave, DevArray<int64_t>& d_ptr, DevArray<int64_t>& d_b,
+                       DevArray<int64_t>& d_scr, DevArray<int>& d_irow, DevArray<int>& d_ipart, int64_t& n_items) {
+        std::vector<int64_t> ptr(static_cast<size_t>(M + 1), 0), bnd, scr(static_cast<size_t>(M), 0);
+        std::vector<int> P(static_cast<size_t>(M), 0);
+        int64_t so = 0;
+        for (int64_t j = 0; j < M; ++j) {
+          const size_t ju = static_cast<size_t>(j);
+          const int64_t w = LF.width[ju];
+          scr[ju] = so;
+          if (fwd) {
+            const int64_t k0 = in_ptr[ju], k1 = k0 + in_split[ju];
+            bnd.push_back(k0);
+            int64_t acc = 0;
+            for (int64_t k = k0; k < k1; ++k) {
+              acc += w * in_w[static_cast<size_t>(k)];
+              if (acc >= kSlice && k + 1 < k1) {
+                bnd.push_back(k + 1);
+                acc = 0;
+              }
+            }
+            if (k1 > k0) bnd.push_back(k1);
+          } else {
+            const int64_t nseg = 1 + LF.cptr[ju + 1] - LF.cptr[ju];
+            bnd.push_back(0);
+            int64_t acc = 0;
+            for (int64_t sg = 0; sg < nseg; ++sg) {
+              const int64_t rows = sg == 0 ? LF.rank[ju] : cl_nt[static_cast<size_t>(LF.cptr[ju] + sg - 1)];
+              acc += w * rows;
+              if (acc >= kSlice && sg + 1 < nseg) {
+                bnd.push_back(sg + 1);
+                acc = 0;
+              }
+            }
+            bnd.push_back(nseg);
+          }
+          ptr[ju + 1] = static_cast<int64_t>(bnd.size());
+          P[ju] = static_cast<int>(ptr[ju + 1] - ptr[ju]) - 1;
+          so += static_cast<int64_t>(P[ju]) * w;
+        }
+        // items in wave order: the wave's partial tasks, then its finalizes
+        std::vector<int> ord(static_cast<size_t>(M));
+        std::iota(ord.begin(), ord.end(), 0);
+        std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return wave[static_cast<size_t>(x)] < wave[static_cast<size_t>(y)]; });
+        std::vector<int> irow, ipart;
+        for (int64_t a0 = 0; a0 < M;) {
+          int64_t a1 = a0 + 1;
+          const int64_t wv = wave[static_cast<size_t>(ord[static_cast<size_t>(a0)])];
+          while (a1 < M && wave[static_cast<size_t>(ord[static_cast<size_t>(a1)])] == wv) ++a1;
+          // rows with a single slice are one fused item (part -1)
+          for (int pass = 0; pass < 2; ++pass)
+            for (int64_t a = a0; a < a1; ++a) {
+              const int j = ord[static_cast<size_t>(a)];
+              if (LF.width[static_cast<size_t>(j)] == 0) continue;
+              const bool fused = P[static_cast<size_t>(j)] == 1;
+              if (pass == 0) {
+                if (fused) continue;
+                for (int t = 0; t < P[static_cast<size_t>(j)]; ++t) {
+                  irow.push_back(j);
+                  ipart.push_back(t);
+                }
+              } else {
+                irow.push_back(j);
+                ipart.push_back(fused ? -1 : P[static_cast<size_t>(j)]);
+              }
+            }
+          a0 = a1;
+        }
+        d_ptr.upload(ptr, s);
+        d_b.upload(bnd, s);
+        d_scr.upload(scr, s);
+        d_irow.upload(irow, s);
+        d_ipart.upload(ipart, s);
+        n_items = static_cast<int64_t>(irow.size());
+        LF.scratch_doubles = std::max(LF.scratch_doubles, so);
+      };
+      if (std::getenv("CE_PROFILE") && std::getenv("CE_PROFILE")[0] == '1') {
+        const int64_t nwf = M ? *std::max_element(wf.begin(), wf.end()) + 1 : 0;
+        const int64_t nwb = M ? *std::max_element(wb.begin(), wb.end()) + 1 : 0;
+        std::fprintf(stderr, "[ce-profile] level %zu apply waves: forward %lld backward %lld\n", li + 1,
+                     static_cast<long long>(nwf), static_cast<long long>(nwb));
+      }
+      build(true, wf, LF.d_fpart_ptr, LF.d_fpart_b, LF.d_fscr_off, LF.d_fitem_row, LF.d_fitem_part, LF.n_fitems);
+      build(false, wb, LF.d_bpart_ptr, LF.d_bpart_b, LF.d_bscr_off, LF.d_bitem_row, LF.d_bitem_part, LF.n_bitems);
+    }
+    LF.d_linv.alloc(static_cast<size_t>(std::max<int64_t>(lo, 1)));
+    launch_pivot_inverse(M, LF.d_width.p, LF.d_fac.p, LF.d_chol_off.p, LF.d_linv.p, LF.d_linv_off.p, s);
+    CE_CUDA(cudaGetLastError());
+  }
+}
+
 namespace {
 
 // Device copy of a plan's symbolic arrays (freed after the level).
@@ -532,6 +773,8 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
   }
 
   auto F = std::make_unique<Factor>();
+  F->levels.reserve(static_cast<size_t>(std::max<int64_t>(max_levels, 1)) + 1);  // stable addresses for apply_jobs
+  std::vector<std::future<void>> apply_jobs;
   F->ctx = ctx;
   F->n = A->n;
 
@@ -917,158 +1160,6 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     LF.d_basis_off = std::move(dcur.basis_off);
     LF.d_sigma_off = std::move(dcur.sigma_off);
     const double h_ta = now_s();
-    {
-      // Apply pull lists: for row j every close neighbour i with w_i > 0 (ascending), the fac
-      // offset of g_{i->j} and of u_i in v; backward dependencies t > j with w_t > 0; rows of
-      // v_t read by the backward pull; pivot inverses.  Wave orders of both sweeps follow the
-      // same (refined) dependencies.
-      const int64_t M = cur.M;
-      std::vector<int64_t> in_ptr(static_cast<size_t>(M + 1), 0), in_goff, in_uoff, dep_ptr(static_cast<size_t>(M + 1), 0),
-          linv_off(static_cast<size_t>(M), 0);
-      std::vector<int> in_split(static_cast<size_t>(M), 0), in_src, in_w, dep_t, cl_nt(cur.ccol.size());
-      int64_t lo = 0;
-      for (int64_t j = 0; j < M; ++j) {
-        const size_t ju = static_cast<size_t>(j);
-        linv_off[ju] = lo;
-        lo += static_cast<int64_t>(LF.width[ju]) * LF.width[ju];
-        for (int64_t e = cur.cptr[ju]; e < cur.cptr[ju + 1]; ++e) {
-          const int t = cur.ccol[static_cast<size_t>(e)];
-          const size_t tu = static_cast<size_t>(t);
-          cl_nt[static_cast<size_t>(e)] = t > j ? cur.bsz[tu] : LF.rank[tu];
-          if (LF.width[tu] == 0) continue;
-          const int64_t k = csr_find(cur.cptr, cur.ccol, t, static_cast<int>(j));
-          in_src.push_back(t);
-          in_goff.push_back(cur.g_off[tu] + static_cast<int64_t>(LF.rank[tu] + cur.croff[static_cast<size_t>(k)]) * LF.width[tu]);
-          in_w.push_back(LF.width[tu]);
-          in_uoff.push_back(cur.offsets[tu] + LF.rank[tu]);
-          if (t < j) ++in_split[ju];
-          if (t > j) dep_t.push_back(t);
-        }
-        in_ptr[ju + 1] = static_cast<int64_t>(in_src.size());
-        dep_ptr[ju + 1] = static_cast<int64_t>(dep_t.size());
-      }
-      std::vector<int64_t> wf(static_cast<size_t>(M), 0), wb(static_cast<size_t>(M), 0);
-      for (int64_t j = 0; j < M; ++j)
-        for (int64_t k = in_ptr[static_cast<size_t>(j)]; k < in_ptr[static_cast<size_t>(j)] + in_split[static_cast<size_t>(j)]; ++k) {
-          const int i = in_src[static_cast<size_t>(k)];
-          wf[static_cast<size_t>(j)] = std::max(wf[static_cast<size_t>(j)], wf[static_cast<size_t>(i)] + 1);
-        }
-      for (int64_t j = M - 1; j >= 0; --j)
-        for (int64_t k = dep_ptr[static_cast<size_t>(j)]; k < dep_ptr[static_cast<size_t>(j + 1)]; ++k) {
-          const int t = dep_t[static_cast<size_t>(k)];
-          wb[static_cast<size_t>(j)] = std::max(wb[static_cast<size_t>(j)], wb[static_cast<size_t>(t)] + 1);
-        }
-      std::vector<int> of(static_cast<size_t>(M)), ob(static_cast<size_t>(M));
-      std::iota(of.begin(), of.end(), 0);
-      std::iota(ob.begin(), ob.end(), 0);
-      std::stable_sort(of.begin(), of.end(), [&](int x, int y) { return wf[static_cast<size_t>(x)] < wf[static_cast<size_t>(y)]; });
-      std::stable_sort(ob.begin(), ob.end(), [&](int x, int y) {
-        return wb[static_cast<size_t>(x)] < wb[static_cast<size_t>(y)] || (wb[static_cast<size_t>(x)] == wb[static_cast<size_t>(y)] && x > y);
-      });
-      LF.d_fwd_order.upload(of, s);
-      LF.d_bwd_order.upload(ob, s);
-      LF.d_in_ptr.upload(in_ptr, s);
-      LF.d_in_split.upload(in_split, s);
-      LF.d_in_src.upload(in_src, s);
-      LF.d_in_goff.upload(in_goff, s);
-      LF.d_in_w.upload(in_w, s);
-      LF.d_in_uoff.upload(in_uoff, s);
-      LF.d_dep_ptr.upload(dep_ptr, s);
-      LF.d_dep_t.upload(dep_t, s);
-      LF.d_cl_nt.upload(cl_nt, s);
-      LF.d_linv_off.upload(linv_off, s);
-      // split-row task graphs: slices of ~kSlice doubles of factor data per partial task
-      {
-        constexpr int64_t kSlice = 4096;
-        auto build = [&](bool fwd, const std::vector<int64_t>& wave, DevArray<int64_t>& d_ptr, DevArray<int64_t>& d_b,
-                         DevArray<int64_t>& d_scr, DevArray<int>& d_irow, DevArray<int>& d_ipart, int64_t& n_items) {
-          std::vector<int64_t> ptr(static_cast<size_t>(M + 1), 0), bnd, scr(static_cast<size_t>(M), 0);
-          std::vector<int> P(static_cast<size_t>(M), 0);
-          int64_t so = 0;
-          for (int64_t j = 0; j < M; ++j) {
-            const size_t ju = static_cast<size_t>(j);
-            const int64_t w = LF.width[ju];
-            scr[ju] = so;
-            if (fwd) {
-              const int64_t k0 = in_ptr[ju], k1 = k0 + in_split[ju];
-              bnd.push_back(k0);
-              int64_t acc = 0;
-              for (int64_t k = k0; k < k1; ++k) {
-                acc += w * in_w[static_cast<size_t>(k)];
-                if (acc >= kSlice && k + 1 < k1) {
-                  bnd.push_back(k + 1);
-                  acc = 0;
-                }
-              }
-              if (k1 > k0) bnd.push_back(k1);
-            } else {
-              const int64_t nseg = 1 + cur.cptr[ju + 1] - cur.cptr[ju];
-              bnd.push_back(0);
-              int64_t acc = 0;
-              for (int64_t sg = 0; sg < nseg; ++sg) {
-                const int64_t rows = sg == 0 ? LF.rank[ju] : cl_nt[static_cast<size_t>(cur.cptr[ju] + sg - 1)];
-                acc += w * rows;
-                if (acc >= kSlice && sg + 1 < nseg) {
-                  bnd.push_back(sg + 1);
-                  acc = 0;
-                }
-              }
-              bnd.push_back(nseg);
-            }
-            ptr[ju + 1] = static_cast<int64_t>(bnd.size());
-            P[ju] = static_cast<int>(ptr[ju + 1] - ptr[ju]) - 1;
-            so += static_cast<int64_t>(P[ju]) * w;
-          }
-          // items in wave order: the wave's partial tasks, then its finalizes
-          std::vector<int> ord(static_cast<size_t>(M));
-          std::iota(ord.begin(), ord.end(), 0);
-          std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return wave[static_cast<size_t>(x)] < wave[static_cast<size_t>(y)]; });
-          std::vector<int> irow, ipart;
-          for (int64_t a0 = 0; a0 < M;) {
-            int64_t a1 = a0 + 1;
-            const int64_t wv = wave[static_cast<size_t>(ord[static_cast<size_t>(a0)])];
-            while (a1 < M && wave[static_cast<size_t>(ord[static_cast<size_t>(a1)])] == wv) ++a1;
-            // rows with a single slice are one fused item (part -1)
-            for (int pass = 0; pass < 2; ++pass)
-              for (int64_t a = a0; a < a1; ++a) {
-                const int j = ord[static_cast<size_t>(a)];
-                if (LF.width[static_cast<size_t>(j)] == 0) continue;
-                const bool fused = P[static_cast<size_t>(j)] == 1;
-                if (pass == 0) {
-                  if (fused) continue;
-                  for (int t = 0; t < P[static_cast<size_t>(j)]; ++t) {
-                    irow.push_back(j);
-                    ipart.push_back(t);
-                  }
-                } else {
-                  irow.push_back(j);
-                  ipart.push_back(fused ? -1 : P[static_cast<size_t>(j)]);
-                }
-              }
-            a0 = a1;
-          }
-          d_ptr.upload(ptr, s);
-          d_b.upload(bnd, s);
-          d_scr.upload(scr, s);
-          d_irow.upload(irow, s);
-          d_ipart.upload(ipart, s);
-          n_items = static_cast<int64_t>(irow.size());
-          LF.scratch_doubles = std::max(LF.scratch_doubles, so);
-        };
-        if (std::getenv("CE_PROFILE") && std::getenv("CE_PROFILE")[0] == '1') {
-          const int64_t nwf = M ? *std::max_element(wf.begin(), wf.end()) + 1 : 0;
-          const int64_t nwb = M ? *std::max_element(wb.begin(), wb.end()) + 1 : 0;
-          std::fprintf(stderr, "[ce-profile] level %zu apply waves: forward %lld backward %lld\n", li + 1,
-                       static_cast<long long>(nwf), static_cast<long long>(nwb));
-        }
-        build(true, wf, LF.d_fpart_ptr, LF.d_fpart_b, LF.d_fscr_off, LF.d_fitem_row, LF.d_fitem_part, LF.n_fitems);
-        build(false, wb, LF.d_bpart_ptr, LF.d_bpart_b, LF.d_bscr_off, LF.d_bitem_row, LF.d_bitem_part, LF.n_bitems);
-      }
-      LF.d_linv.alloc(static_cast<size_t>(std::max<int64_t>(lo, 1)));
-      launch_pivot_inverse(M, LF.d_width.p, LF.d_fac.p, LF.d_chol_off.p, LF.d_linv.p, LF.d_linv_off.p, s);
-      CE_CUDA(cudaGetLastError());
-    }
-
     const double h_tb = now_s();
     // stats (factorization.cpp:376-405) + §8d algorithmic counts
     {
@@ -1119,6 +1210,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       if (slot_of_group[g] >= 0) next_alive[g] = alive[static_cast<size_t>(slot_of_group[g])];
     alive_map = std::move(next_alive);
     F->levels.push_back(std::move(LF));
+    apply_jobs.push_back(std::async(std::launch::async, build_apply_lists, std::ref(F->levels.back()), li, s));
     if (std::getenv("CE_PROFILE") && std::getenv("CE_PROFILE")[0] == '1')
       std::fprintf(stderr, "[ce-profile] level %zu host: apply lists %.1f ms, stats+rest %.1f ms, iteration %.1f ms\n", li + 1,
                    1e3 * (h_tb - h_ta), 1e3 * (now_s() - h_tb), 1e3 * (now_s() - h_t0));
@@ -1177,6 +1269,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
   F->shift_retries = shifts;
   if (shift_total) *shift_total = shifts;
 
+  for (auto& j : apply_jobs) j.get();  // rethrows a failed list build
   // apply workspaces
   F->w_v.alloc(static_cast<size_t>(std::max<int64_t>(F->n, 1)));
   F->w_active.alloc(static_cast<size_t>(std::max<int64_t>(F->n, 1)));

@@ -24,6 +24,14 @@ struct Breakdown : std::runtime_error {
 void cuda_check(cudaError_t e, const char* what);
 #define CE_CUDA(x) ::ceg::cuda_check((x), #x)
 
+// Caching device allocator: blocks are kept per device on release and reused by later
+// allocations of a similar size (a factorization allocates the same large arrays every
+// time; cudaMalloc/cudaFree would otherwise add host stalls and implicit device syncs
+// between levels).  Releases happen only after the owning stream has drained.
+void* pool_alloc(size_t bytes);
+void pool_free(void* p, size_t bytes);
+void pool_trim();  // return every cached block to the driver
+
 // Owning device array.
 template <class T>
 struct DevArray {
@@ -48,10 +56,10 @@ struct DevArray {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) CE_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+    if (count) p = static_cast<T*>(pool_alloc(count * sizeof(T)));
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) pool_free(p, n * sizeof(T));
     p = nullptr;
     n = 0;
   }
