@@ -34,10 +34,10 @@ namespace {
 // that small problems exercise the multi-task path of fat rows.
 struct Thresholds {
   int64_t pair_inline = int64_t{1} << 19;  // FMA below which a row's Schur pairs stay in A2
-  int64_t leaf_work = int64_t{1} << 20;    // far gather f*b^2 above which TSQR leaves are split off
-  int64_t leaf_cols = 512;                 // far columns per TSQR leaf
-  int64_t strip_work = int64_t{1} << 20;   // strip rotation S*b^2 above which the strip is split off
-  int64_t strip_cols = 256;                // strip columns per task
+  int64_t leaf_work = int64_t{1} << 15;    // far gather f*b^2 above which TSQR leaves are split off
+  int64_t leaf_cols = 0;                   // far columns per TSQR leaf (0: sqrt(f / b) leaves)
+  int64_t strip_work = int64_t{1} << 15;   // strip rotation S*b^2 above which the strip is split off
+  int64_t strip_cols = 64;                 // strip columns per task
   bool small_panels = false;               // one close neighbour per Schur panel
   Thresholds() {
     const char* f = std::getenv("CE_FORCE_TASKS");  // bitmask: 1 leaves, 2 strip tasks, 4 Schur panels
@@ -54,6 +54,15 @@ struct Thresholds {
       pair_inline = 0;
       small_panels = true;
     }
+    // development overrides
+    auto env = [](const char* k, int64_t& v) {
+      if (const char* e = std::getenv(k)) v = std::atoll(e);
+    };
+    env("CE_LEAF_WORK", leaf_work);
+    env("CE_LEAF_COLS", leaf_cols);
+    env("CE_STRIP_WORK", strip_work);
+    env("CE_STRIP_COLS", strip_cols);
+    env("CE_PAIR_INLINE", pair_inline);
   }
 };
 const Thresholds& thresholds() {
@@ -333,7 +342,11 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
     }
     const Thresholds& th = thresholds();
     if (P.fsum[iu] * b * b > th.leaf_work) {
-      const int64_t leaves = std::min<int64_t>(nfar, (P.fsum[iu] + th.leaf_cols - 1) / th.leaf_cols);
+      // leaf time ~ f / n rows, combine time ~ n b rows: n ~ sqrt(f / b) balances them
+      // (leaf_cols > 0 fixes the leaf width instead)
+      const int64_t nl = th.leaf_cols > 0 ? (P.fsum[iu] + th.leaf_cols - 1) / th.leaf_cols
+                                          : static_cast<int64_t>(std::lround(std::sqrt(static_cast<double>(P.fsum[iu]) / std::max<int64_t>(b, 1))));
+      const int64_t leaves = std::min<int64_t>(nfar, nl);
       if (leaves >= 2) {
         P.nA1[iu] = static_cast<int>(leaves);
         P.rs_off[iu] = ro;
