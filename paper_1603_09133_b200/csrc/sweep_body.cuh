@@ -444,10 +444,172 @@ __device__ __noinline__ int jacobi_t(double* X, double* V, int b, int ld, int me
 }
 
 __device__ int jacobi_fast(double* X, double* V, int b, int ld, int meff) {
-  if (b <= 16) return jacobi_t<4, 4>(X, V, b, ld, meff);
-  if (b <= 32) return jacobi_t<8, 4>(X, V, b, ld, meff);
+  // more lanes per pair beats shorter shuffle trees (micro_dense: b=16 897 vs 1174 cycles/round)
+  if (b <= 16) return jacobi_t<16, 1>(X, V, b, ld, meff);
+  if (b <= 32) return jacobi_t<16, 2>(X, V, b, ld, meff);
   if (b <= 64) return jacobi_t<8, 8>(X, V, b, ld, meff);
   return jacobi(X, V, b, ld, meff);
+}
+
+// Register-resident Householder QR of a b x b column-major matrix A (leading dimension
+// ld) in place: R in the upper triangle, reflector tails below the diagonal, tau[k]
+// (LAPACK dlarfg conventions, same results layout as the thread-per-column loop).  Groups
+// of G lanes own NC columns (E rows per lane); the owner of column k+1 prepares reflector
+// k+1 right after its update and publishes it in a double buffer (vb0 / vb1, b doubles
+// each); one barrier per step.
+template <int G, int E, int NC>
+__device__ __noinline__ void hqr_reg_t(double* A, int b, int ld, double* tau, double* vb0, double* vb1) {
+  CE_SHARED(A);
+  CE_SHARED(tau);
+  CE_SHARED(vb0);
+  CE_SHARED(vb1);
+  constexpr int NG = T / G;
+  constexpr unsigned kFull = 0xffffffffu;
+  const int tid = threadIdx.x, grp = tid / G, gl = tid % G, warp = tid >> 5;
+  const int wmax = ((warp + 1) * 32) / G - 1 + (NC - 1) * NG;
+  double x[NC][E];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = grp + c * NG;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int m = gl + e * G;
+      x[c][e] = (j < b && m < b) ? A[j * ld + m] : 0.0;
+    }
+  }
+  auto prep = [&](double (&xc)[E], int j, bool own) {
+    double ss = 0.0, x0 = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int m = gl + e * G;
+      if (m > j && m < b) ss = fma(xc[e], xc[e], ss);
+      if (m == j) x0 = xc[e];
+    }
+    ss = group_sum<G>(ss, kFull);
+    x0 = group_sum<G>(x0, kFull);
+    if (!own) return;
+    double* vb = (j & 1) ? vb1 : vb0;
+    double t = 0.0;
+    if (ss > 0.0) {
+      const double n2 = fma(x0, x0, ss);
+      const bool fast = n2 > 1e-290 && n2 < 1e290;
+      const double nrm = fast ? n2 * rsqrt_nr(n2) : sqrt(n2);
+      const double beta = x0 >= 0.0 ? -nrm : nrm;
+      const double den = x0 - beta;
+      const double scale = fast ? rcp_nr(den) : 1.0 / den;
+      t = fast ? -den * rcp_nr(beta) : (beta - x0) / beta;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int m = gl + e * G;
+        if (m >= b) continue;
+        if (m > j) {
+          xc[e] *= scale;
+          vb[m] = xc[e];
+        } else if (m == j) {
+          xc[e] = beta;
+          vb[m] = 1.0;
+        } else {
+          vb[m] = 0.0;
+        }
+      }
+    }
+    if (gl == 0) tau[j] = t;
+  };
+  if (warp == 0 && b > 0) prep(x[0], 0, grp == 0);
+  __syncthreads();
+  for (int k = 0; k + 1 < b; ++k) {
+    const double t = tau[k];
+    if (t != 0.0 && wmax > k) {
+      const double* vb = (k & 1) ? vb1 : vb0;
+      double v[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int m = gl + e * G;
+        v[e] = m < b ? vb[m] : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int j = grp + c * NG;
+        double sd = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) sd = fma(v[e], x[c][e], sd);
+        sd = group_sum<G>(sd, kFull);
+        const double d = (j > k && j < b) ? t * sd : 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[c][e] = fma(-d, v[e], x[c][e]);
+      }
+    }
+    const int jn = k + 1, og = jn % NG, oc = jn / NG;
+    if ((og * G) >> 5 == warp) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (c == oc) prep(x[c], jn, grp == og);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = grp + c * NG;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int m = gl + e * G;
+      if (j < b && m < b) A[j * ld + m] = x[c][e];
+    }
+  }
+  __syncthreads();
+}
+
+// V <- Q2 V, Q2 = H_0 ... H_{b-2} from the reflectors below the diagonal of A: every group
+// applies all reflectors to the V columns it keeps in registers; the reflectors are
+// read-only, so no barriers are needed between steps.
+template <int G, int E, int NC>
+__device__ __noinline__ void apply_refl_reg_t(const double* A, const double* tau, double* V, int b, int ld) {
+  CE_SHARED(A);
+  CE_SHARED(tau);
+  CE_SHARED(V);
+  constexpr int NG = T / G;
+  constexpr unsigned kFull = 0xffffffffu;
+  const int tid = threadIdx.x, grp = tid / G, gl = tid % G;
+  double x[NC][E];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = grp + c * NG;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int m = gl + e * G;
+      x[c][e] = (j < b && m < b) ? V[j * ld + m] : 0.0;
+    }
+  }
+  for (int k = b - 2; k >= 0; --k) {
+    const double t = tau[k];
+    if (t == 0.0) continue;
+    double v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int m = gl + e * G;
+      v[e] = m == k ? 1.0 : ((m > k && m < b) ? A[k * ld + m] : 0.0);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double sd = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) sd = fma(v[e], x[c][e], sd);
+      const double d = t * group_sum<G>(sd, kFull);
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[c][e] = fma(-d, v[e], x[c][e]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = grp + c * NG;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int m = gl + e * G;
+      if (j < b && m < b) V[j * ld + m] = x[c][e];
+    }
+  }
+  __syncthreads();
 }
 
 // QR preconditioning of the Jacobi SVD (Drmac-Veselic; oracle/dense.cpp svd_left):
@@ -465,6 +627,17 @@ __device__ __noinline__ void precondition_qr(const Buf& s_, int b) {
     Aq[j * ld + i] = s.R[i * b + j];
   }
   __syncthreads();
+  if (b <= 64) {
+    if (b <= 16) hqr_reg_t<16, 1, 1>(Aq, b, ld, s.tau, s.nrm, s.sig);
+    else if (b <= 32) hqr_reg_t<8, 4, 1>(Aq, b, ld, s.tau, s.nrm, s.sig);
+    else hqr_reg_t<8, 8, 2>(Aq, b, ld, s.tau, s.nrm, s.sig);
+    for (int idx = threadIdx.x; idx < b * b; idx += T) {
+      const int j = idx / b, i = idx % b;
+      s.R[j * ld + i] = i >= j ? Aq[i * ld + j] : 0.0;
+    }
+    __syncthreads();
+    return;
+  }
   if (threadIdx.x == 0 && b > 0) {
     double beta;
     const double tau = house_prep(Aq[0], Aq + 1, b - 1, &beta);
@@ -505,6 +678,12 @@ __device__ __noinline__ void apply_q2(const Buf& s_, int b) {
   CE_SHARED_BUF(s);
   const int ld = pad_ld(b);
   const double* Aq = s.C;
+  if (b <= 64) {
+    if (b <= 16) apply_refl_reg_t<16, 1, 1>(Aq, s.tau, s.V, b, ld);
+    else if (b <= 32) apply_refl_reg_t<8, 4, 1>(Aq, s.tau, s.V, b, ld);
+    else apply_refl_reg_t<8, 8, 2>(Aq, s.tau, s.V, b, ld);
+    return;
+  }
   for (int k = b - 2; k >= 0; --k) {
     const double tau = s.tau[k];
     if (tau == 0.0) continue;

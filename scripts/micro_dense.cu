@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(T) micro_kernel(int which, int b, int K, int r
   int nsw_tot = 0;
   for (int rep = 0; rep < reps; ++rep) {
     const uint64_t seed = (static_cast<uint64_t>(blockIdx.x) * 1000003ull + rep) * 7919ull;
-    if (which != 3 && which != 13) {
+    if (which != 3 && which != 13 && which < 30) {
       for (int idx = threadIdx.x; idx < b * b; idx += T) R[idx] = 0.0;
       for (int idx = threadIdx.x; idx < K * b; idx += T) C[(idx / K) * ldc + idx % K] = hrand(seed + idx);
     } else {
@@ -431,6 +431,15 @@ __global__ void __launch_bounds__(T) micro_kernel(int which, int b, int K, int r
     else if (which == 20) tsqr_reg_t<16, 8, 1>(R, C, K, b, ldc, shr);
     else if (which == 21) tsqr_stamp_t<16, 8, 1>(R, C, K, b, ldc, shr);
     else if (which == 23) tsqr_abl_t<16, 8, 1, 0>(R, C, K, b, ldc, shr);
+    else if (which == 30) nsw_tot += jacobi_t<1, 16>(R, V, b, ld, b);
+    else if (which == 31) nsw_tot += jacobi_t<2, 8>(R, V, b, ld, b);
+    else if (which == 32) nsw_tot += jacobi_t<4, 4>(R, V, b, ld, b);
+    else if (which == 33) nsw_tot += jacobi_t<8, 2>(R, V, b, ld, b);
+    else if (which == 34) nsw_tot += jacobi_t<16, 1>(R, V, b, ld, b);
+    else if (which == 35) nsw_tot += jacobi_t<1, 40>(R, V, b, ld, b);
+    else if (which == 36) nsw_tot += jacobi_t<2, 20>(R, V, b, ld, b);
+    else if (which == 37) nsw_tot += jacobi_t<4, 10>(R, V, b, ld, b);
+    else if (which == 38) nsw_tot += jacobi_t<8, 5>(R, V, b, ld, b);
     else if (which == 24) tsqr_abl_t<16, 8, 1, 1>(R, C, K, b, ldc, shr);
     else if (which == 25) tsqr_abl_t<16, 8, 1, 2>(R, C, K, b, ldc, shr);
     else if (which == 26) tsqr_abl_t<16, 8, 1, 3>(R, C, K, b, ldc, shr);
@@ -443,7 +452,7 @@ __global__ void __launch_bounds__(T) micro_kernel(int which, int b, int K, int r
     cyc[blockIdx.x] = acc / reps;
     sweeps[blockIdx.x] = nsw_tot;
     if (blockIdx.x == 0)
-      for (int k = 0; k < b; ++k) out[k] = (which != 3 && which != 13) ? fabs(R[k * b + k]) : R[k * ld + k];
+      for (int k = 0; k < b; ++k) out[k] = (which != 3 && which != 13 && which < 30) ? fabs(R[k * b + k]) : R[k * ld + k];
   }
 }
 
@@ -564,8 +573,8 @@ int main() {
     }
   }
   struct Case { int which, b, K; };
-  const Case cases[] = {{23, 16, 128}, {24, 16, 128}, {25, 16, 128}, {26, 16, 128}};
-  const char* names[] = {"tsqr_warps", "tsqr_update", "tsqr_group", "jacobi", "tsqr_g4", "tsqr_g16", "tsqr_g32", "noprep", "noupdate", "fastdiv", "probe_full", "stamp", "tsqr_fast", "jacobi_fast", "reg16x8x3", "reg8x16x2", "reg4x32x1", "reg16x8x4", "reg32x4x6", "reg8x16x1", "reg16x8x1", "stamp16", "stamp40", "abl_full", "abl_noprep", "abl_noupd", "abl_none"};
+  const Case cases[] = {{30, 16, 0}, {31, 16, 0}, {32, 16, 0}, {33, 16, 0}, {34, 16, 0}, {35, 40, 0}, {36, 40, 0}, {37, 40, 0}, {38, 40, 0}};
+  const char* names[] = {"tsqr_warps", "tsqr_update", "tsqr_group", "jacobi", "tsqr_g4", "tsqr_g16", "tsqr_g32", "noprep", "noupdate", "fastdiv", "probe_full", "stamp", "tsqr_fast", "jacobi_fast", "reg16x8x3", "reg8x16x2", "reg4x32x1", "reg16x8x4", "reg32x4x6", "reg8x16x1", "reg16x8x1", "stamp16", "stamp40", "abl_full", "abl_noprep", "abl_noupd", "abl_none", "", "", "", "j1x16", "j2x8", "j4x4", "j8x2", "j16x1", "j1x40", "j2x20", "j4x10", "j8x5"};
   const int only = getenv("MICRO_CASE") ? atoi(getenv("MICRO_CASE")) : -1;
   for (const Case& c : cases) {
     if (only >= 0 && c.which != only) continue;
@@ -592,7 +601,7 @@ int main() {
     }
     std::printf("%-12s b=%3d K=%3d  cycles/call %9.0f  (%.1f us @1.9GHz)", names[c.which], c.b, c.K, mean,
                 mean / 1900.0);
-    if (c.which == 3 || c.which == 13) std::printf("  sweeps %.2f  cycles/round %.0f", sws, mean / (sws * ((c.b + (c.b & 1)) - 1)));
+    if (c.which == 3 || c.which == 13 || c.which >= 30) std::printf("  sweeps %.2f  cycles/round %.0f", sws, mean / (sws * ((c.b + (c.b & 1)) - 1)));
     std::printf("  out[0..2] %.6f %.6f %.6f\n", out[0], out[1], out[2]);
     if (c.which == 21 || c.which == 22) {
       long long st[16];
