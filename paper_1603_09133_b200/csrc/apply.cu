@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(T) forward_task_kernel(ApplyLevelArgs A) {
       const int64_t k0 = A.part_b[pp + part], k1 = A.part_b[pp + part + 1];
       for (int64_t k = k0 + threadIdx.x; k < k1; k += T)
         while (ld_acquire(A.flags + A.in_src[k]) == 0) __nanosleep(32);
-      __threadfence();
+      if (threadIdx.x == 0) __threadfence();
       __syncthreads();
       double* pw = z + kWmax + warp * 2 * kWmax;
       double* ub = pw + kWmax;
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(T) backward_task_kernel(ApplyLevelArgs A) {
         if (t > j && A.width[t] > 0)
           while (ld_acquire(A.flags + t) == 0) __nanosleep(32);
       }
-      __threadfence();
+      if (threadIdx.x == 0) __threadfence();
       __syncthreads();
       double* vj = A.v + A.offsets[j];
       const double* G = A.fac + A.g_off[j];

@@ -1177,6 +1177,28 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
   const int mx = ldt / 4, my = lds / 4;
   for (int mt = tid; mt < mx * my; mt += T) {
     const int x0 = (mt / my) * 4, y0 = (mt % my) * 4;
+    // issue the tile's X loads first so they overlap the w-long outer-product loop
+    double* xp[4][4];
+    double xv[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int x = x0 + a;
+      const int kt = x < rtn ? xblk[x] : 0, xl = x < rtn ? xloc[x] : 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int y = y0 + c;
+        xp[a][c] = nullptr;
+        xv[a][c] = 0.0;
+        if (x < rtn && y < rsn) {
+          const int ks = yblk[y];
+          const long long off = slot_tab[kt * ns + ks];
+          if (off >= 0) {
+            xp[a][c] = A.store + off + static_cast<int64_t>(xl) * tab_bs[ks] + yloc[y];
+            xv[a][c] = ldg(xp[a][c]);
+          }
+        }
+      }
+    }
     double acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -1194,21 +1216,10 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
         for (int c = 0; c < 4; ++c) acc[a][c] += av[a] * cv[c];
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int x = x0 + a;
-      if (x >= rtn) break;
-      const int kt = xblk[x], xl = xloc[x];
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int y = y0 + c;
-        if (y >= rsn) break;
-        const int ks = yblk[y];
-        const long long off = slot_tab[kt * ns + ks];
-        if (off < 0) continue;
-        double* X = A.store + off + static_cast<int64_t>(xl) * tab_bs[ks] + yloc[y];
-        *X = ldg(X) - acc[a][c];
-      }
-    }
+      for (int c = 0; c < 4; ++c)
+        if (xp[a][c]) *xp[a][c] = xv[a][c] - acc[a][c];
   }
   __syncthreads();
 }
@@ -1559,11 +1570,9 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
         }
         if (s_stop) break;
       }
-      __threadfence();
     }
     if (threadIdx.x == 0) {
-      if (first) {
-      } else {
+      if (!first) {
         while (ld_acquire(A.done + i) < need) {
           if (*reinterpret_cast<volatile int*>(A.err) != 0) {
             s_stop = 1;
