@@ -568,7 +568,7 @@ void build_apply_lists(LevelFactor& LF, size_t li, cudaStream_t main_stream) {
     LF.d_linv_off.upload(linv_off, s);
     // split-row task graphs: slices of ~kSlice doubles of factor data per partial task
     {
-      constexpr int64_t kSlice = 4096;
+      static const int64_t kSlice = std::getenv("CE_APPLY_SLICE") ? std::atoll(std::getenv("CE_APPLY_SLICE")) : 256;
       auto build = [&](bool fwd, const std::vector<int64_t>& wave, DevArray<int64_t>& d_ptr, DevArray<int64_t>& d_b,
                        DevArray<int64_t>& d_scr, DevArray<int>& d_irow, DevArray<int>& d_ipart, int64_t& n_items) {
         std::vector<int64_t> ptr(static_cast<size_t>(M + 1), 0), bnd, scr(static_cast<size_t>(M), 0);
