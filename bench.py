@@ -51,6 +51,19 @@ def workload_name(cfg, grid):
     return s
 
 
+def sweep_traffic(args):
+    """DRAM bytes (read + write) of the level-sweep launches of one factorization, from the
+    committed ncu capture (profiles/r1_sweep_traffic_cfg2.json) when it matches this
+    workload, else None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_sweep_traffic_cfg2.json")
+    if args.cfg != 2 or any(args.grid) or not os.path.exists(path):
+        return None
+    try:
+        return float(json.load(open(path))["total_dram_bytes"])
+    except Exception:
+        return None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -302,7 +315,7 @@ def run_product(args):
                          "achieved": gbs if bound == "hbm" else tfl,
                          "peak": peaks["hbm_gbs"] if bound == "hbm" else fp64_peak,
                          "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
-                         "frac": f_hbm if bound == "hbm" else f_fp64, "traffic": None,
+                         "frac": f_hbm if bound == "hbm" else f_fp64, "traffic": sweep_traffic(args),
                          "hbm": {"achieved_gbs": gbs, "peak_gbs": peaks["hbm_gbs"], "frac": f_hbm, "peak_kind": peak_kind},
                          "fp64": {"achieved_tflops": tfl, "peak_tflops": fp64_peak, "frac": f_fp64,
                                   "peak_kind": "measured live: cuBLAS DGEMM 8192^3"},
