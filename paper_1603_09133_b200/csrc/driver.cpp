@@ -12,6 +12,7 @@
 #include <future>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <memory>
 #include <numeric>
 #include <sstream>
@@ -141,6 +142,25 @@ void pool_trim() {
 
 namespace {
 
+// Run f(r0, r1) over row chunks on up to 16 host threads (small ranges run inline).
+template <class F>
+void parallel_rows(int64_t M, F&& f) {
+  const int64_t hw = std::max<int64_t>(1, static_cast<int64_t>(std::thread::hardware_concurrency()));
+  const int64_t nt = std::min<int64_t>(16, hw);
+  if (M < 64 || nt <= 1) {
+    f(int64_t{0}, M);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int64_t chunk = (M + nt - 1) / nt;
+  for (int64_t t = 1; t < nt; ++t) {
+    const int64_t a = t * chunk, b = std::min(M, a + chunk);
+    if (a < b) th.emplace_back([&f, a, b]() { f(a, b); });
+  }
+  f(int64_t{0}, std::min(M, chunk));
+  for (auto& x : th) x.join();
+}
+
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -163,28 +183,50 @@ struct Events {
 };
 
 // pattern_square (proj/src/pattern.cpp:64-86), CSR in / CSR out.
+template <class F>
+void parallel_rows(int64_t M, F&& f);
+
+// sq(P) = pattern of P^2 (sorted rows), two parallel passes: count, then fill + sort.
 void square_pattern(int64_t m, const std::vector<int64_t>& ptr, const std::vector<int>& col, std::vector<int64_t>& sptr,
                     std::vector<int>& scol) {
-  std::vector<int64_t> mark(static_cast<size_t>(m), -1);
-  std::vector<int> touched;
   sptr.assign(static_cast<size_t>(m + 1), 0);
-  scol.clear();
-  for (int64_t i = 0; i < m; ++i) {
-    touched.clear();
-    for (int64_t k = ptr[static_cast<size_t>(i)]; k < ptr[static_cast<size_t>(i + 1)]; ++k) {
-      const int kk = col[static_cast<size_t>(k)];
-      for (int64_t e = ptr[static_cast<size_t>(kk)]; e < ptr[static_cast<size_t>(kk + 1)]; ++e) {
-        const int j = col[static_cast<size_t>(e)];
-        if (mark[static_cast<size_t>(j)] != i) {
-          mark[static_cast<size_t>(j)] = i;
-          touched.push_back(j);
+  std::vector<int64_t> cnt(static_cast<size_t>(m), 0);
+  parallel_rows(m, [&](int64_t r0, int64_t r1) {
+    std::vector<int64_t> mark(static_cast<size_t>(m), -1);
+    for (int64_t i = r0; i < r1; ++i) {
+      int64_t c = 0;
+      for (int64_t k = ptr[static_cast<size_t>(i)]; k < ptr[static_cast<size_t>(i + 1)]; ++k) {
+        const int kk = col[static_cast<size_t>(k)];
+        for (int64_t e = ptr[static_cast<size_t>(kk)]; e < ptr[static_cast<size_t>(kk + 1)]; ++e) {
+          const int j = col[static_cast<size_t>(e)];
+          if (mark[static_cast<size_t>(j)] != i) {
+            mark[static_cast<size_t>(j)] = i;
+            ++c;
+          }
         }
       }
+      cnt[static_cast<size_t>(i)] = c;
     }
-    std::sort(touched.begin(), touched.end());
-    scol.insert(scol.end(), touched.begin(), touched.end());
-    sptr[static_cast<size_t>(i + 1)] = static_cast<int64_t>(scol.size());
-  }
+  });
+  for (int64_t i = 0; i < m; ++i) sptr[static_cast<size_t>(i + 1)] = sptr[static_cast<size_t>(i)] + cnt[static_cast<size_t>(i)];
+  scol.assign(static_cast<size_t>(sptr[static_cast<size_t>(m)]), 0);
+  parallel_rows(m, [&](int64_t r0, int64_t r1) {
+    std::vector<int64_t> mark(static_cast<size_t>(m), -1);
+    for (int64_t i = r0; i < r1; ++i) {
+      int64_t at = sptr[static_cast<size_t>(i)];
+      for (int64_t k = ptr[static_cast<size_t>(i)]; k < ptr[static_cast<size_t>(i + 1)]; ++k) {
+        const int kk = col[static_cast<size_t>(k)];
+        for (int64_t e = ptr[static_cast<size_t>(kk)]; e < ptr[static_cast<size_t>(kk + 1)]; ++e) {
+          const int j = col[static_cast<size_t>(e)];
+          if (mark[static_cast<size_t>(j)] != i) {
+            mark[static_cast<size_t>(j)] = i;
+            scol[static_cast<size_t>(at++)] = j;
+          }
+        }
+      }
+      std::sort(scol.begin() + sptr[static_cast<size_t>(i)], scol.begin() + sptr[static_cast<size_t>(i + 1)]);
+    }
+  });
 }
 
 bool csr_contains(const std::vector<int64_t>& ptr, const std::vector<int>& col, int64_t i, int j) {
@@ -215,24 +257,35 @@ LevelPlan plan_symbolic(int64_t M, std::vector<int64_t> bptr, std::vector<int> b
     for (int64_t k = P.bptr[static_cast<size_t>(i)]; k < P.bptr[static_cast<size_t>(i + 1)]; ++k)
       if (P.bcol[static_cast<size_t>(k)] <= i) ++P.lower_blocks;
 
+  const bool prof = std::getenv("CE_PROFILE") && std::getenv("CE_PROFILE")[0] == '1';
+  const double t0 = now_s();
   square_pattern(M, P.bptr, P.bcol, P.sptr, P.scol);
+  const double t1 = now_s();
   const int64_t nnz = static_cast<int64_t>(P.scol.size());
   P.skind.resize(static_cast<size_t>(nnz));
   P.sslot.assign(static_cast<size_t>(nnz), -1);
+  parallel_rows(M, [&](int64_t r0, int64_t r1) {
+    for (int64_t i = r0; i < r1; ++i)
+      for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e) {
+        const int j = P.scol[static_cast<size_t>(e)];
+        P.skind[static_cast<size_t>(e)] = j == i ? 0 : (csr_contains(P.bptr, P.bcol, i, j) ? 1 : 2);
+      }
+  });
   int64_t slot = 0;
   for (int64_t i = 0; i < M; ++i)
     for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e) {
-      const int j = P.scol[static_cast<size_t>(e)];
-      P.skind[static_cast<size_t>(e)] = j == i ? 0 : (csr_contains(P.bptr, P.bcol, i, j) ? 1 : 2);
-      if (j <= i) P.sslot[static_cast<size_t>(e)] = slot++;
+      if (P.scol[static_cast<size_t>(e)] > i) break;
+      P.sslot[static_cast<size_t>(e)] = slot++;
     }
   P.nslots = slot;
-  for (int64_t i = 0; i < M; ++i)
-    for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e) {
-      const int j = P.scol[static_cast<size_t>(e)];
-      if (j <= i) continue;
-      P.sslot[static_cast<size_t>(e)] = P.sslot[static_cast<size_t>(csr_find(P.sptr, P.scol, j, static_cast<int>(i)))];
-    }
+  parallel_rows(M, [&](int64_t r0, int64_t r1) {
+    for (int64_t i = r0; i < r1; ++i)
+      for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e) {
+        const int j = P.scol[static_cast<size_t>(e)];
+        if (j <= i) continue;
+        P.sslot[static_cast<size_t>(e)] = P.sslot[static_cast<size_t>(csr_find(P.sptr, P.scol, j, static_cast<int>(i)))];
+      }
+  });
 
   P.cptr.assign(static_cast<size_t>(M + 1), 0);
   for (int64_t i = 0; i < M; ++i) {
@@ -264,12 +317,16 @@ LevelPlan plan_symbolic(int64_t M, std::vector<int64_t> bptr, std::vector<int> b
   std::iota(P.order.begin(), P.order.end(), 0);
   std::stable_sort(P.order.begin(), P.order.end(),
                    [&](int x, int y) { return P.wave[static_cast<size_t>(x)] < P.wave[static_cast<size_t>(y)]; });
+  if (prof)
+    std::fprintf(stderr, "[ce-profile] plan_symbolic M=%lld nnz=%zu: square %.1f ms, rest %.1f ms\n", static_cast<long long>(M),
+                 P.scol.size(), 1e3 * (t1 - t0), 1e3 * (now_s() - t1));
   return P;
 }
 
 // Numeric part: everything that depends on the block sizes.
 void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
   const int64_t M = P.M;
+  const double tn0 = now_s();
   P.bsz = std::move(bsz);
   P.offsets.assign(static_cast<size_t>(M + 1), 0);
   for (int64_t i = 0; i < M; ++i) P.offsets[static_cast<size_t>(i + 1)] = P.offsets[static_cast<size_t>(i)] + P.bsz[static_cast<size_t>(i)];
@@ -319,6 +376,57 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
   // (sweep.cu kPanelRows / kPanelNb bound the panel height / neighbour count)
   const int64_t cap = thresholds().small_panels ? bmax : std::max<int64_t>(bmax, std::min<int64_t>(256, buf / (2 * bmax) - 4));
   constexpr int64_t kPanelNb = 32;
+  // per-row task counts (parallel over rows), then prefix offsets
+  const Thresholds& th = thresholds();
+  std::vector<int> np_row(static_cast<size_t>(M), 0);
+  parallel_rows(M, [&](int64_t r0, int64_t r1) {
+    for (int64_t i = r0; i < r1; ++i) {
+      const size_t iu = static_cast<size_t>(i);
+      const int64_t b = P.bsz[iu];
+      // A1: TSQR leaves when the far gather is large (work ~ f b^2)
+      int64_t nfar = 0, nstrip = 0, strip_cols = 0;
+      for (int64_t e = P.sptr[iu]; e < P.sptr[iu + 1]; ++e) {
+        if (P.skind[static_cast<size_t>(e)] == 2) ++nfar;
+        if (P.skind[static_cast<size_t>(e)] != 0) {
+          ++nstrip;
+          strip_cols += P.bsz[static_cast<size_t>(P.scol[static_cast<size_t>(e)])];
+        }
+      }
+      if (P.fsum[iu] * b * b > th.leaf_work) {
+        // leaf time ~ f / n rows, combine time ~ n b rows: n ~ sqrt(f / b) balances them
+        // (leaf_cols > 0 fixes the leaf width instead)
+        const int64_t nl = th.leaf_cols > 0 ? (P.fsum[iu] + th.leaf_cols - 1) / th.leaf_cols
+                                            : static_cast<int64_t>(std::lround(std::sqrt(static_cast<double>(P.fsum[iu]) / std::max<int64_t>(b, 1))));
+        const int64_t leaves = std::min<int64_t>(nfar, nl);
+        if (leaves >= 2) P.nA1[iu] = static_cast<int>(leaves);
+      }
+      // A3: strip tasks when rotating the strip is large (work ~ S b^2)
+      if (strip_cols * b * b > th.strip_work) {
+        const int64_t tasks = std::min<int64_t>(nstrip, (strip_cols + th.strip_cols - 1) / th.strip_cols);
+        if (tasks >= 2) P.nA3[iu] = static_cast<int>(tasks);
+      }
+      // B: Schur panels of the close list (greedy, <= cap rows each)
+      int64_t np = 0, rows = 0, nbs = 0, sq2 = 0;
+      for (int64_t k = P.cptr[iu]; k < P.cptr[iu + 1]; ++k) {
+        const int64_t bt = P.bsz[static_cast<size_t>(P.ccol[static_cast<size_t>(k)])];
+        if (np == 0 || rows + bt > cap || nbs == kPanelNb) {
+          ++np;
+          rows = 0;
+          nbs = 0;
+        }
+        rows += bt;
+        ++nbs;
+        sq2 += bt * bt;
+      }
+      np_row[iu] = static_cast<int>(np);
+      // Schur pair work: sum_{s<=t in close} b_s b_t * w, with w <= b
+      const int64_t cs = P.csum[iu];
+      const int64_t work = (cs * cs + sq2) / 2 * b;
+      if (work > th.pair_inline && np * (np + 1) / 2 > 1) P.nB[iu] = static_cast<int>(np * (np + 1) / 2);
+      // with strip tasks the Schur update must follow all of them: one task runs every panel pair
+      if (P.nA3[iu] > 0 && P.nB[iu] == 0 && np > 0) P.nB[iu] = 1;
+    }
+  });
   int64_t fo = 0, bo = 0, so = 0, ro = 0;
   for (int64_t i = 0; i < M; ++i) {
     const size_t iu = static_cast<size_t>(i);
@@ -331,41 +439,22 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
     bo += b * b;
     P.sigma_off[iu] = so;
     so += std::min<int64_t>(b, P.fsum[iu]);
-    // A1: TSQR leaves when the far gather is large (work ~ f b^2)
-    int64_t nfar = 0, nstrip = 0, strip_cols = 0;
-    for (int64_t e = P.sptr[iu]; e < P.sptr[iu + 1]; ++e) {
-      if (P.skind[static_cast<size_t>(e)] == 2) ++nfar;
-      if (P.skind[static_cast<size_t>(e)] != 0) {
-        ++nstrip;
-        strip_cols += P.bsz[static_cast<size_t>(P.scol[static_cast<size_t>(e)])];
-      }
+    if (P.nA1[iu] > 0) {
+      P.rs_off[iu] = ro;
+      ro += static_cast<int64_t>(P.nA1[iu]) * b * b;
     }
-    const Thresholds& th = thresholds();
-    if (P.fsum[iu] * b * b > th.leaf_work) {
-      // leaf time ~ f / n rows, combine time ~ n b rows: n ~ sqrt(f / b) balances them
-      // (leaf_cols > 0 fixes the leaf width instead)
-      const int64_t nl = th.leaf_cols > 0 ? (P.fsum[iu] + th.leaf_cols - 1) / th.leaf_cols
-                                          : static_cast<int64_t>(std::lround(std::sqrt(static_cast<double>(P.fsum[iu]) / std::max<int64_t>(b, 1))));
-      const int64_t leaves = std::min<int64_t>(nfar, nl);
-      if (leaves >= 2) {
-        P.nA1[iu] = static_cast<int>(leaves);
-        P.rs_off[iu] = ro;
-        ro += leaves * b * b;
-      }
-    }
-    // A3: strip tasks when rotating the strip is large (work ~ S b^2)
-    if (strip_cols * b * b > th.strip_work) {
-      const int64_t tasks = std::min<int64_t>(nstrip, (strip_cols + th.strip_cols - 1) / th.strip_cols);
-      if (tasks >= 2) P.nA3[iu] = static_cast<int>(tasks);
-    }
-    // B: Schur panels of the close list (greedy, <= cap rows each)
-    int64_t np = 0;
-    {
-      int64_t rows = 0, nbs = 0;
+    P.pan_ptr[iu + 1] = P.pan_ptr[iu] + np_row[iu] + 1;
+  }
+  P.rscratch_doubles = ro;
+  P.pan_start.assign(static_cast<size_t>(P.pan_ptr[static_cast<size_t>(M)]), 0);
+  parallel_rows(M, [&](int64_t r0, int64_t r1) {
+    for (int64_t i = r0; i < r1; ++i) {
+      const size_t iu = static_cast<size_t>(i);
+      int64_t at = P.pan_ptr[iu], np = 0, rows = 0, nbs = 0;
       for (int64_t k = P.cptr[iu]; k < P.cptr[iu + 1]; ++k) {
         const int64_t bt = P.bsz[static_cast<size_t>(P.ccol[static_cast<size_t>(k)])];
         if (np == 0 || rows + bt > cap || nbs == kPanelNb) {
-          P.pan_start.push_back(static_cast<int>(k - P.cptr[iu]));
+          P.pan_start[static_cast<size_t>(at++)] = static_cast<int>(k - P.cptr[iu]);
           ++np;
           rows = 0;
           nbs = 0;
@@ -373,22 +462,9 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
         rows += bt;
         ++nbs;
       }
-      P.pan_start.push_back(static_cast<int>(P.cptr[iu + 1] - P.cptr[iu]));
-      P.pan_ptr[iu + 1] = static_cast<int64_t>(P.pan_start.size());
+      P.pan_start[static_cast<size_t>(at)] = static_cast<int>(P.cptr[iu + 1] - P.cptr[iu]);
     }
-    // Schur pair work: sum_{s<=t in close} b_s b_t * w, with w <= b
-    int64_t sq2 = 0;
-    for (int64_t k = P.cptr[iu]; k < P.cptr[iu + 1]; ++k) {
-      const int64_t bt = P.bsz[static_cast<size_t>(P.ccol[static_cast<size_t>(k)])];
-      sq2 += bt * bt;
-    }
-    const int64_t cs = P.csum[iu];
-    const int64_t work = (cs * cs + sq2) / 2 * b;
-    if (work > th.pair_inline && np * (np + 1) / 2 > 1) P.nB[iu] = static_cast<int>(np * (np + 1) / 2);
-    // with strip tasks the Schur update must follow all of them: one task runs every panel pair
-    if (P.nA3[iu] > 0 && P.nB[iu] == 0 && np > 0) P.nB[iu] = 1;
-  }
-  P.rscratch_doubles = ro;
+  });
   // Per-entry metadata the sweep tasks load in one coalesced pass (no dependent chains
   // sq_col -> bsz, sq_slot -> slot_off, close-list search on the device), the diagonal
   // entry and completion target of every row, and the entry ranges of the A1 / A3 tasks
@@ -401,37 +477,51 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
     P.target.resize(static_cast<size_t>(M));
     P.leaf_ptr.assign(static_cast<size_t>(M + 1), 0);
     P.strip_ptr.assign(static_cast<size_t>(M + 1), 0);
-    P.leaf_e.clear();
-    P.strip_e.clear();
     for (int64_t i = 0; i < M; ++i) {
       const size_t iu = static_cast<size_t>(i);
-      std::vector<int64_t> far_e, strip_e;
-      for (int64_t e = P.sptr[iu]; e < P.sptr[iu + 1]; ++e) {
-        const size_t eu = static_cast<size_t>(e);
-        const int j = P.scol[eu];
-        P.sboff[eu] = P.slot_off[static_cast<size_t>(P.sslot[eu])];
-        P.sbsz[eu] = P.bsz[static_cast<size_t>(j)];
-        if (P.skind[eu] == 1) {
-          const int64_t k = csr_find(P.cptr, P.ccol, i, j);
-          P.sroff[eu] = P.croff[static_cast<size_t>(k)];
-        }
-        if (P.skind[eu] == 2) far_e.push_back(e);
-        if (P.skind[eu] != 0) strip_e.push_back(e);
-      }
       P.target[iu] = 1 + P.nA1[iu] + P.nA3[iu] + P.nB[iu];
-      const int64_t pend = P.sptr[iu + 1];
-      const int64_t nf = static_cast<int64_t>(far_e.size()), ns = static_cast<int64_t>(strip_e.size());
-      for (int k = 0; k <= P.nA1[iu]; ++k) {
-        const int64_t o = P.nA1[iu] > 0 ? nf * k / P.nA1[iu] : 0;
-        P.leaf_e.push_back(o < nf ? far_e[static_cast<size_t>(o)] : pend);
-      }
-      P.leaf_ptr[iu + 1] = static_cast<int64_t>(P.leaf_e.size());
-      for (int k = 0; k <= P.nA3[iu]; ++k) {
-        const int64_t o = P.nA3[iu] > 0 ? ns * k / P.nA3[iu] : 0;
-        P.strip_e.push_back(o < ns ? strip_e[static_cast<size_t>(o)] : pend);
-      }
-      P.strip_ptr[iu + 1] = static_cast<int64_t>(P.strip_e.size());
+      P.leaf_ptr[iu + 1] = P.leaf_ptr[iu] + P.nA1[iu] + 1;
+      P.strip_ptr[iu + 1] = P.strip_ptr[iu] + P.nA3[iu] + 1;
     }
+    P.leaf_e.assign(static_cast<size_t>(P.leaf_ptr[static_cast<size_t>(M)]), 0);
+    P.strip_e.assign(static_cast<size_t>(P.strip_ptr[static_cast<size_t>(M)]), 0);
+    parallel_rows(M, [&](int64_t r0, int64_t r1) {
+      for (int64_t i = r0; i < r1; ++i) {
+        const size_t iu = static_cast<size_t>(i);
+        int64_t nf = 0, ns = 0;
+        for (int64_t e = P.sptr[iu]; e < P.sptr[iu + 1]; ++e) {
+          const size_t eu = static_cast<size_t>(e);
+          const int j = P.scol[eu];
+          P.sboff[eu] = P.slot_off[static_cast<size_t>(P.sslot[eu])];
+          P.sbsz[eu] = P.bsz[static_cast<size_t>(j)];
+          if (P.skind[eu] == 1) {
+            const int64_t k = csr_find(P.cptr, P.ccol, i, j);
+            P.sroff[eu] = P.croff[static_cast<size_t>(k)];
+          }
+          nf += P.skind[eu] == 2;
+          ns += P.skind[eu] != 0;
+        }
+        // first entry of the leaf / strip task with ordinal o = n k / parts (row end if none)
+        const int64_t pend = P.sptr[iu + 1];
+        const int na1 = P.nA1[iu], na3 = P.nA3[iu];
+        int kl = 0, ks = 0;
+        int64_t of = 0, os = 0;
+        auto next_o = [](int64_t n, int k, int parts) { return parts > 0 ? n * k / parts : 0; };
+        for (int64_t e = P.sptr[iu]; e < pend; ++e) {
+          const unsigned char kind = P.skind[static_cast<size_t>(e)];
+          if (kind == 2) {
+            while (kl <= na1 && next_o(nf, kl, na1) == of && of < nf) P.leaf_e[static_cast<size_t>(P.leaf_ptr[iu] + kl++)] = e;
+            ++of;
+          }
+          if (kind != 0) {
+            while (ks <= na3 && next_o(ns, ks, na3) == os && os < ns) P.strip_e[static_cast<size_t>(P.strip_ptr[iu] + ks++)] = e;
+            ++os;
+          }
+        }
+        while (kl <= na1) P.leaf_e[static_cast<size_t>(P.leaf_ptr[iu] + kl++)] = pend;
+        while (ks <= na3) P.strip_e[static_cast<size_t>(P.strip_ptr[iu] + ks++)] = pend;
+      }
+    });
   }
   // ticket order of the row tasks (wave order from the symbolic plan)
   {
@@ -483,6 +573,8 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
   P.fac_doubles = fo;
   P.basis_doubles = bo;
   P.sigma_doubles = so;
+  if (std::getenv("CE_PROFILE") && std::getenv("CE_PROFILE")[0] == '1')
+    std::fprintf(stderr, "[ce-profile] plan_numeric M=%lld: %.1f ms\n", static_cast<long long>(M), 1e3 * (now_s() - tn0));
 }
 
 LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vector<int> bcol) {
