@@ -378,6 +378,9 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
   constexpr int64_t kPanelNb = 32;
   // per-row task counts (parallel over rows), then prefix offsets
   const Thresholds& th = thresholds();
+  const int64_t kcap = sweep_kcap(static_cast<int>(bmax));
+  const int64_t lcols = th.leaf_cols > 0 ? th.leaf_cols : kcap;  // far columns per TSQR leaf
+  P.nleaf.assign(static_cast<size_t>(M), 0);
   std::vector<int> np_row(static_cast<size_t>(M), 0);
   parallel_rows(M, [&](int64_t r0, int64_t r1) {
     for (int64_t i = r0; i < r1; ++i) {
@@ -392,13 +395,29 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
           strip_cols += P.bsz[static_cast<size_t>(P.scol[static_cast<size_t>(e)])];
         }
       }
-      if (P.fsum[iu] * b * b > th.leaf_work) {
-        // leaf time ~ f / n rows, combine time ~ n b rows: n ~ sqrt(f / b) balances them
-        // (leaf_cols > 0 fixes the leaf width instead)
-        const int64_t nl = th.leaf_cols > 0 ? (P.fsum[iu] + th.leaf_cols - 1) / th.leaf_cols
-                                            : static_cast<int64_t>(std::lround(std::sqrt(static_cast<double>(P.fsum[iu]) / std::max<int64_t>(b, 1))));
-        const int64_t leaves = std::min<int64_t>(nfar, nl);
-        if (leaves >= 2) P.nA1[iu] = static_cast<int>(leaves);
+      if (P.fsum[iu] * b * b > th.leaf_work && P.fsum[iu] > lcols) {
+        // TSQR tree: leaves of <= lcols far columns (greedy over the far blocks), then
+        // levels combining F = max(2, kcap / b) triangles each, down to one triangle
+        int64_t n0 = 0, cols = 0;
+        for (int64_t e = P.sptr[iu]; e < P.sptr[iu + 1]; ++e) {
+          if (P.skind[static_cast<size_t>(e)] != 2) continue;
+          const int64_t bj = P.bsz[static_cast<size_t>(P.scol[static_cast<size_t>(e)])];
+          if (n0 == 0 || cols + bj > lcols) {
+            ++n0;
+            cols = 0;
+          }
+          cols += bj;
+        }
+        if (n0 >= 2) {
+          const int64_t F = std::max<int64_t>(2, kcap / std::max<int64_t>(b, 1));
+          int64_t items = 0;
+          for (int64_t n = n0;; n = (n + F - 1) / F) {
+            items += n;
+            if (n == 1) break;
+          }
+          P.nleaf[iu] = static_cast<int>(n0);
+          P.nA1[iu] = static_cast<int>(items);
+        }
       }
       // A3: strip tasks when rotating the strip is large (work ~ S b^2)
       if (strip_cols * b * b > th.strip_work) {
@@ -480,7 +499,7 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
     for (int64_t i = 0; i < M; ++i) {
       const size_t iu = static_cast<size_t>(i);
       P.target[iu] = 1 + P.nA1[iu] + P.nA3[iu] + P.nB[iu];
-      P.leaf_ptr[iu + 1] = P.leaf_ptr[iu] + P.nA1[iu] + 1;
+      P.leaf_ptr[iu + 1] = P.leaf_ptr[iu] + P.nleaf[iu] + 1;
       P.strip_ptr[iu + 1] = P.strip_ptr[iu] + P.nA3[iu] + 1;
     }
     P.leaf_e.assign(static_cast<size_t>(P.leaf_ptr[static_cast<size_t>(M)]), 0);
@@ -501,25 +520,31 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
           nf += P.skind[eu] == 2;
           ns += P.skind[eu] != 0;
         }
-        // first entry of the leaf / strip task with ordinal o = n k / parts (row end if none)
+        // leaf boundaries: greedy packing of the far blocks into <= lcols columns (as counted);
+        // strip task k starts at the strip entry with ordinal ns k / nA3 (row end if none)
         const int64_t pend = P.sptr[iu + 1];
-        const int na1 = P.nA1[iu], na3 = P.nA3[iu];
+        const int nl = P.nleaf[iu], na3 = P.nA3[iu];
         int kl = 0, ks = 0;
-        int64_t of = 0, os = 0;
+        int64_t os = 0, cols = 0;
         auto next_o = [](int64_t n, int k, int parts) { return parts > 0 ? n * k / parts : 0; };
         for (int64_t e = P.sptr[iu]; e < pend; ++e) {
           const unsigned char kind = P.skind[static_cast<size_t>(e)];
-          if (kind == 2) {
-            while (kl <= na1 && next_o(nf, kl, na1) == of && of < nf) P.leaf_e[static_cast<size_t>(P.leaf_ptr[iu] + kl++)] = e;
-            ++of;
+          if (kind == 2 && nl > 0) {
+            const int64_t bj = P.sbsz[static_cast<size_t>(e)];
+            if (kl == 0 || cols + bj > lcols) {
+              P.leaf_e[static_cast<size_t>(P.leaf_ptr[iu] + kl++)] = e;
+              cols = 0;
+            }
+            cols += bj;
           }
           if (kind != 0) {
             while (ks <= na3 && next_o(ns, ks, na3) == os && os < ns) P.strip_e[static_cast<size_t>(P.strip_ptr[iu] + ks++)] = e;
             ++os;
           }
         }
-        while (kl <= na1) P.leaf_e[static_cast<size_t>(P.leaf_ptr[iu] + kl++)] = pend;
+        while (kl <= nl) P.leaf_e[static_cast<size_t>(P.leaf_ptr[iu] + kl++)] = pend;
         while (ks <= na3) P.strip_e[static_cast<size_t>(P.strip_ptr[iu] + ks++)] = pend;
+        (void)nf;
       }
     });
   }
@@ -755,7 +780,7 @@ namespace {
 
 // Device copy of a plan's symbolic arrays (freed after the level).
 struct DevPlan {
-  DevArray<int> bsz, scol, ccol, croff, order, nA1, nA3, nB, pan_start, item_row, item_part, sbsz, sroff, target;
+  DevArray<int> bsz, scol, ccol, croff, order, nA1, nA3, nB, pan_start, item_row, item_part, sbsz, sroff, target, nleaf;
   DevArray<int64_t> sptr, sslot, slot_off, cptr, chol_off, g_off, basis_off, sigma_off, item_start, offsets, cl_slot,
       fsum, rs_off, pan_ptr, sboff, sdiag, leaf_ptr, leaf_e, strip_ptr, strip_e;
   DevArray<unsigned char> skind;
@@ -764,6 +789,7 @@ struct DevPlan {
     item_row.upload(P.item_row, s);
     item_part.upload(P.item_part, s);
     nA1.upload(P.nA1, s);
+    nleaf.upload(P.nleaf, s);
     nA3.upload(P.nA3, s);
     nB.upload(P.nB, s);
     pan_start.upload(P.pan_start, s);
@@ -1020,6 +1046,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     a.item_row = dcur.item_row.p;
     a.item_part = dcur.item_part.p;
     a.nA1 = dcur.nA1.p;
+    a.nleaf = dcur.nleaf.p;
     a.nA3 = dcur.nA3.p;
     a.nB = dcur.nB.p;
     a.fsum = dcur.fsum.p;
@@ -1083,6 +1110,13 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       d_prof.zero(s);
       a.prof = d_prof.p;
     }
+    DevArray<unsigned long long> d_trace;
+    static const int trace_level = std::getenv("CE_TRACE") ? std::atoi(std::getenv("CE_TRACE")) : 0;
+    if (trace_level == static_cast<int>(li) + 1) {
+      d_trace.alloc(static_cast<size_t>(4 * cur.n_items));
+      d_trace.zero(s);
+      a.trace = d_trace.p;
+    }
     Events ev_lvl, ev_sw;
     const double h_t1 = now_s();
     CE_CUDA(cudaEventRecord(ev_lvl.a, s));
@@ -1107,7 +1141,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       d_prof.download(hp, s);
       CE_CUDA(cudaStreamSynchronize(s));
       const char* names[] = {"wait", "A1", "A2", "A2.tsqr", "A2.svd", "A2.basis", "A2.pivot", "A2.strip", "A2.panels",
-                             "A3", "B", "nA1", "nA2", "nA3", "nB", "svd.pre", "svd.jac", "svd.post", "sweeps", "svds"};
+                             "A3", "B", "nA1", "nA2", "nA3", "nB", "svd.pre", "svd.jac", "svd.post", "sweeps", "svds", "B.setup", "B.stage", "B.tiles"};
       std::fprintf(stderr, "[ce-profile] level %zu M=%lld grid=%d waves=%lld items=%lld sweep=%.3f ms |", li + 1,
                    static_cast<long long>(cur.M), grid, static_cast<long long>(cur.n_waves),
                    static_cast<long long>(cur.n_items), 1e3 * ev_sw.seconds());
@@ -1117,6 +1151,24 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     }
     if (herr[0] == kErrPattern) throw std::logic_error("update outside the squared pattern");
     if (herr[0] != 0) throw std::logic_error("internal sweep error");
+    if (a.trace) {  // development trace: items (row, part) + timestamps -> CE_TRACE_FILE
+      std::vector<unsigned long long> tr;
+      d_trace.download(tr, s);
+      CE_CUDA(cudaStreamSynchronize(s));
+      const char* path = std::getenv("CE_TRACE_FILE") ? std::getenv("CE_TRACE_FILE") : "/tmp/ce_trace.bin";
+      if (FILE* fp = std::fopen(path, "wb")) {
+        const int64_t n = cur.n_items, m = cur.M;
+        std::fwrite(&n, sizeof n, 1, fp);
+        std::fwrite(&m, sizeof m, 1, fp);
+        std::fwrite(cur.item_row.data(), sizeof(int), static_cast<size_t>(n), fp);
+        std::fwrite(cur.item_part.data(), sizeof(int), static_cast<size_t>(n), fp);
+        std::fwrite(cur.nA1.data(), sizeof(int), static_cast<size_t>(cur.M), fp);
+        std::fwrite(cur.nA3.data(), sizeof(int), static_cast<size_t>(cur.M), fp);
+        std::fwrite(cur.wave.data(), sizeof(int64_t), static_cast<size_t>(cur.M), fp);
+        std::fwrite(tr.data(), sizeof(unsigned long long), tr.size(), fp);
+        std::fclose(fp);
+      }
+    }
     launch_pending_rotation(a, s);
     CE_CUDA(cudaGetLastError());
     LF.d_rank.download(LF.rank, s);

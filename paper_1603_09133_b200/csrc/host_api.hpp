@@ -132,6 +132,7 @@ struct LevelPlan {
   std::vector<int64_t> wave;         // wave index of every row
   std::vector<int> item_row, item_part;  // ticket -> (row, task index within the row)
   std::vector<int> nA1, nA3, nB;     // per-row task counts (sweep.cu header)
+  std::vector<int> nleaf;            // per-row TSQR tree leaves (nA1 = all tree nodes)
   std::vector<int64_t> pan_ptr, rs_off;
   std::vector<int> pan_start;
   int64_t rscratch_doubles = 0;

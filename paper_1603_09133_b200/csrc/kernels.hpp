@@ -49,7 +49,8 @@ struct SweepArgs {
   const int* order;           // rows in wave order
   const int* item_row;        // ticket -> row
   const int* item_part;       // ticket -> task index within the row
-  const int* nA1;             // TSQR leaf tasks per row (0 = gather inside A2)
+  const int* nA1;             // TSQR tree tasks per row (0 = gather inside A2): leaves, then combine levels
+  const int* nleaf;           // TSQR tree leaves per row
   const int* nA3;             // strip tasks per row (0 = strip inside A2)
   const int* nB;              // Schur panel-pair tasks per row (0 = inline)
   const int64_t* fsum;        // far columns per row
@@ -84,13 +85,14 @@ struct SweepArgs {
   int use_global_scratch;
   int dbg;  // CE_DBG bitmask (development): 1 generic TSQR, 2 generic Jacobi
   unsigned long long* prof;  // CE_PROFILE=1: per-stage SM-cycle counters (kProf*), else nullptr
+  unsigned long long* trace; // CE_TRACE=<level>: per item {claim, run, end (globaltimer ns), smid}, else nullptr
 };
 
 // Cycle counters of the sweep kernel (CE_PROFILE=1).
 enum : int {
   kProfWait = 0, kProfA1, kProfA2, kProfA2Tsqr, kProfA2Svd, kProfA2Basis, kProfA2Pivot, kProfA2Strip,
   kProfA2Panels, kProfA3, kProfB, kProfNA1, kProfNA2, kProfNA3, kProfNB, kProfSvdPre, kProfSvdJac, kProfSvdPost,
-  kProfSweeps, kProfSvds, kProfCount
+  kProfSweeps, kProfSvds, kProfBSetup, kProfBStage, kProfBTiles, kProfCount
 };
 
 // smem doubles needed by one sweep CTA for a level

@@ -234,6 +234,145 @@ __device__ __noinline__ void tsqr_reg_t(double* R, double* C, int K, int b, int 
   }
 }
 
+// Blocked TSQR update (same contract as tsqr_update): panels of NB columns are factored
+// by warp 0 alone (rows spread over lanes, columns in registers: no CTA barrier inside
+// the panel), then every group applies the panel's NB reflectors to the columns it keeps
+// in registers (reflectors read-only in shared memory: no barriers between them).  Two
+// barriers per panel instead of one per column.
+template <int G, int E, int NC, int NB>
+__device__ __noinline__ void tsqr_blk_t(double* R, double* C, int K, int b, int ldc, double* shr) {
+  CE_SHARED(R);
+  CE_SHARED(C);
+  constexpr int NG = T / G;
+  constexpr int EP = 4;  // panel rows per lane (K <= 128)
+  constexpr unsigned kFull = 0xffffffffu;
+  __shared__ double ptau[NB];
+  const int tid = threadIdx.x, grp = tid / G, gl = tid % G, warp = tid >> 5, lane = tid & 31;
+  double x[NC][E];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = grp + c * NG;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int m = gl + e * G;
+      x[c][e] = (j < b && m < K) ? C[static_cast<int64_t>(j) * ldc + m] : 0.0;
+    }
+  }
+  for (int p0 = 0; p0 < b; p0 += NB) {
+    const int nb = b - p0 < NB ? b - p0 : NB;
+    if (p0 > 0) {  // owners publish the (updated) panel columns
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int j = grp + c * NG;
+        if (j >= p0 && j < p0 + nb)
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int m = gl + e * G;
+            if (m < K) C[static_cast<int64_t>(j) * ldc + m] = x[c][e];
+          }
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double pc[NB][EP];
+#pragma unroll
+      for (int jj = 0; jj < NB; ++jj)
+#pragma unroll
+        for (int e = 0; e < EP; ++e) {
+          const int m = lane + 32 * e;
+          pc[jj][e] = (jj < nb && m < K) ? C[static_cast<int64_t>(p0 + jj) * ldc + m] : 0.0;
+        }
+#pragma unroll
+      for (int kk = 0; kk < NB; ++kk) {
+        if (kk >= nb) break;
+        const int k = p0 + kk;
+        double ss = 0.0;
+#pragma unroll
+        for (int e = 0; e < EP; ++e) ss = fma(pc[kk][e], pc[kk][e], ss);
+        const double x0 = R[k * b + k];
+        ss = warp_sum(ss);
+        double t = 0.0;
+        if (ss > 0.0) {
+          const double n2 = fma(x0, x0, ss);
+          const bool fast = n2 > 1e-290 && n2 < 1e290;
+          const double nrm = fast ? n2 * rsqrt_nr(n2) : sqrt(n2);
+          const double beta = x0 >= 0.0 ? -nrm : nrm;
+          const double den = x0 - beta;
+          const double scale = fast ? rcp_nr(den) : 1.0 / den;
+          t = fast ? -den * rcp_nr(beta) : (beta - x0) / beta;
+#pragma unroll
+          for (int e = 0; e < EP; ++e) pc[kk][e] *= scale;
+          __syncwarp();
+          if (lane == 0) R[k * b + k] = beta;
+        }
+        if (lane == 0) ptau[kk] = t;
+        if (t != 0.0) {
+          double dsum[NB];
+#pragma unroll
+          for (int jj = 0; jj < NB; ++jj) {
+            dsum[jj] = 0.0;
+            if (jj > kk)
+#pragma unroll
+              for (int e = 0; e < EP; ++e) dsum[jj] = fma(pc[kk][e], pc[jj][e], dsum[jj]);
+          }
+#pragma unroll
+          for (int jj = 0; jj < NB; ++jj)
+            if (jj > kk) dsum[jj] = warp_sum(dsum[jj]);
+#pragma unroll
+          for (int jj = 0; jj < NB; ++jj) {
+            if (jj <= kk || jj >= nb) continue;
+            const double rkj = R[(p0 + jj) * b + k];
+            const double d = t * (rkj + dsum[jj]);
+#pragma unroll
+            for (int e = 0; e < EP; ++e) pc[jj][e] = fma(-d, pc[kk][e], pc[jj][e]);
+            __syncwarp();
+            if (lane == 0) R[(p0 + jj) * b + k] = rkj - d;
+          }
+        }
+      }
+      // reflector tails back to the panel columns of C
+#pragma unroll
+      for (int jj = 0; jj < NB; ++jj)
+#pragma unroll
+        for (int e = 0; e < EP; ++e) {
+          const int m = lane + 32 * e;
+          if (jj < nb && m < K) C[static_cast<int64_t>(p0 + jj) * ldc + m] = pc[jj][e];
+        }
+    }
+    __syncthreads();
+    // trailing columns: apply the panel's reflectors (read-only) without barriers
+    for (int kk = 0; kk < nb; ++kk) {
+      const double t = ptau[kk];
+      if (t == 0.0) continue;
+      const int k = p0 + kk;
+      const double* Ck = C + static_cast<int64_t>(k) * ldc;
+      double v[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int m = gl + e * G;
+        v[e] = m < K ? Ck[m] : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int j = grp + c * NG;
+        double sd = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) sd = fma(v[e], x[c][e], sd);
+        sd = group_sum<G>(sd, kFull);
+        if (j >= p0 + nb && j < b) {
+          const double rkj = R[j * b + k];
+          const double d = t * (rkj + sd);
+#pragma unroll
+          for (int e = 0; e < E; ++e) x[c][e] = fma(-d, v[e], x[c][e]);
+          if (gl == 0) R[j * b + k] = rkj - d;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  (void)shr;
+}
+
 // Dispatch: register-resident variants for b <= 64 and K <= 128, else the generic one.
 __device__ void tsqr_fast(double* R, double* C, int K, int b, int ldc, double* shr) {
   if (K <= 128 && b <= 16) tsqr_reg_t<16, 8, 1>(R, C, K, b, ldc, shr);
@@ -1095,6 +1234,7 @@ __device__ __noinline__ void strip_range(const SweepArgs& A, int i, int b, int r
 // g rows of both panels are staged in shared memory.
 __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int w, int P, int Q, double* sm) {
   CE_SHARED(sm);
+  const long long tb0 = clock64();
   __shared__ long long slot_tab[kPanelNb * kPanelNb];  // value offset of stored (t, s), -1: not updated
   __shared__ int tab_bs[kPanelNb];
   __shared__ int roff_s[kPanelNb], roff_t[kPanelNb];
@@ -1157,22 +1297,41 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
     slot_tab[idx] = off;
   }
   __syncthreads();
+  const long long tb1 = clock64();
+  prof_add(A, kProfBSetup, tb1 - tb0);
   const int rsn = n_live[0], rtn = n_live[1];
   const int lds = (rsn + 3) & ~3, ldt = (rtn + 3) & ~3;
   // g rows transposed into shared memory: GsT[q][y], GtT[q][x] (live rows only)
   const double* G = A.fac + A.g_off[i];
   double* GsT = sm;
   double* GtT = P == Q ? sm : sm + static_cast<int64_t>(lds) * w;
-  for (int idx = tid; idx < lds * w; idx += T) {
-    const int y = idx / w, q = idx % w;
-    GsT[q * lds + y] = y < rsn ? ldg(G + static_cast<int64_t>(r + roff_s[yblk[y]] + yloc[y]) * w + q) : 0.0;
-  }
-  if (P != Q)
-    for (int idx = tid; idx < ldt * w; idx += T) {
-      const int x = idx / w, q = idx % w;
-      GtT[q * ldt + x] = x < rtn ? ldg(G + static_cast<int64_t>(r + roff_t[xblk[x]] + xloc[x]) * w + q) : 0.0;
+  // staged with 4 independent loads in flight per thread (the rows are short, latency dominates)
+  auto stage = [&](double* dst, int ld, int n, const int* roff, const unsigned char* blk, const unsigned short* loc) {
+    const int tot = ld * w;
+    for (int base = tid; base < tot; base += 4 * T) {
+      double v[4];
+      int di[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = base + u * T;
+        di[u] = -1;
+        v[u] = 0.0;
+        if (idx < tot) {
+          const int y = idx / w, q = idx % w;
+          di[u] = q * ld + y;
+          if (y < n) v[u] = ldg(G + static_cast<int64_t>(r + roff[blk[y]] + loc[y]) * w + q);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (di[u] >= 0) dst[di[u]] = v[u];
     }
+  };
+  stage(GsT, lds, rsn, roff_s, yblk, yloc);
+  if (P != Q) stage(GtT, ldt, rtn, roff_t, xblk, xloc);
   __syncthreads();
+  const long long tb2 = clock64();
+  prof_add(A, kProfBStage, tb2 - tb1);
   // rtn x rsn outer product in 4x4 register tiles; epilogue scatters into the (t, s) blocks
   const int mx = ldt / 4, my = lds / 4;
   for (int mt = tid; mt < mx * my; mt += T) {
@@ -1222,6 +1381,7 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
         if (xp[a][c]) *xp[a][c] = xv[a][c] - acc[a][c];
   }
   __syncthreads();
+  prof_add(A, kProfBTiles, clock64() - tb2);
 }
 
 __device__ void all_panels(const SweepArgs& A, int i, int r, int w, double* sm) {
@@ -1255,19 +1415,9 @@ __device__ void task_a2(const SweepArgs& A, int i, const Buf& s_, int nA1, int n
     fcols = gather_tsqr(A, i, b, s, p0, p1, &sflag[0], shr, W);
   } else {
     fcols = static_cast<int>(A.fsum[i]);
-    // fold the leaf triangles, as many per chunk as fit (chunk rows <= kcap)
-    const int per = A.kcap / b > 0 ? A.kcap / b : 1;
-    for (int k0 = 0; k0 < nA1; k0 += per) {
-      const int nk = nA1 - k0 < per ? nA1 - k0 : per;
-      const int K = nk * b;
-      for (int idx = tid; idx < K * b; idx += T) {
-        const int j = idx / K, m = idx % K;  // chunk element (m, j) = R_{k0 + m/b}[m%b][j]
-        const double* Rk = A.rscratch + A.rs_off[i] + static_cast<int64_t>(k0 + m / b) * b * b;
-        s.C[static_cast<int64_t>(j) * chunk_ld(A.kcap) + m] = ldg(Rk + j * b + m % b);
-      }
-      __syncthreads();
-      tsqr_sel(A, s.R, s.C, K, b, chunk_ld(A.kcap), shr);
-    }
+    // the TSQR tree's root triangle (its last node)
+    const double* Rr = A.rscratch + A.rs_off[i] + static_cast<int64_t>(nA1 - 1) * b * b;
+    for (int idx = tid; idx < b * b; idx += T) s.R[idx] = ldg(Rr + idx);
     if (tid == 0) sflag[0] = ld_acquire(A.nzflag + i);
     __syncthreads();
   }
@@ -1533,14 +1683,32 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
     if (s_stop) break;
     const long long item = s_item;
     if (item >= A.n_items) break;
+    if (A.trace && threadIdx.x == 0) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      A.trace[4 * item] = g;
+    }
     const int i = A.item_row[item];
     const int part = A.item_part[item];
     const int nA1 = A.nA1[i], nA3 = A.nA3[i], nB = A.nB[i];
     // stage of the item and the number of this row's items it must wait for
     int stage, k = 0, need = 0;
+    int tlev = 0, tprev = 0, tprevn = 0;  // TSQR tree: level, first node / size of the level below
     if (part < nA1) {
       stage = 1;
-      k = part;
+      // node `part` of the TSQR tree: leaves first, then levels of F-way combines
+      const int F = A.kcap / A.bsz[i] > 2 ? A.kcap / A.bsz[i] : 2;
+      int n = A.nleaf[i], start = 0, p = part;
+      while (p >= n) {
+        p -= n;
+        tprev = start;
+        tprevn = n;
+        start += n;
+        n = (n + F - 1) / F;
+        ++tlev;
+      }
+      k = p;
+      need = start;  // combines wait for every node of the levels below
     } else if (part == nA1) {
       stage = 2;
       need = nA1;
@@ -1553,7 +1721,7 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
       k = part - nA1 - 1 - nA3;
       need = nA1 + 1 + nA3;
     }
-    const bool first = (stage == 1) || (stage == 2 && nA1 == 0);
+    const bool first = (stage == 1 && tlev == 0) || (stage == 2 && nA1 == 0);
     const long long t_wait = clock64();
     if (first) {
       // every predecessor j < i of sq(i) finished (one poller per entry, in parallel)
@@ -1588,14 +1756,45 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
     if (s_stop) break;
     const long long t_run = clock64();
     prof_add(A, kProfWait, t_run - t_wait);
+    if (A.trace && threadIdx.x == 0) {
+      unsigned long long g;
+      unsigned sm;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      A.trace[4 * item + 1] = g;
+      A.trace[4 * item + 3] = sm;
+    }
     if (stage == 1) {
       const int b = A.bsz[i];
       for (int idx = threadIdx.x; idx < b * b; idx += T) s.R[idx] = 0.0;
       __syncthreads();
-      // far-entry range of this leaf
-      const int64_t* le = A.leaf_e + A.leaf_ptr[i] + k;
-      gather_tsqr(A, i, b, s, le[0], le[1], &nz, shr, W);
-      double* Rk = A.rscratch + A.rs_off[i] + static_cast<int64_t>(k) * b * b;
+      if (tlev == 0) {
+        // leaf: far-entry range of this leaf
+        const int64_t* le = A.leaf_e + A.leaf_ptr[i] + k;
+        gather_tsqr(A, i, b, s, le[0], le[1], &nz, shr, W);
+      } else {
+        // combine the F child triangles (tree nodes tprev + F k ...): the first becomes R,
+        // the others are folded in as stacked chunks of <= kcap rows
+        const int F = A.kcap / b > 2 ? A.kcap / b : 2;
+        const int per = A.kcap / b > 1 ? A.kcap / b : 1;
+        const int c0 = F * k, nc = tprevn - c0 < F ? tprevn - c0 : F;
+        const int ldc = chunk_ld(A.kcap);
+        const double* R0 = A.rscratch + A.rs_off[i] + static_cast<int64_t>(tprev + c0) * b * b;
+        for (int idx = threadIdx.x; idx < b * b; idx += T) s.R[idx] = ldg(R0 + idx);
+        __syncthreads();
+        for (int f0 = 1; f0 < nc; f0 += per) {
+          const int nk = nc - f0 < per ? nc - f0 : per;
+          const int K = nk * b;
+          const double* Rf = R0 + static_cast<int64_t>(f0) * b * b;
+          for (int idx = threadIdx.x; idx < K * b; idx += T) {
+            const int j = idx / K, m = idx % K;  // chunk element (m, j) = R_child(m / b)[m % b][j]
+            s.C[static_cast<int64_t>(j) * ldc + m] = ldg(Rf + static_cast<int64_t>(m / b) * b * b + j * b + m % b);
+          }
+          __syncthreads();
+          tsqr_sel(A, s.R, s.C, K, b, ldc, shr);
+        }
+      }
+      double* Rk = A.rscratch + A.rs_off[i] + static_cast<int64_t>(part) * b * b;
       for (int idx = threadIdx.x; idx < b * b; idx += T) Rk[idx] = s.R[idx];
       if (threadIdx.x == 0 && nz) atomicOr(A.nzflag + i, 1);
     } else if (stage == 2) {
@@ -1627,6 +1826,11 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
       prof_add(A, stage == 1 ? kProfNA1 : stage == 2 ? kProfNA2 : stage == 3 ? kProfNA3 : kProfNB, 1);
     }
     if (threadIdx.x == 0) {
+      if (A.trace) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        A.trace[4 * item + 2] = g;
+      }
       __threadfence();
       atomicAdd(A.done + i, 1);
     }

@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(T) micro_kernel(int which, int b, int K, int r
   int nsw_tot = 0;
   for (int rep = 0; rep < reps; ++rep) {
     const uint64_t seed = (static_cast<uint64_t>(blockIdx.x) * 1000003ull + rep) * 7919ull;
-    if (which != 3 && which != 13 && which < 30) {
+    if (which != 3 && which != 13 && (which < 30 || which >= 40)) {
       for (int idx = threadIdx.x; idx < b * b; idx += T) R[idx] = 0.0;
       for (int idx = threadIdx.x; idx < K * b; idx += T) C[(idx / K) * ldc + idx % K] = hrand(seed + idx);
     } else {
@@ -431,6 +431,11 @@ __global__ void __launch_bounds__(T) micro_kernel(int which, int b, int K, int r
     else if (which == 20) tsqr_reg_t<16, 8, 1>(R, C, K, b, ldc, shr);
     else if (which == 21) tsqr_stamp_t<16, 8, 1>(R, C, K, b, ldc, shr);
     else if (which == 23) tsqr_abl_t<16, 8, 1, 0>(R, C, K, b, ldc, shr);
+    else if (which == 40) tsqr_blk_t<16, 8, 1, 8>(R, C, K, b, ldc, shr);
+    else if (which == 41) tsqr_blk_t<8, 16, 1, 8>(R, C, K, b, ldc, shr);
+    else if (which == 42) tsqr_blk_t<8, 16, 2, 4>(R, C, K, b, ldc, shr);
+    else if (which == 43) tsqr_blk_t<8, 16, 2, 8>(R, C, K, b, ldc, shr);
+    else if (which == 44) tsqr_blk_t<16, 8, 3, 8>(R, C, K, b, ldc, shr);
     else if (which == 30) nsw_tot += jacobi_t<1, 16>(R, V, b, ld, b);
     else if (which == 31) nsw_tot += jacobi_t<2, 8>(R, V, b, ld, b);
     else if (which == 32) nsw_tot += jacobi_t<4, 4>(R, V, b, ld, b);
@@ -452,7 +457,7 @@ __global__ void __launch_bounds__(T) micro_kernel(int which, int b, int K, int r
     cyc[blockIdx.x] = acc / reps;
     sweeps[blockIdx.x] = nsw_tot;
     if (blockIdx.x == 0)
-      for (int k = 0; k < b; ++k) out[k] = (which != 3 && which != 13 && which < 30) ? fabs(R[k * b + k]) : R[k * ld + k];
+      for (int k = 0; k < b; ++k) out[k] = (which != 3 && which != 13 && (which < 30 || which >= 40)) ? fabs(R[k * b + k]) : R[k * ld + k];
   }
 }
 
@@ -573,8 +578,8 @@ int main() {
     }
   }
   struct Case { int which, b, K; };
-  const Case cases[] = {{30, 16, 0}, {31, 16, 0}, {32, 16, 0}, {33, 16, 0}, {34, 16, 0}, {35, 40, 0}, {36, 40, 0}, {37, 40, 0}, {38, 40, 0}};
-  const char* names[] = {"tsqr_warps", "tsqr_update", "tsqr_group", "jacobi", "tsqr_g4", "tsqr_g16", "tsqr_g32", "noprep", "noupdate", "fastdiv", "probe_full", "stamp", "tsqr_fast", "jacobi_fast", "reg16x8x3", "reg8x16x2", "reg4x32x1", "reg16x8x4", "reg32x4x6", "reg8x16x1", "reg16x8x1", "stamp16", "stamp40", "abl_full", "abl_noprep", "abl_noupd", "abl_none", "", "", "", "j1x16", "j2x8", "j4x4", "j8x2", "j16x1", "j1x40", "j2x20", "j4x10", "j8x5"};
+  const Case cases[] = {{12, 16, 128}, {40, 16, 128}, {12, 16, 48}, {40, 16, 48}, {12, 32, 128}, {41, 32, 128}, {12, 40, 104}, {42, 40, 104}, {43, 40, 104}, {44, 40, 104}, {12, 40, 120}, {42, 40, 120}};
+  const char* names[] = {"tsqr_warps", "tsqr_update", "tsqr_group", "jacobi", "tsqr_g4", "tsqr_g16", "tsqr_g32", "noprep", "noupdate", "fastdiv", "probe_full", "stamp", "tsqr_fast", "jacobi_fast", "reg16x8x3", "reg8x16x2", "reg4x32x1", "reg16x8x4", "reg32x4x6", "reg8x16x1", "reg16x8x1", "stamp16", "stamp40", "abl_full", "abl_noprep", "abl_noupd", "abl_none", "", "", "", "j1x16", "j2x8", "j4x4", "j8x2", "j16x1", "j1x40", "j2x20", "j4x10", "j8x5", "", "blk16", "blk32", "blk40nb4", "blk40nb8", "blk40g16"};
   const int only = getenv("MICRO_CASE") ? atoi(getenv("MICRO_CASE")) : -1;
   for (const Case& c : cases) {
     if (only >= 0 && c.which != only) continue;
@@ -601,7 +606,7 @@ int main() {
     }
     std::printf("%-12s b=%3d K=%3d  cycles/call %9.0f  (%.1f us @1.9GHz)", names[c.which], c.b, c.K, mean,
                 mean / 1900.0);
-    if (c.which == 3 || c.which == 13 || c.which >= 30) std::printf("  sweeps %.2f  cycles/round %.0f", sws, mean / (sws * ((c.b + (c.b & 1)) - 1)));
+    if (c.which == 3 || c.which == 13 || (c.which >= 30 && c.which < 40)) std::printf("  sweeps %.2f  cycles/round %.0f", sws, mean / (sws * ((c.b + (c.b & 1)) - 1)));
     std::printf("  out[0..2] %.6f %.6f %.6f\n", out[0], out[1], out[2]);
     if (c.which == 21 || c.which == 22) {
       long long st[16];
