@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libce_gpu.so")
+LIB_PATH = os.environ.get("CE_LIB_OVERRIDE") or os.path.join(_HERE, "libce_gpu.so")  # override: development A/B builds
 
 
 class LibraryMissing(ImportError):

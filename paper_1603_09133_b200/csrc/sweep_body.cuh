@@ -1336,28 +1336,30 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
   const int mx = ldt / 4, my = lds / 4;
   for (int mt = tid; mt < mx * my; mt += T) {
     const int x0 = (mt / my) * 4, y0 = (mt % my) * 4;
-    // issue the tile's X loads first so they overlap the w-long outer-product loop
-    double* xp[4][4];
-    double xv[4][4];
+    // issue the tile's X loads first so they overlap the w-long outer-product loop; keep
+    // only the small per-row / per-column indices and recompute the offsets at the store
+    int kt4[4], xl4[4], ks4[4], yl4[4], bs4[4];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       const int x = x0 + a;
-      const int kt = x < rtn ? xblk[x] : 0, xl = x < rtn ? xloc[x] : 0;
+      kt4[a] = x < rtn ? xblk[x] : -1;
+      xl4[a] = x < rtn ? xloc[x] : 0;
+      const int y = y0 + a;
+      ks4[a] = y < rsn ? yblk[y] : -1;
+      yl4[a] = y < rsn ? yloc[y] : 0;
+      bs4[a] = ks4[a] >= 0 ? tab_bs[ks4[a]] : 0;
+    }
+    double xv[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const int y = y0 + c;
-        xp[a][c] = nullptr;
         xv[a][c] = 0.0;
-        if (x < rtn && y < rsn) {
-          const int ks = yblk[y];
-          const long long off = slot_tab[kt * ns + ks];
-          if (off >= 0) {
-            xp[a][c] = A.store + off + static_cast<int64_t>(xl) * tab_bs[ks] + yloc[y];
-            xv[a][c] = ldg(xp[a][c]);
-          }
+        if (kt4[a] >= 0 && ks4[c] >= 0) {
+          const long long off = slot_tab[kt4[a] * ns + ks4[c]];
+          if (off >= 0) xv[a][c] = ldg(A.store + off + static_cast<int64_t>(xl4[a]) * bs4[c] + yl4[c]);
         }
       }
-    }
     double acc[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -1378,7 +1380,11 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int c = 0; c < 4; ++c)
-        if (xp[a][c]) *xp[a][c] = xv[a][c] - acc[a][c];
+        if (kt4[a] >= 0 && ks4[c] >= 0) {
+          const long long off = slot_tab[kt4[a] * ns + ks4[c]];
+          if (off >= 0) A.store[off + static_cast<int64_t>(xl4[a]) * bs4[c] + yl4[c]] = xv[a][c] - acc[a][c];
+        }
+
   }
   __syncthreads();
   prof_add(A, kProfBTiles, clock64() - tb2);
@@ -1392,7 +1398,7 @@ __device__ void all_panels(const SweepArgs& A, int i, int r, int w, double* sm) 
 
 // A2: compression decision + basis + pivot factorisation; with nA3 == 0 also the strip,
 // with nB == 0 also the Schur panels.
-__device__ void task_a2(const SweepArgs& A, int i, const Buf& s_, int nA1, int nA3, int nB, EntWin& W) {
+__device__ __noinline__ void task_a2(const SweepArgs& A, int i, const Buf& s_, int nA1, int nA3, int nB, EntWin& W) {
   const Buf s = s_;
   CE_SHARED_BUF(s);
   __shared__ double shr[4];
@@ -1639,7 +1645,7 @@ __device__ void task_a2(const SweepArgs& A, int i, const Buf& s_, int nA1, int n
 }
 
 // A3 tile k: strip entries with strip-ordinal in [k*ns/nA3, (k+1)*ns/nA3).
-__device__ void task_a3(const SweepArgs& A, int i, const Buf& s_, int k, int nA3, int nB, EntWin& W) {
+__device__ __noinline__ void task_a3(const SweepArgs& A, int i, const Buf& s_, int k, int nA3, int nB, EntWin& W) {
   const Buf s = s_;
   CE_SHARED_BUF(s);
   const int tid = threadIdx.x;
@@ -1658,6 +1664,46 @@ __device__ void task_a3(const SweepArgs& A, int i, const Buf& s_, int k, int nA3
   strip_range(A, i, b, r, w, basis, se[0], se[1], s, W);
   (void)nA3;
   (void)nB;
+}
+
+// A1: TSQR tree node `part` of row i (leaf k at level 0, else combine k at level tlev).
+__device__ __noinline__ void task_a1(const SweepArgs& A, int i, const Buf& s_, int part, int k, int tlev, int tprev,
+                                     int tprevn, int* nzp, double* shr, EntWin& W) {
+  const Buf s = s_;
+  CE_SHARED_BUF(s);
+  int& nz = *nzp;
+  const int b = A.bsz[i];
+  for (int idx = threadIdx.x; idx < b * b; idx += T) s.R[idx] = 0.0;
+  __syncthreads();
+  if (tlev == 0) {
+    // leaf: far-entry range of this leaf
+    const int64_t* le = A.leaf_e + A.leaf_ptr[i] + k;
+    gather_tsqr(A, i, b, s, le[0], le[1], &nz, shr, W);
+  } else {
+    // combine the F child triangles (tree nodes tprev + F k ...): the first becomes R,
+    // the others are folded in as stacked chunks of <= kcap rows
+    const int F = A.kcap / b > 2 ? A.kcap / b : 2;
+    const int per = A.kcap / b > 1 ? A.kcap / b : 1;
+    const int c0 = F * k, nc = tprevn - c0 < F ? tprevn - c0 : F;
+    const int ldc = chunk_ld(A.kcap);
+    const double* R0 = A.rscratch + A.rs_off[i] + static_cast<int64_t>(tprev + c0) * b * b;
+    for (int idx = threadIdx.x; idx < b * b; idx += T) s.R[idx] = ldg(R0 + idx);
+    __syncthreads();
+    for (int f0 = 1; f0 < nc; f0 += per) {
+      const int nk = nc - f0 < per ? nc - f0 : per;
+      const int K = nk * b;
+      const double* Rf = R0 + static_cast<int64_t>(f0) * b * b;
+      for (int idx = threadIdx.x; idx < K * b; idx += T) {
+        const int j = idx / K, m = idx % K;  // chunk element (m, j) = R_child(m / b)[m % b][j]
+        s.C[static_cast<int64_t>(j) * ldc + m] = ldg(Rf + static_cast<int64_t>(m / b) * b * b + j * b + m % b);
+      }
+      __syncthreads();
+      tsqr_sel(A, s.R, s.C, K, b, ldc, shr);
+    }
+  }
+  double* Rk = A.rscratch + A.rs_off[i] + static_cast<int64_t>(part) * b * b;
+  for (int idx = threadIdx.x; idx < b * b; idx += T) Rk[idx] = s.R[idx];
+  if (threadIdx.x == 0 && nz) atomicOr(A.nzflag + i, 1);
 }
 
 __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
@@ -1765,38 +1811,7 @@ __global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
       A.trace[4 * item + 3] = sm;
     }
     if (stage == 1) {
-      const int b = A.bsz[i];
-      for (int idx = threadIdx.x; idx < b * b; idx += T) s.R[idx] = 0.0;
-      __syncthreads();
-      if (tlev == 0) {
-        // leaf: far-entry range of this leaf
-        const int64_t* le = A.leaf_e + A.leaf_ptr[i] + k;
-        gather_tsqr(A, i, b, s, le[0], le[1], &nz, shr, W);
-      } else {
-        // combine the F child triangles (tree nodes tprev + F k ...): the first becomes R,
-        // the others are folded in as stacked chunks of <= kcap rows
-        const int F = A.kcap / b > 2 ? A.kcap / b : 2;
-        const int per = A.kcap / b > 1 ? A.kcap / b : 1;
-        const int c0 = F * k, nc = tprevn - c0 < F ? tprevn - c0 : F;
-        const int ldc = chunk_ld(A.kcap);
-        const double* R0 = A.rscratch + A.rs_off[i] + static_cast<int64_t>(tprev + c0) * b * b;
-        for (int idx = threadIdx.x; idx < b * b; idx += T) s.R[idx] = ldg(R0 + idx);
-        __syncthreads();
-        for (int f0 = 1; f0 < nc; f0 += per) {
-          const int nk = nc - f0 < per ? nc - f0 : per;
-          const int K = nk * b;
-          const double* Rf = R0 + static_cast<int64_t>(f0) * b * b;
-          for (int idx = threadIdx.x; idx < K * b; idx += T) {
-            const int j = idx / K, m = idx % K;  // chunk element (m, j) = R_child(m / b)[m % b][j]
-            s.C[static_cast<int64_t>(j) * ldc + m] = ldg(Rf + static_cast<int64_t>(m / b) * b * b + j * b + m % b);
-          }
-          __syncthreads();
-          tsqr_sel(A, s.R, s.C, K, b, ldc, shr);
-        }
-      }
-      double* Rk = A.rscratch + A.rs_off[i] + static_cast<int64_t>(part) * b * b;
-      for (int idx = threadIdx.x; idx < b * b; idx += T) Rk[idx] = s.R[idx];
-      if (threadIdx.x == 0 && nz) atomicOr(A.nzflag + i, 1);
+      task_a1(A, i, s, part, k, tlev, tprev, tprevn, &nz, shr, W);
     } else if (stage == 2) {
       task_a2(A, i, s, nA1, nA3, nB, W);
     } else if (stage == 3) {
