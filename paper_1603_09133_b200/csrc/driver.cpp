@@ -343,8 +343,6 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
       off += static_cast<int64_t>(P.bsz[static_cast<size_t>(i)]) * P.bsz[static_cast<size_t>(j)];
     }
   P.store_doubles = off;
-  // the Schur panel epilogue addresses the store with 32-bit element offsets
-  if (off >= (int64_t{1} << 31)) throw std::length_error("level store exceeds 2^31 doubles (Schur panel offsets are 32-bit)");
   P.csum.assign(static_cast<size_t>(M), 0);
   P.fsum.assign(static_cast<size_t>(M), 0);
   P.croff.assign(P.ccol.size(), 0);
