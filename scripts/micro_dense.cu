@@ -376,6 +376,21 @@ __device__ __noinline__ void tsqr_abl_t(double* R, double* C, int K, int b, int 
 }
 
 
+// barrier-loop floor: per step LDS of a flag written by one thread + barrier
+__device__ __noinline__ void barrier_loop(double* R, double* C, int b, double* shr) {
+  double acc = 0.0;
+  for (int k = 0; k + 1 < b; ++k) {
+    const double t = shr[k & 1];
+    if (t != 0.0) acc += t * C[threadIdx.x];
+    if (threadIdx.x == (k & 255)) shr[(k + 1) & 1] = acc + 1.0;
+    __syncthreads();
+  }
+  if (acc == 12345.0) R[0] = acc;
+}
+__device__ __noinline__ void barrier_only(int b) {
+  for (int k = 0; k + 1 < b; ++k) __syncthreads();
+}
+
 __device__ __forceinline__ double hrand(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;
   x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -398,6 +413,7 @@ __global__ void __launch_bounds__(T) micro_kernel(int which, int b, int K, int r
   for (int rep = 0; rep < reps; ++rep) {
     const uint64_t seed = (static_cast<uint64_t>(blockIdx.x) * 1000003ull + rep) * 7919ull;
     if (which != 3 && which != 13 && (which < 30 || which >= 40)) {
+      if (which == 50 && threadIdx.x == 0) { shr[0] = 1.0; shr[1] = 1.0; }
       for (int idx = threadIdx.x; idx < b * b; idx += T) R[idx] = 0.0;
       for (int idx = threadIdx.x; idx < K * b; idx += T) C[(idx / K) * ldc + idx % K] = hrand(seed + idx);
     } else {
@@ -436,6 +452,8 @@ __global__ void __launch_bounds__(T) micro_kernel(int which, int b, int K, int r
     else if (which == 42) tsqr_blk_t<8, 16, 2, 4>(R, C, K, b, ldc, shr);
     else if (which == 43) tsqr_blk_t<8, 16, 2, 8>(R, C, K, b, ldc, shr);
     else if (which == 44) tsqr_blk_t<16, 8, 3, 8>(R, C, K, b, ldc, shr);
+    else if (which == 50) barrier_loop(R, C, b, shr);
+    else if (which == 51) barrier_only(b);
     else if (which == 30) nsw_tot += jacobi_t<1, 16>(R, V, b, ld, b);
     else if (which == 31) nsw_tot += jacobi_t<2, 8>(R, V, b, ld, b);
     else if (which == 32) nsw_tot += jacobi_t<4, 4>(R, V, b, ld, b);
@@ -578,8 +596,8 @@ int main() {
     }
   }
   struct Case { int which, b, K; };
-  const Case cases[] = {{12, 16, 128}, {40, 16, 128}, {12, 16, 48}, {40, 16, 48}, {12, 32, 128}, {41, 32, 128}, {12, 40, 104}, {42, 40, 104}, {43, 40, 104}, {44, 40, 104}, {12, 40, 120}, {42, 40, 120}};
-  const char* names[] = {"tsqr_warps", "tsqr_update", "tsqr_group", "jacobi", "tsqr_g4", "tsqr_g16", "tsqr_g32", "noprep", "noupdate", "fastdiv", "probe_full", "stamp", "tsqr_fast", "jacobi_fast", "reg16x8x3", "reg8x16x2", "reg4x32x1", "reg16x8x4", "reg32x4x6", "reg8x16x1", "reg16x8x1", "stamp16", "stamp40", "abl_full", "abl_noprep", "abl_noupd", "abl_none", "", "", "", "j1x16", "j2x8", "j4x4", "j8x2", "j16x1", "j1x40", "j2x20", "j4x10", "j8x5", "", "blk16", "blk32", "blk40nb4", "blk40nb8", "blk40g16"};
+  const Case cases[] = {{50, 64, 64}, {51, 64, 64}, {12, 16, 128}};
+  const char* names[] = {"tsqr_warps", "tsqr_update", "tsqr_group", "jacobi", "tsqr_g4", "tsqr_g16", "tsqr_g32", "noprep", "noupdate", "fastdiv", "probe_full", "stamp", "tsqr_fast", "jacobi_fast", "reg16x8x3", "reg8x16x2", "reg4x32x1", "reg16x8x4", "reg32x4x6", "reg8x16x1", "reg16x8x1", "stamp16", "stamp40", "abl_full", "abl_noprep", "abl_noupd", "abl_none", "", "", "", "j1x16", "j2x8", "j4x4", "j8x2", "j16x1", "j1x40", "j2x20", "j4x10", "j8x5", "", "blk16", "blk32", "blk40nb4", "blk40nb8", "blk40g16", "", "", "", "", "", "barrier_loop", "barrier_only"};
   const int only = getenv("MICRO_CASE") ? atoi(getenv("MICRO_CASE")) : -1;
   for (const Case& c : cases) {
     if (only >= 0 && c.which != only) continue;
