@@ -932,6 +932,8 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
   int64_t shifts = 0;
   int64_t elim_total = 0;
 
+  const double t_loop0 = now_s();
+  double t_loop1 = t_loop0;
   while (cur.dim > dense_threshold && static_cast<int64_t>(F->levels.size()) < max_levels) {
     const size_t li = F->levels.size();
     const double h_t0 = now_s();
@@ -1379,6 +1381,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     if (nM == 0) break;
   }
 
+  t_loop1 = now_s();
   // ---- dense tail (factorization.cpp:419-436) ----
   F->tail_dim = cur.M > 0 ? cur.dim : 0;
   if (F->tail_dim > 0) {
@@ -1446,6 +1449,10 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
   for (const auto& L : F->levels) scr = std::max(scr, L.scratch_doubles);
   F->w_scratch.alloc(static_cast<size_t>(scr));
   F->total_seconds = now_s() - t_start;
+  if (std::getenv("CE_PROFILE") && std::getenv("CE_PROFILE")[0] == '1')
+    std::fprintf(stderr, "[ce-profile] factorize host: before level loop %.1f ms, level loop %.1f ms, after %.1f ms, total %.1f ms\n",
+                 1e3 * (t_loop0 - t_start), 1e3 * (t_loop1 - t_loop0), 1e3 * (now_s() - t_start - (t_loop1 - t_start)),
+                 1e3 * F->total_seconds);
   return F.release();
 }
 
