@@ -374,7 +374,8 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
   const int64_t bmax = std::max(P.bmax, 1);
   const int64_t buf = sweep_smem_doubles(static_cast<int>(bmax), sweep_kcap(static_cast<int>(bmax)));
   // (sweep.cu kPanelRows / kPanelNb bound the panel height / neighbour count)
-  const int64_t cap = thresholds().small_panels ? bmax : std::max<int64_t>(bmax, std::min<int64_t>(256, buf / (2 * bmax) - 4));
+  // (rows + 16 bounds the padded row strides of both staged panels, sweep_body.cuh panel_update)
+  const int64_t cap = thresholds().small_panels ? bmax : std::max<int64_t>(bmax, std::min<int64_t>(256, buf / (2 * bmax) - 16));
   constexpr int64_t kPanelNb = 32;
   // per-row task counts (parallel over rows), then prefix offsets
   const Thresholds& th = thresholds();

@@ -1300,7 +1300,9 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
   const long long tb1 = clock64();
   prof_add(A, kProfBSetup, tb1 - tb0);
   const int rsn = n_live[0], rtn = n_live[1];
-  const int lds = (rsn + 3) & ~3, ldt = (rtn + 3) & ~3;
+  // row strides = 8 (mod 16) doubles: the four k-rows of an m8n8k4 fragment load hit
+  // disjoint bank halves (two wavefronts, the minimum for 32 doubles)
+  const int lds = ((rsn + 7) & ~15) + 8, ldt = ((rtn + 7) & ~15) + 8;
   // g rows transposed into shared memory: GsT[q][y], GtT[q][x] (live rows only)
   const double* G = A.fac + A.g_off[i];
   double* GsT = sm;
@@ -1332,59 +1334,73 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
   __syncthreads();
   const long long tb2 = clock64();
   prof_add(A, kProfBStage, tb2 - tb1);
-  // rtn x rsn outer product in 4x4 register tiles; epilogue scatters into the (t, s) blocks
-  const int mx = ldt / 4, my = lds / 4;
-  for (int mt = tid; mt < mx * my; mt += T) {
-    const int x0 = (mt / my) * 4, y0 = (mt % my) * 4;
-    // issue the tile's X loads first so they overlap the w-long outer-product loop; keep
-    // only the small per-row / per-column indices and recompute the offsets at the store
-    int kt4[4], xl4[4], ks4[4], yl4[4], bs4[4];
+  // rtn x rsn product on the FP64 tensor cores (mma.m8n8k4): a warp owns a 16 x 32 tile
+  // (2 x 4 fragments), the k loop runs over the w g-columns in steps of 4 (masked tail);
+  // the tile's X values are prefetched before the k loop, the epilogue scatters into the
+  // (t, s) blocks.
+  {
+    const int lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int ntx = (rtn + 15) / 16, nty = (rsn + 31) / 32;
+    for (int wt = warp; wt < ntx * nty; wt += T / 32) {
+      const int xb = (wt / nty) * 16, yb = (wt % nty) * 32;
+      int ktv[2], xlv[2], ksv[8], ylv[8], bsv[8];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int x = x0 + a;
-      kt4[a] = x < rtn ? xblk[x] : -1;
-      xl4[a] = x < rtn ? xloc[x] : 0;
-      const int y = y0 + a;
-      ks4[a] = y < rsn ? yblk[y] : -1;
-      yl4[a] = y < rsn ? yloc[y] : 0;
-      bs4[a] = ks4[a] >= 0 ? tab_bs[ks4[a]] : 0;
-    }
-    double xv[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        xv[a][c] = 0.0;
-        if (kt4[a] >= 0 && ks4[c] >= 0) {
-          const long long off = slot_tab[kt4[a] * ns + ks4[c]];
-          if (off >= 0) xv[a][c] = ldg(A.store + off + static_cast<int64_t>(xl4[a]) * bs4[c] + yl4[c]);
-        }
+      for (int i2 = 0; i2 < 2; ++i2) {
+        const int x = xb + 8 * i2 + g;
+        ktv[i2] = x < rtn ? xblk[x] : -1;
+        xlv[i2] = x < rtn ? xloc[x] : 0;
       }
-    double acc[4][4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+      for (int j2 = 0; j2 < 8; ++j2) {
+        const int y = yb + 8 * (j2 >> 1) + 2 * t4 + (j2 & 1);
+        ksv[j2] = y < rsn ? yblk[y] : -1;
+        ylv[j2] = y < rsn ? yloc[y] : 0;
+        bsv[j2] = ksv[j2] >= 0 ? tab_bs[ksv[j2]] : 0;
+      }
+      double xv[2][8], acc[2][8];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
-    for (int q = 0; q < w; ++q) {
-      const double2 ta = *reinterpret_cast<const double2*>(GtT + q * ldt + x0);
-      const double2 tb = *reinterpret_cast<const double2*>(GtT + q * ldt + x0 + 2);
-      const double2 sa = *reinterpret_cast<const double2*>(GsT + q * lds + y0);
-      const double2 sb = *reinterpret_cast<const double2*>(GsT + q * lds + y0 + 2);
-      const double av[4] = {ta.x, ta.y, tb.x, tb.y}, cv[4] = {sa.x, sa.y, sb.x, sb.y};
+      for (int i2 = 0; i2 < 2; ++i2)
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[a][c] += av[a] * cv[c];
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (kt4[a] >= 0 && ks4[c] >= 0) {
-          const long long off = slot_tab[kt4[a] * ns + ks4[c]];
-          if (off >= 0) A.store[off + static_cast<int64_t>(xl4[a]) * bs4[c] + yl4[c]] = xv[a][c] - acc[a][c];
+        for (int j2 = 0; j2 < 8; ++j2) {
+          xv[i2][j2] = 0.0;
+          acc[i2][j2] = 0.0;
+          if (ktv[i2] >= 0 && ksv[j2] >= 0) {
+            const long long off = slot_tab[ktv[i2] * ns + ksv[j2]];
+            if (off >= 0) xv[i2][j2] = ldg(A.store + off + static_cast<int64_t>(xlv[i2]) * bsv[j2] + ylv[j2]);
+          }
         }
-
+      for (int q0 = 0; q0 < w; q0 += 4) {
+        const int q = q0 + t4;
+        double af[2], bf[4];
+#pragma unroll
+        for (int i2 = 0; i2 < 2; ++i2) {
+          const int x = xb + 8 * i2 + g;
+          af[i2] = (q < w && x < ldt) ? GtT[q * ldt + x] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int y = yb + 8 * j + g;
+          bf[j] = (q < w && y < lds) ? GsT[q * lds + y] : 0.0;
+        }
+#pragma unroll
+        for (int i2 = 0; i2 < 2; ++i2)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[i2][2 * j]), "+d"(acc[i2][2 * j + 1])
+                         : "d"(af[i2]), "d"(bf[j]));
+      }
+#pragma unroll
+      for (int i2 = 0; i2 < 2; ++i2)
+#pragma unroll
+        for (int j2 = 0; j2 < 8; ++j2)
+          if (ktv[i2] >= 0 && ksv[j2] >= 0) {
+            const long long off = slot_tab[ktv[i2] * ns + ksv[j2]];
+            if (off >= 0)
+              A.store[off + static_cast<int64_t>(xlv[i2]) * bsv[j2] + ylv[j2]] = xv[i2][j2] - acc[i2][j2];
+          }
+    }
   }
   __syncthreads();
   prof_add(A, kProfBTiles, clock64() - tb2);
