@@ -698,11 +698,165 @@ __device__ __noinline__ void hqr_reg_t(double* A, int b, int ld, double* tau, do
   __syncthreads();
 }
 
+// Householder QR with column pivoting (largest remaining column norm first) of a b x b
+// column-major A, register-resident as hqr_reg_t.  Step k: every warp finds the pivot p
+// from the published trailing norms (double buffered), the group owning p prepares
+// reflector k from rows >= k of column p and records perm[k] = p; after the barrier the
+// other groups apply it and downdate their trailing norms (selection only: the reflector
+// itself always uses an exact norm).  Result layout: column perm[k] holds R(0..k, k) and
+// the tail of reflector k below row k; tau[k].  Rank-revealing R makes the one-sided
+// Jacobi on X = R^T converge in fewer sweeps (Drmac-Veselic preconditioning).
+constexpr int kQrcpMin = 17;  // block size from which the preconditioning QR pivots (thin level-1 rows converge fast anyway)
+
+template <int G, int E, int NC>
+__device__ __noinline__ void hqrcp_reg_t(double* A, int b, int ld, double* tau, double* vb0, double* vb1, int* perm,
+                                         double* cn0, double* cn1) {
+  CE_SHARED(A);
+  CE_SHARED(tau);
+  CE_SHARED(vb0);
+  CE_SHARED(vb1);
+  CE_SHARED(perm);
+  CE_SHARED(cn0);
+  CE_SHARED(cn1);
+  constexpr int NG = T / G;
+  constexpr unsigned kFull = 0xffffffffu;
+  const int tid = threadIdx.x, grp = tid / G, gl = tid % G, warp = tid >> 5, lane = tid & 31;
+  double x[NC][E], n2[NC];
+  bool chosen[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = grp + c * NG;
+    double ss = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int m = gl + e * G;
+      x[c][e] = (j < b && m < b) ? A[j * ld + m] : 0.0;
+      ss = fma(x[c][e], x[c][e], ss);
+    }
+    n2[c] = group_sum<G>(ss, kFull);
+    chosen[c] = false;
+    if (j < b && gl == 0) cn0[j] = n2[c];
+  }
+  __syncthreads();
+  for (int k = 0; k < b; ++k) {
+    const double* cn = (k & 1) ? cn1 : cn0;
+    double* cnn = (k & 1) ? cn0 : cn1;
+    // pivot: largest published norm, ties to the smaller index (every warp, same answer)
+    double bv = -2.0;
+    int bi = b;
+    for (int jj = lane; jj < b; jj += 32) {
+      const double v = cn[jj];
+      if (v > bv) {
+        bv = v;
+        bi = jj;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(kFull, bv, o);
+      const int oi = __shfl_xor_sync(kFull, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    const int p = bi, pg = p % NG, pc = p / NG;
+    if ((pg * G) >> 5 == warp) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        if (c != pc) continue;
+        const bool own = grp == pg;
+        double ss = 0.0, x0 = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int m = gl + e * G;
+          if (m > k && m < b) ss = fma(x[c][e], x[c][e], ss);
+          if (m == k) x0 = x[c][e];
+        }
+        ss = group_sum<G>(ss, kFull);
+        x0 = group_sum<G>(x0, kFull);
+        if (own) {
+          double* vb = (k & 1) ? vb1 : vb0;
+          double t = 0.0;
+          if (ss > 0.0) {
+            const double nn = fma(x0, x0, ss);
+            const bool fast = nn > 1e-290 && nn < 1e290;
+            const double nrm = fast ? nn * rsqrt_nr(nn) : sqrt(nn);
+            const double beta = x0 >= 0.0 ? -nrm : nrm;
+            const double den = x0 - beta;
+            const double scale = fast ? rcp_nr(den) : 1.0 / den;
+            t = fast ? -den * rcp_nr(beta) : (beta - x0) / beta;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const int m = gl + e * G;
+              if (m >= b) continue;
+              if (m > k) {
+                x[c][e] *= scale;
+                vb[m] = x[c][e];
+              } else if (m == k) {
+                x[c][e] = beta;
+                vb[m] = 1.0;
+              } else {
+                vb[m] = 0.0;
+              }
+            }
+          }
+          chosen[c] = true;
+          if (gl == 0) {
+            tau[k] = t;
+            perm[k] = p;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const double t = tau[k];
+    const double* vb = (k & 1) ? vb1 : vb0;
+    double v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int m = gl + e * G;
+      v[e] = (t != 0.0 && m < b) ? vb[m] : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int j = grp + c * NG;
+      const bool live = j < b && !chosen[c];
+      double sd = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) sd = fma(v[e], x[c][e], sd);
+      sd = group_sum<G>(sd, kFull);
+      const double d = (live && t != 0.0) ? t * sd : 0.0;
+      double xk = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        x[c][e] = fma(-d, v[e], x[c][e]);
+        if (gl + e * G == k) xk = x[c][e];
+      }
+      xk = group_sum<G>(xk, kFull);  // the row-k entry leaves the trailing part
+      n2[c] = fmax(n2[c] - xk * xk, 0.0);
+      if (j < b && gl == 0) cnn[j] = live ? n2[c] : -1.0;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int j = grp + c * NG;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int m = gl + e * G;
+      if (j < b && m < b) A[j * ld + m] = x[c][e];
+    }
+  }
+  __syncthreads();
+}
+
 // V <- Q2 V, Q2 = H_0 ... H_{b-2} from the reflectors below the diagonal of A: every group
 // applies all reflectors to the V columns it keeps in registers; the reflectors are
 // read-only, so no barriers are needed between steps.
 template <int G, int E, int NC>
-__device__ __noinline__ void apply_refl_reg_t(const double* A, const double* tau, double* V, int b, int ld) {
+__device__ __noinline__ void apply_refl_reg_t(const double* A, const double* tau, double* V, int b, int ld,
+                                              const int* perm = nullptr) {
   CE_SHARED(A);
   CE_SHARED(tau);
   CE_SHARED(V);
@@ -719,14 +873,14 @@ __device__ __noinline__ void apply_refl_reg_t(const double* A, const double* tau
       x[c][e] = (j < b && m < b) ? V[j * ld + m] : 0.0;
     }
   }
-  for (int k = b - 2; k >= 0; --k) {
+  for (int k = b - (perm ? 1 : 2); k >= 0; --k) {
     const double t = tau[k];
     if (t == 0.0) continue;
     double v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int m = gl + e * G;
-      v[e] = m == k ? 1.0 : ((m > k && m < b) ? A[k * ld + m] : 0.0);
+      v[e] = m == k ? 1.0 : ((m > k && m < b) ? A[(perm ? perm[k] : k) * ld + m] : 0.0);
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -767,12 +921,23 @@ __device__ __noinline__ void precondition_qr(const Buf& s_, int b) {
   }
   __syncthreads();
   if (b <= 64) {
-    if (b <= 16) hqr_reg_t<16, 1, 1>(Aq, b, ld, s.tau, s.nrm, s.sig);
-    else if (b <= 32) hqr_reg_t<8, 4, 1>(Aq, b, ld, s.tau, s.nrm, s.sig);
-    else hqr_reg_t<8, 8, 2>(Aq, b, ld, s.tau, s.nrm, s.sig);
-    for (int idx = threadIdx.x; idx < b * b; idx += T) {
-      const int j = idx / b, i = idx % b;
-      s.R[j * ld + i] = i >= j ? Aq[i * ld + j] : 0.0;
+    if (b >= kQrcpMin) {
+      // column-pivoted (pays off beyond the thin level-1 blocks: fewer Jacobi sweeps than the pivot search
+      // costs); trailing norms double-buffered in the (still unused) U tile
+      if (b <= 32) hqrcp_reg_t<8, 4, 1>(Aq, b, ld, s.tau, s.nrm, s.sig, s.perm, s.U, s.U + b);
+      else hqrcp_reg_t<8, 8, 2>(Aq, b, ld, s.tau, s.nrm, s.sig, s.perm, s.U, s.U + b);
+      for (int idx = threadIdx.x; idx < b * b; idx += T) {
+        const int j = idx / b, i = idx % b;  // X(i, j) = R(j, i) = row j of the step-i pivot column
+        s.R[j * ld + i] = i >= j ? Aq[s.perm[i] * ld + j] : 0.0;
+      }
+    } else {
+      if (b <= 16) hqr_reg_t<16, 1, 1>(Aq, b, ld, s.tau, s.nrm, s.sig);
+      else if (b <= 32) hqr_reg_t<8, 4, 1>(Aq, b, ld, s.tau, s.nrm, s.sig);
+      else hqr_reg_t<8, 8, 2>(Aq, b, ld, s.tau, s.nrm, s.sig);
+      for (int idx = threadIdx.x; idx < b * b; idx += T) {
+        const int j = idx / b, i = idx % b;
+        s.R[j * ld + i] = i >= j ? Aq[i * ld + j] : 0.0;
+      }
     }
     __syncthreads();
     return;
@@ -818,9 +983,10 @@ __device__ __noinline__ void apply_q2(const Buf& s_, int b) {
   const int ld = pad_ld(b);
   const double* Aq = s.C;
   if (b <= 64) {
-    if (b <= 16) apply_refl_reg_t<16, 1, 1>(Aq, s.tau, s.V, b, ld);
-    else if (b <= 32) apply_refl_reg_t<8, 4, 1>(Aq, s.tau, s.V, b, ld);
-    else apply_refl_reg_t<8, 8, 2>(Aq, s.tau, s.V, b, ld);
+    const int* pv = b >= kQrcpMin ? s.perm : nullptr;
+    if (b <= 16) apply_refl_reg_t<16, 1, 1>(Aq, s.tau, s.V, b, ld, pv);
+    else if (b <= 32) apply_refl_reg_t<8, 4, 1>(Aq, s.tau, s.V, b, ld, pv);
+    else apply_refl_reg_t<8, 8, 2>(Aq, s.tau, s.V, b, ld, pv);
     return;
   }
   for (int k = b - 2; k >= 0; --k) {
