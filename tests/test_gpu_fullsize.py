@@ -63,3 +63,18 @@ def test_cfg1_full_pcg(gpu_ctx):
     f = ce.ce_factorize(a, p.plan, p.strategy())
     rep, x = ce.pcg(a, p.n, p.rhs, f, ce.PcgOptions(tol=p.tol))
     assert rep.converged and rep.final_true_residual <= 10 * p.tol
+
+
+def test_cfg3_fullsize_properties(gpu_ctx):
+    """BASELINE cfg3 (2-D variable-coefficient FV, n = 4.2 M): telescoping dimensions and PCG to
+    the stated tolerance with the true residual below target."""
+    p = ce.Problem(3)
+    a = ce.DeviceMatrix(p.matrix())
+    f = ce.ce_factorize(a, p.plan, p.strategy())
+    dim = p.n
+    for s in f.level_stats():
+        assert s["eliminated"] + s["retained"] == dim
+        dim = s["retained"]
+    assert dim == f.stats["tail_dim"]
+    rep, x = ce.pcg(a, p.n, p.rhs, f, ce.PcgOptions(tol=p.tol, maxit=200))
+    assert rep.converged and rep.final_true_residual <= 10 * p.tol
