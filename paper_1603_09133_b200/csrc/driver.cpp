@@ -783,49 +783,54 @@ namespace {
 struct DevPlan {
   DevArray<int> bsz, scol, ccol, croff, order, nA1, nA3, nB, pan_start, item_row, item_part, sbsz, sroff, target, nleaf;
   DevArray<int64_t> sptr, sslot, slot_off, cptr, chol_off, g_off, basis_off, sigma_off, item_start, offsets, cl_slot,
-      fsum, rs_off, pan_ptr, sboff, sdiag, leaf_ptr, leaf_e, strip_ptr, strip_e;
+      fsum, rs_off, pan_ptr, sboff, sdiag, leaf_ptr, leaf_e, strip_ptr, strip_e;  // (cl_slot unused)
   DevArray<unsigned char> skind;
+  // All plan arrays go through one pinned staging buffer (grow-only, per host thread): the
+  // host copies them in and the DMAs run asynchronously (pageable copies would stage
+  // synchronously).  The buffer is reused by the next level's upload, which happens
+  // after the stream has been synchronised.
   void upload(const LevelPlan& P, cudaStream_t s) {
-    order.upload(P.order, s);
-    item_row.upload(P.item_row, s);
-    item_part.upload(P.item_part, s);
-    nA1.upload(P.nA1, s);
-    nleaf.upload(P.nleaf, s);
-    nA3.upload(P.nA3, s);
-    nB.upload(P.nB, s);
-    pan_start.upload(P.pan_start, s);
-    fsum.upload(P.fsum, s);
-    rs_off.upload(P.rs_off, s);
-    pan_ptr.upload(P.pan_ptr, s);
-    bsz.upload(P.bsz, s);
-    scol.upload(P.scol, s);
-    ccol.upload(P.ccol, s);
-    croff.upload(P.croff, s);
-    sptr.upload(P.sptr, s);
-    sslot.upload(P.sslot, s);
-    slot_off.upload(P.slot_off, s);
-    cptr.upload(P.cptr, s);
-    chol_off.upload(P.chol_off, s);
-    g_off.upload(P.g_off, s);
-    basis_off.upload(P.basis_off, s);
-    sigma_off.upload(P.sigma_off, s);
-    item_start.upload(P.item_start, s);
-    offsets.upload(P.offsets, s);
-    skind.upload(P.skind, s);
-    sboff.upload(P.sboff, s);
-    sbsz.upload(P.sbsz, s);
-    sroff.upload(P.sroff, s);
-    sdiag.upload(P.sdiag, s);
-    target.upload(P.target, s);
-    leaf_ptr.upload(P.leaf_ptr, s);
-    leaf_e.upload(P.leaf_e, s);
-    strip_ptr.upload(P.strip_ptr, s);
-    strip_e.upload(P.strip_e, s);
-    std::vector<int64_t> cls(P.ccol.size());
-    for (int64_t i = 0; i < P.M; ++i)
-      for (int64_t k = P.cptr[static_cast<size_t>(i)]; k < P.cptr[static_cast<size_t>(i + 1)]; ++k)
-        cls[static_cast<size_t>(k)] = P.sslot[static_cast<size_t>(csr_find(P.sptr, P.scol, i, P.ccol[static_cast<size_t>(k)]))];
-    cl_slot.upload(cls, s);
+    struct Stage {
+      char* p = nullptr;
+      size_t cap = 0;
+      ~Stage() {
+        if (p) cudaFreeHost(p);
+      }
+    };
+    thread_local Stage st;
+    size_t total = 0;
+    auto add = [&](size_t bytes) { total += (bytes + 255) / 256 * 256; };
+    auto sz = [](const auto& v) { return v.size() * sizeof(v[0]); };
+    add(sz(P.order)); add(sz(P.item_row)); add(sz(P.item_part)); add(sz(P.nA1)); add(sz(P.nleaf)); add(sz(P.nA3));
+    add(sz(P.nB)); add(sz(P.pan_start)); add(sz(P.fsum)); add(sz(P.rs_off)); add(sz(P.pan_ptr)); add(sz(P.bsz));
+    add(sz(P.scol)); add(sz(P.ccol)); add(sz(P.croff)); add(sz(P.sptr)); add(sz(P.sslot)); add(sz(P.slot_off));
+    add(sz(P.cptr)); add(sz(P.chol_off)); add(sz(P.g_off)); add(sz(P.basis_off)); add(sz(P.sigma_off));
+    add(sz(P.item_start)); add(sz(P.offsets)); add(sz(P.skind)); add(sz(P.sboff)); add(sz(P.sbsz)); add(sz(P.sroff));
+    add(sz(P.sdiag)); add(sz(P.target)); add(sz(P.leaf_ptr)); add(sz(P.leaf_e)); add(sz(P.strip_ptr)); add(sz(P.strip_e));
+    if (total > st.cap) {
+      if (st.p) cudaFreeHost(st.p);
+      st.p = nullptr;
+      st.cap = total + total / 4;
+      CE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&st.p), st.cap, cudaHostAllocDefault));
+    }
+    size_t off = 0;
+    auto put = [&](auto& d, const auto& h) {
+      const size_t bytes = h.size() * sizeof(h[0]);
+      d.alloc(h.size());
+      if (bytes) {
+        std::memcpy(st.p + off, h.data(), bytes);
+        CE_CUDA(cudaMemcpyAsync(d.p, st.p + off, bytes, cudaMemcpyHostToDevice, s));
+      }
+      off += (bytes + 255) / 256 * 256;
+    };
+    put(order, P.order); put(item_row, P.item_row); put(item_part, P.item_part); put(nA1, P.nA1); put(nleaf, P.nleaf);
+    put(nA3, P.nA3); put(nB, P.nB); put(pan_start, P.pan_start); put(fsum, P.fsum); put(rs_off, P.rs_off);
+    put(pan_ptr, P.pan_ptr); put(bsz, P.bsz); put(scol, P.scol); put(ccol, P.ccol); put(croff, P.croff);
+    put(sptr, P.sptr); put(sslot, P.sslot); put(slot_off, P.slot_off); put(cptr, P.cptr); put(chol_off, P.chol_off);
+    put(g_off, P.g_off); put(basis_off, P.basis_off); put(sigma_off, P.sigma_off); put(item_start, P.item_start);
+    put(offsets, P.offsets); put(skind, P.skind); put(sboff, P.sboff); put(sbsz, P.sbsz); put(sroff, P.sroff);
+    put(sdiag, P.sdiag); put(target, P.target); put(leaf_ptr, P.leaf_ptr); put(leaf_e, P.leaf_e);
+    put(strip_ptr, P.strip_ptr); put(strip_e, P.strip_e);
   }
 };
 
