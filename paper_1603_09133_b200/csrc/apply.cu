@@ -16,7 +16,7 @@ namespace {
 
 constexpr int T = kApplyThreads;
 constexpr int kApplyWarps = T / 32;
-constexpr int kWmax = 256;  // max eliminated width per block handled by the apply sweeps
+constexpr int kWmax = kApplyWmax;  // max eliminated width per block handled by the apply sweeps
 // dynamic shared memory of the sweeps: z/s (kWmax) + per-warp partial sums and u staging
 constexpr size_t kSweepSmem = (kWmax + 2 * kWmax * kApplyWarps) * sizeof(double);
 

@@ -40,7 +40,9 @@ struct Thresholds {
   int64_t strip_work = int64_t{1} << 15;   // strip rotation S*b^2 above which the strip is split off
   int64_t strip_cols = 64;                 // strip columns per task
   bool small_panels = false;               // one close neighbour per Schur panel
+  bool no_tri_table = false;               // CE_NO_TRI=1: binary-search slot lookups at every level
   Thresholds() {
+    no_tri_table = std::getenv("CE_NO_TRI") && std::getenv("CE_NO_TRI")[0] == '1';
     const char* f = std::getenv("CE_FORCE_TASKS");  // bitmask: 1 leaves, 2 strip tasks, 4 Schur panels
     const int m = f ? std::atoi(f) : 0;
     if (m & 1) {
@@ -1032,6 +1034,14 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     a.sq_slot = dcur.sslot.p;
     a.sq_kind = dcur.skind.p;
     a.slot_off = dcur.slot_off.p;
+    // Schur panels look up stored (t, s) blocks; with M <= 8192 a dense triangular table
+    // (<= 268 MB) replaces the per-pair binary search of the squared pattern
+    DevArray<int64_t> d_tri;
+    if (cur.M <= 8192 && !thresholds().no_tri_table) {
+      d_tri.alloc(static_cast<size_t>(cur.M) * static_cast<size_t>(cur.M + 1) / 2);
+      launch_tri_table(cur.M, dcur.sptr.p, dcur.scol.p, dcur.sslot.p, dcur.slot_off.p, d_tri.p, s);
+      a.tri_off = d_tri.p;
+    }
     a.store = store.p;
     a.cl_ptr = dcur.cptr.p;
     a.cl_col = dcur.ccol.p;
@@ -1187,7 +1197,12 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     CE_CUDA(cudaStreamSynchronize(s));
     const double h_ts = now_s();
     int64_t eliminated = 0;
-    for (int w : LF.width) eliminated += w;
+    for (int w : LF.width) {
+      eliminated += w;
+      if (w > kApplyWmax)
+        throw std::runtime_error("eliminated block width " + std::to_string(w) + " exceeds the apply limit " +
+                                 std::to_string(kApplyWmax));
+    }
     if (eliminated == 0) break;  // factorization.cpp:374 (store untouched: every r_i = b_i)
     shifts += hsh;
     LF.shift_retries = hsh;

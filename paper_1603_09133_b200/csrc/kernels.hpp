@@ -9,6 +9,7 @@ namespace ceg {
 
 constexpr int kSweepThreads = 256;
 constexpr int kApplyThreads = 128;
+constexpr int kApplyWmax = 256;  // largest eliminated width per block the apply sweeps stage in shared memory
 
 enum : int { kErrNone = 0, kErrBreakdown = 2, kErrPattern = 5, kErrInternal = 6 };
 
@@ -28,6 +29,7 @@ struct SweepArgs {
   const int64_t* sq_slot;
   const unsigned char* sq_kind;
   const int64_t* slot_off;
+  const int64_t* tri_off;  // dense lower-triangular (t, s) -> value offset table (-1: not stored), or null
   double* store;
   const int64_t* cl_ptr;
   const int* cl_col;
@@ -131,6 +133,9 @@ struct RemainderArgs {
   int* err;
 };
 void launch_remainder(const RemainderArgs& a, cudaStream_t s);
+// dense lower-triangular (t, s) -> value offset table of the squared pattern (for small M)
+void launch_tri_table(int64_t M, const int64_t* sq_ptr, const int* sq_col, const int64_t* sq_slot,
+                      const int64_t* slot_off, int64_t* tab, cudaStream_t s);
 
 // Dense tail (factorization.cpp:419-436): densify the last store, Cholesky, inverse.
 void launch_densify(int64_t M, const int* bsz, const int64_t* offsets, const int64_t* sq_ptr, const int* sq_col,

@@ -18,10 +18,15 @@
 //               row's strip blocks (fat rows only; thin rows do it in A2)
 //   [B  x nB ]  Schur panel-pair updates X_st -= g_s g_t^T from smem tiles
 // Thin rows (level 1) are a single task done by one CTA.
+#include <algorithm>
 #include <cfloat>
 #include <cstdio>
 
 #include "kernels.hpp"
+
+#ifndef CE_SWEEP_MIN_BLOCKS
+#define CE_SWEEP_MIN_BLOCKS 1  // resident sweep CTAs per SM the register allocation must allow
+#endif
 
 namespace ceg {
 namespace {
@@ -226,7 +231,7 @@ namespace {
 namespace {
 
 // g_t <- U_t^T g_t for every pending (row i, neighbor t > i) pair.
-__global__ void __launch_bounds__(T) pending_kernel(SweepArgs A) {
+__global__ void __launch_bounds__(T) pending_kernel(SweepArgs A, int cap) {
   extern __shared__ double tmp[];
   const int i = blockIdx.x;
   const int w = A.width[i];
@@ -240,15 +245,20 @@ __global__ void __launch_bounds__(T) pending_kernel(SweepArgs A) {
     const int bt = A.bsz[t];
     const double* U = A.basis + A.basis_off[t];
     double* g = G + static_cast<int64_t>(r + A.cl_roff[e]) * w;
-    for (int idx = threadIdx.x; idx < bt * w; idx += T) tmp[idx] = g[idx];
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < bt * w; idx += T) {
-      const int a = idx / w, q = idx % w;
-      double acc = 0.0;
-      for (int c = 0; c < bt; ++c) acc += U[c * bt + a] * tmp[c * w + q];
-      g[idx] = acc;
+    // g (bt x w, row stride w) <- U^T g, in column chunks of qc so bt x qc fits the buffer
+    const int qc = min(w, max(1, cap / bt));
+    for (int q0 = 0; q0 < w; q0 += qc) {
+      const int nq = min(qc, w - q0);
+      for (int idx = threadIdx.x; idx < bt * nq; idx += T) tmp[idx] = g[(idx / nq) * w + q0 + idx % nq];
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < bt * nq; idx += T) {
+        const int a = idx / nq, q = idx % nq;
+        double acc = 0.0;
+        for (int c = 0; c < bt; ++c) acc += U[c * bt + a] * tmp[c * nq + q];
+        g[a * w + q0 + q] = acc;
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
@@ -349,10 +359,12 @@ void launch_sweep(const SweepArgs& a, int grid, size_t smem_bytes, cudaStream_t 
 
 void launch_pending_rotation(const SweepArgs& a, cudaStream_t s) {
   if (a.M <= 0) return;
-  const size_t smem = static_cast<size_t>(a.bmax) * a.bmax * sizeof(double);
+  // bmax^2 doubles, capped at 128 KB (deep 3-D levels have blocks of several hundred)
+  const int cap = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(a.bmax) * a.bmax, 16384));
+  const size_t smem = static_cast<size_t>(cap) * sizeof(double);
   cudaFuncSetAttribute(pending_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   note_launch();
-  pending_kernel<<<static_cast<unsigned>(a.M), T, smem, s>>>(a);
+  pending_kernel<<<static_cast<unsigned>(a.M), T, smem, s>>>(a, cap);
 }
 
 void launch_init_store_from_matrix(int64_t M, const int* bsz, const int64_t* a_row_ptr, const int* a_col,
@@ -364,6 +376,23 @@ void launch_init_store_from_matrix(int64_t M, const int* bsz, const int64_t* a_r
   note_launch();
   init_store_kernel<<<grid, 128, 0, s>>>(M, bsz, a_row_ptr, a_col, a_val_ptr, a_values, sq_ptr, sq_col, sq_slot,
                                          slot_off, store);
+}
+
+__global__ void tri_table_kernel(int64_t M, const int64_t* sq_ptr, const int* sq_col, const int64_t* sq_slot,
+                                 const int64_t* slot_off, int64_t* tab) {
+  for (int64_t t = blockIdx.x; t < M; t += gridDim.x)
+    for (int64_t e = sq_ptr[t] + threadIdx.x; e < sq_ptr[t + 1]; e += blockDim.x) {
+      const int s = sq_col[e];
+      if (s <= t) tab[t * (t + 1) / 2 + s] = slot_off[sq_slot[e]];
+    }
+}
+
+void launch_tri_table(int64_t M, const int64_t* sq_ptr, const int* sq_col, const int64_t* sq_slot,
+                      const int64_t* slot_off, int64_t* tab, cudaStream_t s) {
+  if (M <= 0) return;
+  cudaMemsetAsync(tab, 0xff, static_cast<size_t>(M) * (M + 1) / 2 * sizeof(int64_t), s);
+  note_launch();
+  tri_table_kernel<<<static_cast<unsigned>(M < 65535 ? M : 65535), 128, 0, s>>>(M, sq_ptr, sq_col, sq_slot, slot_off, tab);
 }
 
 void launch_remainder(const RemainderArgs& a, cudaStream_t s) {

@@ -1456,9 +1456,14 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
     long long off = -1;
     if (!(P == Q && ks > kt)) {
       const int t = A.cl_col[c0 + t0 + kt], s = A.cl_col[c0 + s0 + ks];
-      const int64_t slot = find_slot(A.sq_ptr, A.sq_col, A.sq_slot, t, s);
-      if (slot < 0) set_error(A.err, kErrPattern, A.level, i);
-      else off = A.slot_off[slot];
+      if (A.tri_off) {  // one independent load per pair instead of a binary search chain
+        off = __ldg(A.tri_off + static_cast<int64_t>(t) * (t + 1) / 2 + s);
+        if (off < 0) set_error(A.err, kErrPattern, A.level, i);
+      } else {
+        const int64_t slot = find_slot(A.sq_ptr, A.sq_col, A.sq_slot, t, s);
+        if (slot < 0) set_error(A.err, kErrPattern, A.level, i);
+        else off = A.slot_off[slot];
+      }
     }
     slot_tab[idx] = off;
   }
@@ -1888,7 +1893,7 @@ __device__ __noinline__ void task_a1(const SweepArgs& A, int i, const Buf& s_, i
   if (threadIdx.x == 0 && nz) atomicOr(A.nzflag + i, 1);
 }
 
-__global__ void __launch_bounds__(T) sweep_kernel(SweepArgs A) {
+__global__ void __launch_bounds__(T, CE_SWEEP_MIN_BLOCKS) sweep_kernel(SweepArgs A) {
   extern __shared__ double smem_dyn[];
 #if CE_SMEM_BUFFER
   double* base = smem_dyn;

@@ -23,7 +23,7 @@ for rep in range(2):
 for lv in f.level_stats():
     print("  ", {k: (round(v, 5) if isinstance(v, float) else v) for k, v in lv.items()
                  if k in ("block_count", "max_block", "max_far_cols", "max_close", "eliminated", "retained", "seconds",
-                          "sweep_seconds", "max_rank")}, flush=True)
+                          "sweep_seconds", "max_rank", "n_waves", "pattern_blocks", "n_items")}, flush=True)
 t = time.time()
 rep, x = ce.pcg(a, p.n, p.rhs, f, ce.PcgOptions(tol=p.tol))
 print("pcg", rep, "wall", time.time() - t, flush=True)
