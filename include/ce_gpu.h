@@ -171,6 +171,13 @@ int ce_factor_dump(const ce_factor* f, const char* path);
  * (unpreconditioned).  on_device != 0: b, x are device pointers. */
 int ce_pcg(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const double* b, double* x, int64_t n,
            int on_device, const ce_pcg_opts* opts, ce_solve_report* rep);
+/* MINRES (replaces ce::minres, proj/include/ce/minres.hpp:46-47 / proj/src/minres.cpp:22-115, the
+ * paper's solver; ApplyFn pair at proj/src/cli.cpp:198,225-226): x0 = 0, stop when the recurrence
+ * estimate of the preconditioned residual <= tol relative to its start, or on a Lanczos beta
+ * < 1e-30 beta1; iterations = number of A*v products.  Same options, report, error codes and
+ * memory conventions as ce_pcg (opts->track_true_residual = the MinresOptions field). */
+int ce_minres(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const double* b, double* x, int64_t n,
+              int on_device, const ce_pcg_opts* opts, ce_solve_report* rep);
 
 /* ---- BASELINE problem generation (setup, untimed; SURVEY.md §8d conventions) ----
  * cfg 1..5, optional grid override (0 = keep).  Builds the permuted CSB, plan and rhs on the host

@@ -150,4 +150,22 @@ inline SolveReport pcg(Context& ctx, const BlockSparseMatrix& a, index_t n, cons
   return SolveReport{rep.converged != 0, rep.iterations, rep.final_recurrence_residual, rep.final_true_residual};
 }
 
+struct MinresOptions {  // minres.hpp:34-38
+  double tol = 1e-10;
+  index_t maxit = 1000;
+  bool track_true_residual = true;
+};
+
+// minres(a, n, b, precond, opts, x) (minres.hpp:46-47) on the device.
+inline SolveReport minres(Context& ctx, const BlockSparseMatrix& a, index_t n, const Vector& b,
+                          const CEFactorization* precond, const MinresOptions& o, Vector& x) {
+  x.assign(static_cast<size_t>(n), 0.0);
+  ce_pcg_opts opts{o.tol, o.maxit, o.track_true_residual ? 1 : 0};
+  ce_solve_report rep{};
+  const int rc =
+      ce_minres(ctx.get(), a.get(), precond ? precond->get() : nullptr, b.data(), x.data(), n, 0, &opts, &rep);
+  if (rc != CE_OK && rc != CE_ENOCONV) check(rc);
+  return SolveReport{rep.converged != 0, rep.iterations, rep.final_recurrence_residual, rep.final_true_residual};
+}
+
 }  // namespace ce_b200

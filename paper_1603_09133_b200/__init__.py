@@ -18,11 +18,13 @@ from .ce import (  # noqa: F401
     Context,
     DeviceMatrix,
     FactorOptions,
+    MinresOptions,
     PcgOptions,
     Problem,
     SolveReport,
     ce_factorize,
     device_count,
+    minres,
     pcg,
 )
 
@@ -35,10 +37,12 @@ __all__ = [
     "Context",
     "DeviceMatrix",
     "FactorOptions",
+    "MinresOptions",
     "PcgOptions",
     "Problem",
     "SolveReport",
     "ce_factorize",
     "device_count",
+    "minres",
     "pcg",
 ]

@@ -94,6 +94,7 @@ SIGNATURES = {
     "ce_factor_get_level_stats": (C.c_int, [vp, i64, C.POINTER(LevelStats)]),
     "ce_factor_dump": (C.c_int, [vp, C.c_char_p]),
     "ce_pcg": (C.c_int, [vp, vp, vp, vp, vp, i64, C.c_int, C.POINTER(PcgOpts), C.POINTER(Report)]),
+    "ce_minres": (C.c_int, [vp, vp, vp, vp, vp, i64, C.c_int, C.POINTER(PcgOpts), C.POINTER(Report)]),
     "ce_problem_create": (C.c_int, [C.c_int, i64, i64, i64, C.POINTER(vp)]),
     "ce_problem_free": (None, [vp]),
     "ce_problem_csb": (C.c_int, [vp, C.POINTER(CsbHost)]),

@@ -9,6 +9,7 @@ Reference names kept (proj/include/ce/):
   BreakdownError(level, block)   types.hpp:26-36
   SolveReport            minres.hpp:25-31
   pcg                    the minres contract (minres.hpp:46-47) with PCG, SURVEY.md §8b
+  minres / MinresOptions minres.hpp:34-47 (minres.cpp:22-115) on the device
 Vectors are numpy float64 arrays (host) or torch float64 CUDA tensors (device).
 """
 
@@ -117,6 +118,13 @@ class PcgOptions:
     tol: float = 1e-10
     maxit: int = 1000
     track_true_residual: bool = False
+
+
+@dataclass
+class MinresOptions:  # proj/include/ce/minres.hpp:34-38
+    tol: float = 1e-10
+    maxit: int = 1000
+    track_true_residual: bool = True
 
 
 @dataclass
@@ -313,33 +321,43 @@ def ce_factorize(a, plan: Optional[CoarseningPlan], strategy: CompressionStrateg
     return f
 
 
-def pcg(a: DeviceMatrix, n: int, b, precond: Optional[CEFactorization], opts: Optional[PcgOptions] = None):
-    """Preconditioned CG with the minres contract; returns (SolveReport, x).
-
-    `a` must be a DeviceMatrix and `precond` a CEFactorization or None (the
-    device loop has no host callbacks).  Non-convergence is reported in the
-    SolveReport, not raised, as in the reference."""
+def _krylov(entry, what, a, n, b, precond, opts):
     if not isinstance(a, DeviceMatrix):
-        raise TypeError("pcg runs on the device: `a` must be a DeviceMatrix")
+        raise TypeError(f"{what} runs on the device: `a` must be a DeviceMatrix")
     if precond is not None and not isinstance(precond, CEFactorization):
         raise TypeError("precond must be a CEFactorization or None")
-    opts = opts or PcgOptions()
     co = L.PcgOpts(float(opts.tol), int(opts.maxit), int(opts.track_true_residual))
     rep = L.Report()
     ph = precond.handle if precond is not None else None
     if _is_torch(b):
         import torch
         x = torch.empty_like(b)
-        rc = lib.ce_pcg(a.ctx.handle, a.handle, ph, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()), n, 1,
-                        C.byref(co), C.byref(rep))
+        rc = entry(a.ctx.handle, a.handle, ph, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()), n, 1,
+                   C.byref(co), C.byref(rep))
     else:
         b = _f64(b)
         x = np.empty(n)
-        rc = lib.ce_pcg(a.ctx.handle, a.handle, ph, b.ctypes.data, x.ctypes.data, n, 0, C.byref(co), C.byref(rep))
+        rc = entry(a.ctx.handle, a.handle, ph, b.ctypes.data, x.ctypes.data, n, 0, C.byref(co), C.byref(rep))
     if rc not in (CE_OK, CE_ENOCONV):
         _check(rc)
     return SolveReport(bool(rep.converged), int(rep.iterations), rep.final_recurrence_residual,
                        rep.final_true_residual, rep.seconds), x
+
+
+def pcg(a: DeviceMatrix, n: int, b, precond: Optional[CEFactorization], opts: Optional[PcgOptions] = None):
+    """Preconditioned CG with the minres contract; returns (SolveReport, x).
+
+    `a` must be a DeviceMatrix and `precond` a CEFactorization or None (the
+    device loop has no host callbacks).  Non-convergence is reported in the
+    SolveReport, not raised, as in the reference."""
+    return _krylov(lib.ce_pcg, "pcg", a, n, b, precond, opts or PcgOptions())
+
+
+def minres(a: DeviceMatrix, n: int, b, precond: Optional[CEFactorization], opts: Optional[MinresOptions] = None):
+    """MINRES (proj/src/minres.cpp:22-115, the paper's solver) on the device; returns
+    (SolveReport, x).  Same contract as pcg: x0 = 0, recurrence stopping rule relative to
+    the starting preconditioned residual, non-convergence reported, not raised."""
+    return _krylov(lib.ce_minres, "minres", a, n, b, precond, opts or MinresOptions())
 
 
 class Problem:

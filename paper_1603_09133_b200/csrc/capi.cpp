@@ -408,23 +408,31 @@ int ce_factor_dump(const ce_factor* f, const char* path) {
   });
 }
 
-int ce_pcg(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const double* b, double* x, int64_t n,
-           int on_device, const ce_pcg_opts* opts, ce_solve_report* rep) {
+namespace {
+// shared body of the two Krylov entry points (minres.hpp:46-47 contract)
+int krylov(bool use_minres, ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const double* b, double* x,
+           int64_t n, int on_device, const ce_pcg_opts* opts, ce_solve_report* rep) {
   if (rep) std::memset(rep, 0, sizeof *rep);
   ceg::SolveOut so;
+  const char* what = use_minres ? "minres" : "pcg";
+  auto run = [&](const ce_matrix* am, const ceg::Factor* m, const double* db, double* dx, double tol, int64_t maxit,
+                 bool track) {
+    return use_minres ? ceg::minres_device(am->m, m, db, dx, tol, maxit, track)
+                      : ceg::pcg_device(am->m, m, db, dx, tol, maxit, track);
+  };
   const int rc = guarded([&] {
-    if (!ctx || !a || n != a->m.n) throw std::invalid_argument("pcg dimension mismatch");
+    if (!ctx || !a || n != a->m.n) throw std::invalid_argument(std::string(what) + " dimension mismatch");
     if (precond && precond->f->n != n) throw std::invalid_argument("preconditioner dimension mismatch");
     const double tol = opts ? opts->tol : 1e-10;
     const int64_t maxit = opts ? opts->maxit : 1000;
     const bool track = opts && opts->track_true_residual;
     cudaStream_t s = ctx->ctx.stream;
     if (on_device) {
-      so = ceg::pcg_device(a->m, precond ? precond->f.get() : nullptr, b, x, tol, maxit, track);
+      so = run(a, precond ? precond->f.get() : nullptr, b, x, tol, maxit, track);
     } else {
       ceg::DevArray<double> db(static_cast<size_t>(n)), dx(static_cast<size_t>(n));
       CE_CUDA(cudaMemcpyAsync(db.p, b, static_cast<size_t>(n) * sizeof(double), cudaMemcpyHostToDevice, s));
-      so = ceg::pcg_device(a->m, precond ? precond->f.get() : nullptr, db.p, dx.p, tol, maxit, track);
+      so = run(a, precond ? precond->f.get() : nullptr, db.p, dx.p, tol, maxit, track);
       CE_CUDA(cudaMemcpyAsync(x, dx.p, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost, s));
       CE_CUDA(cudaStreamSynchronize(s));
     }
@@ -438,10 +446,21 @@ int ce_pcg(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const doub
     rep->seconds = so.seconds;
   }
   if (!so.converged) {
-    g_err = "pcg did not converge";
+    g_err = std::string(what) + " did not converge";
     return CE_ENOCONV;
   }
   return CE_OK;
+}
+}  // namespace
+
+int ce_pcg(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const double* b, double* x, int64_t n,
+           int on_device, const ce_pcg_opts* opts, ce_solve_report* rep) {
+  return krylov(false, ctx, a, precond, b, x, n, on_device, opts, rep);
+}
+
+int ce_minres(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const double* b, double* x, int64_t n,
+              int on_device, const ce_pcg_opts* opts, ce_solve_report* rep) {
+  return krylov(true, ctx, a, precond, b, x, n, on_device, opts, rep);
 }
 
 int ce_problem_create(int cfg, int64_t nx, int64_t ny, int64_t nz, ce_problem** out) {

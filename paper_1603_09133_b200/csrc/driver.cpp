@@ -1734,6 +1734,110 @@ SolveOut pcg_device(const Matrix& A, const Factor* M, const double* d_b, double*
   return out;
 }
 
+// MINRES (minres.cpp:22-115): Lanczos on the preconditioned operator with Givens QR of the
+// tridiagonal; the vectors live on the device, the scalar recurrence runs on the host with
+// the two inner products of each iteration fetched (one 8-byte read each).  Same stopping
+// rules as the reference: recurrence <= tol, or a Lanczos beta below 1e-30 beta1 (exact
+// solution); a negative / non-finite r' M^-1 r is an error (minres.cpp:11-18).
+SolveOut minres_device(const Matrix& A, const Factor* M, const double* d_b, double* d_x, double tol, int64_t maxit,
+                       bool track_true) {
+  cudaStream_t s = A.ctx->stream;
+  const int64_t n = A.n;
+  SolveOut out;
+  const double t0 = now_s();
+  DevArray<double> v(static_cast<size_t>(n)), ya(static_cast<size_t>(n)), r1a(static_cast<size_t>(n)),
+      r2a(static_cast<size_t>(n)), wa(static_cast<size_t>(n)), w1a(static_cast<size_t>(n)), w2a(static_cast<size_t>(n)),
+      tmp(static_cast<size_t>(n));
+  DevArray<double> part(static_cast<size_t>(dot_partials_capacity())), sc(2);
+  double *y = ya.p, *r1 = r1a.p, *r2 = r2a.p, *w = wa.p, *w1 = w1a.p, *w2 = w2a.p;
+  auto dot = [&](const double* a, const double* b) {
+    const int np = launch_dot(a, b, n, part.p, s);
+    launch_sum_partials(part.p, np, sc.p, s);
+    double h = 0.0;
+    CE_CUDA(cudaMemcpyAsync(&h, sc.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CE_CUDA(cudaStreamSynchronize(s));
+    return h;
+  };
+  auto checked_inner = [&](const double* r, const double* z) {  // minres.cpp:11-18
+    const double h = dot(r, z);
+    if (!std::isfinite(h)) throw std::runtime_error("preconditioner produced non-finite values");
+    if (h < 0.0) throw std::runtime_error("preconditioner is not positive definite: r' M^-1 r < 0");
+    return h;
+  };
+  auto precond = [&](const double* in, double* o) {
+    if (M) apply_device(*M, in, o, s);
+    else launch_copy(o, in, n, s);
+  };
+  auto true_resid = [&](double bnorm) {  // relative_residual (minres.cpp:117-122)
+    matvec_device(A, d_x, tmp.p, s);
+    launch_lincomb(tmp.p, d_b, tmp.p, 1.0, nullptr, 0.0, 1.0, n, s);  // b - A x
+    return std::sqrt(dot(tmp.p, tmp.p)) / bnorm;
+  };
+  CE_CUDA(cudaMemsetAsync(d_x, 0, static_cast<size_t>(n) * sizeof(double), s));
+  const double bnorm = std::sqrt(dot(d_b, d_b));
+  if (bnorm == 0.0) {
+    out.converged = true;
+    out.seconds = now_s() - t0;
+    return out;
+  }
+  launch_copy(r1, d_b, n, s);
+  precond(d_b, y);
+  double beta1 = checked_inner(r1, y);
+  if (beta1 == 0.0) {  // minres.cpp:43-47: report left at its defaults
+    out.converged = true;
+    out.seconds = now_s() - t0;
+    return out;
+  }
+  beta1 = std::sqrt(beta1);
+  double oldb = 0.0, beta = beta1, dbar = 0.0, epsln = 0.0, qrnorm = beta1, phibar = beta1, cs = -1.0, sn = 0.0;
+  launch_copy(r2, r1, n, s);
+  CE_CUDA(cudaMemsetAsync(w, 0, static_cast<size_t>(n) * sizeof(double), s));
+  CE_CUDA(cudaMemsetAsync(w2, 0, static_cast<size_t>(n) * sizeof(double), s));
+  const double tiny = 1e-290;
+  for (int64_t itn = 1; itn <= maxit; ++itn) {
+    launch_scale(v.p, 1.0 / beta, y, false, n, s);                              // v = y / beta
+    matvec_device(A, v.p, y, s);                                                 // y = A v
+    if (itn >= 2) launch_lincomb(y, y, r1, beta / oldb, nullptr, 0.0, 1.0, n, s);  // y -= (beta/oldb) r1
+    const double alfa = dot(v.p, y);
+    launch_lincomb(y, y, r2, alfa / beta, nullptr, 0.0, 1.0, n, s);             // y -= (alfa/beta) r2
+    std::swap(r1, r2);  // r1 = r2
+    std::swap(r2, y);   // r2 = y (the old r1 buffer becomes the next y)
+    precond(r2, y);
+    oldb = beta;
+    beta = std::sqrt(checked_inner(r2, y));
+    const double oldeps = epsln;
+    const double delta = cs * dbar + sn * alfa;
+    const double gbar = sn * dbar - cs * alfa;
+    epsln = sn * beta;
+    dbar = -cs * beta;
+    double gamma = std::sqrt(gbar * gbar + beta * beta);
+    gamma = std::max(gamma, tiny);
+    cs = gbar / gamma;
+    sn = beta / gamma;
+    const double phi = cs * phibar;
+    phibar = sn * phibar;
+    // w1 = w2, w2 = w, w = (v - oldeps w1 - delta w2) / gamma; x += phi w
+    std::swap(w1, w2);  // w1 = old w2
+    std::swap(w2, w);   // w2 = old w; w = old w1 buffer (overwritten)
+    launch_lincomb(w, v.p, w1, oldeps, w2, delta, gamma, n, s);
+    launch_scale(d_x, phi, w, true, n, s);
+    qrnorm = phibar;
+    const double rec = qrnorm / beta1;
+    out.iterations = itn;
+    out.trace_rec.push_back(rec);
+    if (track_true) out.trace_true.push_back(true_resid(bnorm));
+    if (rec <= tol || beta / beta1 < 1e-30) {
+      out.converged = true;
+      break;
+    }
+  }
+  out.final_rec = qrnorm / beta1;
+  out.final_true = true_resid(bnorm);
+  CE_CUDA(cudaGetLastError());
+  out.seconds = now_s() - t0;
+  return out;
+}
+
 // ---------------------------------------------------------------- dump
 void dump_factor(const Factor& f, const std::string& path) {
   std::FILE* fp = std::fopen(path.c_str(), "wb");

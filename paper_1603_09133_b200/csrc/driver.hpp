@@ -27,6 +27,10 @@ struct SolveOut {
 SolveOut pcg_device(const Matrix& A, const Factor* M, const double* d_b, double* d_x, double tol, int64_t maxit,
                     bool track_true);
 
+// MINRES with an SPD preconditioner (minres.cpp:22-115, the paper's solver) on the device.
+SolveOut minres_device(const Matrix& A, const Factor* M, const double* d_b, double* d_x, double tol, int64_t maxit,
+                       bool track_true);
+
 void dump_factor(const Factor& f, const std::string& path);
 
 }  // namespace ceg

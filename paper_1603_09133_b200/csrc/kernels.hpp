@@ -221,5 +221,9 @@ void launch_axpy(double* y, const double* x, const double* alpha_num, const doub
 void launch_pcg_update_p(double* p, const double* z, const double* rz_new, const double* rz_old, int64_t n,
                          cudaStream_t s);
 void launch_copy(double* dst, const double* src, int64_t n, cudaStream_t s);
+// MINRES vector steps with host scalars: out = (x - a y - c z) / g (y, z may be null); out (+)= sc x
+void launch_lincomb(double* out, const double* x, const double* y, double a, const double* z, double c, double g,
+                    int64_t n, cudaStream_t s);
+void launch_scale(double* out, double sc, const double* x, bool accumulate, int64_t n, cudaStream_t s);
 
 }  // namespace ceg

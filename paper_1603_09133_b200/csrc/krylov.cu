@@ -83,6 +83,26 @@ __global__ void copy_kernel(double* dst, const double* src, int64_t n) {
     dst[k] = src[k];
 }
 
+// MINRES vector step (minres.cpp:57-89), IEEE operations in the reference's order (no
+// contraction): out = (x - a y - c z) / g, with y / z optional (null = term absent).
+__global__ void lincomb_kernel(double* out, const double* x, const double* y, double a, const double* z, double c,
+                               double g, int64_t n) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double v = x[k];
+    if (y) v = __dsub_rn(v, __dmul_rn(a, y[k]));
+    if (z) v = __dsub_rn(v, __dmul_rn(c, z[k]));
+    out[k] = g == 1.0 ? v : __ddiv_rn(v, g);
+  }
+}
+
+// out = s x  /  out += s x (accumulate), single-rounded products as in the reference
+__global__ void scale_kernel(double* out, double s, const double* x, int accumulate, int64_t n) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[k] = accumulate ? __dadd_rn(out[k], __dmul_rn(s, x[k])) : __dmul_rn(s, x[k]);
+}
+
 unsigned vec_grid(int64_t n) {
   const int64_t g = (n + 255) / 256;
   return static_cast<unsigned>(g < 148 * 16 ? (g > 0 ? g : 1) : 148 * 16);
@@ -128,6 +148,17 @@ void launch_pcg_update_p(double* p, const double* z, const double* rz_new, const
                          cudaStream_t s) {
   note_launch();
   update_p_kernel<<<vec_grid(n), 256, 0, s>>>(p, z, rz_new, rz_old, n);
+}
+
+void launch_lincomb(double* out, const double* x, const double* y, double a, const double* z, double c, double g,
+                    int64_t n, cudaStream_t s) {
+  note_launch();
+  lincomb_kernel<<<vec_grid(n), 256, 0, s>>>(out, x, y, a, z, c, g, n);
+}
+
+void launch_scale(double* out, double sc, const double* x, bool accumulate, int64_t n, cudaStream_t s) {
+  note_launch();
+  scale_kernel<<<vec_grid(n), 256, 0, s>>>(out, sc, x, accumulate ? 1 : 0, n);
 }
 
 void launch_copy(double* dst, const double* src, int64_t n, cudaStream_t s) {

@@ -1397,13 +1397,17 @@ __device__ __noinline__ void strip_range(const SweepArgs& A, int i, int b, int r
 
 // Schur update of one panel pair (P, Q), P <= Q, of row i's close list:
 // X_ts -= g_t g_s^T for s in panel P, t in panel Q, s <= t (level_matrix.cpp:148-162).
-// g rows of both panels are staged in shared memory.
+// g rows of both panels are staged in shared memory.  The task is a short chain of
+// dependent global loads (close columns -> slot offsets -> g rows / X tile), so the
+// first X tile of every warp is loaded before the panels are staged and both sets of
+// loads are in flight together.
 __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int w, int P, int Q, double* sm) {
   CE_SHARED(sm);
   const long long tb0 = clock64();
   __shared__ long long slot_tab[kPanelNb * kPanelNb];  // value offset of stored (t, s), -1: not updated
   __shared__ int tab_bs[kPanelNb];
   __shared__ int roff_s[kPanelNb], roff_t[kPanelNb];
+  __shared__ int col_s[kPanelNb], col_t[kPanelNb];
   __shared__ int n_live[2];
   __shared__ unsigned char xblk[kPanelRows], yblk[kPanelRows];
   __shared__ unsigned short xloc[kPanelRows], yloc[kPanelRows];
@@ -1418,10 +1422,10 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
   // is compacted to live rows (bit-identical result: the skipped terms are exact zeros).
   if (warp < 2) {
     const int n = warp == 0 ? ns : nt, base = warp == 0 ? s0 : t0;
-    int live = 0, roff = 0, bu = 0;
+    int live = 0, roff = 0, bu = 0, u = 0;
     if (lane < n) {
       const int64_t e = c0 + base + lane;
-      const int u = A.cl_col[e];
+      u = A.cl_col[e];
       bu = A.bsz[u];
       roff = A.cl_roff[e];
       live = u < i ? __ldcg(A.rank + u) : bu;
@@ -1437,12 +1441,14 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
       if (warp == 0) {
         tab_bs[lane] = bu;
         roff_s[lane] = roff;
+        col_s[lane] = u;
         for (int y = 0; y < live; ++y) {
           yblk[y0 + y] = static_cast<unsigned char>(lane);
           yloc[y0 + y] = static_cast<unsigned short>(y);
         }
       } else {
         roff_t[lane] = roff;
+        col_t[lane] = u;
         for (int x = 0; x < live; ++x) {
           xblk[y0 + x] = static_cast<unsigned char>(lane);
           xloc[y0 + x] = static_cast<unsigned short>(x);
@@ -1451,41 +1457,88 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
     }
     if (lane == 31) n_live[warp] = incl;
   }
-  for (int idx = tid; idx < nt * ns; idx += T) {
-    const int kt = idx / ns, ks = idx % ns;
-    long long off = -1;
-    if (!(P == Q && ks > kt)) {
-      const int t = A.cl_col[c0 + t0 + kt], s = A.cl_col[c0 + s0 + ks];
-      if (A.tri_off) {  // one independent load per pair instead of a binary search chain
-        off = __ldg(A.tri_off + static_cast<int64_t>(t) * (t + 1) / 2 + s);
-        if (off < 0) set_error(A.err, kErrPattern, A.level, i);
-      } else {
+  if (!A.tri_off) {
+    // binary search of the squared pattern (large levels): a chain of dependent loads per
+    // pair, started before the panel columns are known to the other warps
+    for (int idx = tid; idx < nt * ns; idx += T) {
+      const int kt = idx / ns, ks = idx % ns;
+      long long off = -1;
+      if (!(P == Q && ks > kt)) {
+        const int t = A.cl_col[c0 + t0 + kt], s = A.cl_col[c0 + s0 + ks];
         const int64_t slot = find_slot(A.sq_ptr, A.sq_col, A.sq_slot, t, s);
         if (slot < 0) set_error(A.err, kErrPattern, A.level, i);
         else off = A.slot_off[slot];
       }
+      slot_tab[idx] = off;
     }
-    slot_tab[idx] = off;
   }
   __syncthreads();
+  if (A.tri_off) {  // one independent load per pair
+    for (int idx = tid; idx < nt * ns; idx += T) {
+      const int kt = idx / ns, ks = idx % ns;
+      long long off = -1;
+      if (!(P == Q && ks > kt)) {
+        const int t = col_t[kt], s = col_s[ks];
+        off = __ldg(A.tri_off + static_cast<int64_t>(t) * (t + 1) / 2 + s);
+        if (off < 0) set_error(A.err, kErrPattern, A.level, i);
+      }
+      slot_tab[idx] = off;
+    }
+    __syncthreads();
+  }
   const long long tb1 = clock64();
   prof_add(A, kProfBSetup, tb1 - tb0);
   const int rsn = n_live[0], rtn = n_live[1];
   // row strides = 8 (mod 16) doubles: the four k-rows of an m8n8k4 fragment load hit
   // disjoint bank halves (two wavefronts, the minimum for 32 doubles)
   const int lds = ((rsn + 7) & ~15) + 8, ldt = ((rtn + 7) & ~15) + 8;
+  // rtn x rsn product on the FP64 tensor cores (mma.m8n8k4): a warp owns a 16 x 32 tile
+  // (2 x 4 fragments), the k loop runs over the w g-columns in steps of 4 (masked tail);
+  // the epilogue scatters into the (t, s) blocks.
+  const int g = lane >> 2, t4 = lane & 3;
+  const int ntx = (rtn + 15) / 16, nty = (rsn + 31) / 32;
+  int ktv[2], xlv[2], ksv[8], ylv[8], bsv[8];
+  double xv[2][8];
+  auto load_tile = [&](int wt) {
+    const int xb = (wt / nty) * 16, yb = (wt % nty) * 32;
+#pragma unroll
+    for (int i2 = 0; i2 < 2; ++i2) {
+      const int x = xb + 8 * i2 + g;
+      ktv[i2] = x < rtn ? xblk[x] : -1;
+      xlv[i2] = x < rtn ? xloc[x] : 0;
+    }
+#pragma unroll
+    for (int j2 = 0; j2 < 8; ++j2) {
+      const int y = yb + 8 * (j2 >> 1) + 2 * t4 + (j2 & 1);
+      ksv[j2] = y < rsn ? yblk[y] : -1;
+      ylv[j2] = y < rsn ? yloc[y] : 0;
+      bsv[j2] = ksv[j2] >= 0 ? tab_bs[ksv[j2]] : 0;
+    }
+#pragma unroll
+    for (int i2 = 0; i2 < 2; ++i2)
+#pragma unroll
+      for (int j2 = 0; j2 < 8; ++j2) {
+        xv[i2][j2] = 0.0;
+        if (ktv[i2] >= 0 && ksv[j2] >= 0) {
+          const long long off = slot_tab[ktv[i2] * ns + ksv[j2]];
+          if (off >= 0) xv[i2][j2] = ldg(A.store + off + static_cast<int64_t>(xlv[i2]) * bsv[j2] + ylv[j2]);
+        }
+      }
+  };
+  // first tile's X in flight while the panels are staged
+  if (warp < ntx * nty) load_tile(warp);
   // g rows transposed into shared memory: GsT[q][y], GtT[q][x] (live rows only)
   const double* G = A.fac + A.g_off[i];
   double* GsT = sm;
   double* GtT = P == Q ? sm : sm + static_cast<int64_t>(lds) * w;
-  // staged with 4 independent loads in flight per thread (the rows are short, latency dominates)
+  // staged with 8 independent loads in flight per thread (the rows are short, latency dominates)
   auto stage = [&](double* dst, int ld, int n, const int* roff, const unsigned char* blk, const unsigned short* loc) {
     const int tot = ld * w;
-    for (int base = tid; base < tot; base += 4 * T) {
-      double v[4];
-      int di[4];
+    for (int base = tid; base < tot; base += 8 * T) {
+      double v[8];
+      int di[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const int idx = base + u * T;
         di[u] = -1;
         v[u] = 0.0;
@@ -1496,7 +1549,7 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 8; ++u)
         if (di[u] >= 0) dst[di[u]] = v[u];
     }
   };
@@ -1505,73 +1558,44 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
   __syncthreads();
   const long long tb2 = clock64();
   prof_add(A, kProfBStage, tb2 - tb1);
-  // rtn x rsn product on the FP64 tensor cores (mma.m8n8k4): a warp owns a 16 x 32 tile
-  // (2 x 4 fragments), the k loop runs over the w g-columns in steps of 4 (masked tail);
-  // the tile's X values are prefetched before the k loop, the epilogue scatters into the
-  // (t, s) blocks.
-  {
-    const int lane = tid & 31, warp = tid >> 5;
-    const int g = lane >> 2, t4 = lane & 3;
-    const int ntx = (rtn + 15) / 16, nty = (rsn + 31) / 32;
-    for (int wt = warp; wt < ntx * nty; wt += T / 32) {
-      const int xb = (wt / nty) * 16, yb = (wt % nty) * 32;
-      int ktv[2], xlv[2], ksv[8], ylv[8], bsv[8];
+  for (int wt = warp; wt < ntx * nty; wt += T / 32) {
+    if (wt != warp) load_tile(wt);
+    const int xb = (wt / nty) * 16, yb = (wt % nty) * 32;
+    double acc[2][8];
+#pragma unroll
+    for (int i2 = 0; i2 < 2; ++i2)
+#pragma unroll
+      for (int j2 = 0; j2 < 8; ++j2) acc[i2][j2] = 0.0;
+    for (int q0 = 0; q0 < w; q0 += 4) {
+      const int q = q0 + t4;
+      double af[2], bf[4];
 #pragma unroll
       for (int i2 = 0; i2 < 2; ++i2) {
         const int x = xb + 8 * i2 + g;
-        ktv[i2] = x < rtn ? xblk[x] : -1;
-        xlv[i2] = x < rtn ? xloc[x] : 0;
+        af[i2] = (q < w && x < ldt) ? GtT[q * ldt + x] : 0.0;
       }
 #pragma unroll
-      for (int j2 = 0; j2 < 8; ++j2) {
-        const int y = yb + 8 * (j2 >> 1) + 2 * t4 + (j2 & 1);
-        ksv[j2] = y < rsn ? yblk[y] : -1;
-        ylv[j2] = y < rsn ? yloc[y] : 0;
-        bsv[j2] = ksv[j2] >= 0 ? tab_bs[ksv[j2]] : 0;
-      }
-      double xv[2][8], acc[2][8];
-#pragma unroll
-      for (int i2 = 0; i2 < 2; ++i2)
-#pragma unroll
-        for (int j2 = 0; j2 < 8; ++j2) {
-          xv[i2][j2] = 0.0;
-          acc[i2][j2] = 0.0;
-          if (ktv[i2] >= 0 && ksv[j2] >= 0) {
-            const long long off = slot_tab[ktv[i2] * ns + ksv[j2]];
-            if (off >= 0) xv[i2][j2] = ldg(A.store + off + static_cast<int64_t>(xlv[i2]) * bsv[j2] + ylv[j2]);
-          }
-        }
-      for (int q0 = 0; q0 < w; q0 += 4) {
-        const int q = q0 + t4;
-        double af[2], bf[4];
-#pragma unroll
-        for (int i2 = 0; i2 < 2; ++i2) {
-          const int x = xb + 8 * i2 + g;
-          af[i2] = (q < w && x < ldt) ? GtT[q * ldt + x] : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int y = yb + 8 * j + g;
-          bf[j] = (q < w && y < lds) ? GsT[q * lds + y] : 0.0;
-        }
-#pragma unroll
-        for (int i2 = 0; i2 < 2; ++i2)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                         : "+d"(acc[i2][2 * j]), "+d"(acc[i2][2 * j + 1])
-                         : "d"(af[i2]), "d"(bf[j]));
+      for (int j = 0; j < 4; ++j) {
+        const int y = yb + 8 * j + g;
+        bf[j] = (q < w && y < lds) ? GsT[q * lds + y] : 0.0;
       }
 #pragma unroll
       for (int i2 = 0; i2 < 2; ++i2)
 #pragma unroll
-        for (int j2 = 0; j2 < 8; ++j2)
-          if (ktv[i2] >= 0 && ksv[j2] >= 0) {
-            const long long off = slot_tab[ktv[i2] * ns + ksv[j2]];
-            if (off >= 0)
-              A.store[off + static_cast<int64_t>(xlv[i2]) * bsv[j2] + ylv[j2]] = xv[i2][j2] - acc[i2][j2];
-          }
+        for (int j = 0; j < 4; ++j)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[i2][2 * j]), "+d"(acc[i2][2 * j + 1])
+                       : "d"(af[i2]), "d"(bf[j]));
     }
+#pragma unroll
+    for (int i2 = 0; i2 < 2; ++i2)
+#pragma unroll
+      for (int j2 = 0; j2 < 8; ++j2)
+        if (ktv[i2] >= 0 && ksv[j2] >= 0) {
+          const long long off = slot_tab[ktv[i2] * ns + ksv[j2]];
+          if (off >= 0)
+            A.store[off + static_cast<int64_t>(xlv[i2]) * bsv[j2] + ylv[j2]] = xv[i2][j2] - acc[i2][j2];
+        }
   }
   __syncthreads();
   prof_add(A, kProfBTiles, clock64() - tb2);

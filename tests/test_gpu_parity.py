@@ -163,6 +163,44 @@ def test_pcg_parity(runs, name):
 
 
 @pytest.mark.parametrize("name", IDS)
+def test_minres_parity(runs, name):
+    """Device MINRES (minres.cpp:22-115, the paper's solver) against the oracle's
+    restatement: same preconditioner contract, iteration counts within +-1 preconditioned, true
+    residual at the oracle's level; unpreconditioned counts within 2% (rounding drift)."""
+    R = runs[name]
+    p = R["p"]
+    rg, xg = ce.minres(R["a"], p.n, p.rhs, R["g_free"], ce.MinresOptions(tol=p.tol, maxit=500, track_true_residual=False))
+    ro, xo = R["op"].krylov(p.rhs, R["fo"], "minres", tol=p.tol, maxit=500)
+    assert rg.converged and ro["converged"]
+    assert abs(rg.iterations - ro["iterations"]) <= 1
+    assert rg.final_recurrence_residual <= p.tol
+    assert rg.final_true_residual <= max(10 * p.tol, 10 * ro["true_resid"])
+    rg0, _ = ce.minres(R["a"], p.n, p.rhs, None, ce.MinresOptions(tol=1e-6, maxit=4000, track_true_residual=False))
+    ro0, _ = R["op"].krylov(p.rhs, None, "minres", tol=1e-6, maxit=4000)
+    assert rg0.converged and ro0["converged"]
+    assert abs(rg0.iterations - ro0["iterations"]) <= max(1, 0.02 * ro0["iterations"])
+
+
+def test_minres_edge_cases(gpu_ctx):
+    """Zero rhs converges at once with x = 0 (minres.cpp:33-37); device (torch) vectors give the
+    host result; maxit exhaustion is reported, not raised; a dimension mismatch is an error."""
+    import torch
+    p = ce.Problem(1, 32, 32)
+    a = ce.DeviceMatrix(p.matrix())
+    f = ce.ce_factorize(a, p.plan, p.strategy(), ce.FactorOptions(dense_threshold=256))
+    rep, x = ce.minres(a, p.n, np.zeros(p.n), f)
+    assert rep.converged and rep.iterations == 0 and not np.any(x)
+    rh, xh = ce.minres(a, p.n, p.rhs, f, ce.MinresOptions(tol=1e-10))
+    rd, xd = ce.minres(a, p.n, torch.from_numpy(p.rhs).cuda(), f, ce.MinresOptions(tol=1e-10))
+    assert rh.converged and rd.iterations == rh.iterations
+    assert np.array_equal(xd.cpu().numpy(), xh)
+    r1, _ = ce.minres(a, p.n, p.rhs, None, ce.MinresOptions(tol=1e-14, maxit=3, track_true_residual=True))
+    assert not r1.converged and r1.iterations == 3
+    with pytest.raises(RuntimeError):
+        ce.minres(a, p.n + 1, np.zeros(p.n + 1), f)
+
+
+@pytest.mark.parametrize("name", IDS)
 def test_apply_q_round_trip_and_orthogonality(runs, name):
     """SPEC.md:281-285 round trip; SPEC.md:319 orthogonal bases (<= 1e-12) from the GPU dump."""
     R = runs[name]
