@@ -185,6 +185,18 @@ int ce_minres(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const d
  * cli.cpp:33-58, extended with the 2-D/FV/random-k/RNG inputs BASELINE.json names). */
 int ce_problem_create(int cfg, int64_t nx, int64_t ny, int64_t nz, ce_problem** out);
 void ce_problem_free(ce_problem* p);
+/* The reference CLI's `file` problem (proj/src/cli.cpp:114-133 load_problem + finish_load :49-58):
+ * Matrix Market "coordinate real general|symmetric" (matrix_market.cpp:21-59), a CoarseningPlan
+ * file (problems.cpp:140-174; NULL = CoarseningPlan::trivial(n, block), problems.cpp:175-182) and
+ * an rhs vector file (NULL = ones); the plan's initial permutation is applied and the CSB built
+ * with BlockSparseMatrix::from_triplets semantics (block_matrix.cpp:48-90: duplicates summed,
+ * symmetry checked to 1e-12 max|a|, full diagonal).  Errors (IO, asymmetric input, invalid plan)
+ * return CE_EUSAGE with the reference's message in ce_last_error(). */
+int ce_problem_load(const char* matrix_path, const char* plan_path, const char* rhs_path, int64_t block,
+                    ce_problem** out);
+/* run_gen's writer (cli.cpp:136-150): natural-order matrix (write_matrix_market, lower triangle,
+ * 17 digits), rhs (write_vector) and plan (CoarseningPlan::save); any path may be NULL (skipped). */
+int ce_problem_save(const ce_problem* p, const char* matrix_path, const char* plan_path, const char* rhs_path);
 /* Views into the problem (valid until ce_problem_free). */
 int ce_problem_csb(const ce_problem* p, ce_csb_host* out);
 int ce_problem_plan(const ce_problem* p, ce_plan_host* out);

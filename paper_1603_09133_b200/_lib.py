@@ -97,6 +97,8 @@ SIGNATURES = {
     "ce_minres": (C.c_int, [vp, vp, vp, vp, vp, i64, C.c_int, C.POINTER(PcgOpts), C.POINTER(Report)]),
     "ce_problem_create": (C.c_int, [C.c_int, i64, i64, i64, C.POINTER(vp)]),
     "ce_problem_free": (None, [vp]),
+    "ce_problem_load": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, i64, C.POINTER(vp)]),
+    "ce_problem_save": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_char_p]),
     "ce_problem_csb": (C.c_int, [vp, C.POINTER(CsbHost)]),
     "ce_problem_plan": (C.c_int, [vp, C.POINTER(PlanHost)]),
     "ce_problem_rhs": (dblp, [vp]),

@@ -16,6 +16,7 @@ Vectors are numpy float64 arrays (host) or torch float64 CUDA tensors (device).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -363,9 +364,12 @@ def minres(a: DeviceMatrix, n: int, b, precond: Optional[CEFactorization], opts:
 class Problem:
     """A BASELINE.json configuration generated on the host."""
 
-    def __init__(self, cfg: int, nx: int = 0, ny: int = 0, nz: int = 0):
-        h = C.c_void_p()
-        _check(lib.ce_problem_create(int(cfg), int(nx), int(ny), int(nz), C.byref(h)))
+    def __init__(self, cfg: int, nx: int = 0, ny: int = 0, nz: int = 0, _handle=None):
+        if _handle is None:
+            h = C.c_void_p()
+            _check(lib.ce_problem_create(int(cfg), int(nx), int(ny), int(nz), C.byref(h)))
+        else:
+            h = _handle
         self.handle = h
         self.cfg = cfg
         csb = L.CsbHost()
@@ -396,6 +400,20 @@ class Problem:
         if getattr(self, "handle", None):
             lib.ce_problem_free(self.handle)
             self.handle = None
+
+    @classmethod
+    def load(cls, matrix: str, plan: Optional[str] = None, rhs: Optional[str] = None, block: int = 8) -> "Problem":
+        """The reference CLI's `file` problem (cli.cpp:114-133): Matrix Market matrix, optional
+        plan file (else the trivial plan with `block`), optional rhs file (else ones)."""
+        h = C.c_void_p()
+        enc = lambda x: None if x is None else os.fsencode(x)  # noqa: E731
+        _check(lib.ce_problem_load(enc(matrix), enc(plan), enc(rhs), int(block), C.byref(h)))
+        return cls(0, _handle=h)
+
+    def save(self, matrix: Optional[str] = None, plan: Optional[str] = None, rhs: Optional[str] = None) -> None:
+        """run_gen's files (cli.cpp:136-150): natural-order matrix.mtx, plan.txt, rhs.txt."""
+        enc = lambda x: None if x is None else os.fsencode(x)  # noqa: E731
+        _check(lib.ce_problem_save(self.handle, enc(matrix), enc(plan), enc(rhs)))
 
     def matrix(self) -> BlockSparseMatrix:
         return BlockSparseMatrix(self.offsets, self.row_ptr, self.col_idx, self.val_ptr, self.values)

@@ -471,6 +471,23 @@ int ce_problem_create(int cfg, int64_t nx, int64_t ny, int64_t nz, ce_problem** 
   });
 }
 
+int ce_problem_load(const char* matrix_path, const char* plan_path, const char* rhs_path, int64_t block,
+                    ce_problem** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("null argument");
+    auto p = std::make_unique<ce_problem>();
+    p->p.load(matrix_path, plan_path, rhs_path, block);
+    *out = p.release();
+  });
+}
+
+int ce_problem_save(const ce_problem* p, const char* matrix_path, const char* plan_path, const char* rhs_path) {
+  return guarded([&] {
+    if (!p) throw std::invalid_argument("null argument");
+    p->p.save(matrix_path, plan_path, rhs_path);
+  });
+}
+
 void ce_problem_free(ce_problem* p) { delete p; }
 
 int ce_problem_csb(const ce_problem* p, ce_csb_host* out) {
