@@ -301,6 +301,31 @@ LevelPlan plan_symbolic(int64_t M, std::vector<int64_t> bptr, std::vector<int> b
   }
   P.sdiag.resize(static_cast<size_t>(M));
   for (int64_t i = 0; i < M; ++i) P.sdiag[static_cast<size_t>(i)] = csr_find(P.sptr, P.scol, i, static_cast<int>(i));
+  // Far blocks still exactly zero when their row is compressed (kind 3): a far block (i, j)
+  // starts at zero (not in the level's base pattern) and only the Schur update of an earlier
+  // row k with i, j in close(k) writes it (level_matrix.cpp:148-162).  Without such a k < i
+  // it contributes zero columns to F_i, and the compression gather / strip skip it; sizes,
+  // nsig and the F-empty test keep counting it (kind 2 or 3 = far).
+  if (!(std::getenv("CE_NO_DEAD_FAR") && std::getenv("CE_NO_DEAD_FAR")[0] == '1'))
+    parallel_rows(M, [&](int64_t r0, int64_t r1) {
+      std::vector<int64_t> mark(static_cast<size_t>(M), -1);
+      for (int64_t i = r0; i < r1; ++i) {
+        for (int64_t k = P.cptr[static_cast<size_t>(i)]; k < P.cptr[static_cast<size_t>(i + 1)]; ++k) {
+          const int t = P.ccol[static_cast<size_t>(k)];
+          if (t < i) mark[static_cast<size_t>(t)] = i;
+        }
+        for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e) {
+          if (P.skind[static_cast<size_t>(e)] != 2) continue;
+          const int j = P.scol[static_cast<size_t>(e)];
+          bool live = false;
+          for (int64_t k = P.cptr[static_cast<size_t>(j)]; k < P.cptr[static_cast<size_t>(j + 1)] && !live; ++k) {
+            const int t = P.ccol[static_cast<size_t>(k)];
+            live = t < i && mark[static_cast<size_t>(t)] == i;
+          }
+          if (!live) P.skind[static_cast<size_t>(e)] = 3;
+        }
+      }
+    });
   // Wave (topological) order of the dependency DAG: row j depends on every i < j in sq(j)
   // (SURVEY.md A.2).  Items are issued in this order, so the ticket window always holds
   // the current wavefront instead of a run of consecutive (mutually dependent) rows.
@@ -358,7 +383,7 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
     P.csum[static_cast<size_t>(i)] = c;
     int64_t f = 0;
     for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e)
-      if (P.skind[static_cast<size_t>(e)] == 2) f += P.bsz[static_cast<size_t>(P.scol[static_cast<size_t>(e)])];
+      if (P.skind[static_cast<size_t>(e)] >= 2) f += P.bsz[static_cast<size_t>(P.scol[static_cast<size_t>(e)])];
     P.fsum[static_cast<size_t>(i)] = f;
     P.fmax = std::max(P.fmax, f);
   }
@@ -390,15 +415,19 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
       const size_t iu = static_cast<size_t>(i);
       const int64_t b = P.bsz[iu];
       // A1: TSQR leaves when the far gather is large (work ~ f b^2)
-      int64_t nfar = 0, nstrip = 0, strip_cols = 0;
+      int64_t nfar = 0, nstrip = 0, strip_cols = 0, flive = 0;
       for (int64_t e = P.sptr[iu]; e < P.sptr[iu + 1]; ++e) {
-        if (P.skind[static_cast<size_t>(e)] == 2) ++nfar;
-        if (P.skind[static_cast<size_t>(e)] != 0) {
+        const unsigned char kind = P.skind[static_cast<size_t>(e)];
+        if (kind == 2) {
+          ++nfar;
+          flive += P.bsz[static_cast<size_t>(P.scol[static_cast<size_t>(e)])];
+        }
+        if (kind == 1 || kind == 2) {
           ++nstrip;
           strip_cols += P.bsz[static_cast<size_t>(P.scol[static_cast<size_t>(e)])];
         }
       }
-      if (P.fsum[iu] * b * b > th.leaf_work && P.fsum[iu] > lcols) {
+      if (flive * b * b > th.leaf_work && flive > lcols) {
         // TSQR tree: leaves of <= lcols far columns (greedy over the far blocks), then
         // levels combining F = max(2, kcap / b) triangles each, down to one triangle
         int64_t n0 = 0, cols = 0;
@@ -521,7 +550,7 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
             P.sroff[eu] = P.croff[static_cast<size_t>(k)];
           }
           nf += P.skind[eu] == 2;
-          ns += P.skind[eu] != 0;
+          ns += P.skind[eu] == 1 || P.skind[eu] == 2;
         }
         // leaf boundaries: greedy packing of the far blocks into <= lcols columns (as counted);
         // strip task k starts at the strip entry with ordinal ns k / nA3 (row end if none)
@@ -540,7 +569,7 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
             }
             cols += bj;
           }
-          if (kind != 0) {
+          if (kind == 1 || kind == 2) {
             while (ks <= na3 && next_o(ns, ks, na3) == os && os < ns) P.strip_e[static_cast<size_t>(P.strip_ptr[iu] + ks++)] = e;
             ++os;
           }

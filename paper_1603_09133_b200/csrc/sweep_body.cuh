@@ -1281,7 +1281,7 @@ __device__ __noinline__ void strip_range(const SweepArgs& A, int i, int b, int r
       if (tid == 0) {
         int kk = k, cols = 0;
         for (; kk < n; ++kk) {
-          if (W.kind[kk] == 0) continue;
+          if (W.kind[kk] == 0 || W.kind[kk] == 3) continue;  // diagonal / far block still exactly zero
           const int bj = W.bsz[kk];
           if (cols + bj > cw) break;
           for (int c = 0; c < bj; ++c) {
@@ -1629,7 +1629,8 @@ __device__ __noinline__ void task_a2(const SweepArgs& A, int i, const Buf& s_, i
   // ---- far-block triangle (compression.cpp:38-48) ----
   int fcols;
   if (nA1 == 0) {
-    fcols = gather_tsqr(A, i, b, s, p0, p1, &sflag[0], shr, W);
+    gather_tsqr(A, i, b, s, p0, p1, &sflag[0], shr, W);
+    fcols = static_cast<int>(A.fsum[i]);  // every far column, also the still-zero ones it skipped
   } else {
     fcols = static_cast<int>(A.fsum[i]);
     // the TSQR tree's root triangle (its last node)
