@@ -24,6 +24,15 @@
 
 #include "kernels.hpp"
 
+#ifndef CE_SWEEP_BUDGET
+#define CE_SWEEP_BUDGET 18000  // per-CTA buffer target (doubles): strip chunk width, Schur panel height (A/B: 11k 2.03 s, 14k 1.94, 16k 1.93, 18k 1.89, 20k 1.91, 24k 2.03 on cfg2)
+#endif
+#ifndef CE_KCAP
+#define CE_KCAP 128  // TSQR chunk height (far columns per leaf)
+#endif
+#ifndef CE_KCAP_BUDGET
+#define CE_KCAP_BUDGET 11000
+#endif
 #ifndef CE_SWEEP_MIN_BLOCKS
 #define CE_SWEEP_MIN_BLOCKS 1  // resident sweep CTAs per SM the register allocation must allow
 #endif
@@ -105,7 +114,7 @@ __host__ __device__ inline Layout sweep_layout(int bmax, int kcap) {
   L.creg = static_cast<int64_t>((kcap + 1) | 1) * bmax;             // F^T chunk
   L.base = 4 * L.bb + L.creg + 3LL * bmax + (bmax + 1) / 2 + 4;    // R V U D C sig tau nrm perm
   const int64_t dreg = L.bb + L.creg;
-  const int64_t budget = 11000;  // doubles per CTA (two CTAs per SM next to ~22 KB static smem)
+  const int64_t budget = CE_SWEEP_BUDGET;  // doubles per CTA of dynamic shared memory
   int64_t cw = dreg / (2 * bmax);
   const int64_t cwb = (budget - L.base + dreg) / (2 * bmax);
   if (cwb > cw) cw = cwb;
@@ -321,8 +330,8 @@ __global__ void remainder_kernel(RemainderArgs A) {
 int sweep_kcap(int bmax) {
   // F^T chunk height: 128 rows, shortened (not below 64) so that the per-CTA buffer of
   // wide-block levels still allows two CTAs per SM
-  int k = 128;
-  while (k > bmax && k > 64 && sweep_layout(bmax, k).base > 11000) k -= 8;
+  int k = CE_KCAP;
+  while (k > bmax && k > 64 && sweep_layout(bmax, k).base > CE_KCAP_BUDGET) k -= 8;
   return k > bmax ? k : bmax;
 }
 
