@@ -407,7 +407,8 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
   // per-row task counts (parallel over rows), then prefix offsets
   const Thresholds& th = thresholds();
   const int64_t kcap = sweep_kcap(static_cast<int>(bmax));
-  const int64_t lcols = th.leaf_cols > 0 ? th.leaf_cols : kcap;  // far columns per TSQR leaf
+  // far columns per TSQR leaf (<= 128: the register-resident leaf QR)
+  const int64_t lcols = th.leaf_cols > 0 ? th.leaf_cols : std::min<int64_t>(kcap, 128);
   P.nleaf.assign(static_cast<size_t>(M), 0);
   std::vector<int> np_row(static_cast<size_t>(M), 0);
   parallel_rows(M, [&](int64_t r0, int64_t r1) {

@@ -28,10 +28,10 @@
 #define CE_SWEEP_BUDGET 18000  // per-CTA buffer target (doubles): strip chunk width, Schur panel height (A/B: 11k 2.03 s, 14k 1.94, 16k 1.93, 18k 1.89, 20k 1.91, 24k 2.03 on cfg2)
 #endif
 #ifndef CE_KCAP
-#define CE_KCAP 128  // TSQR chunk height (far columns per leaf)
+#define CE_KCAP 192  // TSQR chunk height: leaves take <= 128 far columns, tree nodes fold up to kcap / b children (A/B on cfg2: 128 1.90 s, 176 1.88, 192 1.85)
 #endif
 #ifndef CE_KCAP_BUDGET
-#define CE_KCAP_BUDGET 11000
+#define CE_KCAP_BUDGET 18000
 #endif
 #ifndef CE_SWEEP_MIN_BLOCKS
 #define CE_SWEEP_MIN_BLOCKS 1  // resident sweep CTAs per SM the register allocation must allow

@@ -378,6 +378,12 @@ __device__ void tsqr_fast(double* R, double* C, int K, int b, int ldc, double* s
   if (K <= 128 && b <= 16) tsqr_reg_t<16, 8, 1>(R, C, K, b, ldc, shr);
   else if (K <= 128 && b <= 32) tsqr_reg_t<8, 16, 1>(R, C, K, b, ldc, shr);
   else if (K <= 128 && b <= 64) tsqr_reg_t<8, 16, 2>(R, C, K, b, ldc, shr);
+#if CE_KCAP > 128
+  // taller combine chunks (more children per TSQR tree node)
+  else if (K <= 192 && b <= 16) tsqr_reg_t<16, 12, 1>(R, C, K, b, ldc, shr);
+  else if (K <= 192 && b <= 32) tsqr_reg_t<8, 24, 1>(R, C, K, b, ldc, shr);
+  else if (K <= 192 && b <= 64) tsqr_reg_t<8, 24, 2>(R, C, K, b, ldc, shr);
+#endif
   else tsqr_group(R, C, K, b, ldc, shr);
 }
 
