@@ -16,11 +16,28 @@ namespace {
 
 constexpr int T = kApplyThreads;
 constexpr int kApplyWarps = T / 32;
+#ifndef CE_APPLY_PREFETCH
+#define CE_APPLY_PREFETCH 1
+#endif
 constexpr int kWmax = kApplyWmax;  // max eliminated width per block handled by the apply sweeps
 // dynamic shared memory of the sweeps: z/s (kWmax) + per-warp partial sums and u staging
 constexpr size_t kSweepSmem = (kWmax + 2 * kWmax * kApplyWarps) * sizeof(double);
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldcg(p); }
+
+// Pull [p, p + n doubles) into L2 (one prefetch per 128-byte line, lanes of the calling
+// warp split the lines).  Issued before a task waits for its dependencies: the factor
+// data does not depend on them, so after the wait its loads hit L2 instead of HBM.
+__device__ __forceinline__ void prefetch_l2(const double* p, int64_t n, int lane) {
+#if CE_APPLY_PREFETCH
+  const char* b = reinterpret_cast<const char*>(p);
+  const int64_t bytes = n * static_cast<int64_t>(sizeof(double));
+  for (int64_t o = static_cast<int64_t>(lane) * 128; o < bytes; o += 32 * 128)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(b + o));
+#else
+  (void)p; (void)n; (void)lane;
+#endif
+}
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -288,6 +305,11 @@ __global__ void __launch_bounds__(T) forward_task_kernel(ApplyLevelArgs A) {
     const int part = fused ? 0 : part0;
     if (part < P) {
       const int64_t k0 = A.part_b[pp + part], k1 = A.part_b[pp + part + 1];
+      for (int64_t k = k0 + warp; k < k1; k += kApplyWarps) {
+        const int wi = A.in_w[k];
+        prefetch_l2(A.fac + A.in_goff[k] + static_cast<int64_t>(r) * wi, static_cast<int64_t>(w) * wi, lane);
+      }
+      if (fused && warp == kApplyWarps - 1) prefetch_l2(A.linv + A.linv_off[j], static_cast<int64_t>(w) * w, lane);
       for (int64_t k = k0 + threadIdx.x; k < k1; k += T)
         while (ld_acquire(A.flags + A.in_src[k]) == 0) __nanosleep(32);
       if (threadIdx.x == 0) __threadfence();
@@ -341,6 +363,7 @@ __global__ void __launch_bounds__(T) forward_task_kernel(ApplyLevelArgs A) {
     }
     {
       if (!fused) {
+        if (warp == 1) prefetch_l2(A.linv + A.linv_off[j], static_cast<int64_t>(w) * w, lane);
         if (threadIdx.x == 0) {
           while (ld_acquire(A.parts_done + j) < P) __nanosleep(32);
           __threadfence();
@@ -398,6 +421,13 @@ __global__ void __launch_bounds__(T) backward_task_kernel(ApplyLevelArgs A) {
     const int part = fused ? 0 : part0;
     if (part < P) {
       const int s0 = static_cast<int>(A.part_b[pp + part]), s1 = static_cast<int>(A.part_b[pp + part + 1]);
+      for (int sgi = s0 + warp; sgi < s1; sgi += kApplyWarps) {
+        const double* G = A.fac + A.g_off[j];
+        if (sgi == 0) prefetch_l2(G, static_cast<int64_t>(r) * w, lane);
+        else prefetch_l2(G + static_cast<int64_t>(r + A.cl_roff[c0 + sgi - 1]) * w,
+                         static_cast<int64_t>(A.cl_nt[c0 + sgi - 1]) * w, lane);
+      }
+      if (fused && warp == kApplyWarps - 1) prefetch_l2(A.linv + A.linv_off[j], static_cast<int64_t>(w) * w, lane);
       for (int sgi = s0 + threadIdx.x; sgi < s1; sgi += T) {
         if (sgi == 0) continue;
         const int t = A.cl_col[c0 + sgi - 1];
@@ -468,6 +498,7 @@ __global__ void __launch_bounds__(T) backward_task_kernel(ApplyLevelArgs A) {
     {
       double* vj = A.v + A.offsets[j];
       if (!fused) {
+        if (warp == 1) prefetch_l2(A.linv + A.linv_off[j], static_cast<int64_t>(w) * w, lane);
         if (threadIdx.x == 0) {
           while (ld_acquire(A.parts_done + j) < P) __nanosleep(32);
           __threadfence();
