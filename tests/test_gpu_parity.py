@@ -290,3 +290,64 @@ def test_wide_blocks_generic_paths(gpu_ctx):
     x = rng.standard_normal(n)
     y = np.linalg.solve(a, x)
     assert np.linalg.norm(f.solve(x) - y) <= 1e-8 * np.linalg.norm(y)
+
+
+@pytest.mark.parametrize("strategy", ["rank3", "rank6", "abs1e-4"])
+def test_strategy_modes_parity(gpu_ctx, strategy):
+    """The other CompressionStrategy modes (compression.hpp:15-38, compression.cpp:20-61): FixedRank
+    (r = min(rank, b), basis only when F != 0 and r < b) and absolute eps.  The
+    ranks are decided identically, so the operators agree at the north-star tolerance.  The cfg3
+    stencil (random k) is used: on the constant-k grids a fixed rank can cut through an exactly
+    degenerate singular-value cluster, where the retained subspace itself is not unique."""
+    p = ce.Problem(3, 64, 64)
+    op = O.OProblem.config(3, 64, 64)
+    pp = O.OProblem.config(3, 64, 64)
+    O.lib.oracle_problem_perturb(pp.h, 1e-16, 5)  # the oracle's own sensitivity (DESIGN.md §3)
+    if strategy.startswith("rank"):
+        k = int(strategy[4:])
+        s = ce.CompressionStrategy.fixed_rank(k)
+        fo = op.factorize(mode=1, rank=k, dense_threshold=256)
+        fp = pp.factorize(mode=1, rank=k, dense_threshold=256)
+    else:
+        s = ce.CompressionStrategy.adaptive(1e-4, absolute=True)
+        fo = op.factorize(eps=1e-4, absolute=True, dense_threshold=256)
+        fp = pp.factorize(eps=1e-4, absolute=True, dense_threshold=256)
+    a = ce.DeviceMatrix(p.matrix())
+    f = ce.ce_factorize(a, p.plan, s, ce.FactorOptions(dense_threshold=256))
+    assert f.stats["n_levels"] == fo.levels and f.stats["tail_dim"] == fo.tail_dim
+    x = np.random.default_rng(9).standard_normal(p.n)
+    yo = fo.solve(x)
+    err = np.linalg.norm(f.solve(x) - yo) / np.linalg.norm(yo)
+    probe = np.linalg.norm(fp.solve(x) - yo) / np.linalg.norm(yo)
+    print(f"{strategy}: levels {fo.levels} gpu rel {err:.2e} oracle probe {probe:.2e}")
+    assert err <= max(1e-10, 100 * probe)
+
+
+def _solve_in_subprocess(env_extra, cfg=2, grid=(64, 64), dth=64):
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1603_09133_b200 as ce; "
+            "p = ce.Problem(%d, %d, %d); a = ce.DeviceMatrix(p.matrix()); "
+            "f = ce.ce_factorize(a, p.plan, p.strategy(), ce.FactorOptions(dense_threshold=%d)); "
+            "x = np.random.default_rng(0).standard_normal(p.n); np.save(sys.argv[1], f.solve(x))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = tempfile.mktemp(suffix=".npy")
+    env = dict(os.environ, **env_extra)
+    subprocess.run([sys.executable, "-c", code % (root, cfg, grid[0], grid[1], dth), path], env=env, check=True,
+                   timeout=300)
+    return np.load(path)
+
+
+def test_slot_table_and_zero_far_skip_paths(gpu_ctx):
+    """Schur panels looking stored blocks up through the dense triangular table vs the squared-
+    pattern binary search give the bit-identical factor (same offsets); skipping the far blocks
+    that are still exactly zero (kind 3) changes only the TSQR chunking, so the operator stays
+    within roundoff of the full gather and of the oracle."""
+    y0 = _solve_in_subprocess({})
+    y_bs = _solve_in_subprocess({"CE_NO_TRI": "1"})
+    y_full = _solve_in_subprocess({"CE_NO_DEAD_FAR": "1"})
+    assert np.array_equal(y0, y_bs)
+    op = O.OProblem.config(2, 64, 64)
+    yo = op.factorize(eps=1e-6, dense_threshold=64).solve(np.random.default_rng(0).standard_normal(op.n))
+    e_full, e_o = np.linalg.norm(y_full - y0) / np.linalg.norm(y0), np.linalg.norm(y0 - yo) / np.linalg.norm(yo)
+    print(f"skip vs full gather {e_full:.2e}, vs oracle {e_o:.2e}")
+    # deep levels amplify roundoff (DESIGN.md §3): the same bound as test_task_split_paths_agree
+    assert e_full <= 1e-6 and e_o <= 1e-6
