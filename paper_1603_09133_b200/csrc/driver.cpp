@@ -593,40 +593,89 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
     P.item_start[static_cast<size_t>(M)] = it;
     P.n_items = it;
     // Ticket order: wave by wave, and inside a wave stage by stage across its (independent)
-    // rows, so the rows of one wave advance through their stages together.
-    P.item_row.clear();
-    P.item_part.clear();
-    P.item_row.reserve(static_cast<size_t>(it));
-    P.item_part.reserve(static_cast<size_t>(it));
-    for (int64_t w0 = 0; w0 < M;) {
-      int64_t w1 = w0 + 1;
-      const int64_t wv = wave[static_cast<size_t>(P.order[static_cast<size_t>(w0)])];
-      while (w1 < M && wave[static_cast<size_t>(P.order[static_cast<size_t>(w1)])] == wv) ++w1;
-      for (int stage = 0; stage < 4; ++stage)
-        for (int64_t k = w0; k < w1; ++k) {
-          const int row = P.order[static_cast<size_t>(k)];
-          const size_t r = static_cast<size_t>(row);
-          int pb, pe;
-          if (stage == 0) {
-            pb = 0;
-            pe = P.nA1[r];
-          } else if (stage == 1) {
-            pb = P.nA1[r];
-            pe = pb + 1;
-          } else if (stage == 2) {
-            pb = P.nA1[r] + 1;
-            pe = pb + P.nA3[r];
-          } else {
-            pb = P.nA1[r] + 1 + P.nA3[r];
-            pe = pb + P.nB[r];
+    // rows, so the rows of one wave advance through their stages together.  Lookahead: the
+    // Schur panel pairs of wave k that touch a row of wave k+1 ("urgent", U) are issued right
+    // after wave k's A stages; wave k+1's TSQR leaves follow, then wave k's remaining pairs
+    // (R), then wave k+1's tree combines, A2 and strips.  R(k) thus fills the CTAs while wave
+    // k+1's compression chain runs (the A stages of one row leave most CTAs idle).  A row's A
+    // stages wait only for the pairs of its close predecessors that touch its own panel
+    // (sq_pan), its Schur pairs for every task of every predecessor; every wait is on an
+    // earlier ticket (no deadlock).  Rows whose Schur update is 0 or 1 task keep the full wait.
+    std::vector<int64_t> wstart;
+    for (int64_t k = 0; k < M;) {
+      wstart.push_back(k);
+      const int64_t wv = wave[static_cast<size_t>(P.order[static_cast<size_t>(k)])];
+      while (k < M && wave[static_cast<size_t>(P.order[static_cast<size_t>(k)])] == wv) ++k;
+    }
+    wstart.push_back(M);
+    const int64_t nw = static_cast<int64_t>(wstart.size()) - 1;
+    std::vector<std::vector<int>> rest_of(static_cast<size_t>(M)), urg_of(static_cast<size_t>(M));
+    const bool lookahead = !(std::getenv("CE_NO_LOOKAHEAD") && std::getenv("CE_NO_LOOKAHEAD")[0] == '1');
+    parallel_rows(M, [&](int64_t r0, int64_t r1) {
+      std::vector<char> hot;
+      for (int64_t i = r0; i < r1; ++i) {
+        const size_t iu = static_cast<size_t>(i);
+        const int nb = P.nB[iu];
+        if (nb == 0) continue;
+        const int np = static_cast<int>(P.pan_ptr[iu + 1] - P.pan_ptr[iu]) - 1;
+        const int b0 = P.nA1[iu] + 1 + P.nA3[iu];
+        if (nb == 1 || !lookahead) {
+          for (int k = 0; k < nb; ++k) urg_of[iu].push_back(b0 + k);
+          continue;
+        }
+        hot.assign(static_cast<size_t>(np), 0);
+        const int64_t wnext = wave[iu] + 1;
+        for (int p = 0; p < np; ++p)
+          for (int q = P.pan_start[static_cast<size_t>(P.pan_ptr[iu] + p)];
+               q < P.pan_start[static_cast<size_t>(P.pan_ptr[iu] + p + 1)]; ++q) {
+            const int t = P.ccol[static_cast<size_t>(P.cptr[iu] + q)];
+            if (t > i && wave[static_cast<size_t>(t)] == wnext) hot[static_cast<size_t>(p)] = 1;
           }
-          for (int p = pb; p < pe; ++p) {
-            P.item_row.push_back(row);
-            P.item_part.push_back(p);
+        int k = 0;
+        for (int pp = 0; pp < np; ++pp)
+          for (int qq = pp; qq < np; ++qq, ++k)
+            (hot[static_cast<size_t>(pp)] || hot[static_cast<size_t>(qq)] ? urg_of[iu] : rest_of[iu]).push_back(b0 + k);
+      }
+    });
+    auto emit_rows = [&](int64_t w, auto&& parts) {
+      if (w < 0) return;
+      for (int64_t k = wstart[static_cast<size_t>(w)]; k < wstart[static_cast<size_t>(w + 1)]; ++k) {
+        const int row = P.order[static_cast<size_t>(k)];
+        parts(row, static_cast<size_t>(row));
+      }
+    };
+    auto push = [&](int row, int p) {
+      P.item_row.push_back(row);
+      P.item_part.push_back(p);
+    };
+    for (int64_t w = 0; w <= nw; ++w) {
+      if (w < nw) emit_rows(w, [&](int row, size_t r) { for (int p = 0; p < P.nleaf[r]; ++p) push(row, p); });
+      emit_rows(w - 1, [&](int row, size_t r) { for (int p : rest_of[r]) push(row, p); });
+      if (w == nw) break;
+      emit_rows(w, [&](int row, size_t r) { for (int p = P.nleaf[r]; p < P.nA1[r]; ++p) push(row, p); });
+      emit_rows(w, [&](int row, size_t r) { push(row, P.nA1[r]); });
+      emit_rows(w, [&](int row, size_t r) { for (int p = P.nA1[r] + 1; p <= P.nA1[r] + P.nA3[r]; ++p) push(row, p); });
+      emit_rows(w, [&](int row, size_t r) { for (int p : urg_of[r]) push(row, p); });
+    }
+    if (static_cast<int64_t>(P.item_row.size()) != it) throw std::logic_error("ticket order lost items");
+    // sq_pan: panel of j inside close(i) for each close predecessor entry (j, i), i < j
+    P.sq_pan.assign(P.scol.size(), -1);
+    if (lookahead)
+      parallel_rows(M, [&](int64_t r0, int64_t r1) {
+        for (int64_t j = r0; j < r1; ++j) {
+          for (int64_t e = P.sptr[static_cast<size_t>(j)]; e < P.sdiag[static_cast<size_t>(j)]; ++e) {
+            if (P.skind[static_cast<size_t>(e)] != 1) continue;
+            const int i = P.scol[static_cast<size_t>(e)];
+            const size_t iu = static_cast<size_t>(i);
+            if (P.nB[iu] <= 1) continue;
+            const int64_t q = csr_find(P.cptr, P.ccol, i, static_cast<int>(j)) - P.cptr[iu];
+            const int np = static_cast<int>(P.pan_ptr[iu + 1] - P.pan_ptr[iu]) - 1;
+            int p = 0;
+            while (p + 1 < np && P.pan_start[static_cast<size_t>(P.pan_ptr[iu] + p + 1)] <= q) ++p;
+            P.sq_pan[static_cast<size_t>(e)] = p;
           }
         }
-      w0 = w1;
-    }
+      });
   }
   P.fac_doubles = fo;
   P.basis_doubles = bo;
@@ -813,7 +862,8 @@ namespace {
 
 // Device copy of a plan's symbolic arrays (freed after the level).
 struct DevPlan {
-  DevArray<int> bsz, scol, ccol, croff, order, nA1, nA3, nB, pan_start, item_row, item_part, sbsz, sroff, target, nleaf;
+  DevArray<int> bsz, scol, ccol, croff, order, nA1, nA3, nB, pan_start, item_row, item_part, sbsz, sroff, target, nleaf,
+      sq_pan;
   DevArray<int64_t> sptr, sslot, slot_off, cptr, chol_off, g_off, basis_off, sigma_off, item_start, offsets, cl_slot,
       fsum, rs_off, pan_ptr, sboff, sdiag, leaf_ptr, leaf_e, strip_ptr, strip_e;  // (cl_slot unused)
   DevArray<unsigned char> skind;
@@ -839,6 +889,7 @@ struct DevPlan {
     add(sz(P.cptr)); add(sz(P.chol_off)); add(sz(P.g_off)); add(sz(P.basis_off)); add(sz(P.sigma_off));
     add(sz(P.item_start)); add(sz(P.offsets)); add(sz(P.skind)); add(sz(P.sboff)); add(sz(P.sbsz)); add(sz(P.sroff));
     add(sz(P.sdiag)); add(sz(P.target)); add(sz(P.leaf_ptr)); add(sz(P.leaf_e)); add(sz(P.strip_ptr)); add(sz(P.strip_e));
+    add(sz(P.sq_pan));
     if (total > st.cap) {
       if (st.p) cudaFreeHost(st.p);
       st.p = nullptr;
@@ -862,7 +913,7 @@ struct DevPlan {
     put(g_off, P.g_off); put(basis_off, P.basis_off); put(sigma_off, P.sigma_off); put(item_start, P.item_start);
     put(offsets, P.offsets); put(skind, P.skind); put(sboff, P.sboff); put(sbsz, P.sbsz); put(sroff, P.sroff);
     put(sdiag, P.sdiag); put(target, P.target); put(leaf_ptr, P.leaf_ptr); put(leaf_e, P.leaf_e);
-    put(strip_ptr, P.strip_ptr); put(strip_e, P.strip_e);
+    put(strip_ptr, P.strip_ptr); put(strip_e, P.strip_e); put(sq_pan, P.sq_pan);
   }
 };
 
@@ -1113,6 +1164,13 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     DevArray<double> d_rscratch(static_cast<size_t>(std::max<int64_t>(cur.rscratch_doubles, 1)));
     DevArray<int> d_nz(static_cast<size_t>(cur.M));
     d_nz.zero(s);
+    DevArray<int> d_pdone(static_cast<size_t>(std::max<int64_t>(cur.pan_ptr[static_cast<size_t>(cur.M)], 1)));
+    d_pdone.zero(s);
+    DevArray<int> d_bready(static_cast<size_t>(cur.M));
+    d_bready.zero(s);
+    a.sq_pan = dcur.sq_pan.p;
+    a.pdone = d_pdone.p;
+    a.bready = d_bready.p;
     a.rscratch = d_rscratch.p;
     a.nzflag = d_nz.p;
     a.done = d_done.p;

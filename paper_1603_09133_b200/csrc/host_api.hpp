@@ -143,6 +143,8 @@ struct LevelPlan {
   std::vector<int> sbsz, sroff;      // per sq entry: block size, close-list row offset (-1: not close)
   std::vector<int64_t> sdiag;        // per row: sq entry of the diagonal
   std::vector<int> target;           // per row: items of the row (completion count)
+  std::vector<int> sq_pan;           // per sq entry (j, i), i < j close: panel of j in close(i)
+                                     // (-1: far, or i's Schur runs in <= 1 task -> wait for all of i)
   std::vector<int64_t> leaf_ptr, leaf_e, strip_ptr, strip_e;  // A1 / A3 task entry ranges
   int64_t n_items = 0, n_waves = 0;
   int bmax = 0;

@@ -66,6 +66,9 @@ struct SweepArgs {
   const int* sq_roff;         // per sq entry: row offset in the close list (-1: not close)
   const int64_t* sq_diag;     // per row: sq entry of the diagonal block
   const int* target;          // per row: number of items (done[] value when the row is finished)
+  const int* sq_pan;          // per sq entry (j, i < j) close: panel of j in close(i), -1: wait for all of i
+  int* pdone;                 // per (row, panel) (pan_ptr index): finished Schur pairs touching the panel
+  int* bready;                // per row: every predecessor finished (set by the row's first Schur task)
   const int64_t* leaf_ptr;    // per row: range into leaf_e (nA1 + 1 entries)
   const int64_t* leaf_e;      // first sq entry of each TSQR leaf (last = row end)
   const int64_t* strip_ptr;   // per row: range into strip_e (nA3 + 1 entries)

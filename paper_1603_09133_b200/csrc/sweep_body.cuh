@@ -1938,6 +1938,7 @@ __global__ void __launch_bounds__(T, CE_SWEEP_MIN_BLOCKS) sweep_kernel(SweepArgs
   __shared__ EntWin W;
   __shared__ double shr[4];
   __shared__ int nz;
+  __shared__ int s_bready;
   for (;;) {
     if (threadIdx.x == 0) {
       s_stop = *reinterpret_cast<volatile int*>(A.err) != 0;
@@ -1988,12 +1989,22 @@ __global__ void __launch_bounds__(T, CE_SWEEP_MIN_BLOCKS) sweep_kernel(SweepArgs
     const bool first = (stage == 1 && tlev == 0) || (stage == 2 && nA1 == 0);
     const long long t_wait = clock64();
     if (first) {
-      // every predecessor j < i of sq(i) finished (one poller per entry, in parallel)
+      // every predecessor j < i of sq(i) far enough along (one poller per entry, in parallel):
+      // a far predecessor's A stages (its Schur pairs never touch row i), a close one's A stages
+      // and the Schur pairs touching row i's panel (sq_pan), else all of its tasks
       const int64_t pb = A.sq_ptr[i], pe = A.sq_diag[i];
       for (int64_t e = pb + threadIdx.x; e < pe; e += T) {
         const int j = A.sq_col[e];
-        const int tgt = A.target[j];
-        while (ld_acquire(A.done + j) < tgt) {
+        const int pan = A.sq_pan[e];
+        const bool far = A.sq_kind[e] >= 2;
+        const int tgt = (far || pan >= 0) ? A.nA1[j] + 1 + A.nA3[j] : A.target[j];
+        const int* pd = nullptr;
+        int ptgt = 0;
+        if (!far && pan >= 0) {
+          pd = A.pdone + A.pan_ptr[j] + pan;
+          ptgt = static_cast<int>(A.pan_ptr[j + 1] - A.pan_ptr[j]) - 1;
+        }
+        while (ld_acquire(A.done + j) < tgt || (pd && ld_acquire(pd) < ptgt)) {
           if (*reinterpret_cast<volatile int*>(A.err) != 0) {
             s_stop = 1;
             break;
@@ -2001,6 +2012,31 @@ __global__ void __launch_bounds__(T, CE_SWEEP_MIN_BLOCKS) sweep_kernel(SweepArgs
           __nanosleep(64);
         }
         if (s_stop) break;
+      }
+    }
+    if (stage == 4) {
+      // Schur pairs write blocks shared with every predecessor's pairs: all of them first
+      if (threadIdx.x == 0) s_bready = ld_acquire(A.bready + i);
+      __syncthreads();
+      if (!s_bready) {
+        const int64_t pb = A.sq_ptr[i], pe = A.sq_diag[i];
+        for (int64_t e = pb + threadIdx.x; e < pe; e += T) {
+          const int j = A.sq_col[e];
+          const int tgt = A.target[j];
+          while (ld_acquire(A.done + j) < tgt) {
+            if (*reinterpret_cast<volatile int*>(A.err) != 0) {
+              s_stop = 1;
+              break;
+            }
+            __nanosleep(64);
+          }
+          if (s_stop) break;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && !s_bready) {
+        __threadfence();
+        atomicExch(A.bready + i, 1);
       }
     }
     if (threadIdx.x == 0) {
@@ -2036,19 +2072,22 @@ __global__ void __launch_bounds__(T, CE_SWEEP_MIN_BLOCKS) sweep_kernel(SweepArgs
       task_a3(A, i, s, k, nA3, nB, W);
     } else {
       const int w = __ldcg(A.width + i);
-      if (w > 0) {
-        const int r = __ldcg(A.rank + i);
-        const int np = static_cast<int>(A.pan_ptr[i + 1] - A.pan_ptr[i]) - 1;
-        if (nB == 1) {
-          all_panels(A, i, r, w, s.R);
-        } else {
-          // tile k -> panel pair (P, Q), P <= Q
-          int P = 0, kk = k;
-          while (kk >= np - P) {
-            kk -= np - P;
-            ++P;
-          }
-          panel_update(A, i, r, w, P, P + kk, s.R);
+      const int np = static_cast<int>(A.pan_ptr[i + 1] - A.pan_ptr[i]) - 1;
+      if (nB == 1) {
+        if (w > 0) all_panels(A, i, __ldcg(A.rank + i), w, s.R);
+      } else {
+        // tile k -> panel pair (P, Q), P <= Q
+        int P = 0, kk = k;
+        while (kk >= np - P) {
+          kk -= np - P;
+          ++P;
+        }
+        if (w > 0) panel_update(A, i, __ldcg(A.rank + i), w, P, P + kk, s.R);
+        __syncthreads();
+        if (threadIdx.x == 0) {  // panel-pair completion for the lookahead waits (above)
+          __threadfence();
+          atomicAdd(A.pdone + A.pan_ptr[i] + P, 1);
+          if (kk != 0) atomicAdd(A.pdone + A.pan_ptr[i] + P + kk, 1);
         }
       }
     }
