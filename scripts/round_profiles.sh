@@ -12,3 +12,6 @@ timeout 900 $NCU --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_
 timeout 1200 $NCU --set full --import-source on --clock-control none -k regex:sweep_kernel --launch-skip 5 -c 1 \
   -o gpurun_out/sweep_L6 python scripts/ncu_sweep.py 1024 > gpurun_out/ncu_full.log 2>&1
 ls -la gpurun_out
+# auxiliary bench lines: cfg3 at full size, cfg4 stencil at 64^3 (cfg4's 128^3 exceeds HBM)
+timeout 900 python bench.py --cfg 3 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_cfg3.json 2> gpurun_out/bench_cfg3.err
+timeout 1500 python bench.py --cfg 4 --grid 64 64 64 --steps 1 --warmup 1 --e2e-steps 1 --no-cpu-baseline > gpurun_out/bench_cfg4_64.json 2> gpurun_out/bench_cfg4_64.err
