@@ -404,6 +404,7 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
   // (rows + 16 bounds the padded row strides of both staged panels, sweep_body.cuh panel_update)
   const int64_t cap = thresholds().small_panels ? bmax : std::max<int64_t>(bmax, std::min<int64_t>(256, buf / (2 * bmax) - 16));
   constexpr int64_t kPanelNb = 32;
+  const double tp1 = now_s();
   // per-row task counts (parallel over rows), then prefix offsets
   const Thresholds& th = thresholds();
   const int64_t kcap = sweep_kcap(static_cast<int>(bmax));
@@ -498,6 +499,7 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
     P.pan_ptr[iu + 1] = P.pan_ptr[iu] + np_row[iu] + 1;
   }
   P.rscratch_doubles = ro;
+  const double tp2 = now_s();
   P.pan_start.assign(static_cast<size_t>(P.pan_ptr[static_cast<size_t>(M)]), 0);
   parallel_rows(M, [&](int64_t r0, int64_t r1) {
     for (int64_t i = r0; i < r1; ++i) {
@@ -517,6 +519,7 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
       P.pan_start[static_cast<size_t>(at)] = static_cast<int>(P.cptr[iu + 1] - P.cptr[iu]);
     }
   });
+  const double tp3 = now_s();
   // Per-entry metadata the sweep tasks load in one coalesced pass (no dependent chains
   // sq_col -> bsz, sq_slot -> slot_off, close-list search on the device), the diagonal
   // entry and completion target of every row, and the entry ranges of the A1 / A3 tasks
@@ -581,6 +584,8 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
       }
     });
   }
+  const double tp4 = now_s();
+  double tp5 = tp4;
   // ticket order of the row tasks (wave order from the symbolic plan)
   {
     const std::vector<int64_t>& wave = P.wave;
@@ -658,6 +663,7 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
       emit_rows(w, [&](int row, size_t r) { for (int p : urg_of[r]) push(row, p); });
     }
     if (static_cast<int64_t>(P.item_row.size()) != it) throw std::logic_error("ticket order lost items");
+    tp5 = now_s();
     // sq_pan: panel of j inside close(i) for each close predecessor entry (j, i), i < j
     P.sq_pan.assign(P.scol.size(), -1);
     if (lookahead)
@@ -681,7 +687,9 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
   P.basis_doubles = bo;
   P.sigma_doubles = so;
   if (std::getenv("CE_PROFILE") && std::getenv("CE_PROFILE")[0] == '1')
-    std::fprintf(stderr, "[ce-profile] plan_numeric M=%lld: %.1f ms\n", static_cast<long long>(M), 1e3 * (now_s() - tn0));
+    std::fprintf(stderr, "[ce-profile] plan_numeric M=%lld: %.1f ms (offsets %.1f, counts %.1f, panels %.1f, entries %.1f, tickets %.1f, sq_pan %.1f)\n",
+                 static_cast<long long>(M), 1e3 * (now_s() - tn0), 1e3 * (tp1 - tn0), 1e3 * (tp2 - tp1), 1e3 * (tp3 - tp2),
+                 1e3 * (tp4 - tp3), 1e3 * (tp5 - tp4), 1e3 * (now_s() - tp5));
 }
 
 LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vector<int> bcol) {
