@@ -41,6 +41,8 @@ struct Thresholds {
   int64_t strip_cols = 64;                 // strip columns per task
   bool small_panels = false;               // one close neighbour per Schur panel
   bool no_tri_table = false;               // CE_NO_TRI=1: binary-search slot lookups at every level
+  int64_t pair_group = 1;                  // Schur panel pairs (P, Q..Q+g-1) per task, panel P staged once
+                                           // (A/B on cfg2: g=1 1.82 s, 2 1.89, 3 1.97, 5 2.19: per-wave parallelism wins)
   Thresholds() {
     no_tri_table = std::getenv("CE_NO_TRI") && std::getenv("CE_NO_TRI")[0] == '1';
     const char* f = std::getenv("CE_FORCE_TASKS");  // bitmask: 1 leaves, 2 strip tasks, 4 Schur panels
@@ -66,6 +68,8 @@ struct Thresholds {
     env("CE_STRIP_WORK", strip_work);
     env("CE_STRIP_COLS", strip_cols);
     env("CE_PAIR_INLINE", pair_inline);
+    env("CE_PAIR_GROUP", pair_group);
+    if (pair_group < 1) pair_group = 1;
   }
 };
 const Thresholds& thresholds() {
@@ -350,6 +354,13 @@ LevelPlan plan_symbolic(int64_t M, std::vector<int64_t> bptr, std::vector<int> b
   return P;
 }
 
+// Schur tasks of a row with np panels: for each P, the pairs (P, Q >= P) in groups of g.
+int64_t pair_tasks(int64_t np, int64_t g) {
+  int64_t t = 0;
+  for (int64_t p = 0; p < np; ++p) t += (np - p + g - 1) / g;
+  return t;
+}
+
 // Numeric part: everything that depends on the block sizes.
 void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
   const int64_t M = P.M;
@@ -475,7 +486,7 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
       // Schur pair work: sum_{s<=t in close} b_s b_t * w, with w <= b
       const int64_t cs = P.csum[iu];
       const int64_t work = (cs * cs + sq2) / 2 * b;
-      if (work > th.pair_inline && np * (np + 1) / 2 > 1) P.nB[iu] = static_cast<int>(np * (np + 1) / 2);
+      if (work > th.pair_inline && np * (np + 1) / 2 > 1) P.nB[iu] = static_cast<int>(pair_tasks(np, th.pair_group));
       // with strip tasks the Schur update must follow all of them: one task runs every panel pair
       if (P.nA3[iu] > 0 && P.nB[iu] == 0 && np > 0) P.nB[iu] = 1;
     }
@@ -636,10 +647,14 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
             const int t = P.ccol[static_cast<size_t>(P.cptr[iu] + q)];
             if (t > i && wave[static_cast<size_t>(t)] == wnext) hot[static_cast<size_t>(p)] = 1;
           }
+        const int g = static_cast<int>(thresholds().pair_group);
         int k = 0;
         for (int pp = 0; pp < np; ++pp)
-          for (int qq = pp; qq < np; ++qq, ++k)
-            (hot[static_cast<size_t>(pp)] || hot[static_cast<size_t>(qq)] ? urg_of[iu] : rest_of[iu]).push_back(b0 + k);
+          for (int q0 = pp; q0 < np; q0 += g, ++k) {
+            bool h = hot[static_cast<size_t>(pp)];
+            for (int qq = q0; qq < std::min(np, q0 + g); ++qq) h = h || hot[static_cast<size_t>(qq)];
+            (h ? urg_of[iu] : rest_of[iu]).push_back(b0 + k);
+          }
       }
     });
     auto emit_rows = [&](int64_t w, auto&& parts) {
@@ -1177,6 +1192,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     DevArray<int> d_bready(static_cast<size_t>(cur.M));
     d_bready.zero(s);
     a.sq_pan = dcur.sq_pan.p;
+    a.pair_group = static_cast<int>(thresholds().pair_group);
     a.pdone = d_pdone.p;
     a.bready = d_bready.p;
     a.rscratch = d_rscratch.p;

@@ -81,6 +81,7 @@ struct SweepArgs {
   int absolute;
   double eps;
   int fixed_rank;
+  int pair_group;             // Schur pairs (P, Q..Q+pair_group-1) per B task
   int* err;           // [0] code, [1] level, [2] row (low), [3] row (high)
   int* shifts;
   int bmax;

@@ -1407,7 +1407,8 @@ __device__ __noinline__ void strip_range(const SweepArgs& A, int i, int b, int r
 // dependent global loads (close columns -> slot offsets -> g rows / X tile), so the
 // first X tile of every warp is loaded before the panels are staged and both sets of
 // loads are in flight together.
-__device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int w, int P, int Q, double* sm) {
+__device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int w, int P, int Q, double* sm,
+                                          bool reuse_s) {
   CE_SHARED(sm);
   const long long tb0 = clock64();
   __shared__ long long slot_tab[kPanelNb * kPanelNb];  // value offset of stored (t, s), -1: not updated
@@ -1426,7 +1427,9 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
   // this level, its block row is zero below its rank, so g_u (= columns of X_iu) is zero
   // in rows >= rank(u) and X_st only changes in the retained rows / columns.  The panel
   // is compacted to live rows (bit-identical result: the skipped terms are exact zeros).
-  if (warp < 2) {
+  // reuse_s: panel P's tables and staged rows are still in shared memory from the previous
+  // pair of this task (same P, P != Q now), only panel Q is rebuilt
+  if (warp < 2 && !(reuse_s && warp == 0)) {
     const int n = warp == 0 ? ns : nt, base = warp == 0 ? s0 : t0;
     int live = 0, roff = 0, bu = 0, u = 0;
     if (lane < n) {
@@ -1559,7 +1562,7 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
         if (di[u] >= 0) dst[di[u]] = v[u];
     }
   };
-  stage(GsT, lds, rsn, roff_s, yblk, yloc);
+  if (!reuse_s) stage(GsT, lds, rsn, roff_s, yblk, yloc);
   if (P != Q) stage(GtT, ldt, rtn, roff_t, xblk, xloc);
   __syncthreads();
   const long long tb2 = clock64();
@@ -1610,7 +1613,7 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
 __device__ void all_panels(const SweepArgs& A, int i, int r, int w, double* sm) {
   const int np = static_cast<int>(A.pan_ptr[i + 1] - A.pan_ptr[i]) - 1;
   for (int P = 0; P < np; ++P)
-    for (int Q = P; Q < np; ++Q) panel_update(A, i, r, w, P, Q, sm);
+    for (int Q = P; Q < np; ++Q) panel_update(A, i, r, w, P, Q, sm, Q > P);
 }
 
 // A2: compression decision + basis + pivot factorisation; with nA3 == 0 also the strip,
@@ -2076,18 +2079,23 @@ __global__ void __launch_bounds__(T, CE_SWEEP_MIN_BLOCKS) sweep_kernel(SweepArgs
       if (nB == 1) {
         if (w > 0) all_panels(A, i, __ldcg(A.rank + i), w, s.R);
       } else {
-        // tile k -> panel pair (P, Q), P <= Q
+        // task k -> panel P and pairs (P, Q0 .. Q0 + g - 1), Q0 >= P (driver.cpp pair_tasks)
+        const int g = A.pair_group;
         int P = 0, kk = k;
-        while (kk >= np - P) {
-          kk -= np - P;
+        while (kk >= (np - P + g - 1) / g) {
+          kk -= (np - P + g - 1) / g;
           ++P;
         }
-        if (w > 0) panel_update(A, i, __ldcg(A.rank + i), w, P, P + kk, s.R);
+        const int q0 = P + kk * g, q1 = min(np, q0 + g);
+        for (int Q = q0; Q < q1; ++Q)
+          if (w > 0) panel_update(A, i, __ldcg(A.rank + i), w, P, Q, s.R, Q > q0);
         __syncthreads();
         if (threadIdx.x == 0) {  // panel-pair completion for the lookahead waits (above)
           __threadfence();
-          atomicAdd(A.pdone + A.pan_ptr[i] + P, 1);
-          if (kk != 0) atomicAdd(A.pdone + A.pan_ptr[i] + P + kk, 1);
+          for (int Q = q0; Q < q1; ++Q) {
+            atomicAdd(A.pdone + A.pan_ptr[i] + P, 1);
+            if (Q != P) atomicAdd(A.pdone + A.pan_ptr[i] + Q, 1);
+          }
         }
       }
     }
