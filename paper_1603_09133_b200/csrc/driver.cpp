@@ -41,6 +41,7 @@ struct Thresholds {
   int64_t strip_cols = 64;                 // strip columns per task
   bool small_panels = false;               // one close neighbour per Schur panel
   bool no_tri_table = false;               // CE_NO_TRI=1: binary-search slot lookups at every level
+  int64_t panel_cap = 0;                   // Schur panel height limit in rows (0: buffer-derived)
   int64_t pair_group = 1;                  // Schur panel pairs (P, Q..Q+g-1) per task, panel P staged once
                                            // (A/B on cfg2: g=1 1.82 s, 2 1.89, 3 1.97, 5 2.19: per-wave parallelism wins)
   Thresholds() {
@@ -69,6 +70,7 @@ struct Thresholds {
     env("CE_STRIP_COLS", strip_cols);
     env("CE_PAIR_INLINE", pair_inline);
     env("CE_PAIR_GROUP", pair_group);
+    env("CE_PANEL_CAP", panel_cap);
     if (pair_group < 1) pair_group = 1;
   }
 };
@@ -413,7 +415,8 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
   const int64_t buf = sweep_smem_doubles(static_cast<int>(bmax), sweep_kcap(static_cast<int>(bmax)));
   // (sweep.cu kPanelRows / kPanelNb bound the panel height / neighbour count)
   // (rows + 16 bounds the padded row strides of both staged panels, sweep_body.cuh panel_update)
-  const int64_t cap = thresholds().small_panels ? bmax : std::max<int64_t>(bmax, std::min<int64_t>(256, buf / (2 * bmax) - 16));
+  int64_t cap = thresholds().small_panels ? bmax : std::max<int64_t>(bmax, std::min<int64_t>(256, buf / (2 * bmax) - 16));
+  if (thresholds().panel_cap > 0) cap = std::max<int64_t>(bmax, std::min(cap, thresholds().panel_cap));
   constexpr int64_t kPanelNb = 32;
   const double tp1 = now_s();
   // per-row task counts (parallel over rows), then prefix offsets
