@@ -33,6 +33,9 @@
 #ifndef CE_KCAP_BUDGET
 #define CE_KCAP_BUDGET 18000
 #endif
+#ifndef CE_NO_WIDE_JACOBI
+#define CE_NO_WIDE_JACOBI 0
+#endif
 #ifndef CE_SWEEP_MIN_BLOCKS
 #define CE_SWEEP_MIN_BLOCKS 1  // resident sweep CTAs per SM the register allocation must allow
 #endif

@@ -588,11 +588,96 @@ __device__ __noinline__ int jacobi_t(double* X, double* V, int b, int ld, int me
   return nsw;
 }
 
+// Wide blocks (64 < b <= 256, typically 3-D deep levels whose tiles live in global scratch):
+// a whole warp per column pair, both columns and both V columns held in registers for the
+// step (all loads of a pair in flight together instead of a dependent loop over the rows),
+// warp-shuffle dot products.  Same rotation arithmetic and stopping rule as `jacobi`.
+__device__ __noinline__ int jacobi_wide(double* X, double* V, int b, int ld, int meff) {
+  constexpr int E = 8;  // b <= 32 E
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < b * ld; idx += T) V[idx] = (idx / ld == idx % ld) ? 1.0 : 0.0;
+  __syncthreads();
+  const double tol = sqrt(static_cast<double>(meff > 1 ? meff : 1)) * DBL_EPSILON;
+  const double tol2 = tol * tol;
+  const int nb = b + (b & 1);
+  const int np = nb / 2;
+  int nsw = 100;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    int rotated = 0;
+    for (int round = 0; round < nb - 1; ++round) {
+      for (int pi = warp; pi < np; pi += NW) {
+        int p = rr_player(pi, round, nb), q = rr_player(nb - 1 - pi, round, nb);
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        if (q >= b) continue;  // warp-uniform
+        double* cp = X + p * ld;
+        double* cq = X + q * ld;
+        double x[E], y[E];
+        double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int k = lane + 32 * e;
+          x[e] = k < b ? cp[k] : 0.0;
+          y[e] = k < b ? cq[k] : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          al += x[e] * x[e];
+          be += y[e] * y[e];
+          ga += x[e] * y[e];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (al != 0.0 && be != 0.0 && ga * ga > tol2 * al * be) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = rsqrt(1.0 + t * t);
+          const double sn = cs * t;
+          double* vp = V + p * ld;
+          double* vq = V + q * ld;
+          double u[E], v[E];
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int k = lane + 32 * e;
+            u[e] = k < b ? vp[k] : 0.0;
+            v[e] = k < b ? vq[k] : 0.0;
+          }
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int k = lane + 32 * e;
+            if (k < b) {
+              cp[k] = cs * x[e] - sn * y[e];
+              cq[k] = sn * x[e] + cs * y[e];
+              vp[k] = cs * u[e] - sn * v[e];
+              vq[k] = sn * u[e] + cs * v[e];
+            }
+          }
+          rotated = 1;
+        }
+      }
+      if (round < nb - 2) __syncthreads();
+    }
+    if (!__syncthreads_or(rotated)) {
+      nsw = sweep + 1;
+      break;
+    }
+  }
+  return nsw;
+}
+
 __device__ int jacobi_fast(double* X, double* V, int b, int ld, int meff) {
   // more lanes per pair beats shorter shuffle trees (micro_dense: b=16 897 vs 1174 cycles/round)
   if (b <= 16) return jacobi_t<16, 1>(X, V, b, ld, meff);
   if (b <= 32) return jacobi_t<16, 2>(X, V, b, ld, meff);
   if (b <= 64) return jacobi_t<8, 8>(X, V, b, ld, meff);
+  if (b <= 256 && !(CE_NO_WIDE_JACOBI)) return jacobi_wide(X, V, b, ld, meff);
   return jacobi(X, V, b, ld, meff);
 }
 
