@@ -42,7 +42,8 @@ struct Thresholds {
   bool small_panels = false;               // one close neighbour per Schur panel
   bool no_tri_table = false;               // CE_NO_TRI=1: binary-search slot lookups at every level
   int64_t panel_cap = 0;                   // Schur panel height limit in rows (0: buffer-derived)
-  int64_t pair_group = 1;                  // Schur panel pairs (P, Q..Q+g-1) per task, panel P staged once
+  int64_t pair_group = 0;                  // Schur panel pairs (P, Q..Q+g-1) per task, panel P staged once;
+                                           // 0: per row, kernels.hpp row_pair_group(np)
                                            // (A/B on cfg2: g=1 1.82 s, 2 1.89, 3 1.97, 5 2.19: per-wave parallelism wins)
   Thresholds() {
     no_tri_table = std::getenv("CE_NO_TRI") && std::getenv("CE_NO_TRI")[0] == '1';
@@ -71,7 +72,7 @@ struct Thresholds {
     env("CE_PAIR_INLINE", pair_inline);
     env("CE_PAIR_GROUP", pair_group);
     env("CE_PANEL_CAP", panel_cap);
-    if (pair_group < 1) pair_group = 1;
+    if (pair_group < 0) pair_group = 0;
   }
 };
 const Thresholds& thresholds() {
@@ -489,7 +490,7 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
       // Schur pair work: sum_{s<=t in close} b_s b_t * w, with w <= b
       const int64_t cs = P.csum[iu];
       const int64_t work = (cs * cs + sq2) / 2 * b;
-      if (work > th.pair_inline && np * (np + 1) / 2 > 1) P.nB[iu] = static_cast<int>(pair_tasks(np, th.pair_group));
+      if (work > th.pair_inline && np * (np + 1) / 2 > 1) P.nB[iu] = static_cast<int>(pair_tasks(np, row_pair_group(static_cast<int>(th.pair_group), static_cast<int>(np))));
       // with strip tasks the Schur update must follow all of them: one task runs every panel pair
       if (P.nA3[iu] > 0 && P.nB[iu] == 0 && np > 0) P.nB[iu] = 1;
     }
@@ -650,7 +651,7 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
             const int t = P.ccol[static_cast<size_t>(P.cptr[iu] + q)];
             if (t > i && wave[static_cast<size_t>(t)] == wnext) hot[static_cast<size_t>(p)] = 1;
           }
-        const int g = static_cast<int>(thresholds().pair_group);
+        const int g = row_pair_group(static_cast<int>(thresholds().pair_group), np);
         int k = 0;
         for (int pp = 0; pp < np; ++pp)
           for (int q0 = pp; q0 < np; q0 += g, ++k) {

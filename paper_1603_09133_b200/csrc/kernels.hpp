@@ -9,7 +9,16 @@ namespace ceg {
 
 constexpr int kSweepThreads = 256;
 constexpr int kApplyThreads = 128;
-constexpr int kApplyWmax = 256;  // largest eliminated width per block the apply sweeps stage in shared memory
+constexpr int kApplyWmax = 256;
+// Schur pairs per B task of a row with np panels (forced > 0, else adaptive): one pair per task
+// while the row has few panels (the wave needs the parallelism: A/B on cfg2, g = 2 / 3 / 5 lose
+// 4 / 8 / 20%), more once a row has hundreds of panels (3-D deep levels, each panel is staged
+// once per pair otherwise).
+__host__ __device__ inline int row_pair_group(int forced, int np) {
+  if (forced > 0) return forced;
+  const int g = np / 48;
+  return g < 1 ? 1 : (g > 8 ? 8 : g);
+}  // largest eliminated width per block the apply sweeps stage in shared memory
 
 enum : int { kErrNone = 0, kErrBreakdown = 2, kErrPattern = 5, kErrInternal = 6 };
 

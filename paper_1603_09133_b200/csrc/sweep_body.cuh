@@ -2165,7 +2165,7 @@ __global__ void __launch_bounds__(T, CE_SWEEP_MIN_BLOCKS) sweep_kernel(SweepArgs
         if (w > 0) all_panels(A, i, __ldcg(A.rank + i), w, s.R);
       } else {
         // task k -> panel P and pairs (P, Q0 .. Q0 + g - 1), Q0 >= P (driver.cpp pair_tasks)
-        const int g = A.pair_group;
+        const int g = row_pair_group(A.pair_group, np);
         int P = 0, kk = k;
         while (kk >= (np - P + g - 1) / g) {
           kk -= (np - P + g - 1) / g;
