@@ -641,8 +641,6 @@ unsigned grid_for(int64_t M) { return static_cast<unsigned>(M < 65535 * 8 ? (M >
 
 void launch_basis_apply(const ApplyLevelArgs& a, int transpose, cudaStream_t s) {
   if (a.M == 0) return;
-  int bmax = 0;
-  (void)bmax;
   note_launch();
   basis_kernel<<<grid_for(a.M), T, 1024 * sizeof(double), s>>>(a, transpose);
 }

@@ -86,18 +86,6 @@ __device__ int64_t find_slot(const int64_t* sq_ptr, const int* sq_col, const int
   return -1;
 }
 
-// index of neighbour t in row i's close list (or -1)
-__device__ int64_t close_index(const SweepArgs& A, int i, int t) {
-  int64_t lo = A.cl_ptr[i], hi = A.cl_ptr[i + 1];
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    const int c = A.cl_col[mid];
-    if (c == t) return mid;
-    if (c < t) lo = mid + 1;
-    else hi = mid;
-  }
-  return -1;
-}
 
 // leading dimension of the column-major F^T chunk (odd: column walks are bank-conflict free)
 __device__ __forceinline__ int chunk_ld(int kcap) { return kcap | 1; }

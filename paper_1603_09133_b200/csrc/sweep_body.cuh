@@ -394,7 +394,7 @@ __device__ void tsqr_fast(double* R, double* C, int K, int b, int ldc, double* s
 // warp 0 with no CTA barrier; larger ones use the whole CTA with one barrier per round.
 // Rotation test |gamma| > tol sqrt(alpha beta), tol = sqrt(m) eps (oracle/dense.cpp svd_left).
 __device__ int jacobi(double* X, double* V, int b, int ld, int meff) {
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   for (int idx = tid; idx < b * ld; idx += T) V[idx] = (idx / ld == idx % ld) ? 1.0 : 0.0;
   __syncthreads();
   const double tol = sqrt(static_cast<double>(meff > 1 ? meff : 1)) * DBL_EPSILON;
