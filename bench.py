@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--grid", type=int, nargs=3, default=[0, 0, 0])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-threads", type=int, default=0, help="reference arm: concurrent oracle copies (0 = all host threads)")
     return ap.parse_args()
 
 
@@ -164,30 +165,55 @@ def job_throughput(world, n, steps, max_time):
 
 
 def run_reference(args):
+    """The reference arm: the CPU oracle restatement (the reference is single-threaded by design,
+    SPEC.md:338,457) run as one independent copy per host core on the bounded sample, so the arm
+    uses every host thread; value = copies x n / slowest copy's factorization time."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     grid = CPU_SAMPLE_GRID[args.cfg]
+    cli = os.path.join(ROOT, "oracle", "oracle_cli")
+    if not os.path.exists(cli):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "-j8"], check=True, capture_output=True)
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count() or 1
+    copies = args.ref_threads if args.ref_threads > 0 else cores
+    cmd = [cli, str(args.cfg)] + [str(g) for g in grid if g > 0]
+
+    def step():
+        procs = [subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True) for _ in range(copies)]
+        outs = [json.loads(p.communicate()[0].strip().splitlines()[-1]) for p in procs]
+        if any(p.returncode != 0 for p in procs):
+            raise RuntimeError("oracle_cli failed")
+        return outs
+
     for _ in range(args.warmup):
-        cpu_oracle_run(args.cfg, grid)
-    vals, fac, pcg_s = [], [], []
+        step()
+    vals, fac, pcg_s, single = [], [], [], []
     t0 = time.time()
     for _ in range(args.steps):
-        r = cpu_oracle_run(args.cfg, grid)
-        vals.append(r["unknowns_per_sec"])
-        fac.append(r["factor_seconds"])
-        pcg_s.append(r.get("pcg_seconds", 0.0))
+        outs = step()
+        slow = max(o["factor_seconds"] for o in outs)
+        vals.append(copies * outs[0]["n"] / slow)
+        fac.append(slow)
+        pcg_s.append(max(o.get("pcg_seconds", 0.0) for o in outs))
+        single.append(statistics.mean(o["unknowns_per_sec"] for o in outs))
     wall = time.time() - t0
     v = statistics.mean(vals)
+    n = outs[0]["n"]
     sample = (f"oracle/oracle_cli cfg{args.cfg} on a {grid[0]}x{grid[1]}" + (f"x{grid[2]}" if grid[2] else "") +
-              f" grid (n={r['n']}, same stencil/B/eps), full factorization + PCG, 1 thread")
+              f" grid (n={n}, same stencil/B/eps), full factorization + PCG; {copies} independent copies, one per "
+              f"host thread ({cores} available); value = copies x n / slowest copy's factorization time")
     line = {"metric": METRIC, "value": v, "unit": "unknowns/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(args.cfg, args.grid), "cfg": args.cfg,
                        "cpu_sample_grid": list(grid)},
             "pcg_solve_ms": 1e3 * statistics.mean(pcg_s), "factor_ms": 1e3 * statistics.mean(fac),
-            "cpu_baseline": {"value": v, "unit": "unknowns/s", "cores": 1, "kind": "port", "sample": sample},
+            "single_thread_value": statistics.mean(single),
+            "cpu_baseline": {"value": v, "unit": "unknowns/s", "cores": copies, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
