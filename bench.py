@@ -38,17 +38,22 @@ def parse():
     ap.add_argument("--grid", type=int, nargs=3, default=[0, 0, 0])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--plan", default="reference", choices=["reference", "merge_all_axes"],
+                    help="plan family: the reference's geometric_block_ordering (join 2, one axis per level) or "
+                         "every axis merging by 2 per level (J = 2^d; the 3-D configs at full size, DESIGN.md)")
     ap.add_argument("--ref-threads", type=int, default=0, help="reference arm: concurrent oracle copies (0 = all host threads)")
     return ap.parse_args()
 
 
-def workload_name(cfg, grid):
+def workload_name(cfg, grid, plan="reference"):
     names = {1: "2D Poisson 128x128 B=8 eps=1e-4 PCG 1e-8", 2: "2D Poisson 1024x1024 B=16 eps=1e-6 PCG 1e-10",
              3: "2D variable-k diffusion 2048x2048 B=16 eps=1e-6 PCG 1e-8",
              4: "3D Poisson 128^3 B=32 eps=1e-5 PCG 1e-8", 5: "3D variable-k diffusion 256^3 B=32 eps=1e-4 PCG 1e-6"}
     s = f"cfg{cfg}: {names[cfg]}"
     if any(grid):
         s += f" (grid override {grid[0]}x{grid[1]}x{grid[2]})"
+    if plan != "reference":
+        s += f" [plan {plan}]"
     return s
 
 
@@ -137,12 +142,12 @@ def fp64_gemm_tflops(torch, dev):
     return best
 
 
-def cpu_oracle_run(cfg, grid, solve=True):
+def cpu_oracle_run(cfg, grid, solve=True, plan="reference"):
     """Time the CPU oracle restatement (single thread, as the reference) on one sample."""
     cli = os.path.join(ROOT, "oracle", "oracle_cli")
     if not os.path.exists(cli):
         subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "-j8"], check=True, capture_output=True)
-    args = [cli, str(cfg)] + [str(g) for g in grid if g > 0]
+    args = [cli, str(cfg)] + [str(g) for g in grid if g > 0] + (["--merge-all"] if plan == "merge_all_axes" else [])
     if not solve:
         args.append("--no-solve")
     out = subprocess.run(args, check=True, capture_output=True, text=True).stdout
@@ -180,7 +185,7 @@ def run_reference(args):
     except AttributeError:
         cores = os.cpu_count() or 1
     copies = args.ref_threads if args.ref_threads > 0 else cores
-    cmd = [cli, str(args.cfg)] + [str(g) for g in grid if g > 0]
+    cmd = [cli, str(args.cfg)] + [str(g) for g in grid if g > 0] + (["--merge-all"] if args.plan == "merge_all_axes" else [])
 
     def step():
         procs = [subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True) for _ in range(copies)]
@@ -209,7 +214,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": v, "unit": "unknowns/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args.cfg, args.grid), "cfg": args.cfg,
+            "config": {"workload": workload_name(args.cfg, args.grid, args.plan), "cfg": args.cfg,
                        "cpu_sample_grid": list(grid)},
             "pcg_solve_ms": 1e3 * statistics.mean(pcg_s), "factor_ms": 1e3 * statistics.mean(fac),
             "single_thread_value": statistics.mean(single),
@@ -242,7 +247,7 @@ def run_product(args):
     def allmax(x):
         return reduce_max(x, dist, dev)
 
-    prob = ce.Problem(args.cfg, *args.grid)
+    prob = ce.Problem(args.cfg, *args.grid, plan=args.plan)
     n = prob.n
     ctx = ce.Context.get(local)
     host_a = prob.matrix()
@@ -332,7 +337,7 @@ def run_product(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         grid = CPU_SAMPLE_GRID[args.cfg]
-        r = cpu_oracle_run(args.cfg, grid, solve=False)
+        r = cpu_oracle_run(args.cfg, grid, solve=False, plan=args.plan)
         cpu = {"value": r["unknowns_per_sec"], "unit": "unknowns/s", "cores": 1, "kind": "port",
                "sample": f"oracle/oracle_cli cfg{args.cfg} on a {grid[0]}x{grid[1]}" + (f"x{grid[2]}" if grid[2] else "")
                + f" grid (n={r['n']}), full factorization, 1 thread of {os.cpu_count()}"}
@@ -343,7 +348,7 @@ def run_product(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * step_total / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE cfg generator, seeded N(0,1) rhs)",
-            "config": {"workload": workload_name(args.cfg, args.grid), "cfg": args.cfg, "n": n,
+            "config": {"workload": workload_name(args.cfg, args.grid, args.plan), "cfg": args.cfg, "n": n,
                        "parallelism": f"replicas x{world}", "l2": "inputs > L2 (A is %.2f GB)" % (host_a.values.nbytes / 1e9)},
             "factor_ms": 1e3 * fac_total / args.steps, "pcg_solve_ms": 1e3 * (step_total - fac_total) / args.steps,
             "factor_ms_steps": [round(1e3 * r["fac"], 1) for r in recs],

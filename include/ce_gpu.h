@@ -184,6 +184,15 @@ int ce_minres(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const d
  * (replaces assemble_diffusion_3d + geometric_block_ordering + finish_load, problems.cpp:18-258,
  * cli.cpp:33-58, extended with the 2-D/FV/random-k/RNG inputs BASELINE.json names). */
 int ce_problem_create(int cfg, int64_t nx, int64_t ny, int64_t nz, ce_problem** out);
+/* Same, choosing the plan family: CE_PLAN_REFERENCE = geometric_block_ordering(grid, block, 2)
+ * (problems.cpp:195-258: join 2 along one cyclically alternating axis per level);
+ * CE_PLAN_MERGE_ALL_AXES = every non-exhausted axis merges by 2 at each level (2x2 / 2x2x2
+ * groups, J = 2^d).  The latter is an ordinary CoarseningPlan (problems.hpp:51-65) that the
+ * reference's ce_factorize takes through its plan file (problems.cpp:114-171); its block
+ * pattern reach stays bounded, so the 3-D configs fit in HBM at full size. */
+#define CE_PLAN_REFERENCE 0
+#define CE_PLAN_MERGE_ALL_AXES 1
+int ce_problem_create_plan(int cfg, int64_t nx, int64_t ny, int64_t nz, int plan_kind, ce_problem** out);
 void ce_problem_free(ce_problem* p);
 /* The reference CLI's `file` problem (proj/src/cli.cpp:114-133 load_problem + finish_load :49-58):
  * Matrix Market "coordinate real general|symmetric" (matrix_market.cpp:21-59), a CoarseningPlan

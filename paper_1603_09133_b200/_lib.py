@@ -96,6 +96,7 @@ SIGNATURES = {
     "ce_pcg": (C.c_int, [vp, vp, vp, vp, vp, i64, C.c_int, C.POINTER(PcgOpts), C.POINTER(Report)]),
     "ce_minres": (C.c_int, [vp, vp, vp, vp, vp, i64, C.c_int, C.POINTER(PcgOpts), C.POINTER(Report)]),
     "ce_problem_create": (C.c_int, [C.c_int, i64, i64, i64, C.POINTER(vp)]),
+    "ce_problem_create_plan": (C.c_int, [C.c_int, i64, i64, i64, C.c_int, C.POINTER(vp)]),
     "ce_problem_free": (None, [vp]),
     "ce_problem_load": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, i64, C.POINTER(vp)]),
     "ce_problem_save": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_char_p]),

@@ -364,10 +364,16 @@ def minres(a: DeviceMatrix, n: int, b, precond: Optional[CEFactorization], opts:
 class Problem:
     """A BASELINE.json configuration generated on the host."""
 
-    def __init__(self, cfg: int, nx: int = 0, ny: int = 0, nz: int = 0, _handle=None):
+    PLANS = {"reference": 0, "merge_all_axes": 1}
+
+    def __init__(self, cfg: int, nx: int = 0, ny: int = 0, nz: int = 0, _handle=None, plan: str = "reference"):
+        """plan: "reference" = geometric_block_ordering(grid, block, 2) (problems.cpp:195-258);
+        "merge_all_axes" = every non-exhausted axis merges by 2 per level (J = 2^d)."""
         if _handle is None:
             h = C.c_void_p()
-            _check(lib.ce_problem_create(int(cfg), int(nx), int(ny), int(nz), C.byref(h)))
+            if plan not in self.PLANS:
+                raise ValueError(f"plan must be one of {sorted(self.PLANS)}")
+            _check(lib.ce_problem_create_plan(int(cfg), int(nx), int(ny), int(nz), self.PLANS[plan], C.byref(h)))
         else:
             h = _handle
         self.handle = h

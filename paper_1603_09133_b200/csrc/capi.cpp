@@ -464,9 +464,16 @@ int ce_minres(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const d
 }
 
 int ce_problem_create(int cfg, int64_t nx, int64_t ny, int64_t nz, ce_problem** out) {
+  return ce_problem_create_plan(cfg, nx, ny, nz, CE_PLAN_REFERENCE, out);
+}
+
+int ce_problem_create_plan(int cfg, int64_t nx, int64_t ny, int64_t nz, int plan_kind, ce_problem** out) {
   return guarded([&] {
+    if (!out) throw std::invalid_argument("null argument");
+    if (plan_kind != CE_PLAN_REFERENCE && plan_kind != CE_PLAN_MERGE_ALL_AXES)
+      throw std::invalid_argument("plan_kind must be CE_PLAN_REFERENCE or CE_PLAN_MERGE_ALL_AXES");
     auto p = std::make_unique<ce_problem>();
-    p->p.build(cfg, nx, ny, nz);
+    p->p.build(cfg, nx, ny, nz, plan_kind == CE_PLAN_MERGE_ALL_AXES);
     *out = p.release();
   });
 }

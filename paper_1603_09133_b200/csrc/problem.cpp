@@ -50,7 +50,7 @@ int ilog2_exact(int64_t block) {
 
 }  // namespace
 
-void Problem::build(int cfg_id, int64_t onx, int64_t ony, int64_t onz) {
+void Problem::build(int cfg_id, int64_t onx, int64_t ony, int64_t onz, bool merge_all_axes) {
   cfg = cfg_id;
   int dims = 2;
   double ksig = 0.0;
@@ -103,7 +103,8 @@ void Problem::build(int cfg_id, int64_t onx, int64_t ony, int64_t onz) {
   for (int64_t b = 0; b < m; ++b)
     for (int64_t p = offsets[static_cast<size_t>(b)]; p < offsets[static_cast<size_t>(b + 1)]; ++p) blk_of[static_cast<size_t>(p)] = b;
 
-  // plan levels: pairwise merges along cyclically alternating non-exhausted axes
+  // plan levels: pairwise merges along cyclically alternating non-exhausted axes (the
+  // reference's geometric_block_ordering), or along all of them at once (merge_all_axes)
   join = 2;
   plan_level_blocks.clear();
   plan_assign.clear();
@@ -116,14 +117,19 @@ void Problem::build(int cfg_id, int64_t onx, int64_t ony, int64_t onz) {
         axis = (axis + 1) % 3;
         ++tries;
       }
+      // merge_all_axes: every non-exhausted axis halves at once (2x2 / 2x2x2 groups)
+      bool merged[3];
+      for (int a = 0; a < 3; ++a) merged[a] = merge_all_axes ? cur[a] > 1 : a == axis;
       int64_t next[3] = {cur[0], cur[1], cur[2]};
-      next[axis] = (cur[axis] + join - 1) / join;
+      for (int a = 0; a < 3; ++a)
+        if (merged[a]) next[a] = (cur[a] + join - 1) / join;
       plan_level_blocks.push_back(cur[0] * cur[1] * cur[2]);
       for (int64_t cz = 0; cz < cur[2]; ++cz)
         for (int64_t cy = 0; cy < cur[1]; ++cy)
           for (int64_t cx = 0; cx < cur[0]; ++cx) {
             int64_t gc[3] = {cx, cy, cz};
-            gc[axis] /= join;
+            for (int a = 0; a < 3; ++a)
+              if (merged[a]) gc[a] /= join;
             plan_assign.push_back(gc[0] + next[0] * (gc[1] + next[1] * gc[2]));
           }
       cur[0] = next[0];

@@ -13,7 +13,7 @@ import paper_1603_09133_b200 as ce  # noqa: E402
 cfg = int(sys.argv[1])
 grid = [int(x) for x in sys.argv[2:5]] if len(sys.argv) > 4 else [0, 0, 0]
 t = time.time()
-p = ce.Problem(cfg, *grid)
+p = ce.Problem(cfg, *grid, plan=os.environ.get("CE_PLAN", "reference"))
 print("gen", time.time() - t, "n", p.n, flush=True)
 a = ce.DeviceMatrix(p.matrix())
 for rep in range(2):

@@ -30,6 +30,7 @@ lib = C.CDLL(LIB)
 _sig = {
     "oracle_last_error": (C.c_char_p, []),
     "oracle_problem_config": (C.c_int, [C.c_int, i64, i64, i64, C.POINTER(vp)]),
+    "oracle_problem_config_plan": (C.c_int, [C.c_int, i64, i64, i64, C.c_int, C.POINTER(vp)]),
     "oracle_problem_reference": (C.c_int, [C.c_int, i64, i64, i64, i64, C.POINTER(vp)]),
     "oracle_problem_triplets": (C.c_int, [i64, i64, i64p, i64p, dblp, i64, i64p, C.c_int, C.POINTER(vp)]),
     "oracle_problem_free": (None, [vp]),
@@ -95,9 +96,9 @@ class OProblem:
         self.m = int(lib.oracle_problem_m(handle))
 
     @staticmethod
-    def config(cfg, nx=0, ny=0, nz=0):
+    def config(cfg, nx=0, ny=0, nz=0, plan="reference"):
         h = vp()
-        _check(lib.oracle_problem_config(cfg, nx, ny, nz, C.byref(h)))
+        _check(lib.oracle_problem_config_plan(cfg, nx, ny, nz, {"reference": 0, "merge_all_axes": 1}[plan], C.byref(h)))
         return OProblem(h)
 
     @staticmethod

@@ -31,9 +31,14 @@ pytestmark = pytest.mark.gpu
 O.lib.oracle_problem_perturb.argtypes = [C.c_void_p, C.c_double, C.c_ulonglong]
 O.lib.oracle_problem_perturb.restype = None
 
-CASES = [(1, (0, 0, 0), 2048), (2, (64, 64, 0), 2048), (3, (64, 64, 0), 2048), (2, (128, 128, 0), 512),
-         (4, (16, 16, 16), 512), (5, (16, 16, 16), 512)]
-IDS = ["cfg1-128", "cfg2-64", "cfg3-64", "cfg2-128", "cfg4-16", "cfg5-16"]
+# (cfg, grid, dense threshold, plan family); "merge_all" = CE_PLAN_MERGE_ALL_AXES (J = 2^d), the plan
+# the full-size 3-D configs run with
+CASES = [(1, (0, 0, 0), 2048, "reference"), (2, (64, 64, 0), 2048, "reference"), (3, (64, 64, 0), 2048, "reference"),
+         (2, (128, 128, 0), 512, "reference"), (4, (16, 16, 16), 512, "reference"), (5, (16, 16, 16), 512, "reference"),
+         (2, (128, 128, 0), 256, "merge_all_axes"), (4, (16, 16, 16), 256, "merge_all_axes"),
+         (5, (16, 16, 32), 256, "merge_all_axes")]
+IDS = ["cfg1-128", "cfg2-64", "cfg3-64", "cfg2-128", "cfg4-16", "cfg5-16", "cfg2-128-merge_all", "cfg4-16-merge_all",
+       "cfg5-16x16x32-merge_all"]
 
 
 def _dump(f, d, name):
@@ -53,13 +58,13 @@ def _level(dmp, lv):
 def runs(gpu_ctx):
     out = {}
     d = tempfile.mkdtemp()
-    for (cfg, grid, dth), name in zip(CASES, IDS):
-        p = ce.Problem(cfg, *grid)
-        op = O.OProblem.config(cfg, *grid)
+    for (cfg, grid, dth, plan), name in zip(CASES, IDS):
+        p = ce.Problem(cfg, *grid, plan=plan)
+        op = O.OProblem.config(cfg, *grid, plan=plan)
         fo = op.factorize(eps=p.eps, dense_threshold=dth)
         o = _dump(fo, d, name + "-o.bin")
         forced = [L["retained"].tolist() for L in o["levels"]]
-        pp = O.OProblem.config(cfg, *grid)
+        pp = O.OProblem.config(cfg, *grid, plan=plan)
         O.lib.oracle_problem_perturb(pp.h, 1e-16, 5)
         fp = pp.factorize(eps=p.eps, dense_threshold=dth, forced=forced)
         probe = _dump(fp, d, name + "-p.bin")

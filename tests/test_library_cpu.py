@@ -66,6 +66,27 @@ def test_generator_matches_oracle_bitwise(cfg, grid):
         assert np.array_equal(x, y)
 
 
+@pytest.mark.parametrize("cfg,grid", [(2, (64, 32, 0)), (4, (16, 16, 16)), (5, (12, 8, 20)), (4, (32, 16, 8))])
+def test_merge_all_axes_plan_matches_oracle(cfg, grid):
+    """CE_PLAN_MERGE_ALL_AXES: same CSB as the reference plan (level-1 ordering is shared), and the
+    plan levels equal the oracle's; every plan level groups at most 2^d blocks, and each axis
+    halves per level until exhausted."""
+    p = ce.Problem(cfg, *grid, plan="merge_all_axes")
+    r = ce.Problem(cfg, *grid)
+    o = OProblem.config(cfg, *grid, plan="merge_all_axes")
+    assert np.array_equal(p.values, r.values) and np.array_equal(p.perm, r.perm)
+    assigns, join = o.plan_assigns()
+    assert join == p.plan.join == 2 and len(assigns) == len(p.plan.assigns)
+    for x, y in zip(assigns, p.plan.assigns):
+        assert np.array_equal(x, y)
+    d = 3 if cfg in (4, 5) else 2
+    for a in p.plan.assigns:
+        assert np.bincount(a).max() <= 2 ** d
+    assert len(p.plan.assigns) < len(r.plan.assigns)
+    with pytest.raises(ValueError):
+        ce.Problem(cfg, *grid, plan="nope")
+
+
 def test_generator_sizes_match_baseline_configs():
     """BASELINE.json configs: n and block size."""
     expect = {1: (16384, 8), 2: (1048576, 16)}
