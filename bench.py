@@ -25,6 +25,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "factorization unknowns/sec (fp64) + PCG solve time; % of HBM/FP64 roofline"
 # CPU sample of the same workload family (stencil, B, eps) sized for ~10 s of oracle work (cfg2 256^2: ~9 s)
+PLAN_FLAGS = {"reference": [], "merge_all_axes": ["--merge-all"], "merge_all_colored": ["--colored"]}
 CPU_SAMPLE_GRID = {1: (128, 128, 0), 2: (256, 256, 0), 3: (256, 256, 0), 4: (16, 16, 16), 5: (16, 16, 16)}
 
 
@@ -38,7 +39,7 @@ def parse():
     ap.add_argument("--grid", type=int, nargs=3, default=[0, 0, 0])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--plan", default="reference", choices=["reference", "merge_all_axes"],
+    ap.add_argument("--plan", default="reference", choices=["reference", "merge_all_axes", "merge_all_colored"],
                     help="plan family: the reference's geometric_block_ordering (join 2, one axis per level) or "
                          "every axis merging by 2 per level (J = 2^d; the 3-D configs at full size, DESIGN.md)")
     ap.add_argument("--ref-threads", type=int, default=0, help="reference arm: concurrent oracle copies (0 = all host threads)")
@@ -62,7 +63,7 @@ def sweep_traffic(args):
     committed ncu capture (profiles/r1_sweep_traffic_cfg2.json) when it matches this
     workload, else None."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_sweep_traffic_cfg2.json")
-    if args.cfg != 2 or any(args.grid) or not os.path.exists(path):
+    if args.cfg != 2 or any(args.grid) or args.plan != "reference" or not os.path.exists(path):
         return None
     try:
         return float(json.load(open(path))["total_dram_bytes"])
@@ -147,7 +148,7 @@ def cpu_oracle_run(cfg, grid, solve=True, plan="reference"):
     cli = os.path.join(ROOT, "oracle", "oracle_cli")
     if not os.path.exists(cli):
         subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "-j8"], check=True, capture_output=True)
-    args = [cli, str(cfg)] + [str(g) for g in grid if g > 0] + (["--merge-all"] if plan == "merge_all_axes" else [])
+    args = [cli, str(cfg)] + [str(g) for g in grid if g > 0] + PLAN_FLAGS[plan]
     if not solve:
         args.append("--no-solve")
     out = subprocess.run(args, check=True, capture_output=True, text=True).stdout
@@ -185,7 +186,7 @@ def run_reference(args):
     except AttributeError:
         cores = os.cpu_count() or 1
     copies = args.ref_threads if args.ref_threads > 0 else cores
-    cmd = [cli, str(args.cfg)] + [str(g) for g in grid if g > 0] + (["--merge-all"] if args.plan == "merge_all_axes" else [])
+    cmd = [cli, str(args.cfg)] + [str(g) for g in grid if g > 0] + PLAN_FLAGS[args.plan]
 
     def step():
         procs = [subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True) for _ in range(copies)]

@@ -192,6 +192,11 @@ int ce_problem_create(int cfg, int64_t nx, int64_t ny, int64_t nz, ce_problem** 
  * pattern reach stays bounded, so the 3-D configs fit in HBM at full size. */
 #define CE_PLAN_REFERENCE 0
 #define CE_PLAN_MERGE_ALL_AXES 1
+/* CE_PLAN_MERGE_ALL_COLORED = CE_PLAN_MERGE_ALL_AXES with every level's cells ordered
+ * colour-major, colour = (cx mod 3, cy mod 3, cz mod 3): with all-axis merges a row's squared
+ * pattern stays within Chebyshev distance 2 (in cells), so rows of one colour are independent
+ * and each level's sweep has at most 9 (2-D) / 27 (3-D) waves. */
+#define CE_PLAN_MERGE_ALL_COLORED 2
 int ce_problem_create_plan(int cfg, int64_t nx, int64_t ny, int64_t nz, int plan_kind, ce_problem** out);
 void ce_problem_free(ce_problem* p);
 /* The reference CLI's `file` problem (proj/src/cli.cpp:114-133 load_problem + finish_load :49-58):

@@ -47,7 +47,7 @@ int oracle_problem_config(int id, long long nx, long long ny, long long nz, void
 int oracle_problem_config_plan(int id, long long nx, long long ny, long long nz, int merge_all_axes, void** out) {
   try {
     ProblemConfig c = baseline_config(id);
-    c.merge_all_axes = merge_all_axes != 0;
+    c.plan_kind = merge_all_axes;
     if (nx > 0) c.nx = nx;
     if (ny > 0) c.ny = ny;
     if (nz > 0 && c.dims == 3) c.nz = nz;

@@ -4,7 +4,7 @@
 // JSON object.  Mirrors the timed regions of proj/src/cli.cpp:102-110
 // (factor_problem) and :211-228 (solve), with PCG in place of MINRES.
 //
-// usage: oracle_cli <cfg 1..5> [nx ny nz] [--no-solve] [--dump PATH] [--levels] [--merge-all]
+// usage: oracle_cli <cfg 1..5> [nx ny nz] [--no-solve] [--dump PATH] [--levels] [--merge-all | --colored]
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -20,7 +20,7 @@ using namespace oracle;
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::fprintf(stderr, "usage: oracle_cli <cfg 1..5> [nx ny nz] [--no-solve] [--dump PATH] [--levels] [--merge-all]\n");
+    std::fprintf(stderr, "usage: oracle_cli <cfg 1..5> [nx ny nz] [--no-solve] [--dump PATH] [--levels] [--merge-all | --colored]\n");
     return 1;
   }
   try {
@@ -31,7 +31,8 @@ int main(int argc, char** argv) {
     for (int a = 2; a < argc; ++a) {
       if (!std::strcmp(argv[a], "--no-solve")) solve = false;
       else if (!std::strcmp(argv[a], "--levels")) levels = true;
-      else if (!std::strcmp(argv[a], "--merge-all")) c.merge_all_axes = true;
+      else if (!std::strcmp(argv[a], "--merge-all")) c.plan_kind = 1;
+      else if (!std::strcmp(argv[a], "--colored")) c.plan_kind = 2;
       else if (!std::strcmp(argv[a], "--dump") && a + 1 < argc) dump = argv[++a];
       else {
         const long long v = std::atoll(argv[a]);

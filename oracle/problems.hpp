@@ -66,7 +66,7 @@ struct CoarseningPlan {
 CoarseningPlan geometric_block_ordering(const Grid3D& grid, index_t block, index_t join = 2);
 // Same ordering with an explicit cell shape (2-D: 2^bx x 2^by x 1, bx >= by).
 CoarseningPlan geometric_block_ordering_shape(const Grid3D& grid, std::array<index_t, 3> shape,
-                                              index_t join = 2, bool merge_all_axes = false);
+                                              index_t join = 2, int plan_kind = 0);
 std::array<index_t, 3> cell_shape_3d(index_t block);
 std::array<index_t, 3> cell_shape_2d(index_t block);
 
@@ -92,7 +92,9 @@ struct ProblemConfig {
   // at each level (2x2 / 2x2x2 groups, J = 2^d), a plan the reference's ce_factorize
   // accepts through its plan-file interface (problems.cpp:114-171); its pattern reach
   // stays bounded, which is what lets the 3-D configs fit in memory at full size.
-  bool merge_all_axes = false;
+  // 2: as true, with every level's cells ordered colour-major (mod-3 colouring; see
+  // geometric_block_ordering_shape)
+  int plan_kind = 0;
 };
 ProblemConfig baseline_config(int id);
 

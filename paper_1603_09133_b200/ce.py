@@ -364,11 +364,12 @@ def minres(a: DeviceMatrix, n: int, b, precond: Optional[CEFactorization], opts:
 class Problem:
     """A BASELINE.json configuration generated on the host."""
 
-    PLANS = {"reference": 0, "merge_all_axes": 1}
+    PLANS = {"reference": 0, "merge_all_axes": 1, "merge_all_colored": 2}
 
     def __init__(self, cfg: int, nx: int = 0, ny: int = 0, nz: int = 0, _handle=None, plan: str = "reference"):
         """plan: "reference" = geometric_block_ordering(grid, block, 2) (problems.cpp:195-258);
-        "merge_all_axes" = every non-exhausted axis merges by 2 per level (J = 2^d)."""
+        "merge_all_axes" = every non-exhausted axis merges by 2 per level (J = 2^d);
+        "merge_all_colored" = the same with each level's cells in mod-3 colour-major order."""
         if _handle is None:
             h = C.c_void_p()
             if plan not in self.PLANS:

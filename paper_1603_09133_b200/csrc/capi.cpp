@@ -470,10 +470,10 @@ int ce_problem_create(int cfg, int64_t nx, int64_t ny, int64_t nz, ce_problem** 
 int ce_problem_create_plan(int cfg, int64_t nx, int64_t ny, int64_t nz, int plan_kind, ce_problem** out) {
   return guarded([&] {
     if (!out) throw std::invalid_argument("null argument");
-    if (plan_kind != CE_PLAN_REFERENCE && plan_kind != CE_PLAN_MERGE_ALL_AXES)
-      throw std::invalid_argument("plan_kind must be CE_PLAN_REFERENCE or CE_PLAN_MERGE_ALL_AXES");
+    if (plan_kind != CE_PLAN_REFERENCE && plan_kind != CE_PLAN_MERGE_ALL_AXES && plan_kind != CE_PLAN_MERGE_ALL_COLORED)
+      throw std::invalid_argument("plan_kind must be one of CE_PLAN_REFERENCE / _MERGE_ALL_AXES / _MERGE_ALL_COLORED");
     auto p = std::make_unique<ce_problem>();
-    p->p.build(cfg, nx, ny, nz, plan_kind == CE_PLAN_MERGE_ALL_AXES);
+    p->p.build(cfg, nx, ny, nz, plan_kind);
     *out = p.release();
   });
 }

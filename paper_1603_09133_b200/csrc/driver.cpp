@@ -1212,6 +1212,11 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     a.err = d_err.p;
     a.shifts = d_shifts.p;
     a.bmax = std::max(cur.bmax, 1);
+    if (a.bmax > kSweepBlockMax) {
+      std::ostringstream os;
+      os << "level " << li + 1 << ": block size " << a.bmax << " exceeds the sweep kernel's limit " << kSweepBlockMax;
+      throw std::invalid_argument(os.str());
+    }
     a.kcap = sweep_kcap(a.bmax);
     // per-CTA buffer, rounded to 256 B so every CTA's (global-scratch) base keeps double2 alignment
     int64_t need = (sweep_smem_doubles(a.bmax, a.kcap) + 31) / 32 * 32;
@@ -1284,7 +1289,15 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       std::fprintf(stderr, "  (cycle sums in SM-seconds @1.9GHz)\n");
     }
     if (herr[0] == kErrPattern) throw std::logic_error("update outside the squared pattern");
-    if (herr[0] != 0) throw std::logic_error("internal sweep error");
+    if (herr[0] != 0) {
+      const int64_t row = static_cast<int64_t>(herr[2]) | (static_cast<int64_t>(herr[3]) << 31);
+      const char* what = herr[0] == kErrChunk ? "far-gather chunk narrower than a block"
+                         : herr[0] == kErrStrip ? "strip chunk narrower than a block"
+                         : herr[0] == kErrNaN ? "non-finite column norm" : "internal";
+      std::ostringstream os;
+      os << "internal sweep error (" << what << ") at level " << herr[1] << " row " << row;
+      throw std::logic_error(os.str());
+    }
     if (a.trace) {  // development trace: items (row, part) + timestamps -> CE_TRACE_FILE
       std::vector<unsigned long long> tr;
       d_trace.download(tr, s);

@@ -86,7 +86,7 @@ struct Problem {
   std::vector<double> values, rhs;
   int64_t join = 2;
   std::vector<int64_t> plan_level_blocks, plan_assign;
-  void build(int cfg_id, int64_t nx, int64_t ny, int64_t nz, bool merge_all_axes = false);
+  void build(int cfg_id, int64_t nx, int64_t ny, int64_t nz, int plan_kind = 0);  // CE_PLAN_*
   // reference `file` problems (io.cpp): matrix.mtx + optional plan.txt / rhs.txt
   void load(const char* matrix_path, const char* plan_path, const char* rhs_path, int64_t block);
   void save(const char* matrix_path, const char* plan_path, const char* rhs_path) const;

@@ -20,7 +20,7 @@ __host__ __device__ inline int row_pair_group(int forced, int np) {
   return g < 1 ? 1 : (g > 8 ? 8 : g);
 }  // largest eliminated width per block the apply sweeps stage in shared memory
 
-enum : int { kErrNone = 0, kErrBreakdown = 2, kErrPattern = 5, kErrInternal = 6 };
+enum : int { kErrNone = 0, kErrBreakdown = 2, kErrPattern = 5, kErrInternal = 6, kErrChunk = 7, kErrStrip = 8, kErrNaN = 9 };
 
 // Launch accounting (every launcher calls note_launch once per kernel launch).
 void note_launch(int64_t n = 1);
@@ -112,6 +112,9 @@ enum : int {
 
 // smem doubles needed by one sweep CTA for a level
 int64_t sweep_smem_doubles(int bmax, int kcap);
+// Largest block the level sweep accepts (static shared chunk maps / cluster table); the
+// driver rejects larger levels with an error instead of overrunning them.
+constexpr int kSweepBlockMax = 1024;
 int sweep_kcap(int bmax);  // F^T chunk height for a level
 void launch_sweep(const SweepArgs& a, int grid, size_t smem_bytes, cudaStream_t s);
 int sweep_max_ctas_per_sm(size_t smem_bytes);

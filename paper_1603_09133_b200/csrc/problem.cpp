@@ -50,7 +50,7 @@ int ilog2_exact(int64_t block) {
 
 }  // namespace
 
-void Problem::build(int cfg_id, int64_t onx, int64_t ony, int64_t onz, bool merge_all_axes) {
+void Problem::build(int cfg_id, int64_t onx, int64_t ony, int64_t onz, int plan_kind) {
   cfg = cfg_id;
   int dims = 2;
   double ksig = 0.0;
@@ -82,19 +82,34 @@ void Problem::build(int cfg_id, int64_t onx, int64_t ony, int64_t onz, bool merg
   if (dims == 2) shape = {int64_t{1} << ((lb + 1) / 2), int64_t{1} << (lb / 2), 1};
   else shape = {int64_t{1} << ((lb + 2) / 3), int64_t{1} << ((lb + 1) / 3), int64_t{1} << (lb / 3)};
   const int64_t nc[3] = {(nx + shape[0] - 1) / shape[0], (ny + shape[1] - 1) / shape[1], (nz + shape[2] - 1) / shape[2]};
+  // position -> lexicographic cell id on a cells grid; colour-major (mod-3 colouring) for
+  // CE_PLAN_MERGE_ALL_COLORED, so that one colour's rows share no squared-pattern entry
+  const bool merge_all_axes = plan_kind >= 1, colored = plan_kind == 2;
+  auto order = [&](const int64_t* g) {
+    std::vector<int64_t> ord(static_cast<size_t>(g[0] * g[1] * g[2]));
+    for (size_t q = 0; q < ord.size(); ++q) ord[q] = static_cast<int64_t>(q);
+    if (colored) {
+      auto color = [&](int64_t q) {
+        const int64_t x = q % g[0], y = (q / g[0]) % g[1], z = q / (g[0] * g[1]);
+        return x % 3 + 3 * (y % 3) + 9 * (z % 3);
+      };
+      std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return color(a) < color(b); });
+    }
+    return ord;
+  };
+  std::vector<int64_t> ord = order(nc);
   perm.clear();
   perm.reserve(static_cast<size_t>(N));
   std::vector<int64_t> sizes;
-  for (int64_t cz = 0; cz < nc[2]; ++cz)
-    for (int64_t cy = 0; cy < nc[1]; ++cy)
-      for (int64_t cx = 0; cx < nc[0]; ++cx) {
-        const int64_t x0 = cx * shape[0], y0 = cy * shape[1], z0 = cz * shape[2];
-        const int64_t x1 = std::min(x0 + shape[0], nx), y1 = std::min(y0 + shape[1], ny), z1 = std::min(z0 + shape[2], nz);
-        for (int64_t k = z0; k < z1; ++k)
-          for (int64_t j = y0; j < y1; ++j)
-            for (int64_t i = x0; i < x1; ++i) perm.push_back(i + nx * (j + ny * k));
-        sizes.push_back((x1 - x0) * (y1 - y0) * (z1 - z0));
-      }
+  for (const int64_t q : ord) {
+    const int64_t cx = q % nc[0], cy = (q / nc[0]) % nc[1], cz = q / (nc[0] * nc[1]);
+    const int64_t x0 = cx * shape[0], y0 = cy * shape[1], z0 = cz * shape[2];
+    const int64_t x1 = std::min(x0 + shape[0], nx), y1 = std::min(y0 + shape[1], ny), z1 = std::min(z0 + shape[2], nz);
+    for (int64_t k = z0; k < z1; ++k)
+      for (int64_t j = y0; j < y1; ++j)
+        for (int64_t i = x0; i < x1; ++i) perm.push_back(i + nx * (j + ny * k));
+    sizes.push_back((x1 - x0) * (y1 - y0) * (z1 - z0));
+  }
   m = static_cast<int64_t>(sizes.size());
   offsets.assign(static_cast<size_t>(m + 1), 0);
   for (int64_t b = 0; b < m; ++b) offsets[static_cast<size_t>(b + 1)] = offsets[static_cast<size_t>(b)] + sizes[static_cast<size_t>(b)];
@@ -117,21 +132,22 @@ void Problem::build(int cfg_id, int64_t onx, int64_t ony, int64_t onz, bool merg
         axis = (axis + 1) % 3;
         ++tries;
       }
-      // merge_all_axes: every non-exhausted axis halves at once (2x2 / 2x2x2 groups)
       bool merged[3];
       for (int a = 0; a < 3; ++a) merged[a] = merge_all_axes ? cur[a] > 1 : a == axis;
       int64_t next[3] = {cur[0], cur[1], cur[2]};
       for (int a = 0; a < 3; ++a)
         if (merged[a]) next[a] = (cur[a] + join - 1) / join;
+      const std::vector<int64_t> nord = order(next);
+      std::vector<int64_t> ninv(nord.size());
+      for (size_t p = 0; p < nord.size(); ++p) ninv[static_cast<size_t>(nord[p])] = static_cast<int64_t>(p);
       plan_level_blocks.push_back(cur[0] * cur[1] * cur[2]);
-      for (int64_t cz = 0; cz < cur[2]; ++cz)
-        for (int64_t cy = 0; cy < cur[1]; ++cy)
-          for (int64_t cx = 0; cx < cur[0]; ++cx) {
-            int64_t gc[3] = {cx, cy, cz};
-            for (int a = 0; a < 3; ++a)
-              if (merged[a]) gc[a] /= join;
-            plan_assign.push_back(gc[0] + next[0] * (gc[1] + next[1] * gc[2]));
-          }
+      for (const int64_t q : ord) {
+        int64_t gc[3] = {q % cur[0], (q / cur[0]) % cur[1], q / (cur[0] * cur[1])};
+        for (int a = 0; a < 3; ++a)
+          if (merged[a]) gc[a] /= join;
+        plan_assign.push_back(ninv[static_cast<size_t>(gc[0] + next[0] * (gc[1] + next[1] * gc[2]))]);
+      }
+      ord = nord;
       cur[0] = next[0];
       cur[1] = next[1];
       cur[2] = next[2];

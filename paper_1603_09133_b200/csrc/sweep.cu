@@ -110,6 +110,7 @@ __host__ __device__ inline Layout sweep_layout(int bmax, int kcap) {
   const int64_t cwb = (budget - L.base + dreg) / (2 * bmax);
   if (cwb > cw) cw = cwb;
   if (cw > 256) cw = 256;
+  if (cw < bmax) cw = bmax;  // a strip chunk holds at least one whole block (3-D merge-all levels: b > 256)
   L.cw = static_cast<int>(cw);
   L.extra = 2 * bmax * cw > dreg ? 2 * bmax * cw - dreg : 0;
   return L;

@@ -1105,7 +1105,7 @@ __device__ __noinline__ void canonical_basis(const Buf& s_, int b, int r, int ns
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* A = s.C;   // b x r column-major
   double* Vh = s.R;  // reflectors, column-major
-  __shared__ int cstart[512];
+  __shared__ int cstart[kSweepBlockMax];
   if (threadIdx.x == 0) {
     int k0 = 0;
     while (k0 < r) {
@@ -1243,7 +1243,7 @@ __device__ void tsqr_sel(const SweepArgs& A, double* R, double* C, int K, int b,
 // Window of a row's squared-pattern entries staged in shared memory (one coalesced
 // pass over the host-built per-entry tables) plus the column map of the current chunk.
 constexpr int kEW = 256;
-constexpr int kChunkMax = 512;
+constexpr int kChunkMax = kSweepBlockMax;  // chunk widths are >= bmax (sweep_kcap, sweep_layout)
 struct EntWin {
   long long off[kEW];
   int col[kEW];
@@ -1299,7 +1299,7 @@ __device__ int gather_tsqr(const SweepArgs& A, int i, int b, const Buf& s_, int6
           add += bj;
         }
         if (full && add == 0 && kfill == 0) {  // a block wider than the chunk: impossible by kcap >= bmax
-          set_error(A.err, kErrInternal, A.level, i);
+          set_error(A.err, kErrChunk, A.level, i);
           kk = n;
           full = 0;
         }
@@ -1382,7 +1382,7 @@ __device__ __noinline__ void strip_range(const SweepArgs& A, int i, int b, int r
           cols += bj;
         }
         if (cols == 0 && kk < n) {  // a block wider than the chunk: impossible by cw >= bmax
-          set_error(A.err, kErrInternal, A.level, i);
+          set_error(A.err, kErrStrip, A.level, i);
           kk = n;
         }
         c_n = cols;
@@ -1770,7 +1770,7 @@ __device__ __noinline__ void task_a2(const SweepArgs& A, int i, const Buf& s_, i
       __syncthreads();
       for (int j = tid; j < b; j += T) {
         const double sj = s.nrm[j];
-        if (!isfinite(sj)) set_error(A.err, kErrInternal, A.level, i);  // never rank a NaN
+        if (!isfinite(sj)) set_error(A.err, kErrNaN, A.level, i);  // never rank a NaN
         int rank = 0;
         for (int k = 0; k < b; ++k) {
           const double sk = s.nrm[k];

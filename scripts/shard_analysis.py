@@ -40,7 +40,8 @@ def main():
     cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     grid = [int(x) for x in sys.argv[2:4]] if len(sys.argv) > 3 else [0, 0]
     boxes = [int(x) for x in sys.argv[4:]] if len(sys.argv) > 4 else [2, 4, 8]
-    p = ce.Problem(cfg, grid[0], grid[1], 0)
+    import os
+    p = ce.Problem(cfg, grid[0], grid[1], 0, plan=os.environ.get("CE_PLAN", "reference"))
     nx = int(round(np.sqrt(p.n))) if grid[0] == 0 else grid[0]
     M = p.m
     rows = np.repeat(np.arange(M), np.diff(p.row_ptr))

@@ -66,15 +66,20 @@ def test_generator_matches_oracle_bitwise(cfg, grid):
         assert np.array_equal(x, y)
 
 
+@pytest.mark.parametrize("plan", ["merge_all_axes", "merge_all_colored"])
 @pytest.mark.parametrize("cfg,grid", [(2, (64, 32, 0)), (4, (16, 16, 16)), (5, (12, 8, 20)), (4, (32, 16, 8))])
-def test_merge_all_axes_plan_matches_oracle(cfg, grid):
-    """CE_PLAN_MERGE_ALL_AXES: same CSB as the reference plan (level-1 ordering is shared), and the
-    plan levels equal the oracle's; every plan level groups at most 2^d blocks, and each axis
-    halves per level until exhausted."""
-    p = ce.Problem(cfg, *grid, plan="merge_all_axes")
+def test_merge_all_axes_plan_matches_oracle(cfg, grid, plan):
+    """CE_PLAN_MERGE_ALL_AXES / _COLORED: CSB, rhs, permutation and plan levels identical to the
+    oracle's; every plan level groups at most 2^d blocks, and each axis halves per level until
+    exhausted.  Uncoloured, the level-1 ordering is the reference plan's."""
+    p = ce.Problem(cfg, *grid, plan=plan)
     r = ce.Problem(cfg, *grid)
-    o = OProblem.config(cfg, *grid, plan="merge_all_axes")
-    assert np.array_equal(p.values, r.values) and np.array_equal(p.perm, r.perm)
+    o = OProblem.config(cfg, *grid, plan=plan)
+    off, rp, ci, vp, vals = o.csb()
+    assert np.array_equal(rp, p.row_ptr) and np.array_equal(ci, p.col_idx) and np.array_equal(vals, p.values)
+    assert np.array_equal(o.rhs(), p.rhs) and np.array_equal(o.perm(), p.perm)
+    if plan == "merge_all_axes":
+        assert np.array_equal(p.values, r.values) and np.array_equal(p.perm, r.perm)
     assigns, join = o.plan_assigns()
     assert join == p.plan.join == 2 and len(assigns) == len(p.plan.assigns)
     for x, y in zip(assigns, p.plan.assigns):
@@ -83,6 +88,20 @@ def test_merge_all_axes_plan_matches_oracle(cfg, grid):
     for a in p.plan.assigns:
         assert np.bincount(a).max() <= 2 ** d
     assert len(p.plan.assigns) < len(r.plan.assigns)
+    if plan == "merge_all_colored":  # one colour's blocks share no squared-pattern entry (level 1)
+        import scipy.sparse as sp
+        rows = np.repeat(np.arange(p.m), np.diff(p.row_ptr))
+        B = sp.csr_matrix((np.ones(len(rows)), (rows, p.col_idx)), shape=(p.m, p.m))
+        S = (B @ B).tocoo()
+        first = p.perm[p.offsets[:-1]]
+        # colour of each block from the cell containing its first unknown
+        sh = {2: (4, 4, 1), 4: (4, 4, 2), 5: (4, 4, 2)}[cfg]
+        x, y = first % grid[0], (first // grid[0]) % grid[1]
+        z = first // (grid[0] * grid[1]) if d == 3 else 0 * x
+        col = (x // sh[0]) % 3 + 3 * ((y // sh[1]) % 3) + 9 * ((z // sh[2]) % 3)
+        assert np.all(np.diff(col) >= 0)  # colour-major
+        off_diag = S.row != S.col
+        assert not np.any(col[S.row[off_diag]] == col[S.col[off_diag]])
     with pytest.raises(ValueError):
         ce.Problem(cfg, *grid, plan="nope")
 
