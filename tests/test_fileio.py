@@ -41,10 +41,12 @@ def _same(a, b):
     return all(np.array_equal(np.asarray(x), np.asarray(y)) for x, y in zip(a, b))
 
 
-def test_generated_problems_round_trip(tmp_path):
-    """run_gen -> load_problem reproduces the CSB, permutation, plan and rhs exactly."""
+@pytest.mark.parametrize("plan", ["reference", "merge_all_axes", "merge_all_colored"])
+def test_generated_problems_round_trip(tmp_path, plan):
+    """run_gen -> load_problem reproduces the CSB, permutation, plan and rhs exactly (every plan
+    family travels through the reference's plan-file format)."""
     for cfg, grid in [(1, (32, 32, 0)), (3, (32, 32, 0)), (4, (8, 8, 8))]:
-        p = ce.Problem(cfg, *grid)
+        p = ce.Problem(cfg, *grid, plan=plan)
         m, pl, r = (str(tmp_path / f"{cfg}{s}") for s in ("m.mtx", "plan.txt", "rhs.txt"))
         p.save(m, pl, r)
         q = ce.Problem.load(m, pl, r)
