@@ -39,6 +39,7 @@ def parse():
     ap.add_argument("--grid", type=int, nargs=3, default=[0, 0, 0])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the colour-major plan variant line")
     ap.add_argument("--plan", default="reference", choices=["reference", "merge_all_axes", "merge_all_colored"],
                     help="plan family: the reference's geometric_block_ordering (join 2, one axis per level) or "
                          "every axis merging by 2 per level (J = 2^d; the 3-D configs at full size, DESIGN.md)")
@@ -335,6 +336,36 @@ def run_product(args):
         del f2, a2
     e2e_val = world * n / allmax(statistics.mean(e2e_t))
 
+    # The same config under the colour-major all-axis-merge plan:
+    # reported beside the headline, which stays on the reference's geometric_block_ordering.
+    variant = None
+    if args.plan == "reference" and not args.no_variants:
+        vprob = ce.Problem(args.cfg, *args.grid, plan="merge_all_colored")
+        va = ce.DeviceMatrix(vprob.matrix(), ctx)
+        vb = torch.from_numpy(vprob.rhs).to(dev)
+        vrec = []
+        for k in range(5):
+            with torch.cuda.stream(stream):
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record(stream)
+                vf = ce.ce_factorize(va, vprob.plan, vprob.strategy(), ce.FactorOptions(), ctx)
+                e1.record(stream)
+                vrep, _ = ce.pcg(va, n, vb, vf, popts)
+                e2.record(stream)
+            e2.synchronize()
+            if k >= 2:  # 2 warm-up, 3 timed
+                vrec.append((e0.elapsed_time(e1) * 1e-3, e1.elapsed_time(e2) * 1e-3))
+            del vf
+        vfac = allmax(sum(x[0] for x in vrec))
+        variant = {"plan": "merge_all_colored", "value": job_throughput(world, n, len(vrec), vfac), "unit": "unknowns/s",
+                   "steps": len(vrec), "warmup": 2, "factor_ms": 1e3 * vfac / len(vrec),
+                   "pcg_solve_ms": 1e3 * sum(x[1] for x in vrec) / len(vrec), "pcg_iterations": vrep.iterations,
+                   "pcg_true_residual": vrep.final_true_residual, "pcg_converged": vrep.converged}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            r = cpu_oracle_run(args.cfg, CPU_SAMPLE_GRID[args.cfg], solve=False, plan="merge_all_colored")
+            variant["cpu_baseline_value"] = r["unknowns_per_sec"]
+        del va, vb
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         grid = CPU_SAMPLE_GRID[args.cfg]
@@ -373,6 +404,8 @@ def run_product(args):
         }
         if cpu:
             line["cpu_baseline"] = cpu
+        if variant:
+            line["plan_variant"] = variant
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
