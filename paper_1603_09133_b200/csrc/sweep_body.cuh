@@ -605,91 +605,61 @@ __device__ __noinline__ int jacobi_wide(double* X, double* V, int b, int ld, int
   for (int sweep = 0; sweep < 100; ++sweep) {
     int rotated = 0;
     for (int round = 0; round < nb - 1; ++round) {
-      // two disjoint pairs per warp step: their loads are in flight together and their
-      // reductions share the shuffle stages (per-pair arithmetic unchanged, so bit-identical)
-      for (int pi0 = warp; pi0 < np; pi0 += 2 * NW) {
-        constexpr int NP = 2;
-        double* cp[NP];
-        double* cq[NP];
-        double* vp[NP];
-        double* vq[NP];
-        bool ok[NP];
-#pragma unroll
-        for (int j = 0; j < NP; ++j) {
-          const int pi = pi0 + j * NW;
-          int p = 0, q = 0;
-          ok[j] = false;
-          if (pi < np) {
-            p = rr_player(pi, round, nb);
-            q = rr_player(nb - 1 - pi, round, nb);
-            if (p > q) {
-              const int t = p;
-              p = q;
-              q = t;
-            }
-            ok[j] = q < b;  // warp-uniform
-          }
-          if (!ok[j]) p = q = 0;
-          cp[j] = X + p * ld;
-          cq[j] = X + q * ld;
-          vp[j] = V + p * ld;
-          vq[j] = V + q * ld;
+      for (int pi = warp; pi < np; pi += NW) {
+        int p = rr_player(pi, round, nb), q = rr_player(nb - 1 - pi, round, nb);
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
         }
-        if (!ok[0] && !ok[1]) continue;
-        // the V columns are loaded with X's, before the rotation test: one memory round trip
-        // per step (deep levels keep X and V in L2-resident global scratch)
-        double x[NP][E], y[NP][E], u[NP][E], v[NP][E];
-        double al[NP], be[NP], ga[NP];
+        if (q >= b) continue;  // warp-uniform
+        double* cp = X + p * ld;
+        double* cq = X + q * ld;
+        double x[E], y[E];
+        double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
-        for (int j = 0; j < NP; ++j) {
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            const int k = lane + 32 * e;
-            const bool in = ok[j] && k < b;
-            x[j][e] = in ? cp[j][k] : 0.0;
-            y[j][e] = in ? cq[j][k] : 0.0;
-            u[j][e] = in ? vp[j][k] : 0.0;
-            v[j][e] = in ? vq[j][k] : 0.0;
-          }
+        for (int e = 0; e < E; ++e) {
+          const int k = lane + 32 * e;
+          x[e] = k < b ? cp[k] : 0.0;
+          y[e] = k < b ? cq[k] : 0.0;
         }
 #pragma unroll
-        for (int j = 0; j < NP; ++j) {
-          al[j] = be[j] = ga[j] = 0.0;
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            al[j] += x[j][e] * x[j][e];
-            be[j] += y[j][e] * y[j][e];
-            ga[j] += x[j][e] * y[j][e];
-          }
+        for (int e = 0; e < E; ++e) {
+          al += x[e] * x[e];
+          be += y[e] * y[e];
+          ga += x[e] * y[e];
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-          for (int j = 0; j < NP; ++j) {
-            al[j] += __shfl_xor_sync(0xffffffffu, al[j], o);
-            be[j] += __shfl_xor_sync(0xffffffffu, be[j], o);
-            ga[j] += __shfl_xor_sync(0xffffffffu, ga[j], o);
-          }
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
+        if (al != 0.0 && be != 0.0 && ga * ga > tol2 * al * be) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = rsqrt(1.0 + t * t);
+          const double sn = cs * t;
+          double* vp = V + p * ld;
+          double* vq = V + q * ld;
+          double u[E], v[E];
 #pragma unroll
-        for (int j = 0; j < NP; ++j) {
-          if (ok[j] && al[j] != 0.0 && be[j] != 0.0 && ga[j] * ga[j] > tol2 * al[j] * be[j]) {
-            const double zeta = (be[j] - al[j]) / (2.0 * ga[j]);
-            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            const double cs = rsqrt(1.0 + t * t);
-            const double sn = cs * t;
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-              const int k = lane + 32 * e;
-              if (k < b) {
-                cp[j][k] = cs * x[j][e] - sn * y[j][e];
-                cq[j][k] = sn * x[j][e] + cs * y[j][e];
-                vp[j][k] = cs * u[j][e] - sn * v[j][e];
-                vq[j][k] = sn * u[j][e] + cs * v[j][e];
-              }
-            }
-            rotated = 1;
+          for (int e = 0; e < E; ++e) {
+            const int k = lane + 32 * e;
+            u[e] = k < b ? vp[k] : 0.0;
+            v[e] = k < b ? vq[k] : 0.0;
           }
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int k = lane + 32 * e;
+            if (k < b) {
+              cp[k] = cs * x[e] - sn * y[e];
+              cq[k] = sn * x[e] + cs * y[e];
+              vp[k] = cs * u[e] - sn * v[e];
+              vq[k] = sn * u[e] + cs * v[e];
+            }
+          }
+          rotated = 1;
         }
       }
       if (round < nb - 2) __syncthreads();
