@@ -7,7 +7,10 @@
 
 namespace ceg {
 
-constexpr int kSweepThreads = 256;
+#ifndef CE_SWEEP_THREADS
+#define CE_SWEEP_THREADS 256  // threads per sweep CTA (A/B builds: scripts/build_variant.sh -DCE_SWEEP_THREADS=...)
+#endif
+constexpr int kSweepThreads = CE_SWEEP_THREADS;
 constexpr int kApplyThreads = 128;
 constexpr int kApplyWmax = 256;
 // Schur pairs per B task of a row with np panels (forced > 0, else adaptive): one pair per task
