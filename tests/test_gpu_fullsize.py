@@ -78,3 +78,29 @@ def test_cfg3_fullsize_properties(gpu_ctx):
     assert dim == f.stats["tail_dim"]
     rep, x = ce.pcg(a, p.n, p.rhs, f, ce.PcgOptions(tol=p.tol, maxit=200))
     assert rep.converged and rep.final_true_residual <= 10 * p.tol
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_colored_plan_fullsize_properties(gpu_ctx, cfg):
+    """cfg2 / cfg3 at full size under the colour-major all-axis-merge plan (DESIGN.md "Plan
+    families"): every level's row DAG has at most 9 waves (one per mod-3 colour), dimensions
+    telescope, M (M^-1 x) = x, PCG reaches the stated tolerance with the true residual below
+    target, and re-factorization is bitwise deterministic."""
+    p = ce.Problem(cfg, plan="merge_all_colored")
+    a = ce.DeviceMatrix(p.matrix())
+    f = ce.ce_factorize(a, p.plan, p.strategy())
+    dim = p.n
+    for s in f.level_stats():
+        assert s["n_waves"] <= 9
+        assert s["max_close"] <= 8
+        assert s["eliminated"] + s["retained"] == dim
+        dim = s["retained"]
+    assert dim == f.stats["tail_dim"]
+    x = np.random.default_rng(2).standard_normal(p.n)
+    y = f.solve(x)
+    assert np.linalg.norm(f.apply_operator(y) - x) <= 1e-8 * np.linalg.norm(x)
+    rep, xs = ce.pcg(a, p.n, p.rhs, f, ce.PcgOptions(tol=p.tol, maxit=200))
+    assert rep.converged and rep.iterations <= 3
+    assert np.linalg.norm(p.rhs - a.matvec(xs)) <= 10 * p.tol * np.linalg.norm(p.rhs)
+    g = ce.ce_factorize(a, p.plan, p.strategy())
+    assert np.array_equal(g.solve(x), y)
