@@ -117,7 +117,10 @@ enum : int {
 int64_t sweep_smem_doubles(int bmax, int kcap);
 // Largest block the level sweep accepts (static shared chunk maps / cluster table); the
 // driver rejects larger levels with an error instead of overrunning them.
-constexpr int kSweepBlockMax = 1024;
+#ifndef CE_SWEEP_BLOCK_MAX
+#define CE_SWEEP_BLOCK_MAX 512  // 1024 costs ~1.5% on cfg2 (static shared chunk maps), A/B this round
+#endif
+constexpr int kSweepBlockMax = CE_SWEEP_BLOCK_MAX;
 int sweep_kcap(int bmax);  // F^T chunk height for a level
 void launch_sweep(const SweepArgs& a, int grid, size_t smem_bytes, cudaStream_t s);
 int sweep_max_ctas_per_sm(size_t smem_bytes);
