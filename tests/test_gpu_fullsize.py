@@ -104,3 +104,19 @@ def test_colored_plan_fullsize_properties(gpu_ctx, cfg):
     assert np.linalg.norm(p.rhs - a.matvec(xs)) <= 10 * p.tol * np.linalg.norm(p.rhs)
     g = ce.ce_factorize(a, p.plan, p.strategy())
     assert np.array_equal(g.solve(x), y)
+
+
+def test_block_limit_fails_loudly(gpu_ctx):
+    """3-D all-axis merges grow blocks with the cell surface: cfg4's stencil at 32^3 reaches
+    b ~ 580 at level 3, above the sweep's kSweepBlockMax (512).  The library must refuse with a
+    clear error instead of overrunning its shared-memory chunk maps."""
+    p = ce.Problem(4, 32, 32, 32, plan="merge_all_axes")
+    a = ce.DeviceMatrix(p.matrix())
+    with pytest.raises((RuntimeError, ValueError), match="exceeds"):
+        ce.ce_factorize(a, p.plan, p.strategy())
+    # the context stays usable afterwards
+    q = ce.Problem(1, 32, 32)
+    b = ce.DeviceMatrix(q.matrix())
+    f = ce.ce_factorize(b, q.plan, q.strategy(), ce.FactorOptions(dense_threshold=256))
+    rep, _ = ce.pcg(b, q.n, q.rhs, f, ce.PcgOptions(tol=q.tol))
+    assert rep.converged
