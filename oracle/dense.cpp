@@ -128,20 +128,20 @@ void householder_r(Mat& A) {
   const index_t kmax = std::min(m, n);
   std::vector<double> v(static_cast<size_t>(m));
   for (index_t k = 0; k < kmax; ++k) {
-    double nrm2 = 0.0;
-    for (index_t i = k; i < m; ++i) nrm2 += A(i, k) * A(i, k);
-    const double nrm = std::sqrt(nrm2);
-    if (nrm == 0.0) continue;
+    // Scaled reflector (Eigen makeHouseholder / LAPACK dlarfg): v = [1; x_tail / (x_k - beta)],
+    // tau = (beta - x_k) / beta.  No reflection when the tail's squared norm is <= DBL_MIN, so
+    // roundoff-level columns (norms ~1e-155) cannot overflow tau (the unscaled 2 / v^T v did,
+    // and turned a whole F into NaN singular values).
+    double s2 = 0.0;
+    for (index_t i = k + 1; i < m; ++i) s2 += A(i, k) * A(i, k);
+    if (s2 <= DBL_MIN) continue;
     const double xk = A(k, k);
+    const double nrm = std::sqrt(xk * xk + s2);
     const double beta = xk >= 0.0 ? -nrm : nrm;
-    // v = x - beta e_k, tau = 2 / v^T v
-    v[static_cast<size_t>(k)] = xk - beta;
-    double vtv = v[static_cast<size_t>(k)] * v[static_cast<size_t>(k)];
-    for (index_t i = k + 1; i < m; ++i) {
-      v[static_cast<size_t>(i)] = A(i, k);
-      vtv += A(i, k) * A(i, k);
-    }
-    const double tau = 2.0 / vtv;
+    const double tau = (beta - xk) / beta;
+    const double scale = 1.0 / (xk - beta);
+    v[static_cast<size_t>(k)] = 1.0;
+    for (index_t i = k + 1; i < m; ++i) v[static_cast<size_t>(i)] = A(i, k) * scale;
     A(k, k) = beta;
     for (index_t i = k + 1; i < m; ++i) A(i, k) = 0.0;
     for (index_t j = k + 1; j < n; ++j) {
@@ -177,7 +177,7 @@ SvdLeft svd_left(const Mat& F) {
     for (index_t i = k + 1; i < b; ++i) s2 += Rt(i, k) * Rt(i, k);
     std::vector<double>& v = hv[static_cast<size_t>(k)];
     v.assign(static_cast<size_t>(b), 0.0);
-    if (s2 == 0.0) continue;  // dlarfg: tau = 0
+    if (s2 <= DBL_MIN) continue;  // dlarfg / Eigen makeHouseholder: tau = 0
     const double x0 = Rt(k, k);
     const double nrm = std::sqrt(x0 * x0 + s2);
     const double beta = x0 >= 0.0 ? -nrm : nrm;

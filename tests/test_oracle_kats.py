@@ -288,3 +288,20 @@ def test_minres_and_pcg_examples():
     assert rep["converged"] and rep["iterations"] <= 10
     rep0, _ = q.krylov(np.ones(q.n) / 289.0, None, "minres", tol=1e-10, maxit=2000)
     assert rep0["iterations"] >= 50
+
+
+def test_svd_roundoff_columns_do_not_overflow():
+    """Regression: a far-fill concatenation from the oracle's own run (cfg1, colour-major plan,
+    level 4, row 18; 39 x 174 with 3 nonzero columns, tests/golden/F_roundoff_tail_cfg1_colored_L4.npy)
+    whose QR leaves columns of norm ~1e-155.  The unscaled Householder tau = 2 / v^T v overflowed
+    there and every singular value came out NaN (rank = b).  With the scaled reflector and
+    Eigen's no-reflection rule for tails <= DBL_MIN: rank 3, sigma equal to LAPACK's."""
+    import os
+    F = np.load(os.path.join(os.path.dirname(__file__), "golden", "F_roundoff_tail_cfg1_colored_L4.npy"))
+    r, basis, sigma = compress(F, eps=1e-4)
+    sigma = np.asarray(sigma)
+    ref = np.linalg.svd(F, compute_uv=False)
+    assert np.all(np.isfinite(sigma))
+    assert r == 3
+    assert np.max(np.abs(sigma[:3] - ref[:3])) <= 1e-13 * ref[0]
+    assert np.all(sigma[3:] <= 1e-12 * ref[0])
