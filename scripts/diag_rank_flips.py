@@ -1,3 +1,6 @@
+"""Per-level free-run rank differences GPU vs oracle, with sigma_k / threshold of the differing
+rows, and the preconditioner-apply deviation (development tool; found the oracle's Householder
+overflow on roundoff columns).  Edit cfg / grid / plan below."""
 import sys, os, tempfile
 sys.path.insert(0, "tests"); sys.path.insert(0, ".")
 import numpy as np
