@@ -1,0 +1,46 @@
+"""bench.py's JSON-line contract: the reference arm runs on CPU (the oracle port), so its line is
+checked here without a GPU; the product arm's line is checked on a B200 (-m gpu) on cfg1."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+             "vs_baseline", "dtype", "config", "e2e"}
+
+
+def _run(args, env=None):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, env=dict(os.environ, **(env or {})))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    d = _run(["--impl", "reference", "--cfg", "1", "--steps", "1", "--warmup", "1", "--ref-threads", "2"])
+    assert BASE_KEYS <= set(d)
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["config"]["cfg"] == 1
+
+
+@pytest.mark.gpu
+def test_product_line_cfg1():
+    d = _run(["--cfg", "1", "--steps", "2", "--warmup", "3", "--e2e-steps", "1", "--no-cpu-baseline"])
+    assert BASE_KEYS <= set(d)
+    assert d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] == 3 and d["dtype"] == "f64"
+    assert d["pcg_converged"] and d["pcg_iterations"] <= 3
+    r = d["roofline"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r) and 0 < r["frac"] < 1
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] == 8 * d["config"]["n"]
+    assert d["gpu_launches"] > 0
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    v = d["plan_variant"]
+    assert v["plan"] == "merge_all_colored" and v["value"] > 0 and v["pcg_converged"]
