@@ -61,10 +61,11 @@ def workload_name(cfg, grid, plan="reference"):
 
 def sweep_traffic(args):
     """DRAM bytes (read + write) of the level-sweep launches of one factorization, from the
-    committed ncu capture (profiles/r1_sweep_traffic_cfg2.json) when it matches this
-    workload, else None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_sweep_traffic_cfg2.json")
-    if args.cfg != 2 or any(args.grid) or args.plan != "reference" or not os.path.exists(path):
+    committed ncu capture (profiles/r1_sweep_traffic_cfg2*.json) when it matches this
+    workload (cfg2 full size, reference or colour-major plan), else None."""
+    name = {"reference": "r1_sweep_traffic_cfg2.json", "merge_all_colored": "r1_sweep_traffic_cfg2_colored.json"}
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", name.get(args.plan, ""))
+    if args.cfg != 2 or any(args.grid) or args.plan not in name or not os.path.exists(path):
         return None
     try:
         return float(json.load(open(path))["total_dram_bytes"])
