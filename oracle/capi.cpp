@@ -38,16 +38,17 @@ extern "C" {
 const char* oracle_last_error() { return g_err.c_str(); }
 
 // Problem from a BASELINE config (id 1..5) with optional grid override (0 = keep).
-int oracle_problem_config_plan(int id, long long nx, long long ny, long long nz, int merge_all_axes, void** out);
+int oracle_problem_config_plan(int id, long long nx, long long ny, long long nz, int plan_kind, void** out);
 int oracle_problem_config(int id, long long nx, long long ny, long long nz, void** out) {
   return oracle_problem_config_plan(id, nx, ny, nz, 0, out);
 }
 
-// Same with the plan family (0 = reference geometric_block_ordering, 1 = all axes merge per level).
-int oracle_problem_config_plan(int id, long long nx, long long ny, long long nz, int merge_all_axes, void** out) {
+// Same with the plan family (0 = reference geometric_block_ordering, 1 = all axes merge per level,
+// 2 = all-axis merges with mod-3 colour-major cells).
+int oracle_problem_config_plan(int id, long long nx, long long ny, long long nz, int plan_kind, void** out) {
   try {
     ProblemConfig c = baseline_config(id);
-    c.plan_kind = merge_all_axes;
+    c.plan_kind = plan_kind;
     if (nx > 0) c.nx = nx;
     if (ny > 0) c.ny = ny;
     if (nz > 0 && c.dims == 3) c.nz = nz;
