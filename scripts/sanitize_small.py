@@ -1,4 +1,4 @@
-"""One small factorization + apply for compute-sanitizer runs (development tool):
+"""One small factorization + apply (development tool for debug builds with device asserts):
 python scripts/sanitize_small.py [cfg] [n] [plan]"""
 import os
 import sys
