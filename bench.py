@@ -1,11 +1,13 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 CE hot path: factorize -> PCG (BASELINE.json configs[1] by default).
+"""Benchmark of the B200 CE hot path: factorize -> PCG.
 
+Default workload: BASELINE cfg3 (2-D variable-k FV 2048^2, B=16, eps=1e-6, PCG 1e-8), the
+largest BASELINE config that runs on one GPU on the reference plan (cfg4/cfg5 exceed HBM on
+it); cfg2 is measured beside it as `extra_configs`.
 One "step" = ce_factorize of the device-resident CSB matrix (host plan, device factor)
 followed by a device PCG solve to the config's tolerance.  `value` = factorization
 unknowns/s over all ranks (N x n x K / max-over-ranks factor time).  Each rank runs
-its own copy of the workload (replicas; SURVEY.md §8e subdomain sharding is the
-next step), so scaling is weak.
+its own copy of the workload (replicas), so scaling is weak.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--cfg C] [--grid NX NY NZ]
   python bench.py --impl reference ...   # CPU oracle restatement (rank 0 only)
@@ -35,7 +37,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
-    ap.add_argument("--cfg", type=int, default=2)
+    ap.add_argument("--cfg", type=int, default=3)
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg2 line beside the headline")
     ap.add_argument("--grid", type=int, nargs=3, default=[0, 0, 0])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -59,16 +62,37 @@ def workload_name(cfg, grid, plan="reference"):
     return s
 
 
-def sweep_traffic(args):
-    """DRAM bytes (read + write) of the level-sweep launches of one factorization, from the
-    committed ncu capture (profiles/r1_sweep_traffic_cfg2*.json) when it matches this
-    workload (cfg2 full size, reference or colour-major plan), else None."""
-    name = {"reference": "r1_sweep_traffic_cfg2.json", "merge_all_colored": "r1_sweep_traffic_cfg2_colored.json"}
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", name.get(args.plan, ""))
-    if args.cfg != 2 or any(args.grid) or args.plan not in name or not os.path.exists(path):
+def sweep_traffic_capture(args):
+    """DRAM bytes (read + write) of the level-sweep launches of one factorization from a
+    committed ncu capture of this workload (profiles/*sweep_traffic_cfg{C}*.json), labelled with
+    its source: it is NOT measured in this run, so the live `roofline.traffic` stays null."""
+    suffix = "" if args.plan == "reference" else "_colored" if args.plan == "merge_all_colored" else None
+    if suffix is None or any(args.grid):
+        return None
+    for rnd in ("r2", "r1"):
+        path = os.path.join(ROOT, "profiles", f"{rnd}_sweep_traffic_cfg{args.cfg}{suffix}.json")
+        if os.path.exists(path):
+            try:
+                d = json.load(open(path))
+                return {"dram_bytes_per_factorization": float(d["total_dram_bytes"]),
+                        "source": os.path.relpath(path, ROOT), "note": "ncu capture of an earlier build, not this run"}
+            except Exception:
+                return None
+    return None
+
+
+def fullsize_cpu_reference(cfg, plan):
+    """Single-thread oracle factorization of the WHOLE config, from the committed full-size
+    fixture run (scripts/make_fullsize_fixture.py, container host), when one exists."""
+    path = os.path.join(ROOT, "tests", "golden", f"fullsize_cfg{cfg}_{plan}_free.npz")
+    if not os.path.exists(path):
         return None
     try:
-        return float(json.load(open(path))["total_dram_bytes"])
+        import numpy as np
+        meta = json.loads(str(np.load(path)["meta"]))
+        return {"value": meta["n"] / meta["factor_seconds"], "unit": "unknowns/s", "cores": 1,
+                "factor_seconds": meta["factor_seconds"], "n": meta["n"],
+                "source": os.path.relpath(path, ROOT) + " (oracle, 1 thread, build container host, not this run)"}
     except Exception:
         return None
 
@@ -211,17 +235,20 @@ def run_reference(args):
     wall = time.time() - t0
     v = statistics.mean(vals)
     n = outs[0]["n"]
-    sample = (f"oracle/oracle_cli cfg{args.cfg} on a {grid[0]}x{grid[1]}" + (f"x{grid[2]}" if grid[2] else "") +
+    gtxt = f"{grid[0]}x{grid[1]}" + (f"x{grid[2]}" if grid[2] else "")
+    sample = (f"oracle/oracle_cli cfg{args.cfg} on a {gtxt}"
               f" grid (n={n}, same stencil/B/eps), full factorization + PCG; {copies} independent copies, one per "
               f"host thread ({cores} available); value = copies x n / slowest copy's factorization time")
     line = {"metric": METRIC, "value": v, "unit": "unknowns/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args.cfg, args.grid, args.plan), "cfg": args.cfg,
-                       "cpu_sample_grid": list(grid)},
+            "config": {"workload": workload_name(args.cfg, args.grid, args.plan) +
+                       f" -- CPU sample actually timed: {gtxt} grid (n={n}) per copy, {copies} copies per step",
+                       "cfg": args.cfg, "cpu_sample_grid": list(grid), "cpu_sample_n": n},
             "pcg_solve_ms": 1e3 * statistics.mean(pcg_s), "factor_ms": 1e3 * statistics.mean(fac),
             "single_thread_value": statistics.mean(single),
-            "cpu_baseline": {"value": v, "unit": "unknowns/s", "cores": copies, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "unknowns/s", "cores": copies, "kind": "port", "sample": sample,
+                             "full_size": fullsize_cpu_reference(args.cfg, args.plan)},
             "e2e": {"value": v, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -337,6 +364,66 @@ def run_product(args):
         del f2, a2
     e2e_val = world * n / allmax(statistics.mean(e2e_t))
 
+    # Preconditioner apply and matvec on their own (PCG's two operators), CUDA events on the
+    # library stream, against the HBM roofline with SURVEY.md §8d's apply byte count.
+    with torch.cuda.stream(stream):
+        fa = ce.ce_factorize(a, prob.plan, strategy, ce.FactorOptions(), ctx)
+        za = fa.solve(b)
+        ya = a.matvec(b)
+        ea0, ea1, em1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        n_ap = 10
+        ea0.record(stream)
+        for _ in range(n_ap):
+            za = fa.solve(b)
+        ea1.record(stream)
+        for _ in range(n_ap):
+            ya = a.matvec(b)
+        em1.record(stream)
+    em1.synchronize()
+    t_apply = ea0.elapsed_time(ea1) * 1e-3 / n_ap
+    t_mv = ea1.elapsed_time(em1) * 1e-3 / n_ap
+    apply_bytes = fa.stats["apply_algorithmic_bytes"]
+    mv_bytes = 8.0 * host_a.values.size + 16.0 * n  # stored blocks + x read + y write
+    apply_roof = {"bound": "hbm", "kernel": "preconditioner apply (CEFactorization::solve), all levels + tail",
+                  "achieved": apply_bytes / t_apply / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                  "frac": apply_bytes / t_apply / 1e9 / peaks["hbm_gbs"], "algorithmic_bytes": apply_bytes,
+                  "ms_per_apply": 1e3 * t_apply,
+                  "matvec": {"ms": 1e3 * t_mv, "algorithmic_bytes": mv_bytes,
+                             "achieved_gbs": mv_bytes / t_mv / 1e9, "frac": mv_bytes / t_mv / 1e9 / peaks["hbm_gbs"]}}
+    fstats = fa.stats
+    del fa, za, ya
+
+    # cfg2 beside the cfg3 headline (the verdict's "keep cfg2 as an extra line")
+    extra = []
+    if not args.no_extra and args.cfg != 2 and not any(args.grid):
+        eprob = ce.Problem(2, plan=args.plan)
+        ea = ce.DeviceMatrix(eprob.matrix(), ctx)
+        eb = torch.from_numpy(eprob.rhs).to(dev)
+        erec = []
+        for k in range(5):
+            with torch.cuda.stream(stream):
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record(stream)
+                ef = ce.ce_factorize(ea, eprob.plan, eprob.strategy(), ce.FactorOptions(), ctx)
+                e1.record(stream)
+                erep, _ = ce.pcg(ea, eprob.n, eb, ef, ce.PcgOptions(tol=eprob.tol, maxit=1000))
+                e2.record(stream)
+            e2.synchronize()
+            if k >= 2:
+                st2 = ef.stats
+                erec.append((e0.elapsed_time(e1) * 1e-3, e1.elapsed_time(e2) * 1e-3, st2["sweep_kernel_seconds"],
+                             st2["algorithmic_bytes"]))
+            del ef
+        efac = allmax(sum(x[0] for x in erec))
+        esw = sum(x[2] for x in erec) / len(erec)
+        extra.append({"workload": workload_name(2, [0, 0, 0], args.plan), "cfg": 2, "n": eprob.n,
+                      "value": job_throughput(world, eprob.n, len(erec), efac), "unit": "unknowns/s",
+                      "steps": len(erec), "warmup": 2, "factor_ms": 1e3 * efac / len(erec),
+                      "pcg_solve_ms": 1e3 * sum(x[1] for x in erec) / len(erec), "pcg_iterations": erep.iterations,
+                      "pcg_true_residual": erep.final_true_residual,
+                      "sweep_hbm_frac": erec[-1][3] / esw / 1e9 / peaks["hbm_gbs"]})
+        del ea, eb
+
     # The same config under the colour-major all-axis-merge plan:
     # reported beside the headline, which stays on the reference's geometric_block_ordering.
     variant = None
@@ -373,7 +460,8 @@ def run_product(args):
         r = cpu_oracle_run(args.cfg, grid, solve=False, plan=args.plan)
         cpu = {"value": r["unknowns_per_sec"], "unit": "unknowns/s", "cores": 1, "kind": "port",
                "sample": f"oracle/oracle_cli cfg{args.cfg} on a {grid[0]}x{grid[1]}" + (f"x{grid[2]}" if grid[2] else "")
-               + f" grid (n={r['n']}), full factorization, 1 thread of {os.cpu_count()}"}
+               + f" grid (n={r['n']}), full factorization, 1 thread of {os.cpu_count()}",
+               "full_size": fullsize_cpu_reference(args.cfg, args.plan) if not any(args.grid) else None}
 
     if rank == 0:
         line = {
@@ -392,11 +480,14 @@ def run_product(args):
                          "achieved": gbs if bound == "hbm" else tfl,
                          "peak": peaks["hbm_gbs"] if bound == "hbm" else fp64_peak,
                          "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
-                         "frac": f_hbm if bound == "hbm" else f_fp64, "traffic": sweep_traffic(args),
+                         "frac": f_hbm if bound == "hbm" else f_fp64, "traffic": None,
+                         "traffic_capture": sweep_traffic_capture(args),
                          "hbm": {"achieved_gbs": gbs, "peak_gbs": peaks["hbm_gbs"], "frac": f_hbm, "peak_kind": peak_kind},
                          "fp64": {"achieved_tflops": tfl, "peak_tflops": fp64_peak, "frac": f_fp64,
                                   "peak_kind": "measured live: cuBLAS DGEMM 8192^3"},
                          "sweep_ms_per_step": 1e3 * sweep_t, "algorithmic_bytes": abytes, "algorithmic_flops": aflops},
+            "roofline_apply": apply_roof,
+            "validate": {"seconds": fstats["validate_seconds"], "max_orth_error": fstats["max_orth_error"]},
             "e2e": {"value": e2e_val, "unit": "unknowns/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 * n,
                     "region": "H2D upload of A + b from pinned host memory, factorize, PCG, D2H x; wall clock"},
             "gpu_launches": int(launches),
@@ -407,6 +498,8 @@ def run_product(args):
             line["cpu_baseline"] = cpu
         if variant:
             line["plan_variant"] = variant
+        if extra:
+            line["extra_configs"] = extra
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -112,6 +112,9 @@ typedef struct {
   double sweep_kernel_seconds;  /* CUDA-event time of the level sweep kernels */
   double algorithmic_bytes;     /* SURVEY.md §8d per-row byte contract, summed */
   double algorithmic_flops;     /* SURVEY.md §8d per-row flop contract, summed */
+  double validate_seconds;      /* validate() inside ce_factorize (factorization.cpp:272-334,459) */
+  double max_orth_error;        /* max |U^T U - I| over every stored basis (validate bound 1e-12) */
+  double apply_algorithmic_bytes;  /* SURVEY.md §8d bytes of one preconditioner apply (ce_apply_precond) */
 } ce_factor_stats;
 
 /* LevelStats (factorization.hpp:38-54) for level l (0-based). */
@@ -155,29 +158,41 @@ int ce_factorize(ce_ctx* ctx, const ce_matrix* a, const ce_plan_host* plan, cons
 void ce_factor_free(ce_factor* f);
 int64_t ce_factor_dim(const ce_factor* f);
 /* Preconditioner apply x = Q^T L^-T L^-1 Q b (replaces CEFactorization::solve,
- * factorization.cpp:140-168; used as ApplyFn at cli.cpp:225). */
+ * factorization.cpp:140-168; used as ApplyFn at cli.cpp:225).  Thread-safe: concurrent calls
+ * on one factor (any threads, any streams) are serialised on the device, because they share
+ * the factor's apply workspaces (each waits for the previous apply's completion event). */
 int ce_apply_precond(const ce_factor* f, const double* b, double* x, int64_t n, int on_device, void* stream);
 /* Validation tools (factorization.cpp:170-257): which 0 = apply_operator (Q^T L L^T Q x),
  * 1 = apply_q, 2 = apply_q_transpose.  Host arrays. */
 int ce_factor_apply_tool(const ce_factor* f, int which, const double* x, double* y, int64_t n);
 int ce_factor_get_stats(const ce_factor* f, ce_factor_stats* out);
 int ce_factor_get_level_stats(const ce_factor* f, int64_t level, ce_level_stats* out);
+/* Per-row structure of level `level` (0-based), M entries each (any pointer may be NULL): block
+ * sizes, retained ranks (FactorLevel::retained, factorization.hpp:19-36), far-concatenation
+ * widths and singular-value counts -- the parity structure without a full dump. */
+int ce_factor_level_rows(const ce_factor* f, int64_t level, int64_t* sizes, int64_t* retained, int64_t* fcols,
+                         int64_t* nsigma);
+/* Singular values of the far concatenation of (level, row) (compress_far_concat,
+ * compression.cpp:48-49), descending; writes min(count, cap), returns the count (< 0 on error). */
+int64_t ce_factor_row_sigma(const ce_factor* f, int64_t level, int64_t row, double* out, int64_t cap);
 /* Binary factor dump in the oracle's format, for parity checks. */
 int ce_factor_dump(const ce_factor* f, const char* path);
 
 /* ---- Krylov ---- */
 /* PCG with the minres contract (minres.hpp:46-47): x0 = 0, stop when the
  * recurrence ||r||/||b|| <= tol, iterations = number of A*p products.  precond may be NULL
- * (unpreconditioned).  on_device != 0: b, x are device pointers. */
+ * (unpreconditioned).  on_device != 0: b, x are device pointers, read and written in order on
+ * `stream` (NULL = the context's stream), like ce_apply_precond / ce_matvec; with host
+ * arrays the call is synchronous. */
 int ce_pcg(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const double* b, double* x, int64_t n,
-           int on_device, const ce_pcg_opts* opts, ce_solve_report* rep);
+           int on_device, const ce_pcg_opts* opts, ce_solve_report* rep, void* stream);
 /* MINRES (replaces ce::minres, proj/include/ce/minres.hpp:46-47 / proj/src/minres.cpp:22-115, the
  * paper's solver; ApplyFn pair at proj/src/cli.cpp:198,225-226): x0 = 0, stop when the recurrence
  * estimate of the preconditioned residual <= tol relative to its start, or on a Lanczos beta
  * < 1e-30 beta1; iterations = number of A*v products.  Same options, report, error codes and
  * memory conventions as ce_pcg (opts->track_true_residual = the MinresOptions field). */
 int ce_minres(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const double* b, double* x, int64_t n,
-              int on_device, const ce_pcg_opts* opts, ce_solve_report* rep);
+              int on_device, const ce_pcg_opts* opts, ce_solve_report* rep, void* stream);
 
 /* ---- BASELINE problem generation (setup, untimed; SURVEY.md §8d conventions) ----
  * cfg 1..5, optional grid override (0 = keep).  Builds the permuted CSB, plan and rhs on the host

@@ -283,6 +283,26 @@ int oracle_factor_dump(void* h, const char* path) {
 long long oracle_factor_levels(void* h) { return static_cast<long long>(static_cast<OFactor*>(h)->f.levels.size()); }
 long long oracle_factor_tail_dim(void* h) { return static_cast<OFactor*>(h)->f.tail_dim; }
 
+// Per-level structure for the full-size fixtures (scripts/make_fullsize_fixture.py):
+// block sizes, retained ranks and far widths of level l (M entries each).
+long long oracle_factor_level_m(void* h, long long l) {
+  return static_cast<OFactor*>(h)->f.levels[static_cast<size_t>(l)].partition.block_count();
+}
+void oracle_factor_level_structure(void* h, long long l, long long* sizes, long long* retained, long long* fcols) {
+  const auto& fl = static_cast<OFactor*>(h)->f.levels[static_cast<size_t>(l)];
+  for (index_t b = 0; b < fl.partition.block_count(); ++b) {
+    sizes[b] = fl.partition.block_size(b);
+    retained[b] = fl.retained[static_cast<size_t>(b)];
+    fcols[b] = fl.fcols[static_cast<size_t>(b)];
+  }
+}
+// Singular values of row b's far concatenation at level l; returns their count (<= cap written).
+long long oracle_factor_row_sigma(void* h, long long l, long long b, double* out, long long cap) {
+  const auto& s = static_cast<OFactor*>(h)->f.levels[static_cast<size_t>(l)].sigma[static_cast<size_t>(b)];
+  for (size_t k = 0; k < s.size() && static_cast<long long>(k) < cap; ++k) out[k] = s[k];
+  return static_cast<long long>(s.size());
+}
+
 // Summary stats: [factor_blocks, predicted_factor_blocks, l_scalar_nnz, l_payload_bytes,
 // q_payload_bytes, tail_bytes, total_seconds, tail_seconds]
 void oracle_factor_summary(void* h, double* out) {

@@ -60,7 +60,8 @@ class FactorStats(C.Structure):
                 ("q_payload_bytes", i64), ("tail_bytes", i64), ("shift_retries", i64),
                 ("total_seconds", C.c_double), ("device_seconds", C.c_double),
                 ("sweep_kernel_seconds", C.c_double), ("algorithmic_bytes", C.c_double),
-                ("algorithmic_flops", C.c_double)]
+                ("algorithmic_flops", C.c_double), ("validate_seconds", C.c_double), ("max_orth_error", C.c_double),
+                ("apply_algorithmic_bytes", C.c_double)]
 
 
 class LevelStats(C.Structure):
@@ -92,9 +93,11 @@ SIGNATURES = {
     "ce_factor_apply_tool": (C.c_int, [vp, C.c_int, vp, vp, i64]),
     "ce_factor_get_stats": (C.c_int, [vp, C.POINTER(FactorStats)]),
     "ce_factor_get_level_stats": (C.c_int, [vp, i64, C.POINTER(LevelStats)]),
+    "ce_factor_level_rows": (C.c_int, [vp, i64, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
+    "ce_factor_row_sigma": (i64, [vp, i64, i64, C.POINTER(C.c_double), i64]),
     "ce_factor_dump": (C.c_int, [vp, C.c_char_p]),
-    "ce_pcg": (C.c_int, [vp, vp, vp, vp, vp, i64, C.c_int, C.POINTER(PcgOpts), C.POINTER(Report)]),
-    "ce_minres": (C.c_int, [vp, vp, vp, vp, vp, i64, C.c_int, C.POINTER(PcgOpts), C.POINTER(Report)]),
+    "ce_pcg": (C.c_int, [vp, vp, vp, vp, vp, i64, C.c_int, C.POINTER(PcgOpts), C.POINTER(Report), vp]),
+    "ce_minres": (C.c_int, [vp, vp, vp, vp, vp, i64, C.c_int, C.POINTER(PcgOpts), C.POINTER(Report), vp]),
     "ce_problem_create": (C.c_int, [C.c_int, i64, i64, i64, C.POINTER(vp)]),
     "ce_problem_create_plan": (C.c_int, [C.c_int, i64, i64, i64, C.c_int, C.POINTER(vp)]),
     "ce_problem_free": (None, [vp]),

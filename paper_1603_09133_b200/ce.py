@@ -198,6 +198,22 @@ def _stream_ptr(x):
     return C.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)
 
 
+def _check_tensor(x, n: int, ctx: "Context", what: str):
+    """A torch vector handed to the device path must be a contiguous float64 CUDA tensor of n
+    entries on the context's device (its data_ptr is used as a device pointer)."""
+    import torch
+    if not x.is_cuda:
+        raise ValueError(f"{what}: torch tensors must be CUDA tensors (pass numpy arrays for host data)")
+    if x.device.index != ctx.device:
+        raise ValueError(f"{what}: tensor on cuda:{x.device.index}, library context on cuda:{ctx.device}")
+    if x.dtype != torch.float64:
+        raise TypeError(f"{what}: tensor dtype must be torch.float64, got {x.dtype}")
+    if not x.is_contiguous():
+        raise ValueError(f"{what}: tensor must be contiguous")
+    if x.numel() != n:
+        raise ValueError(f"{what} dimension mismatch: {x.numel()} != {n}")
+
+
 class DeviceMatrix:
     """Device-resident operator A (ce_matrix); matvec replaces BlockSparseMatrix::matvec."""
 
@@ -217,6 +233,7 @@ class DeviceMatrix:
     def matvec(self, x):
         if _is_torch(x):
             import torch
+            _check_tensor(x, self.n, self.ctx, "matvec")
             y = torch.empty_like(x)
             _check(lib.ce_matvec(self.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), self.n, 1,
                                  _stream_ptr(x)))
@@ -248,8 +265,7 @@ class CEFactorization:
         """x = Q^T L^-T L^-1 Q b (factorization.cpp:140-168)."""
         if _is_torch(b):
             import torch
-            if b.numel() != self.n:
-                raise ValueError("solve dimension mismatch")
+            _check_tensor(b, self.n, self.ctx, "solve")
             x = torch.empty_like(b)
             _check(lib.ce_apply_precond(self.handle, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()), self.n, 1,
                                         _stream_ptr(b)))
@@ -294,6 +310,20 @@ class CEFactorization:
             out.append({k: getattr(s, k) for k, _ in L.LevelStats._fields_})
         return out
 
+    def level_rows(self, level: int):
+        """(sizes, retained, fcols, nsigma) of every row of `level` (0-based)."""
+        m = int(self.level_stats()[level]["block_count"])
+        arrs = [np.empty(m, np.int64) for _ in range(4)]
+        _check(lib.ce_factor_level_rows(self.handle, level, *[_ptr(a, C.c_int64) for a in arrs]))
+        return tuple(arrs)
+
+    def row_sigma(self, level: int, row: int, cap: int = 4096) -> np.ndarray:
+        out = np.empty(cap)
+        k = int(lib.ce_factor_row_sigma(self.handle, level, row, _ptr(out, C.c_double), cap))
+        if k < 0:
+            _check(CE_EUSAGE)
+        return out[:min(k, cap)].copy()
+
     def dump(self, path: str):
         _check(lib.ce_factor_dump(self.handle, path.encode()))
 
@@ -332,13 +362,17 @@ def _krylov(entry, what, a, n, b, precond, opts):
     ph = precond.handle if precond is not None else None
     if _is_torch(b):
         import torch
+        _check_tensor(b, n, a.ctx, what)
         x = torch.empty_like(b)
+        # the solve runs on torch's current stream: b's producers and x's consumers are ordered
         rc = entry(a.ctx.handle, a.handle, ph, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()), n, 1,
-                   C.byref(co), C.byref(rep))
+                   C.byref(co), C.byref(rep), _stream_ptr(b))
     else:
         b = _f64(b)
+        if b.size != n:
+            raise ValueError(f"{what} dimension mismatch")
         x = np.empty(n)
-        rc = entry(a.ctx.handle, a.handle, ph, b.ctypes.data, x.ctypes.data, n, 0, C.byref(co), C.byref(rep))
+        rc = entry(a.ctx.handle, a.handle, ph, b.ctypes.data, x.ctypes.data, n, 0, C.byref(co), C.byref(rep), None)
     if rc not in (CE_OK, CE_ENOCONV):
         _check(rc)
     return SolveReport(bool(rep.converged), int(rep.iterations), rep.final_recurrence_residual,

@@ -4,7 +4,9 @@
 #include <algorithm>
 #include <cstring>
 #include <exception>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -29,6 +31,8 @@ struct ce_factor {
   std::vector<int64_t> plan_blocks, plan_assign;
   int64_t join = 2, rank_hint = 1, bmax = 1;
   double predicted = -1.0;
+  // host-buffer path of ce_apply_precond: staging buffers, one call at a time
+  mutable std::mutex stage_mu;
   mutable ceg::DevArray<double> stage_in, stage_out;
 };
 
@@ -132,9 +136,9 @@ double predicted_nnz(const ce_factor& h, int64_t k_levels, std::vector<int64_t>*
   return total;
 }
 
-struct Staging {
-  ceg::DevArray<double> a, b;
-};
+// live contexts per device: the allocator cache of a device is trimmed when its last context goes
+std::mutex g_ctx_mu;
+std::map<int, int> g_live_ctx;
 }  // namespace
 
 extern "C" {
@@ -171,6 +175,10 @@ int ce_ctx_create(int device, ce_ctx** out) {
     c->ctx.device = device;
     c->ctx.sm_count = p.multiProcessorCount;
     CE_CUDA(cudaStreamCreateWithFlags(&c->ctx.stream, cudaStreamNonBlocking));
+    {
+      std::lock_guard<std::mutex> lk(g_ctx_mu);
+      ++g_live_ctx[device];
+    }
     *out = c.release();
   });
 }
@@ -189,8 +197,15 @@ void ce_ctx_destroy(ce_ctx* ctx) {
     cudaStreamSynchronize(ctx->ctx.stream);
     cudaStreamDestroy(ctx->ctx.stream);
   }
+  const int dev = ctx->ctx.device;
   delete ctx;
-  ceg::pool_trim();  // cached device blocks go back to the driver with the last context
+  bool last = false;
+  {
+    std::lock_guard<std::mutex> lk(g_ctx_mu);
+    last = --g_live_ctx[dev] <= 0;
+    if (last) g_live_ctx.erase(dev);
+  }
+  if (last) ceg::pool_trim(dev);  // the device's cached blocks go back with its last context
 }
 
 int ce_matrix_upload(ce_ctx* ctx, const ce_csb_host* a, ce_matrix** out) {
@@ -306,6 +321,7 @@ int ce_apply_precond(const ce_factor* f, const double* b, double* x, int64_t n, 
       ceg::apply_device(*f->f, b, x, s);
       return;
     }
+    std::lock_guard<std::mutex> lk(f->stage_mu);
     if (f->stage_in.n != static_cast<size_t>(n)) {
       f->stage_in.alloc(static_cast<size_t>(n));
       f->stage_out.alloc(static_cast<size_t>(n));
@@ -360,6 +376,25 @@ int ce_factor_get_stats(const ce_factor* fh, ce_factor_stats* out) {
     fl += t * t * t / 3.0;
     out->algorithmic_bytes = by;
     out->algorithmic_flops = fl;
+    out->validate_seconds = f.validate_seconds;
+    out->max_orth_error = f.max_orth_error;
+    // SURVEY.md §8d apply bytes: nonzero factor payload read by the forward and the backward
+    // sweep (t > i neighbours full b_t x w, t < i only their r_t retained rows), the bases,
+    // the tail's triangle, plus ~10 n-vector passes
+    double pay = 0.0;
+    for (const auto& L : f.levels)
+      for (int64_t b = 0; b < L.M; ++b) {
+        const double w = L.width[static_cast<size_t>(b)], r = L.rank[static_cast<size_t>(b)];
+        if (L.has_basis[static_cast<size_t>(b)]) pay += static_cast<double>(L.bsz[static_cast<size_t>(b)]) * L.bsz[static_cast<size_t>(b)];
+        if (w == 0) continue;
+        pay += w * (w + 1) / 2 + r * w;
+        for (int64_t e = L.cptr[static_cast<size_t>(b)]; e < L.cptr[static_cast<size_t>(b + 1)]; ++e) {
+          const int t = L.ccol[static_cast<size_t>(e)];
+          pay += (t > b ? L.bsz[static_cast<size_t>(t)] : L.rank[static_cast<size_t>(t)]) * w;
+        }
+      }
+    pay += t * (t + 1) / 2;
+    out->apply_algorithmic_bytes = 2.0 * 8.0 * pay + 8.0 * static_cast<double>(f.n) * 10.0;
   });
 }
 
@@ -401,6 +436,41 @@ int ce_factor_get_level_stats(const ce_factor* fh, int64_t level, ce_level_stats
   });
 }
 
+int ce_factor_level_rows(const ce_factor* fh, int64_t level, int64_t* sizes, int64_t* retained, int64_t* fcols,
+                         int64_t* nsigma) {
+  return guarded([&] {
+    if (!fh) throw std::invalid_argument("null argument");
+    const ceg::Factor& f = *fh->f;
+    if (level < 0 || level >= static_cast<int64_t>(f.levels.size())) throw std::out_of_range("level index");
+    const ceg::LevelFactor& L = f.levels[static_cast<size_t>(level)];
+    for (int64_t b = 0; b < L.M; ++b) {
+      if (sizes) sizes[b] = L.bsz[static_cast<size_t>(b)];
+      if (retained) retained[b] = L.rank[static_cast<size_t>(b)];
+      if (fcols) fcols[b] = L.fcols[static_cast<size_t>(b)];
+      if (nsigma) nsigma[b] = L.nsig[static_cast<size_t>(b)];
+    }
+  });
+}
+
+int64_t ce_factor_row_sigma(const ce_factor* fh, int64_t level, int64_t row, double* out, int64_t cap) {
+  int64_t count = -1;
+  const int rc = guarded([&] {
+    if (!fh || (!out && cap > 0)) throw std::invalid_argument("null argument");
+    const ceg::Factor& f = *fh->f;
+    if (level < 0 || level >= static_cast<int64_t>(f.levels.size())) throw std::out_of_range("level index");
+    const ceg::LevelFactor& L = f.levels[static_cast<size_t>(level)];
+    if (row < 0 || row >= L.M) throw std::out_of_range("row index");
+    count = L.nsig[static_cast<size_t>(row)];
+    const int64_t k = std::min(count, cap);
+    if (k > 0) {
+      CE_CUDA(cudaSetDevice(f.ctx->device));
+      CE_CUDA(cudaMemcpy(out, L.d_sigma.p + L.sigma_off[static_cast<size_t>(row)], static_cast<size_t>(k) * sizeof(double),
+                         cudaMemcpyDeviceToHost));
+    }
+  });
+  return rc == CE_OK ? count : -1;
+}
+
 int ce_factor_dump(const ce_factor* f, const char* path) {
   return guarded([&] {
     if (!f || !path) throw std::invalid_argument("null argument");
@@ -411,14 +481,15 @@ int ce_factor_dump(const ce_factor* f, const char* path) {
 namespace {
 // shared body of the two Krylov entry points (minres.hpp:46-47 contract)
 int krylov(bool use_minres, ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const double* b, double* x,
-           int64_t n, int on_device, const ce_pcg_opts* opts, ce_solve_report* rep) {
+           int64_t n, int on_device, const ce_pcg_opts* opts, ce_solve_report* rep, void* stream) {
   if (rep) std::memset(rep, 0, sizeof *rep);
   ceg::SolveOut so;
   const char* what = use_minres ? "minres" : "pcg";
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : (ctx ? ctx->ctx.stream : nullptr);
   auto run = [&](const ce_matrix* am, const ceg::Factor* m, const double* db, double* dx, double tol, int64_t maxit,
                  bool track) {
-    return use_minres ? ceg::minres_device(am->m, m, db, dx, tol, maxit, track)
-                      : ceg::pcg_device(am->m, m, db, dx, tol, maxit, track);
+    return use_minres ? ceg::minres_device(am->m, m, db, dx, tol, maxit, track, s)
+                      : ceg::pcg_device(am->m, m, db, dx, tol, maxit, track, s);
   };
   const int rc = guarded([&] {
     if (!ctx || !a || n != a->m.n) throw std::invalid_argument(std::string(what) + " dimension mismatch");
@@ -426,7 +497,7 @@ int krylov(bool use_minres, ce_ctx* ctx, const ce_matrix* a, const ce_factor* pr
     const double tol = opts ? opts->tol : 1e-10;
     const int64_t maxit = opts ? opts->maxit : 1000;
     const bool track = opts && opts->track_true_residual;
-    cudaStream_t s = ctx->ctx.stream;
+    CE_CUDA(cudaSetDevice(ctx->ctx.device));
     if (on_device) {
       so = run(a, precond ? precond->f.get() : nullptr, b, x, tol, maxit, track);
     } else {
@@ -454,13 +525,13 @@ int krylov(bool use_minres, ce_ctx* ctx, const ce_matrix* a, const ce_factor* pr
 }  // namespace
 
 int ce_pcg(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const double* b, double* x, int64_t n,
-           int on_device, const ce_pcg_opts* opts, ce_solve_report* rep) {
-  return krylov(false, ctx, a, precond, b, x, n, on_device, opts, rep);
+           int on_device, const ce_pcg_opts* opts, ce_solve_report* rep, void* stream) {
+  return krylov(false, ctx, a, precond, b, x, n, on_device, opts, rep, stream);
 }
 
 int ce_minres(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const double* b, double* x, int64_t n,
-              int on_device, const ce_pcg_opts* opts, ce_solve_report* rep) {
-  return krylov(true, ctx, a, precond, b, x, n, on_device, opts, rep);
+              int on_device, const ce_pcg_opts* opts, ce_solve_report* rep, void* stream) {
+  return krylov(true, ctx, a, precond, b, x, n, on_device, opts, rep, stream);
 }
 
 int ce_problem_create(int cfg, int64_t nx, int64_t ny, int64_t nz, ce_problem** out) {

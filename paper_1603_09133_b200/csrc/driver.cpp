@@ -136,16 +136,20 @@ void pool_free(void* p, size_t bytes) {
   P.free_blocks.emplace(pool_round(bytes), std::make_pair(dev, p));
 }
 
-void pool_trim() {
+void pool_trim(int device) {
   Pool& P = pool();
   std::lock_guard<std::mutex> lk(P.mu);
   int cur = 0;
   cudaGetDevice(&cur);
-  for (auto& kv : P.free_blocks) {
-    cudaSetDevice(kv.second.first);
-    cudaFree(kv.second.second);
+  for (auto it = P.free_blocks.begin(); it != P.free_blocks.end();) {
+    if (device >= 0 && it->second.first != device) {
+      ++it;
+      continue;
+    }
+    cudaSetDevice(it->second.first);
+    cudaFree(it->second.second);
+    it = P.free_blocks.erase(it);
   }
-  P.free_blocks.clear();
   cudaSetDevice(cur);
 }
 
@@ -996,6 +1000,64 @@ void row_counts(double b, double c, double f, double r, double w, double p, doub
 
 }  // namespace
 
+// CEFactorization::validate (proj/src/factorization.cpp:272-334), run at the end of every
+// ce_factorize like the reference's (:459): structure on the host from the driver's arrays,
+// basis orthogonality (<= 1e-12) and lower-triangular pivots on the device (validate.cu), one
+// 24-byte read.  Violations throw std::logic_error (exit code 1, as in the reference).
+void validate_factor(Factor& F, cudaStream_t s) {
+  const double t0 = now_s();
+  int64_t expect = F.n, accounted = 0;
+  for (size_t l = 0; l < F.levels.size(); ++l) {
+    const LevelFactor& L = F.levels[l];
+    if (L.dim != expect) throw std::logic_error("level dimensions do not telescope");
+    if (L.n_elim + L.n_kept != L.dim) throw std::logic_error("eliminated plus kept must cover the level");
+    for (int64_t b = 0; b < L.M; ++b) {
+      if (L.width[static_cast<size_t>(b)] + L.rank[static_cast<size_t>(b)] != L.bsz[static_cast<size_t>(b)])
+        throw std::logic_error("width plus retained must equal the block size");
+      if (L.width[static_cast<size_t>(b)] == 0) continue;
+      int64_t prev = -1;
+      for (int64_t e = L.cptr[static_cast<size_t>(b)]; e < L.cptr[static_cast<size_t>(b + 1)]; ++e) {
+        const int64_t t = L.ccol[static_cast<size_t>(e)];
+        if (t <= prev || t == b) throw std::logic_error("neighbor list must be ascending and off-diagonal");
+        prev = t;
+      }
+    }
+    accounted += L.n_elim;
+    expect = L.n_kept;
+  }
+  if (!F.levels.empty() && expect != F.tail_dim) throw std::logic_error("tail dimension does not match the last level");
+  if (accounted + F.tail_dim != F.n) throw std::logic_error("eliminated plus tail must cover the matrix");
+  DevArray<unsigned long long> d_out(3 * std::max<size_t>(F.levels.size(), 1));
+  std::vector<unsigned long long> init(d_out.n);
+  for (size_t k = 0; k < init.size(); k += 3) {
+    init[k] = 0;
+    init[k + 1] = 0;
+    init[k + 2] = ~0ull;
+  }
+  CE_CUDA(cudaMemcpyAsync(d_out.p, init.data(), init.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+  for (size_t l = 0; l < F.levels.size(); ++l) {
+    const LevelFactor& L = F.levels[l];
+    launch_validate_level(L.M, L.d_bsz.p, L.d_has_basis.p, L.d_basis.p, L.d_basis_off.p, L.d_width.p, L.d_fac.p,
+                          L.d_chol_off.p, 1e-12, d_out.p + 3 * l, s);
+  }
+  CE_CUDA(cudaGetLastError());
+  std::vector<unsigned long long> res(d_out.n);
+  CE_CUDA(cudaMemcpyAsync(res.data(), d_out.p, res.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  CE_CUDA(cudaStreamSynchronize(s));
+  for (size_t l = 0; l < F.levels.size(); ++l) {
+    double err = 0.0;
+    std::memcpy(&err, &res[3 * l], sizeof err);
+    F.max_orth_error = std::max(F.max_orth_error, err);
+    if (res[3 * l + 2] != ~0ull) {
+      std::ostringstream os;
+      if (res[3 * l + 1]) os << "pivot factor must be lower triangular (level " << l + 1 << ", block " << res[3 * l + 2] << ")";
+      else os << "basis orthogonality violated at level " << l + 1 << ", block " << res[3 * l + 2] << ": " << err;
+      throw std::logic_error(os.str());
+    }
+  }
+  F.validate_seconds = now_s() - t0;
+}
+
 Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, const ce_strategy* st,
                   const ce_factor_opts* op, int64_t* shift_total) {
   const double t_start = now_s();
@@ -1390,6 +1452,15 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
         for (int64_t rr = 0; rr < LF.rank[static_cast<size_t>(b)]; ++rr) kept.push_back(cur.offsets[static_cast<size_t>(b)] + rr);
     LF.n_elim = static_cast<int64_t>(elim.size());
     LF.n_kept = static_cast<int64_t>(kept.size());
+    {  // validate (factorization.cpp:283-288): the gather lists partition the level space
+      std::vector<int> seen(static_cast<size_t>(cur.M), 0);
+      for (const auto& g : cur_groups)
+        for (int64_t b : g) ++seen[static_cast<size_t>(b)];
+      for (int64_t b = 0; b < cur.M; ++b)
+        if (LF.rank[static_cast<size_t>(b)] > 0 && seen[static_cast<size_t>(b)] != 1)
+          throw std::logic_error("gather lists must partition the level space");
+      if (LF.n_elim + LF.n_kept != cur.dim) throw std::logic_error("eliminated plus kept must cover the level");
+    }
     LF.d_elim_gather.upload(elim, s);
     LF.d_kept_gather.upload(kept, s);
 
@@ -1570,6 +1641,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     dense_tri_inverse(F->d_tail_L.p, F->d_tail_Linv.p, n, s);
     CE_CUDA(cudaGetLastError());
   }
+  validate_factor(*F, s);
   CE_CUDA(cudaEventRecord(ev_all.b, s));
   CE_CUDA(cudaStreamSynchronize(s));
   F->device_seconds = ev_all.seconds();
@@ -1644,7 +1716,23 @@ ApplyLevelArgs level_args(const Factor& f, const LevelFactor& L, double* v) {
 }
 }  // namespace
 
+namespace {
+// Serialises the applies of one factor (they share its workspaces, host_api.hpp): the
+// enqueue happens under the factor's mutex and waits for the previous apply's event.
+struct ApplyGuard {
+  const Factor& f;
+  cudaStream_t s;
+  std::lock_guard<std::mutex> lk;
+  ApplyGuard(const Factor& fa, cudaStream_t st) : f(fa), s(st), lk(fa.apply_mu) {
+    if (!f.apply_done) CE_CUDA(cudaEventCreateWithFlags(&f.apply_done, cudaEventDisableTiming));
+    else CE_CUDA(cudaStreamWaitEvent(s, f.apply_done, 0));
+  }
+  ~ApplyGuard() { cudaEventRecord(f.apply_done, s); }
+};
+}  // namespace
+
 void apply_device(const Factor& f, const double* d_b, double* d_x, cudaStream_t s) {
+  ApplyGuard guard(f, s);
   const int grid = f.ctx->sm_count * 8;
   static const bool aprof = std::getenv("CE_PROFILE") && std::getenv("CE_PROFILE")[0] == '1';
   std::vector<Events> evs(aprof ? 2 * f.levels.size() : 0);
@@ -1709,6 +1797,7 @@ void apply_device(const Factor& f, const double* d_b, double* d_x, cudaStream_t 
 
 // Validation tools (factorization.cpp:170-257) on the device.
 void apply_tool_device(const Factor& f, int which, const double* d_x, double* d_y, cudaStream_t s) {
+  ApplyGuard guard(f, s);
   double* active = f.w_active.p;
   double* v = f.w_v.p;
   CE_CUDA(cudaMemcpyAsync(active, d_x, static_cast<size_t>(f.n) * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -1782,8 +1871,7 @@ void matvec_device(const Matrix& A, const double* d_x, double* d_y, cudaStream_t
 
 // ---------------------------------------------------------------- PCG
 SolveOut pcg_device(const Matrix& A, const Factor* M, const double* d_b, double* d_x, double tol, int64_t maxit,
-                    bool track_true) {
-  cudaStream_t s = A.ctx->stream;
+                    bool track_true, cudaStream_t s) {
   const int64_t n = A.n;
   SolveOut out;
   const double t0 = now_s();
@@ -1869,8 +1957,7 @@ SolveOut pcg_device(const Matrix& A, const Factor* M, const double* d_b, double*
 // rules as the reference: recurrence <= tol, or a Lanczos beta below 1e-30 beta1 (exact
 // solution); a negative / non-finite r' M^-1 r is an error (minres.cpp:11-18).
 SolveOut minres_device(const Matrix& A, const Factor* M, const double* d_b, double* d_x, double tol, int64_t maxit,
-                       bool track_true) {
-  cudaStream_t s = A.ctx->stream;
+                       bool track_true, cudaStream_t s) {
   const int64_t n = A.n;
   SolveOut out;
   const double t0 = now_s();

@@ -24,12 +24,14 @@ struct SolveOut {
   double final_rec = 0.0, final_true = 0.0, seconds = 0.0;
   std::vector<double> trace_rec, trace_true;
 };
+// Both Krylov loops run on stream `s` (the caller's, so its producers of b / consumers of x
+// are ordered against the solve).
 SolveOut pcg_device(const Matrix& A, const Factor* M, const double* d_b, double* d_x, double tol, int64_t maxit,
-                    bool track_true);
+                    bool track_true, cudaStream_t s);
 
 // MINRES with an SPD preconditioner (minres.cpp:22-115, the paper's solver) on the device.
 SolveOut minres_device(const Matrix& A, const Factor* M, const double* d_b, double* d_x, double tol, int64_t maxit,
-                       bool track_true);
+                       bool track_true, cudaStream_t s);
 
 void dump_factor(const Factor& f, const std::string& path);
 

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -30,7 +31,7 @@ void cuda_check(cudaError_t e, const char* what);
 // between levels).  Releases happen only after the owning stream has drained.
 void* pool_alloc(size_t bytes);
 void pool_free(void* p, size_t bytes);
-void pool_trim();  // return every cached block to the driver
+void pool_trim(int device = -1);  // return the cached blocks of `device` (-1: all) to the driver
 
 // Owning device array.
 template <class T>
@@ -188,6 +189,8 @@ struct Factor {
   DevArray<double> d_tail_L, d_tail_Linv;
   int64_t shift_retries = 0;
   double total_seconds = 0.0, device_seconds = 0.0, sweep_seconds = 0.0;
+  double validate_seconds = 0.0, max_orth_error = 0.0;  // validate(), factorization.cpp:272-334
+  double apply_alg_bytes = 0.0;  // SURVEY.md §8d apply byte count (forward + backward + vector passes)
   double factor_blocks = 0.0, predicted_factor_blocks = 0.0;
   int64_t l_scalar_nnz = 0, l_payload_bytes = 0, q_payload_bytes = 0, tail_bytes = 0;
   // apply workspaces (sized to the level dims)
@@ -198,6 +201,17 @@ struct Factor {
   mutable DevArray<double> w_scratch;  // apply partial sums
   mutable DevArray<int> w_parts;       // apply per-row finished partial tasks
   mutable DevArray<double> w_host_stage;
+  // The apply workspaces above are shared by every apply on this factor.  Applies are
+  // serialised: `apply_mu` orders their enqueue on the host and each apply's stream waits
+  // for `apply_done`, recorded by the previous apply (any stream), before touching them.
+  mutable std::mutex apply_mu;
+  mutable cudaEvent_t apply_done = nullptr;
+  Factor() = default;
+  Factor(const Factor&) = delete;
+  Factor& operator=(const Factor&) = delete;
+  ~Factor() {
+    if (apply_done) cudaEventDestroy(apply_done);
+  }
 };
 
 }  // namespace ceg

@@ -25,6 +25,12 @@ __host__ __device__ inline int row_pair_group(int forced, int np) {
 
 enum : int { kErrNone = 0, kErrBreakdown = 2, kErrPattern = 5, kErrInternal = 6, kErrChunk = 7, kErrStrip = 8, kErrNaN = 9 };
 
+// validate (factorization.cpp:272-334), device half: basis orthogonality and lower-triangular
+// pivots of one level; d_out = {max |U^T U - I| as double bits, upper nonzeros, first bad block}.
+void launch_validate_level(int64_t M, const int* bsz, const unsigned char* has_basis, const double* basis,
+                           const int64_t* basis_off, const int* width, const double* fac, const int64_t* chol_off,
+                           double tol, unsigned long long* d_out, cudaStream_t s);
+
 // Launch accounting (every launcher calls note_launch once per kernel launch).
 void note_launch(int64_t n = 1);
 int64_t launch_count();

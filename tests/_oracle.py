@@ -58,6 +58,10 @@ _sig = {
     "oracle_factor_tail_dim": (i64, [vp]),
     "oracle_factor_summary": (None, [vp, dblp]),
     "oracle_factor_level_stats": (None, [vp, i64, dblp]),
+    "oracle_factor_level_m": (i64, [vp, i64]),
+    "oracle_factor_level_structure": (None, [vp, i64, i64p, i64p, i64p]),
+    "oracle_factor_row_sigma": (i64, [vp, i64, i64, dblp, i64]),
+    "oracle_problem_perturb": (None, [vp, C.c_double, C.c_ulonglong]),
     "oracle_krylov": (C.c_int, [vp, vp, C.c_int, dblp, dblp, C.c_double, i64, C.c_int, i64p, dblp, dblp,
                                 C.POINTER(C.c_int), dblp]),
     "oracle_compress": (C.c_int, [i64, i64, dblp, C.c_int, C.c_double, C.c_int, i64, i64p, C.POINTER(C.c_int),
@@ -241,6 +245,17 @@ class OFactor:
         keys = ["factor_blocks", "predicted_factor_blocks", "l_scalar_nnz", "l_payload_bytes", "q_payload_bytes",
                 "tail_bytes", "total_seconds", "tail_seconds"]
         return dict(zip(keys, out.tolist()))
+
+    def level_structure(self, lvl):
+        m = int(lib.oracle_factor_level_m(self.h, lvl))
+        sizes, ret, fc = (np.empty(m, np.int64) for _ in range(3))
+        lib.oracle_factor_level_structure(self.h, lvl, _p(sizes, C.c_int64), _p(ret, C.c_int64), _p(fc, C.c_int64))
+        return sizes, ret, fc
+
+    def row_sigma(self, lvl, b, cap=4096):
+        out = np.empty(cap)
+        k = int(lib.oracle_factor_row_sigma(self.h, lvl, b, _p(out), cap))
+        return out[:min(k, cap)].copy()
 
     def level_stats(self):
         keys = ["block_count", "pattern_blocks", "factor_blocks", "eliminated", "retained", "max_rank", "mean_rank",

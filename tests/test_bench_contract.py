@@ -29,11 +29,12 @@ def test_reference_arm_line():
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["cfg"] == 1
+    assert "CPU sample actually timed" in d["config"]["workload"]
 
 
 @pytest.mark.gpu
 def test_product_line_cfg1():
-    d = _run(["--cfg", "1", "--steps", "2", "--warmup", "3", "--e2e-steps", "1", "--no-cpu-baseline"])
+    d = _run(["--cfg", "1", "--steps", "2", "--warmup", "3", "--e2e-steps", "1", "--no-cpu-baseline", "--no-extra"])
     assert BASE_KEYS <= set(d)
     assert d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] == 3 and d["dtype"] == "f64"
     assert d["pcg_converged"] and d["pcg_iterations"] <= 3
@@ -44,3 +45,7 @@ def test_product_line_cfg1():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     v = d["plan_variant"]
     assert v["plan"] == "merge_all_colored" and v["value"] > 0 and v["pcg_converged"]
+    ra = d["roofline_apply"]
+    assert ra["bound"] == "hbm" and ra["algorithmic_bytes"] > 0 and 0 < ra["frac"] < 1 and ra["matvec"]["ms"] > 0
+    assert d["validate"]["max_orth_error"] <= 1e-12 and d["validate"]["seconds"] > 0
+    assert "extra_configs" not in d
