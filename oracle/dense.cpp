@@ -110,13 +110,21 @@ void trsv_lower_t(const Mat& L, double* y) {
   }
 }
 
-double gauge_weight(index_t k) { return gauge_weight2(k, 0); }
+double gauge_weight(index_t k) {
+  // 1 + 0.5 * frac((k+1) * c), c = (sqrt(5)-1)/2: positive, irregular, deterministic.
+  const double x = static_cast<double>(k + 1) * 0.6180339887498949;
+  return 1.0 + 0.5 * (x - std::floor(x));
+}
 
 double gauge_weight2(index_t k, index_t j) {
-  // 1 + 0.5 * frac((k+1) * c_j), c_j = (sqrt(5)-1)/2 + j (sqrt(2)-1)/2: positive, irregular, deterministic.
-  const double cj = 0.6180339887498949 + 0.2071067811865475 * static_cast<double>(j);
-  const double x = static_cast<double>(k + 1) * cj;
-  return 1.0 + 0.5 * (x - std::floor(x));
+  // splitmix64 finaliser of (k, j) -> 53-bit uniform in [0, 1) -> [-1, 1); the GPU computes the
+  // same integers (sweep.cu gauge_weight2).
+  unsigned long long z = static_cast<unsigned long long>(k) * 0x9E3779B97F4A7C15ull +
+                         static_cast<unsigned long long>(j) * 0xD1B54A32D192ED03ull + 0x632BE59BD9B4E019ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return static_cast<double>(z >> 11) * 0x1.0p-52 - 1.0;
 }
 
 namespace {
@@ -293,18 +301,36 @@ Mat canonical_basis(const Mat& V, const std::vector<double>& sigma, index_t r) {
           for (index_t i = 0; i < b; ++i) A(i, k0 + j) += V(i, k0 + q) * m;
         }
       }
-      // modified Gram-Schmidt, two passes
-      for (index_t j = 0; j < c; ++j) {
-        for (int pass = 0; pass < 2; ++pass)
-          for (index_t q = 0; q < j; ++q) {
-            double d = 0.0;
-            for (index_t i = 0; i < b; ++i) d += A(i, k0 + q) * A(i, k0 + j);
-            for (index_t i = 0; i < b; ++i) A(i, k0 + j) -= d * A(i, k0 + q);
+      // Modified Gram-Schmidt (two passes), then project onto span(U_c) once more and
+      // orthonormalise again: the first orthonormalisation amplifies Z's rounding outside
+      // span(U_c) by cond(U_c^T G_c); the re-projection removes it (U1 stays orthogonal to 1e-15).
+      for (int round = 0; round < 2; ++round) {
+        if (round == 1)
+          for (index_t j = 0; j < c; ++j) {
+            std::vector<double> m(static_cast<size_t>(c));
+            for (index_t q = 0; q < c; ++q) {
+              double d = 0.0;
+              for (index_t i = 0; i < b; ++i) d += V(i, k0 + q) * A(i, k0 + j);
+              m[static_cast<size_t>(q)] = d;
+            }
+            for (index_t i = 0; i < b; ++i) {
+              double z = 0.0;
+              for (index_t q = 0; q < c; ++q) z += V(i, k0 + q) * m[static_cast<size_t>(q)];
+              A(i, k0 + j) = z;
+            }
           }
-        double nrm = 0.0;
-        for (index_t i = 0; i < b; ++i) nrm += A(i, k0 + j) * A(i, k0 + j);
-        nrm = std::sqrt(nrm);
-        for (index_t i = 0; i < b; ++i) A(i, k0 + j) /= nrm;
+        for (index_t j = 0; j < c; ++j) {
+          for (int pass = 0; pass < 2; ++pass)
+            for (index_t q = 0; q < j; ++q) {
+              double d = 0.0;
+              for (index_t i = 0; i < b; ++i) d += A(i, k0 + q) * A(i, k0 + j);
+              for (index_t i = 0; i < b; ++i) A(i, k0 + j) -= d * A(i, k0 + q);
+            }
+          double nrm = 0.0;
+          for (index_t i = 0; i < b; ++i) nrm += A(i, k0 + j) * A(i, k0 + j);
+          nrm = std::sqrt(nrm);
+          for (index_t i = 0; i < b; ++i) A(i, k0 + j) /= nrm;
+        }
       }
     }
     k0 = k1;

@@ -61,8 +61,11 @@ void trsv_lower(const Mat& L, double* y);
 // y <- L^{-T} y
 void trsv_lower_t(const Mat& L, double* y);
 
-// Generic weights c_k used by the canonical gauge's sign rules.
+// Generic weights c_k used by the canonical gauge's sign rules (singletons, complement QR).
 double gauge_weight(index_t k);
+// Cluster gauge weights G_c(k, j): zero-mean hash values in [-1, 1), independent across j, so
+// U_c^T G_c stays well conditioned for clusters of any size (the earlier 1 + frac((k+1) c_j)
+// columns were nearly affine in j and lost orthogonality at cluster sizes >= ~4).
 double gauge_weight2(index_t k, index_t j);
 // Singular values closer than kClusterTol * sigma_1 share one canonical basis.
 constexpr double kClusterTol = 1e-9;

@@ -63,12 +63,21 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__device__ __forceinline__ double gauge_weight2(int k, int j) {
-  const double cj = __dadd_rn(0.6180339887498949, __dmul_rn(0.2071067811865475, static_cast<double>(j)));
-  const double x = __dmul_rn(static_cast<double>(k + 1), cj);
+// Canonical-gauge weights, bit-identical to oracle/dense.cpp: singletons' sign rule ...
+__device__ __forceinline__ double gauge_weight(int k) {
+  const double x = __dmul_rn(static_cast<double>(k + 1), 0.6180339887498949);
   return 1.0 + 0.5 * (x - floor(x));
 }
-__device__ __forceinline__ double gauge_weight(int k) { return gauge_weight2(k, 0); }
+// ... and the cluster weights G_c(k, j): splitmix64 of (k, j), zero-mean in [-1, 1), independent
+// across j so U_c^T G_c is well conditioned for any cluster size.
+__device__ __forceinline__ double gauge_weight2(int k, int j) {
+  unsigned long long z = static_cast<unsigned long long>(k) * 0x9E3779B97F4A7C15ull +
+                         static_cast<unsigned long long>(j) * 0xD1B54A32D192ED03ull + 0x632BE59BD9B4E019ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return __dadd_rn(static_cast<double>(z >> 11) * 0x1.0p-52, -1.0);
+}
 
 __device__ __forceinline__ int rr_player(int k, int round, int nb) {
   return k == 0 ? 0 : 1 + (k - 1 + round) % (nb - 1);

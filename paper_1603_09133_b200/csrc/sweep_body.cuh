@@ -1143,22 +1143,46 @@ __device__ __noinline__ void canonical_basis(const Buf& s_, int b, int r, int ns
         }
       }
       __syncwarp();
-      for (int j = 0; j < c; ++j) {
-        double* z = A + (k0 + j) * b;
-        for (int pass = 0; pass < 2; ++pass)
-          for (int q = 0; q < j; ++q) {
-            const double* y = A + (k0 + q) * b;
-            double d = 0.0;
-            for (int a = lane; a < b; a += 32) d += y[a] * z[a];
-            d = warp_sum(d);
-            for (int a = lane; a < b; a += 32) z[a] -= d * y[a];
+      // MGS (two passes), re-projection onto span(U_c), MGS again (oracle/dense.cpp): the
+      // re-projection removes rounding outside the span that the first orthonormalisation
+      // amplified by cond(U_c^T G_c).  s.tau[k0 .. k1) is this cluster's private scratch.
+      for (int round = 0; round < 2; ++round) {
+        if (round == 1)
+          for (int j = 0; j < c; ++j) {
+            double* z = A + (k0 + j) * b;
+            for (int q = 0; q < c; ++q) {
+              const double* v = s.V + static_cast<int64_t>(s.perm[k0 + q]) * pad_ld(b);
+              double d = 0.0;
+              for (int a = lane; a < b; a += 32) d += v[a] * z[a];
+              d = warp_sum(d);
+              if (lane == 0) s.tau[k0 + q] = d;
+            }
+            __syncwarp();
+            for (int a = lane; a < b; a += 32) {
+              double acc = 0.0;
+              for (int q = 0; q < c; ++q)
+                acc += s.V[static_cast<int64_t>(s.perm[k0 + q]) * pad_ld(b) + a] * s.tau[k0 + q];
+              z[a] = acc;
+            }
             __syncwarp();
           }
-        double n2 = 0.0;
-        for (int a = lane; a < b; a += 32) n2 += z[a] * z[a];
-        const double nrm = sqrt(warp_sum(n2));
-        for (int a = lane; a < b; a += 32) z[a] /= nrm;
-        __syncwarp();
+        for (int j = 0; j < c; ++j) {
+          double* z = A + (k0 + j) * b;
+          for (int pass = 0; pass < 2; ++pass)
+            for (int q = 0; q < j; ++q) {
+              const double* y = A + (k0 + q) * b;
+              double d = 0.0;
+              for (int a = lane; a < b; a += 32) d += y[a] * z[a];
+              d = warp_sum(d);
+              for (int a = lane; a < b; a += 32) z[a] -= d * y[a];
+              __syncwarp();
+            }
+          double n2 = 0.0;
+          for (int a = lane; a < b; a += 32) n2 += z[a] * z[a];
+          const double nrm = sqrt(warp_sum(n2));
+          for (int a = lane; a < b; a += 32) z[a] /= nrm;
+          __syncwarp();
+        }
       }
     }
   }
