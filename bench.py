@@ -27,7 +27,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "factorization unknowns/sec (fp64) + PCG solve time; % of HBM/FP64 roofline"
 # CPU sample of the same workload family (stencil, B, eps) sized for ~10 s of oracle work (cfg2 256^2: ~9 s)
-PLAN_FLAGS = {"reference": [], "merge_all_axes": ["--merge-all"], "merge_all_colored": ["--colored"]}
+PLAN_FLAGS = {"reference": [], "merge_all_axes": ["--merge-all"], "merge_all_colored": ["--colored"],
+              "sharded": ["--sharded"]}
 CPU_SAMPLE_GRID = {1: (128, 128, 0), 2: (256, 256, 0), 3: (256, 256, 0), 4: (16, 16, 16), 5: (16, 16, 16)}
 
 
@@ -43,7 +44,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the colour-major plan variant line")
-    ap.add_argument("--plan", default="reference", choices=["reference", "merge_all_axes", "merge_all_colored"],
+    ap.add_argument("--plan", default="reference", choices=["reference", "merge_all_axes", "merge_all_colored", "sharded"],
                     help="plan family: the reference's geometric_block_ordering (join 2, one axis per level) or "
                          "every axis merging by 2 per level (J = 2^d; the 3-D configs at full size, DESIGN.md)")
     ap.add_argument("--ref-threads", type=int, default=0, help="reference arm: concurrent oracle copies (0 = all host threads)")

@@ -115,6 +115,11 @@ typedef struct {
   double validate_seconds;      /* validate() inside ce_factorize (factorization.cpp:272-334,459) */
   double max_orth_error;        /* max |U^T U - I| over every stored basis (validate bound 1e-12) */
   double apply_algorithmic_bytes;  /* SURVEY.md §8d bytes of one preconditioner apply (ce_apply_precond) */
+  int64_t shard_phase1_rows;    /* sharded factorizations: box-interior rows over all levels */
+  int64_t shard_own_rows;       /* ... of which this rank swept */
+  int64_t shard_phase3_rows;    /* interface rows (swept by every rank) */
+  double shard_exchange_bytes;  /* bytes this rank packed / received in the exchanges */
+  double shard_exchange_seconds;
 } ce_factor_stats;
 
 /* LevelStats (factorization.hpp:38-54) for level l (0-based). */
@@ -157,6 +162,32 @@ int ce_factorize(ce_ctx* ctx, const ce_matrix* a, const ce_plan_host* plan, cons
                  const ce_factor_opts* opts, ce_factor** out, ce_status* st);
 void ce_factor_free(ce_factor* f);
 int64_t ce_factor_dim(const ce_factor* f);
+/* ---- subdomain-sharded factorization ----
+ * One process per GPU, each with its own ce_ctx on its device; every rank calls
+ * ce_factorize_sharded with the same matrix, plan and strategy.  The plan must put each
+ * level's box-interior rows first (CE_PLAN_SHARDED does); box b belongs to rank
+ * b * n_ranks / n_boxes.  Each rank sweeps the interior rows of its boxes, the interface rows
+ * are swept by every rank, and the ranks exchange blocks through `bcast` -- an in-place
+ * broadcast of `bytes` device bytes at `dev_ptr` from rank `root` to all ranks (NCCL over
+ * NVLink in the Python binding; it returns 0 on success, must complete before returning, and
+ * every rank issues the same calls in the same order).  The resulting factor is complete on
+ * every rank and bit-identical to ce_factorize of the same plan on one GPU. */
+typedef int (*ce_bcast_fn)(void* user, void* dev_ptr, int64_t bytes, int root);
+typedef struct {
+  int rank;
+  int n_ranks;
+  int64_t n_boxes;
+  const int64_t* box_of_block; /* level-1 block -> box, m entries (ce_problem_boxes) */
+  ce_bcast_fn bcast;
+  void* user;
+} ce_shard;
+int ce_factorize_sharded(ce_ctx* ctx, const ce_matrix* a, const ce_plan_host* plan, const ce_strategy* s,
+                         const ce_factor_opts* opts, const ce_shard* shard, ce_factor** out, ce_status* st);
+/* Host-side symbolic split of a CE_PLAN_SHARDED problem over n_ranks (every group assumed
+ * alive): per level l < *n_levels (<= max_levels), out[l * (2 + n_ranks) + {0, 1, 2 + r}] =
+ * {block count, interior (phase-1) rows, rows rank r sweeps alone}.  No GPU needed. */
+int ce_shard_plan_summary(const ce_problem* p, int n_ranks, int64_t max_levels, int64_t* out, int64_t* n_levels);
+
 /* Preconditioner apply x = Q^T L^-T L^-1 Q b (replaces CEFactorization::solve,
  * factorization.cpp:140-168; used as ApplyFn at cli.cpp:225).  Thread-safe: concurrent calls
  * on one factor (any threads, any streams) are serialised on the device, because they share
@@ -212,6 +243,13 @@ int ce_problem_create(int cfg, int64_t nx, int64_t ny, int64_t nz, ce_problem** 
  * pattern stays within Chebyshev distance 2 (in cells), so rows of one colour are independent
  * and each level's sweep has at most 9 (2-D) / 27 (3-D) waves. */
 #define CE_PLAN_MERGE_ALL_COLORED 2
+/* CE_PLAN_SHARDED = CE_PLAN_MERGE_ALL_COLORED with 8 spatial boxes (4 x 2 in 2-D, 2 x 2 x 2 in
+ * 3-D): at every level the cells >= 2 cells inside their box come first, box by box (each
+ * colour-major), then every other ("interface") cell, colour-major.  An interior row's
+ * squared-pattern row never leaves its box, so the boxes' interiors factor independently:
+ * the plan ce_factorize_sharded distributes over GPUs.  Box labels of the
+ * level-1 blocks: ce_problem_boxes. */
+#define CE_PLAN_SHARDED 3
 int ce_problem_create_plan(int cfg, int64_t nx, int64_t ny, int64_t nz, int plan_kind, ce_problem** out);
 void ce_problem_free(ce_problem* p);
 /* The reference CLI's `file` problem (proj/src/cli.cpp:114-133 load_problem + finish_load :49-58):
@@ -226,6 +264,9 @@ int ce_problem_load(const char* matrix_path, const char* plan_path, const char* 
 /* run_gen's writer (cli.cpp:136-150): natural-order matrix (write_matrix_market, lower triangle,
  * 17 digits), rhs (write_vector) and plan (CoarseningPlan::save); any path may be NULL (skipped). */
 int ce_problem_save(const ce_problem* p, const char* matrix_path, const char* plan_path, const char* rhs_path);
+/* CE_PLAN_SHARDED problems: the box (subdomain) label of every level-1 block and the box count
+ * (*n_boxes = 0, *box_of_block = NULL for the other plan families). */
+int ce_problem_boxes(const ce_problem* p, const int64_t** box_of_block, int64_t* n_boxes);
 /* Views into the problem (valid until ce_problem_free). */
 int ce_problem_csb(const ce_problem* p, ce_csb_host* out);
 int ce_problem_plan(const ce_problem* p, ce_plan_host* out);

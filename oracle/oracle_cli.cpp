@@ -4,7 +4,7 @@
 // JSON object.  Mirrors the timed regions of proj/src/cli.cpp:102-110
 // (factor_problem) and :211-228 (solve), with PCG in place of MINRES.
 //
-// usage: oracle_cli <cfg 1..5> [nx ny nz] [--no-solve] [--dump PATH] [--levels] [--merge-all | --colored]
+// usage: oracle_cli <cfg 1..5> [nx ny nz] [--no-solve] [--dump PATH] [--levels] [--merge-all | --colored | --sharded]
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -20,7 +20,7 @@ using namespace oracle;
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::fprintf(stderr, "usage: oracle_cli <cfg 1..5> [nx ny nz] [--no-solve] [--dump PATH] [--levels] [--merge-all | --colored]\n");
+    std::fprintf(stderr, "usage: oracle_cli <cfg 1..5> [nx ny nz] [--no-solve] [--dump PATH] [--levels] [--merge-all | --colored | --sharded]\n");
     return 1;
   }
   try {
@@ -33,6 +33,7 @@ int main(int argc, char** argv) {
       else if (!std::strcmp(argv[a], "--levels")) levels = true;
       else if (!std::strcmp(argv[a], "--merge-all")) c.plan_kind = 1;
       else if (!std::strcmp(argv[a], "--colored")) c.plan_kind = 2;
+      else if (!std::strcmp(argv[a], "--sharded")) c.plan_kind = 3;
       else if (!std::strcmp(argv[a], "--dump") && a + 1 < argc) dump = argv[++a];
       else {
         const long long v = std::atoll(argv[a]);

@@ -77,6 +77,9 @@ std::vector<double> unpermute_vector(const std::vector<double>& v, const std::ve
 
 // One BASELINE.json configuration, optionally on a
 // smaller grid with the same stencil family / block / eps.
+constexpr index_t kShardBoxes = 8;
+index_t shard_box(const index_t* g, index_t q, int dims, bool* interior);
+
 struct ProblemConfig {
   int id = 0;
   int dims = 2;

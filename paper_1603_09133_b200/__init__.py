@@ -21,11 +21,14 @@ from .ce import (  # noqa: F401
     MinresOptions,
     PcgOptions,
     Problem,
+    ShardComm,
     SolveReport,
     ce_factorize,
+    ce_factorize_sharded,
     device_count,
     minres,
     pcg,
+    shard_plan_summary,
 )
 
 __all__ = [
@@ -40,9 +43,12 @@ __all__ = [
     "MinresOptions",
     "PcgOptions",
     "Problem",
+    "ShardComm",
     "SolveReport",
     "ce_factorize",
+    "ce_factorize_sharded",
     "device_count",
     "minres",
     "pcg",
+    "shard_plan_summary",
 ]

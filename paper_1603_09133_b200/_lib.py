@@ -45,6 +45,14 @@ class Status(C.Structure):
                 ("message", C.c_char * 256)]
 
 
+BcastFn = C.CFUNCTYPE(C.c_int, vp, vp, i64, C.c_int)  # ce_bcast_fn(user, dev_ptr, bytes, root)
+
+
+class Shard(C.Structure):
+    _fields_ = [("rank", C.c_int), ("n_ranks", C.c_int), ("n_boxes", i64), ("box_of_block", i64p),
+                ("bcast", BcastFn), ("user", vp)]
+
+
 class PcgOpts(C.Structure):
     _fields_ = [("tol", C.c_double), ("maxit", i64), ("track_true_residual", C.c_int)]
 
@@ -61,7 +69,9 @@ class FactorStats(C.Structure):
                 ("total_seconds", C.c_double), ("device_seconds", C.c_double),
                 ("sweep_kernel_seconds", C.c_double), ("algorithmic_bytes", C.c_double),
                 ("algorithmic_flops", C.c_double), ("validate_seconds", C.c_double), ("max_orth_error", C.c_double),
-                ("apply_algorithmic_bytes", C.c_double)]
+                ("apply_algorithmic_bytes", C.c_double), ("shard_phase1_rows", i64), ("shard_own_rows", i64),
+                ("shard_phase3_rows", i64), ("shard_exchange_bytes", C.c_double),
+                ("shard_exchange_seconds", C.c_double)]
 
 
 class LevelStats(C.Structure):
@@ -105,6 +115,10 @@ SIGNATURES = {
     "ce_problem_save": (C.c_int, [vp, C.c_char_p, C.c_char_p, C.c_char_p]),
     "ce_problem_csb": (C.c_int, [vp, C.POINTER(CsbHost)]),
     "ce_problem_plan": (C.c_int, [vp, C.POINTER(PlanHost)]),
+    "ce_problem_boxes": (C.c_int, [vp, C.POINTER(C.POINTER(i64)), C.POINTER(i64)]),
+    "ce_factorize_sharded": (C.c_int, [vp, vp, C.POINTER(PlanHost), C.POINTER(Strategy), C.POINTER(FactorOpts),
+                                       C.POINTER(Shard), C.POINTER(vp), C.POINTER(Status)]),
+    "ce_shard_plan_summary": (C.c_int, [vp, C.c_int, i64, i64p, i64p]),
     "ce_problem_rhs": (dblp, [vp]),
     "ce_problem_perm": (i64p, [vp]),
     "ce_problem_params": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), i64p]),

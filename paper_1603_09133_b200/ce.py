@@ -352,6 +352,106 @@ def ce_factorize(a, plan: Optional[CoarseningPlan], strategy: CompressionStrateg
     return f
 
 
+class _DeviceBytes:
+    """A raw device byte range, viewed zero-copy as a torch tensor (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class ShardComm:
+    """torch.distributed plumbing for ce_factorize_sharded (include/ce_gpu.h ce_bcast_fn).
+
+    One process per GPU.  The library calls `bcast(dev_ptr, bytes, root)` in the same order on
+    every rank; it becomes dist.broadcast -- straight on the device buffer under NCCL (NVLink /
+    NVSwitch), staged through host memory under gloo (the multi-process test backend)."""
+
+    def __init__(self, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.backend = dist.get_backend(group)
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else "cpu"
+        self.device = torch.device(device)
+        self.calls, self.bytes, self.error = 0, 0, None
+        self.fn = L.BcastFn(self._bcast)  # kept alive with the object
+
+    def _bcast(self, user, ptr, nbytes, root):
+        try:
+            import torch
+            if self.device.type == "cpu":  # host buffers (the CPU test of this plumbing)
+                t = torch.frombuffer((C.c_uint8 * int(nbytes)).from_address(int(ptr)), dtype=torch.uint8)
+                self.dist.broadcast(t, src=root if self.group is None else self.dist.get_global_rank(self.group, root),
+                                    group=self.group)
+                self.calls += 1
+                self.bytes += int(nbytes)
+                return 0
+            t = torch.as_tensor(_DeviceBytes(ptr, nbytes), device=self.device)
+            src = root if self.group is None else self.dist.get_global_rank(self.group, root)
+            if self.backend == "nccl":
+                self.dist.broadcast(t, src=src, group=self.group)
+                torch.cuda.current_stream(self.device).synchronize()
+            else:
+                h = t.cpu() if self.rank == root else torch.empty(int(nbytes), dtype=torch.uint8)
+                self.dist.broadcast(h, src=src, group=self.group)
+                if self.rank != root:
+                    t.copy_(h)
+                    torch.cuda.synchronize(self.device)
+            self.calls += 1
+            self.bytes += int(nbytes)
+            return 0
+        except Exception as e:  # noqa: BLE001 -- reported through the library's error path
+            self.error = e
+            return 1
+
+
+def ce_factorize_sharded(a, plan: CoarseningPlan, strategy: CompressionStrategy, box_of_block, comm: ShardComm,
+                         opts: Optional[FactorOptions] = None, n_boxes: int = 8,
+                         ctx: Optional[Context] = None) -> CEFactorization:
+    """This rank's part of the subdomain-sharded factorization (ce_factorize_sharded,
+    DESIGN.md §7): every rank passes the same matrix / plan / labels; the returned factor is
+    complete on every rank and identical to ce_factorize of the same plan on one GPU."""
+    opts = opts or FactorOptions()
+    if isinstance(a, BlockSparseMatrix):
+        a = DeviceMatrix(a, ctx)
+    ctx = a.ctx
+    labels = _i64(box_of_block)
+    if labels.size != a.host.m:
+        raise ValueError("box_of_block must label every level-1 block")
+    counts = _i64([len(f) for f in opts.forced_ranks]) if opts.forced_ranks else _i64([0])
+    flat = _i64(np.concatenate([_i64(f) for f in opts.forced_ranks])) if opts.forced_ranks else _i64([0])
+    copts = L.FactorOpts(int(opts.dense_threshold), int(opts.max_levels), len(opts.forced_ranks),
+                         _ptr(counts, C.c_int64), _ptr(flat, C.c_int64))
+    sh = L.Shard(comm.rank, comm.world, int(n_boxes), _ptr(labels, C.c_int64), comm.fn, None)
+    st = L.Status()
+    h = C.c_void_p()
+    rc = lib.ce_factorize_sharded(ctx.handle, a.handle, C.byref(plan._c()), C.byref(strategy._c()), C.byref(copts),
+                                  C.byref(sh), C.byref(h), C.byref(st))
+    if rc == CE_EBREAKDOWN:
+        raise BreakdownError(st.level, st.block, st.message.decode())
+    if rc != CE_OK and comm.error is not None:
+        raise RuntimeError(f"sharded factorization: exchange failed: {comm.error!r}")
+    _check(rc)
+    f = CEFactorization(h, ctx)
+    f.shift_retries = st.shift_retries
+    return f
+
+
+def shard_plan_summary(problem: "Problem", n_ranks: int, max_levels: int = 64) -> List[dict]:
+    """Symbolic phase split of a "sharded"-plan problem over n_ranks (host only, no GPU):
+    per level the block count, the box-interior (phase-1) rows and the rows each rank sweeps
+    alone (ce_shard_plan_summary)."""
+    out = np.zeros(max_levels * (2 + n_ranks), np.int64)
+    nl = C.c_int64()
+    _check(lib.ce_shard_plan_summary(problem.handle, int(n_ranks), int(max_levels), _ptr(out, C.c_int64), C.byref(nl)))
+    rows = out[:nl.value * (2 + n_ranks)].reshape(nl.value, 2 + n_ranks)
+    return [dict(blocks=int(r[0]), interior=int(r[1]), own=[int(x) for x in r[2:]]) for r in rows]
+
+
 def _krylov(entry, what, a, n, b, precond, opts):
     if not isinstance(a, DeviceMatrix):
         raise TypeError(f"{what} runs on the device: `a` must be a DeviceMatrix")
@@ -398,12 +498,13 @@ def minres(a: DeviceMatrix, n: int, b, precond: Optional[CEFactorization], opts:
 class Problem:
     """A BASELINE.json configuration generated on the host."""
 
-    PLANS = {"reference": 0, "merge_all_axes": 1, "merge_all_colored": 2}
+    PLANS = {"reference": 0, "merge_all_axes": 1, "merge_all_colored": 2, "sharded": 3}
 
     def __init__(self, cfg: int, nx: int = 0, ny: int = 0, nz: int = 0, _handle=None, plan: str = "reference"):
         """plan: "reference" = geometric_block_ordering(grid, block, 2) (problems.cpp:195-258);
         "merge_all_axes" = every non-exhausted axis merges by 2 per level (J = 2^d);
-        "merge_all_colored" = the same with each level's cells in mod-3 colour-major order."""
+        "merge_all_colored" = the same with each level's cells in mod-3 colour-major order;
+        "sharded" = merge_all_colored with 8 spatial boxes, box-interior cells first."""
         if _handle is None:
             h = C.c_void_p()
             if plan not in self.PLANS:
@@ -433,6 +534,11 @@ class Problem:
             assigns.append(flat[at:at + nb])
             at += nb
         self.plan = CoarseningPlan(assigns, plan.join)
+        bp, nb = C.POINTER(C.c_int64)(), C.c_int64()
+        lib.ce_problem_boxes(h, C.byref(bp), C.byref(nb))
+        # CE_PLAN_SHARDED: subdomain label of every level-1 block (None for the other families)
+        self.box_of_block = np.ctypeslib.as_array(bp, (self.m,)).copy() if nb.value else None
+        self.n_boxes = int(nb.value)
         eps, tol, blk = C.c_double(), C.c_double(), C.c_int64()
         lib.ce_problem_params(h, C.byref(eps), C.byref(tol), C.byref(blk))
         self.eps, self.tol, self.block = eps.value, tol.value, blk.value

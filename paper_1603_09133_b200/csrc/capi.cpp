@@ -280,8 +280,9 @@ int ce_matvec(const ce_matrix* a, const double* x, double* y, int64_t n, int on_
   });
 }
 
-int ce_factorize(ce_ctx* ctx, const ce_matrix* a, const ce_plan_host* plan, const ce_strategy* s,
-                 const ce_factor_opts* opts, ce_factor** out, ce_status* st) {
+namespace {
+int factorize_impl(ce_ctx* ctx, const ce_matrix* a, const ce_plan_host* plan, const ce_strategy* s,
+                   const ce_factor_opts* opts, const ce_shard* shard, ce_factor** out, ce_status* st) {
   if (st) std::memset(st, 0, sizeof *st);
   return guarded(
       [&] {
@@ -290,7 +291,17 @@ int ce_factorize(ce_ctx* ctx, const ce_matrix* a, const ce_plan_host* plan, cons
         CE_CUDA(cudaSetDevice(ctx->ctx.device));
         int64_t shifts = 0;
         auto h = std::make_unique<ce_factor>();
-        h->f.reset(ceg::factorize(&ctx->ctx, &a->m, plan, s, opts, &shifts));
+        ceg::ShardSpec spec;
+        if (shard) {
+          if (!shard->box_of_block || !shard->bcast) throw std::invalid_argument("sharded factorization: null labels / bcast");
+          spec.rank = shard->rank;
+          spec.n_ranks = shard->n_ranks;
+          spec.n_boxes = shard->n_boxes;
+          spec.box_l1.assign(shard->box_of_block, shard->box_of_block + a->m.m);
+          spec.bcast = shard->bcast;
+          spec.user = shard->user;
+        }
+        h->f.reset(ceg::factorize(&ctx->ctx, &a->m, plan, s, opts, &shifts, shard ? &spec : nullptr));
         h->a_ptr = a->m.row_ptr;
         h->a_col.assign(a->m.col_idx.begin(), a->m.col_idx.end());
         if (plan) {
@@ -308,6 +319,33 @@ int ce_factorize(ce_ctx* ctx, const ce_matrix* a, const ce_plan_host* plan, cons
         *out = h.release();
       },
       st);
+}
+}  // namespace
+
+int ce_factorize(ce_ctx* ctx, const ce_matrix* a, const ce_plan_host* plan, const ce_strategy* s,
+                 const ce_factor_opts* opts, ce_factor** out, ce_status* st) {
+  return factorize_impl(ctx, a, plan, s, opts, nullptr, out, st);
+}
+
+int ce_factorize_sharded(ce_ctx* ctx, const ce_matrix* a, const ce_plan_host* plan, const ce_strategy* s,
+                         const ce_factor_opts* opts, const ce_shard* shard, ce_factor** out, ce_status* st) {
+  if (!shard) {
+    g_err = "ce_factorize_sharded: null shard";
+    return CE_EUSAGE;
+  }
+  return factorize_impl(ctx, a, plan, s, opts, shard, out, st);
+}
+
+int ce_shard_plan_summary(const ce_problem* p, int n_ranks, int64_t max_levels, int64_t* out, int64_t* n_levels) {
+  return guarded([&] {
+    if (!p || !out || !n_levels || n_ranks < 1) throw std::invalid_argument("null argument / n_ranks < 1");
+    if (p->p.box_of_block.empty()) throw std::invalid_argument("not a CE_PLAN_SHARDED problem");
+    ceg::ShardSpec spec;
+    spec.n_ranks = n_ranks;
+    spec.n_boxes = ceg::kShardBoxes;
+    spec.box_l1 = p->p.box_of_block;
+    *n_levels = ceg::shard_symbolic_summary(p->p, spec, max_levels, out);
+  });
 }
 
 void ce_factor_free(ce_factor* f) { delete f; }
@@ -395,6 +433,11 @@ int ce_factor_get_stats(const ce_factor* fh, ce_factor_stats* out) {
       }
     pay += t * (t + 1) / 2;
     out->apply_algorithmic_bytes = 2.0 * 8.0 * pay + 8.0 * static_cast<double>(f.n) * 10.0;
+    out->shard_phase1_rows = f.shard.phase1_rows;
+    out->shard_own_rows = f.shard.own_rows;
+    out->shard_phase3_rows = f.shard.phase3_rows;
+    out->shard_exchange_bytes = f.shard.exchange_bytes;
+    out->shard_exchange_seconds = f.shard.exchange_seconds;
   });
 }
 
@@ -541,8 +584,9 @@ int ce_problem_create(int cfg, int64_t nx, int64_t ny, int64_t nz, ce_problem** 
 int ce_problem_create_plan(int cfg, int64_t nx, int64_t ny, int64_t nz, int plan_kind, ce_problem** out) {
   return guarded([&] {
     if (!out) throw std::invalid_argument("null argument");
-    if (plan_kind != CE_PLAN_REFERENCE && plan_kind != CE_PLAN_MERGE_ALL_AXES && plan_kind != CE_PLAN_MERGE_ALL_COLORED)
-      throw std::invalid_argument("plan_kind must be one of CE_PLAN_REFERENCE / _MERGE_ALL_AXES / _MERGE_ALL_COLORED");
+    if (plan_kind < CE_PLAN_REFERENCE || plan_kind > CE_PLAN_SHARDED)
+      throw std::invalid_argument(
+          "plan_kind must be one of CE_PLAN_REFERENCE / _MERGE_ALL_AXES / _MERGE_ALL_COLORED / _SHARDED");
     auto p = std::make_unique<ce_problem>();
     p->p.build(cfg, nx, ny, nz, plan_kind);
     *out = p.release();
@@ -586,6 +630,13 @@ int ce_problem_plan(const ce_problem* p, ce_plan_host* out) {
   out->n_levels = static_cast<int64_t>(p->p.plan_level_blocks.size());
   out->level_blocks = p->p.plan_level_blocks.data();
   out->assign = p->p.plan_assign.data();
+  return CE_OK;
+}
+
+int ce_problem_boxes(const ce_problem* p, const int64_t** box_of_block, int64_t* n_boxes) {
+  if (!p || !box_of_block || !n_boxes) return CE_EUSAGE;
+  *box_of_block = p->p.box_of_block.empty() ? nullptr : p->p.box_of_block.data();
+  *n_boxes = p->p.box_of_block.empty() ? 0 : ceg::kShardBoxes;
   return CE_OK;
 }
 

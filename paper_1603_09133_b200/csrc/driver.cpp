@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <future>
 #include <map>
 #include <mutex>
@@ -368,6 +369,48 @@ int64_t pair_tasks(int64_t np, int64_t g) {
   return t;
 }
 
+// Ticket order of the row tasks (wave order from the symbolic plan; plan_numeric's comment):
+// wave by wave, stage by stage across the wave's rows, with the lookahead split of every
+// row's Schur pairs into urgent (urg_of) / rest (rest_of).  `mask` (optional) restricts the
+// tickets to a subset of rows -- the sharded sweep's phases; the relative order
+// of the kept tickets is unchanged, so every wait is still on an earlier ticket.
+void build_tickets(const LevelPlan& P, const std::vector<char>* mask, std::vector<int>& item_row,
+                   std::vector<int>& item_part) {
+  const int64_t M = P.M;
+  const std::vector<int64_t>& wave = P.wave;
+  item_row.clear();
+  item_part.clear();
+  std::vector<int64_t> wstart;
+  for (int64_t k = 0; k < M;) {
+    wstart.push_back(k);
+    const int64_t wv = wave[static_cast<size_t>(P.order[static_cast<size_t>(k)])];
+    while (k < M && wave[static_cast<size_t>(P.order[static_cast<size_t>(k)])] == wv) ++k;
+  }
+  wstart.push_back(M);
+  const int64_t nw = static_cast<int64_t>(wstart.size()) - 1;
+  auto emit_rows = [&](int64_t w, auto&& parts) {
+    if (w < 0) return;
+    for (int64_t k = wstart[static_cast<size_t>(w)]; k < wstart[static_cast<size_t>(w + 1)]; ++k) {
+      const int row = P.order[static_cast<size_t>(k)];
+      if (mask && !(*mask)[static_cast<size_t>(row)]) continue;
+      parts(row, static_cast<size_t>(row));
+    }
+  };
+  auto push = [&](int row, int p) {
+    item_row.push_back(row);
+    item_part.push_back(p);
+  };
+  for (int64_t w = 0; w <= nw; ++w) {
+    if (w < nw) emit_rows(w, [&](int row, size_t r) { for (int p = 0; p < P.nleaf[r]; ++p) push(row, p); });
+    emit_rows(w - 1, [&](int row, size_t r) { for (int p : P.rest_of[r]) push(row, p); });
+    if (w == nw) break;
+    emit_rows(w, [&](int row, size_t r) { for (int p = P.nleaf[r]; p < P.nA1[r]; ++p) push(row, p); });
+    emit_rows(w, [&](int row, size_t r) { push(row, P.nA1[r]); });
+    emit_rows(w, [&](int row, size_t r) { for (int p = P.nA1[r] + 1; p <= P.nA1[r] + P.nA3[r]; ++p) push(row, p); });
+    emit_rows(w, [&](int row, size_t r) { for (int p : P.urg_of[r]) push(row, p); });
+  }
+}
+
 // Numeric part: everything that depends on the block sizes.
 void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
   const int64_t M = P.M;
@@ -625,15 +668,10 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
     // stages wait only for the pairs of its close predecessors that touch its own panel
     // (sq_pan), its Schur pairs for every task of every predecessor; every wait is on an
     // earlier ticket (no deadlock).  Rows whose Schur update is 0 or 1 task keep the full wait.
-    std::vector<int64_t> wstart;
-    for (int64_t k = 0; k < M;) {
-      wstart.push_back(k);
-      const int64_t wv = wave[static_cast<size_t>(P.order[static_cast<size_t>(k)])];
-      while (k < M && wave[static_cast<size_t>(P.order[static_cast<size_t>(k)])] == wv) ++k;
-    }
-    wstart.push_back(M);
-    const int64_t nw = static_cast<int64_t>(wstart.size()) - 1;
-    std::vector<std::vector<int>> rest_of(static_cast<size_t>(M)), urg_of(static_cast<size_t>(M));
+    P.rest_of.assign(static_cast<size_t>(M), {});
+    P.urg_of.assign(static_cast<size_t>(M), {});
+    auto& rest_of = P.rest_of;
+    auto& urg_of = P.urg_of;
     const bool lookahead = !(std::getenv("CE_NO_LOOKAHEAD") && std::getenv("CE_NO_LOOKAHEAD")[0] == '1');
     parallel_rows(M, [&](int64_t r0, int64_t r1) {
       std::vector<char> hot;
@@ -665,26 +703,7 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
           }
       }
     });
-    auto emit_rows = [&](int64_t w, auto&& parts) {
-      if (w < 0) return;
-      for (int64_t k = wstart[static_cast<size_t>(w)]; k < wstart[static_cast<size_t>(w + 1)]; ++k) {
-        const int row = P.order[static_cast<size_t>(k)];
-        parts(row, static_cast<size_t>(row));
-      }
-    };
-    auto push = [&](int row, int p) {
-      P.item_row.push_back(row);
-      P.item_part.push_back(p);
-    };
-    for (int64_t w = 0; w <= nw; ++w) {
-      if (w < nw) emit_rows(w, [&](int row, size_t r) { for (int p = 0; p < P.nleaf[r]; ++p) push(row, p); });
-      emit_rows(w - 1, [&](int row, size_t r) { for (int p : rest_of[r]) push(row, p); });
-      if (w == nw) break;
-      emit_rows(w, [&](int row, size_t r) { for (int p = P.nleaf[r]; p < P.nA1[r]; ++p) push(row, p); });
-      emit_rows(w, [&](int row, size_t r) { push(row, P.nA1[r]); });
-      emit_rows(w, [&](int row, size_t r) { for (int p = P.nA1[r] + 1; p <= P.nA1[r] + P.nA3[r]; ++p) push(row, p); });
-      emit_rows(w, [&](int row, size_t r) { for (int p : urg_of[r]) push(row, p); });
-    }
+    build_tickets(P, nullptr, P.item_row, P.item_part);
     if (static_cast<int64_t>(P.item_row.size()) != it) throw std::logic_error("ticket order lost items");
     tp5 = now_s();
     // sq_pan: panel of j inside close(i) for each close predecessor entry (j, i), i < j
@@ -1000,6 +1019,218 @@ void row_counts(double b, double c, double f, double r, double w, double p, doub
 
 }  // namespace
 
+// ---------------------------------------------------------------- sharding
+// A level of a CE_PLAN_SHARDED plan starts with the box-interior rows (row i interior: every
+// row of sq(i) carries i's box label), box by box, then every other ("interface") row.  An
+// interior row's reads and writes stay inside its box, so each rank sweeps the
+// interior rows of the boxes it owns (phase 1) with no communication; then
+//   E1  the owners broadcast the per-row integers of their phase-1 rows and every within-box
+//       block the interface rows will touch (their squared-pattern rows and Schur pairs);
+//   phase 3  every rank sweeps all interface rows (replicated, bit-identical inputs);
+//   E2  owners broadcast their phase-1 rows' factor slices (chol, coupling, g_t), bases, sigma;
+//   E3  owners broadcast the retained corners of the other within-box blocks phase 1 wrote,
+// so every rank ends the level with the whole level factor and a consistent store: the next
+// level, the tail and the apply run on complete data, and the factor is bit-identical to the
+// single-GPU factorization of the same plan (tests/test_gpu_shard.py).
+namespace {
+
+struct Seg {
+  int64_t off;
+  int rows, cols, ld;
+  int owner;
+};
+
+void shard_sync_bcast(const ShardSpec& sh, void* p, int64_t bytes, int root) {
+  if (bytes <= 0) return;
+  if (sh.bcast(sh.user, p, bytes, root) != 0) throw std::runtime_error("sharded factorization: broadcast failed");
+}
+
+// Owners pack their segments of `base` into a buffer, broadcast them in rank order, the
+// other ranks unpack.  Every rank passes the same segment list.
+void shard_exchange(const ShardSpec& sh, cudaStream_t s, double* base, std::vector<Seg> segs, ShardStats& st) {
+  if (segs.empty()) return;
+  const double t0 = now_s();
+  std::stable_sort(segs.begin(), segs.end(), [](const Seg& a, const Seg& b) { return a.owner < b.owner; });
+  const size_t n = segs.size();
+  std::vector<int64_t> off(n), boff(n), lo(static_cast<size_t>(sh.n_ranks) + 1, 0);
+  std::vector<int> rows(n), cols(n), ld(n);
+  std::vector<size_t> first(static_cast<size_t>(sh.n_ranks) + 1, n);
+  int64_t at = 0;
+  for (size_t k = 0; k < n; ++k) {
+    off[k] = segs[k].off;
+    rows[k] = segs[k].rows;
+    cols[k] = segs[k].cols;
+    ld[k] = segs[k].ld;
+    boff[k] = at;
+    at += static_cast<int64_t>(segs[k].rows) * segs[k].cols;
+  }
+  for (int r = sh.n_ranks; r >= 0; --r) {
+    size_t k = 0;
+    while (k < n && segs[k].owner < r) ++k;
+    first[static_cast<size_t>(r)] = k;
+    lo[static_cast<size_t>(r)] = k < n ? boff[k] : at;
+  }
+  DevArray<double> buf(static_cast<size_t>(std::max<int64_t>(at, 1)));
+  DevArray<int64_t> d_off, d_boff;
+  DevArray<int> d_rows, d_cols, d_ld;
+  d_off.upload(off, s);
+  d_boff.upload(boff, s);
+  d_rows.upload(rows, s);
+  d_cols.upload(cols, s);
+  d_ld.upload(ld, s);
+  const size_t s0 = first[static_cast<size_t>(sh.rank)], s1 = first[static_cast<size_t>(sh.rank) + 1];
+  launch_segments(base, buf.p, d_off.p + s0, d_rows.p + s0, d_cols.p + s0, d_ld.p + s0, d_boff.p + s0,
+                  static_cast<int64_t>(s1 - s0), true, s);
+  CE_CUDA(cudaStreamSynchronize(s));
+  for (int r = 0; r < sh.n_ranks; ++r)
+    shard_sync_bcast(sh, buf.p + lo[static_cast<size_t>(r)],
+                     (lo[static_cast<size_t>(r) + 1] - lo[static_cast<size_t>(r)]) * static_cast<int64_t>(sizeof(double)), r);
+  launch_segments(base, buf.p, d_off.p, d_rows.p, d_cols.p, d_ld.p, d_boff.p, static_cast<int64_t>(s0), false, s);
+  launch_segments(base, buf.p, d_off.p + s1, d_rows.p + s1, d_cols.p + s1, d_ld.p + s1, d_boff.p + s1,
+                  static_cast<int64_t>(n - s1), false, s);
+  CE_CUDA(cudaStreamSynchronize(s));
+  st.exchange_bytes += static_cast<double>(at) * sizeof(double);
+  st.exchange_seconds += now_s() - t0;
+}
+
+// Phase split of one level.
+struct ShardLevel {
+  int64_t prefix = 0;                     // rows [0, prefix): interior (phase 1)
+  std::vector<char> own1, phase3;         // masks: this rank's phase-1 rows, interface rows
+  std::vector<int> foreign1;              // phase-1 rows of the other ranks
+  std::vector<std::vector<int>> by_owner; // phase-1 rows per owner rank
+};
+
+ShardLevel shard_level(const ShardSpec& sh, const LevelPlan& P, const std::vector<int64_t>& label) {
+  ShardLevel L;
+  const int64_t M = P.M;
+  L.prefix = M;
+  for (int64_t i = 0; i < M && L.prefix == M; ++i) {
+    bool interior = label[static_cast<size_t>(i)] >= 0;
+    for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)] && interior; ++e)
+      interior = label[static_cast<size_t>(P.scol[static_cast<size_t>(e)])] == label[static_cast<size_t>(i)];
+    if (!interior) L.prefix = i;
+  }
+  L.own1.assign(static_cast<size_t>(M), 0);
+  L.phase3.assign(static_cast<size_t>(M), 0);
+  L.by_owner.assign(static_cast<size_t>(sh.n_ranks), {});
+  for (int64_t i = 0; i < M; ++i) {
+    if (i >= L.prefix) {
+      L.phase3[static_cast<size_t>(i)] = 1;
+      continue;
+    }
+    const int o = sh.owner(label[static_cast<size_t>(i)]);
+    L.by_owner[static_cast<size_t>(o)].push_back(static_cast<int>(i));
+    if (o == sh.rank) L.own1[static_cast<size_t>(i)] = 1;
+    else L.foreign1.push_back(static_cast<int>(i));
+  }
+  return L;
+}
+
+// Per-row integers of the phase-1 rows (rank, width, has_basis, fcols, nsig), owners first.
+void shard_exchange_ints(const ShardSpec& sh, cudaStream_t s, const ShardLevel& L, LevelFactor& LF, ShardStats& st) {
+  const double t0 = now_s();
+  std::vector<int> rows;
+  std::vector<int64_t> lo(static_cast<size_t>(sh.n_ranks) + 1, 0);
+  for (int r = 0; r < sh.n_ranks; ++r) {
+    lo[static_cast<size_t>(r)] = static_cast<int64_t>(rows.size());
+    rows.insert(rows.end(), L.by_owner[static_cast<size_t>(r)].begin(), L.by_owner[static_cast<size_t>(r)].end());
+  }
+  lo[static_cast<size_t>(sh.n_ranks)] = static_cast<int64_t>(rows.size());
+  if (rows.empty()) return;
+  DevArray<int> d_rows;
+  d_rows.upload(rows, s);
+  DevArray<double> buf(5 * rows.size());
+  const int64_t a0 = lo[static_cast<size_t>(sh.rank)], a1 = lo[static_cast<size_t>(sh.rank) + 1];
+  launch_row_ints(d_rows.p + a0, a1 - a0, LF.d_rank.p, LF.d_width.p, LF.d_has_basis.p, LF.d_fcols.p, LF.d_nsig.p,
+                  buf.p + 5 * a0, true, s);
+  CE_CUDA(cudaStreamSynchronize(s));
+  for (int r = 0; r < sh.n_ranks; ++r)
+    shard_sync_bcast(sh, buf.p + 5 * lo[static_cast<size_t>(r)],
+                     5 * (lo[static_cast<size_t>(r) + 1] - lo[static_cast<size_t>(r)]) * static_cast<int64_t>(sizeof(double)), r);
+  launch_row_ints(d_rows.p, a0, LF.d_rank.p, LF.d_width.p, LF.d_has_basis.p, LF.d_fcols.p, LF.d_nsig.p, buf.p, false, s);
+  launch_row_ints(d_rows.p + a1, static_cast<int64_t>(rows.size()) - a1, LF.d_rank.p, LF.d_width.p, LF.d_has_basis.p,
+                  LF.d_fcols.p, LF.d_nsig.p, buf.p + 5 * a1, false, s);
+  CE_CUDA(cudaStreamSynchronize(s));
+  st.exchange_bytes += 40.0 * static_cast<double>(rows.size());
+  st.exchange_seconds += now_s() - t0;
+}
+
+// Every rank's sweep status after a phase: a breakdown / error anywhere stops every rank.
+void shard_check_status(const ShardSpec& sh, cudaStream_t s, int* d_err) {
+  DevArray<double> st(4 * static_cast<size_t>(sh.n_ranks));
+  st.zero(s);
+  std::vector<int> h(4, 0);
+  CE_CUDA(cudaMemcpyAsync(h.data(), d_err, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CE_CUDA(cudaStreamSynchronize(s));
+  const double mine[4] = {static_cast<double>(h[0]), static_cast<double>(h[1]), static_cast<double>(h[2]),
+                          static_cast<double>(h[3])};
+  CE_CUDA(cudaMemcpy(st.p + 4 * sh.rank, mine, sizeof mine, cudaMemcpyHostToDevice));
+  for (int r = 0; r < sh.n_ranks; ++r) shard_sync_bcast(sh, st.p + 4 * r, 4 * sizeof(double), r);
+  std::vector<double> all;
+  st.download(all, s);
+  CE_CUDA(cudaStreamSynchronize(s));
+  for (int r = 0; r < sh.n_ranks; ++r)
+    if (all[static_cast<size_t>(4 * r)] != 0.0 && r != sh.rank) {
+      // adopt the first failing rank's status so every rank raises the same error
+      const int v[4] = {static_cast<int>(all[static_cast<size_t>(4 * r)]), static_cast<int>(all[static_cast<size_t>(4 * r + 1)]),
+                        static_cast<int>(all[static_cast<size_t>(4 * r + 2)]), static_cast<int>(all[static_cast<size_t>(4 * r + 3)])};
+      if (h[0] == 0) CE_CUDA(cudaMemcpy(d_err, v, sizeof v, cudaMemcpyHostToDevice));
+      break;
+    }
+}
+
+// Stored slot of (s, t) in the squared pattern (both triangles map to the lower slot).
+int64_t sq_slot_of(const LevelPlan& P, int64_t s, int64_t t) {
+  const int64_t e = csr_find(P.sptr, P.scol, s, static_cast<int>(t));
+  return e < 0 ? -1 : P.sslot[static_cast<size_t>(e)];
+}
+
+}  // namespace
+
+int64_t shard_symbolic_summary(const Problem& p, const ShardSpec& spec, int64_t max_levels, int64_t* out) {
+  std::vector<int64_t> labels = spec.box_l1;
+  std::vector<int64_t> bptr = p.row_ptr;
+  std::vector<int> bcol(p.col_idx.begin(), p.col_idx.end());
+  int64_t M = p.m, at = 0, lv = 0;
+  const int64_t stride = 2 + spec.n_ranks;
+  for (; lv < max_levels && lv < static_cast<int64_t>(p.plan_level_blocks.size()) && M > 1; ++lv) {
+    LevelPlan P = plan_symbolic(M, bptr, bcol);
+    ShardLevel L = shard_level(spec, P, labels);
+    out[lv * stride] = M;
+    out[lv * stride + 1] = L.prefix;
+    for (int r = 0; r < spec.n_ranks; ++r)
+      out[lv * stride + 2 + r] = static_cast<int64_t>(L.by_owner[static_cast<size_t>(r)].size());
+    // next level: coarsen(sq) over the plan's groups, labels by common membership
+    int64_t ng = 0;
+    for (int64_t b = 0; b < M; ++b) ng = std::max(ng, p.plan_assign[static_cast<size_t>(at + b)] + 1);
+    std::vector<int64_t> gof(static_cast<size_t>(M)), nl(static_cast<size_t>(ng), -2);
+    for (int64_t b = 0; b < M; ++b) {
+      const int64_t g = p.plan_assign[static_cast<size_t>(at + b)];
+      gof[static_cast<size_t>(b)] = g;
+      int64_t& v = nl[static_cast<size_t>(g)];
+      v = v == -2 ? labels[static_cast<size_t>(b)] : (v == labels[static_cast<size_t>(b)] ? v : -1);
+    }
+    at += M;
+    std::vector<std::vector<int>> rows(static_cast<size_t>(ng));
+    for (int64_t i = 0; i < M; ++i)
+      for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e)
+        rows[static_cast<size_t>(gof[static_cast<size_t>(i)])].push_back(static_cast<int>(gof[static_cast<size_t>(P.scol[static_cast<size_t>(e)])]));
+    bptr.assign(static_cast<size_t>(ng + 1), 0);
+    bcol.clear();
+    for (int64_t g = 0; g < ng; ++g) {
+      auto& r = rows[static_cast<size_t>(g)];
+      std::sort(r.begin(), r.end());
+      r.erase(std::unique(r.begin(), r.end()), r.end());
+      bcol.insert(bcol.end(), r.begin(), r.end());
+      bptr[static_cast<size_t>(g + 1)] = static_cast<int64_t>(bcol.size());
+    }
+    labels = std::move(nl);
+    M = ng;
+  }
+  return lv;
+}
+
 // CEFactorization::validate (proj/src/factorization.cpp:272-334), run at the end of every
 // ce_factorize like the reference's (:459): structure on the host from the driver's arrays,
 // basis orthogonality (<= 1e-12) and lower-triangular pivots on the device (validate.cu), one
@@ -1059,8 +1290,17 @@ void validate_factor(Factor& F, cudaStream_t s) {
 }
 
 Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, const ce_strategy* st,
-                  const ce_factor_opts* op, int64_t* shift_total) {
+                  const ce_factor_opts* op, int64_t* shift_total, const ShardSpec* shard) {
   const double t_start = now_s();
+  if (shard && (shard->n_ranks < 1 || shard->rank < 0 || shard->rank >= shard->n_ranks || shard->n_boxes < 1 ||
+                !shard->bcast || static_cast<int64_t>(shard->box_l1.size()) != A->m))
+    throw std::invalid_argument("sharded factorization: invalid shard spec (ranks, boxes, labels, broadcast)");
+  std::vector<int64_t> labels;  // box label of every block of the current level (-1: mixed)
+  if (shard) {
+    labels = shard->box_l1;
+    for (int64_t v : labels)
+      if (v < -1 || v >= shard->n_boxes) throw std::invalid_argument("sharded factorization: box label out of range");
+  }
   cudaStream_t s = ctx->stream;
   const int64_t dense_threshold = op ? op->dense_threshold : 2048;
   const int64_t max_levels = op ? op->max_levels : 64;
@@ -1142,6 +1382,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     }
 
     LevelFactor LF;
+    std::function<void()> shard_post;  // sharded level: exchanges after the pending rotation
     LF.M = cur.M;
     LF.dim = cur.dim;
     LF.pattern_blocks = cur.lower_blocks;
@@ -1318,11 +1559,107 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       d_trace.zero(s);
       a.trace = d_trace.p;
     }
+    // sharded level: phase split, per-phase tickets
+    ShardLevel SL;
+    const bool sharded_level = shard && shard->n_ranks >= 1 && [&] {
+      SL = shard_level(*shard, cur, labels);
+      return SL.prefix > 0;
+    }();
+    DevArray<int> d_it1r, d_it1p, d_it3r, d_it3p, d_foreign;
+    int64_t n_it1 = 0, n_it3 = 0;
+    if (sharded_level) {
+      std::vector<int> r1, p1, r3, p3;
+      build_tickets(cur, &SL.own1, r1, p1);
+      build_tickets(cur, &SL.phase3, r3, p3);
+      n_it1 = static_cast<int64_t>(r1.size());
+      n_it3 = static_cast<int64_t>(r3.size());
+      d_it1r.upload(r1, s);
+      d_it1p.upload(p1, s);
+      d_it3r.upload(r3, s);
+      d_it3p.upload(p3, s);
+      d_foreign.upload(SL.foreign1, s);
+      F->shard.phase1_rows += SL.prefix;
+      F->shard.phase3_rows += cur.M - SL.prefix;
+      F->shard.own_rows += static_cast<int64_t>(SL.by_owner[static_cast<size_t>(shard->rank)].size());
+    }
     Events ev_lvl, ev_sw;
     const double h_t1 = now_s();
     CE_CUDA(cudaEventRecord(ev_lvl.a, s));
     CE_CUDA(cudaEventRecord(ev_sw.a, s));
-    launch_sweep(a, grid, smem, s);
+    if (!sharded_level) {
+      launch_sweep(a, grid, smem, s);
+    } else {
+      // phase 1: this rank's box-interior rows, no communication
+      a.item_row = d_it1r.p;
+      a.item_part = d_it1p.p;
+      a.n_items = n_it1;
+      if (n_it1 > 0) launch_sweep(a, static_cast<int>(std::min<int64_t>(grid, n_it1)), smem, s);
+      CE_CUDA(cudaGetLastError());
+      shard_check_status(*shard, s, d_err.p);
+      int h0 = 0;
+      CE_CUDA(cudaMemcpy(&h0, d_err.p, sizeof h0, cudaMemcpyDeviceToHost));
+      if (h0 == 0) {
+        // E1: phase-1 rows' integers, then every within-box block the interface rows touch
+        shard_exchange_ints(*shard, s, SL, LF, F->shard);
+        std::vector<char> mark(static_cast<size_t>(cur.nslots), 0);
+        std::vector<Seg> segs;
+        auto add_block = [&](int64_t x, int64_t y, std::vector<char>& mk, std::vector<Seg>& out, bool corner) {
+          const int64_t lx = labels[static_cast<size_t>(x)], ly = labels[static_cast<size_t>(y)];
+          if (lx < 0 || lx != ly) return;
+          const int64_t hi = std::max(x, y), lo2 = std::min(x, y);
+          const int64_t sl = sq_slot_of(cur, hi, lo2);
+          if (sl < 0 || mk[static_cast<size_t>(sl)]) return;
+          mk[static_cast<size_t>(sl)] = 1;
+          const int bh = cur.bsz[static_cast<size_t>(hi)], bl = cur.bsz[static_cast<size_t>(lo2)];
+          const int rr = corner ? LF.rank[static_cast<size_t>(hi)] : bh, cc = corner ? LF.rank[static_cast<size_t>(lo2)] : bl;
+          if (rr > 0 && cc > 0) out.push_back({cur.slot_off[static_cast<size_t>(sl)], rr, cc, bl, shard->owner(lx)});
+        };
+        auto footprint = [&](int64_t i, auto&& add) {  // blocks row i reads / writes in its sweep
+          for (int64_t e = cur.sptr[static_cast<size_t>(i)]; e < cur.sptr[static_cast<size_t>(i + 1)]; ++e)
+            add(i, cur.scol[static_cast<size_t>(e)]);
+          const int64_t c0 = cur.cptr[static_cast<size_t>(i)], c1 = cur.cptr[static_cast<size_t>(i + 1)];
+          for (int64_t x = c0; x < c1; ++x)
+            for (int64_t y = x; y < c1; ++y) add(cur.ccol[static_cast<size_t>(x)], cur.ccol[static_cast<size_t>(y)]);
+        };
+        for (int64_t i = SL.prefix; i < cur.M; ++i)
+          footprint(i, [&](int64_t x, int64_t y) { add_block(x, y, mark, segs, false); });
+        shard_exchange(*shard, s, store.p, std::move(segs), F->shard);
+        // phase 3: every interface row on every rank; the other ranks' phase-1 rows are done
+        launch_precomplete(d_foreign.p, static_cast<int64_t>(SL.foreign1.size()), dcur.target.p, dcur.pan_ptr.p,
+                           d_done.p, d_pdone.p, d_bready.p, s);
+        d_ticket.zero(s);
+        a.item_row = d_it3r.p;
+        a.item_part = d_it3p.p;
+        a.n_items = n_it3;
+        if (n_it3 > 0) launch_sweep(a, static_cast<int>(std::min<int64_t>(grid, n_it3)), smem, s);
+        CE_CUDA(cudaGetLastError());
+        shard_check_status(*shard, s, d_err.p);
+        // after the pending rotation below: E2 (factor rows) and E3 (retained corners)
+        shard_post = [&, mark]() mutable {
+          std::vector<Seg> fsegs, bsegs, ssegs, csegs;
+          for (int r = 0; r < shard->n_ranks; ++r)
+            for (int i : SL.by_owner[static_cast<size_t>(r)]) {
+              const size_t iu = static_cast<size_t>(i);
+              const int64_t b = cur.bsz[iu];
+              fsegs.push_back({cur.chol_off[iu], 1, static_cast<int>(b * b + (b + cur.csum[iu]) * b), 0, r});
+              bsegs.push_back({cur.basis_off[iu], 1, static_cast<int>(b * b), 0, r});
+              const int64_t ns = std::min<int64_t>(b, cur.fsum[iu]);
+              if (ns > 0) ssegs.push_back({cur.sigma_off[iu], 1, static_cast<int>(ns), 0, r});
+            }
+          for (auto* v : {&fsegs, &bsegs, &ssegs})
+            for (Seg& g : *v) g.ld = g.cols;
+          shard_exchange(*shard, s, LF.d_fac.p, std::move(fsegs), F->shard);
+          shard_exchange(*shard, s, LF.d_basis.p, std::move(bsegs), F->shard);
+          shard_exchange(*shard, s, LF.d_sigma.p, std::move(ssegs), F->shard);
+          // E3: retained corners of the other within-box blocks the phase-1 rows wrote
+          LF.d_rank.download(LF.rank, s);
+          CE_CUDA(cudaStreamSynchronize(s));
+          for (int64_t i = 0; i < SL.prefix; ++i)
+            footprint(i, [&](int64_t x, int64_t y) { add_block(x, y, mark, csegs, true); });
+          shard_exchange(*shard, s, store.p, std::move(csegs), F->shard);
+        };
+      }
+    }
     CE_CUDA(cudaGetLastError());
     CE_CUDA(cudaEventRecord(ev_sw.b, s));
     int herr[4] = {0, 0, 0, 0};
@@ -1380,6 +1717,10 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     }
     launch_pending_rotation(a, s);
     CE_CUDA(cudaGetLastError());
+    if (shard_post) {
+      shard_post();
+      shard_post = nullptr;
+    }
     LF.d_rank.download(LF.rank, s);
     LF.d_width.download(LF.width, s);
     LF.d_has_basis.download(LF.has_basis, s);
@@ -1585,6 +1926,18 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     }
     elim_total += LF.n_elim;
 
+    if (shard) {  // next level's box labels: a group's common label, -1 when its members differ
+      std::vector<int64_t> nl(static_cast<size_t>(nM), -1);
+      for (int64_t g = 0; g < ng; ++g) {
+        if (alive[static_cast<size_t>(g)] < 0) continue;
+        const auto& mem = cur_groups[static_cast<size_t>(g)];
+        int64_t v = labels[static_cast<size_t>(mem[0])];
+        for (int64_t b : mem)
+          if (labels[static_cast<size_t>(b)] != v) v = -1;
+        nl[static_cast<size_t>(alive[static_cast<size_t>(g)])] = v;
+      }
+      labels = std::move(nl);
+    }
     std::vector<int64_t> next_alive(plan_groups.size(), -1);
     for (size_t g = 0; g < plan_groups.size(); ++g)
       if (slot_of_group[g] >= 0) next_alive[g] = alive[static_cast<size_t>(slot_of_group[g])];

@@ -11,8 +11,13 @@ namespace ceg {
 
 LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vector<int> bcol);
 
+// shard != nullptr: this rank's part of a subdomain-sharded factorization; the
+// returned factor is complete and identical on every rank.
 Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan, const ce_strategy* st,
-                  const ce_factor_opts* opts, int64_t* shift_total);
+                  const ce_factor_opts* opts, int64_t* shift_total, const ShardSpec* shard = nullptr);
+
+// Symbolic phase split of a sharded plan (every group alive), for ce_shard_plan_summary.
+int64_t shard_symbolic_summary(const Problem& p, const ShardSpec& spec, int64_t max_levels, int64_t* out);
 
 void apply_device(const Factor& f, const double* d_b, double* d_x, cudaStream_t s);
 void apply_tool_device(const Factor& f, int which, const double* d_x, double* d_y, cudaStream_t s);

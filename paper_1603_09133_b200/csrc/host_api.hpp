@@ -87,10 +87,33 @@ struct Problem {
   std::vector<double> values, rhs;
   int64_t join = 2;
   std::vector<int64_t> plan_level_blocks, plan_assign;
+  std::vector<int64_t> box_of_block;  // CE_PLAN_SHARDED: subdomain (box) of every level-1 block
   void build(int cfg_id, int64_t nx, int64_t ny, int64_t nz, int plan_kind = 0);  // CE_PLAN_*
   // reference `file` problems (io.cpp): matrix.mtx + optional plan.txt / rhs.txt
   void load(const char* matrix_path, const char* plan_path, const char* rhs_path, int64_t block);
   void save(const char* matrix_path, const char* plan_path, const char* rhs_path) const;
+};
+
+// CE_PLAN_SHARDED geometry (problem.cpp): 8 boxes; box of cell q of grid g, interior flag.
+constexpr int64_t kShardBoxes = 8;
+int64_t shard_box(const int64_t* g, int64_t q, int dims, bool* interior);
+
+// Subdomain-sharded factorization (ce_factorize_sharded): this rank's index, the
+// rank count, the box label of every level-1 block (box -> owner rank box * n_ranks / n_boxes)
+// and the in-place device broadcast every rank calls in the same order.
+struct ShardSpec {
+  int rank = 0, n_ranks = 1;
+  int64_t n_boxes = 0;
+  std::vector<int64_t> box_l1;
+  int (*bcast)(void* user, void* dev_ptr, int64_t bytes, int root) = nullptr;
+  void* user = nullptr;
+  int owner(int64_t box) const { return static_cast<int>(box * n_ranks / n_boxes); }
+};
+
+// Per-factorization sharding statistics (LevelStats-like, host-side).
+struct ShardStats {
+  int64_t phase1_rows = 0, phase3_rows = 0, own_rows = 0;
+  double exchange_bytes = 0.0, exchange_seconds = 0.0;
 };
 
 struct Context {
@@ -135,6 +158,7 @@ struct LevelPlan {
   std::vector<int> order;            // rows in wave (topological) order of the sq-DAG
   std::vector<int64_t> wave;         // wave index of every row
   std::vector<int> item_row, item_part;  // ticket -> (row, task index within the row)
+  std::vector<std::vector<int>> rest_of, urg_of;  // per row: Schur pair tasks after / with the next wave
   std::vector<int> nA1, nA3, nB;     // per-row task counts (sweep.cu header)
   std::vector<int> nleaf;            // per-row TSQR tree leaves (nA1 = all tree nodes)
   std::vector<int64_t> pan_ptr, rs_off;
@@ -190,6 +214,7 @@ struct Factor {
   int64_t shift_retries = 0;
   double total_seconds = 0.0, device_seconds = 0.0, sweep_seconds = 0.0;
   double validate_seconds = 0.0, max_orth_error = 0.0;  // validate(), factorization.cpp:272-334
+  ShardStats shard;                                       // zero unless ce_factorize_sharded
   double apply_alg_bytes = 0.0;  // SURVEY.md §8d apply byte count (forward + backward + vector passes)
   double factor_blocks = 0.0, predicted_factor_blocks = 0.0;
   int64_t l_scalar_nnz = 0, l_payload_bytes = 0, q_payload_bytes = 0, tail_bytes = 0;

@@ -31,6 +31,15 @@ void launch_validate_level(int64_t M, const int* bsz, const unsigned char* has_b
                            const int64_t* basis_off, const int* width, const double* fac, const int64_t* chol_off,
                            double tol, unsigned long long* d_out, cudaStream_t s);
 
+// Sharded factorization exchange (shard.cu): 2-D segments <-> a contiguous buffer, per-row
+// integers <-> 5 doubles per row, and completion of the rows another rank swept.
+void launch_segments(double* base, double* buf, const int64_t* off, const int* rows, const int* cols, const int* ld,
+                     const int64_t* boff, int64_t nseg, bool to_buf, cudaStream_t s);
+void launch_row_ints(const int* rows, int64_t n, int* rank, int* width, unsigned char* has_basis, int* fcols, int* nsig,
+                     double* buf, bool to_buf, cudaStream_t s);
+void launch_precomplete(const int* rows, int64_t n, const int* target, const int64_t* pan_ptr, int* done, int* pdone,
+                        int* bready, cudaStream_t s);
+
 // Launch accounting (every launcher calls note_launch once per kernel launch).
 void note_launch(int64_t n = 1);
 int64_t launch_count();

@@ -41,6 +41,32 @@ double normal01(std::uint64_t seed, std::uint64_t stream, std::uint64_t i) {
   return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
 }
 
+}  // namespace
+
+// CE_PLAN_SHARDED boxes: 8 spatial subdomains, 4 x 2 (2-D) or 2 x 2 x 2 (3-D), of any level's
+// cell grid g; box k along an axis holds the cells x with floor(x * B / g) = k.  A cell is a box
+// interior cell when it is >= 2 cells away from every box face shared with another box: with
+// all-axis merges a row's squared pattern stays within Chebyshev distance 2 in cells at every
+// level, so an interior row's whole squared-pattern row is inside its box.
+// Identical in oracle/problems.cpp (shard_box).
+int64_t shard_box(const int64_t* g, int64_t q, int dims, bool* interior) {
+  const int64_t B[3] = {dims == 2 ? 4 : 2, 2, dims == 2 ? 1 : 2};
+  const int64_t x[3] = {q % g[0], (q / g[0]) % g[1], q / (g[0] * g[1])};
+  int64_t box = 0, stride = 1;
+  bool inner = true;
+  for (int a = 0; a < 3; ++a) {
+    const int64_t k = x[a] * B[a] / g[a];
+    const int64_t lo = (k * g[a] + B[a] - 1) / B[a], hi = ((k + 1) * g[a] + B[a] - 1) / B[a] - 1;
+    if (!(lo == 0 || x[a] - lo >= 2) || !(hi == g[a] - 1 || hi - x[a] >= 2)) inner = false;
+    box += k * stride;
+    stride *= B[a];
+  }
+  if (interior) *interior = inner;
+  return box;
+}
+
+namespace {
+
 int ilog2_exact(int64_t block) {
   int b = 0;
   while ((int64_t{1} << (b + 1)) <= block) ++b;
@@ -83,21 +109,33 @@ void Problem::build(int cfg_id, int64_t onx, int64_t ony, int64_t onz, int plan_
   else shape = {int64_t{1} << ((lb + 2) / 3), int64_t{1} << ((lb + 1) / 3), int64_t{1} << (lb / 3)};
   const int64_t nc[3] = {(nx + shape[0] - 1) / shape[0], (ny + shape[1] - 1) / shape[1], (nz + shape[2] - 1) / shape[2]};
   // position -> lexicographic cell id on a cells grid; colour-major (mod-3 colouring) for
-  // CE_PLAN_MERGE_ALL_COLORED, so that one colour's rows share no squared-pattern entry
-  const bool merge_all_axes = plan_kind >= 1, colored = plan_kind == 2;
+  // CE_PLAN_MERGE_ALL_COLORED, so that one colour's rows share no squared-pattern entry;
+  // CE_PLAN_SHARDED: box-interior cells first, box by box (each colour-major), then every
+  // interface cell (colour-major) -- DESIGN.md §7, shard_box()
+  const bool merge_all_axes = plan_kind >= 1, colored = plan_kind >= 2, sharded = plan_kind == 3;
   auto order = [&](const int64_t* g) {
     std::vector<int64_t> ord(static_cast<size_t>(g[0] * g[1] * g[2]));
     for (size_t q = 0; q < ord.size(); ++q) ord[q] = static_cast<int64_t>(q);
     if (colored) {
-      auto color = [&](int64_t q) {
+      auto key = [&](int64_t q) {
         const int64_t x = q % g[0], y = (q / g[0]) % g[1], z = q / (g[0] * g[1]);
-        return x % 3 + 3 * (y % 3) + 9 * (z % 3);
+        const int64_t color = x % 3 + 3 * (y % 3) + 9 * (z % 3);
+        int64_t section = 0;
+        if (sharded) {
+          bool interior = false;
+          const int64_t box = shard_box(g, q, dims, &interior);
+          section = interior ? box : kShardBoxes;
+        }
+        return section * 27 + color;
       };
-      std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return color(a) < color(b); });
+      std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return key(a) < key(b); });
     }
     return ord;
   };
   std::vector<int64_t> ord = order(nc);
+  box_of_block.clear();
+  if (sharded)
+    for (const int64_t q : ord) box_of_block.push_back(shard_box(nc, q, dims, nullptr));
   perm.clear();
   perm.reserve(static_cast<size_t>(N));
   std::vector<int64_t> sizes;

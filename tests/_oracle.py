@@ -102,7 +102,7 @@ class OProblem:
     @staticmethod
     def config(cfg, nx=0, ny=0, nz=0, plan="reference"):
         h = vp()
-        _check(lib.oracle_problem_config_plan(cfg, nx, ny, nz, {"reference": 0, "merge_all_axes": 1, "merge_all_colored": 2}[plan], C.byref(h)))
+        _check(lib.oracle_problem_config_plan(cfg, nx, ny, nz, {"reference": 0, "merge_all_axes": 1, "merge_all_colored": 2, "sharded": 3}[plan], C.byref(h)))
         return OProblem(h)
 
     @staticmethod

@@ -201,6 +201,9 @@ def test_fullsize_free_run(problems, cfg, plan):
         r_o = fx["retained"][lv[li]]
         level_agree.append(float(np.mean(r_g == r_o)) if len(r_g) == len(r_o) else 0.0)
     sig_l1, n_sig = _sigma_check(f, fx, level_filter={0})
+    # the oracle's own level-1 sigma movement under the 1e-16 perturbation of A (free run)
+    sig_sens = _sigma_sensitivity(fx, _fixture(cfg, plan, "perturbed"))
+    sig_allowed = max(SIGMA_TOL, 10 * sig_sens) if sig_sens is not None else SIGMA_TOL
     errs = _op_errors(f, fx, p.n)
     rep, _ = ce.pcg(a, p.n, p.rhs, f, ce.PcgOptions(tol=p.tol))
     its_o = int(fx["pcg_iterations"])
@@ -208,12 +211,12 @@ def test_fullsize_free_run(problems, cfg, plan):
                  level1_rank_flips=len(flips), level1_flips_near_threshold=int(sum(near)) - roundoff,
                  level1_flips_roundoff_fill=roundoff,
                  rank_agreement_by_level=level_agree, level1_sigma_err=sig_l1, level1_sigma_rows=n_sig,
-                 sigma_allowed=SIGMA_TOL, operator_err=errs, pcg_iterations=rep.iterations, pcg_iterations_oracle=its_o,
+                 sigma_allowed=sig_allowed, oracle_sigma_sensitivity_1e16=sig_sens, operator_err=errs, pcg_iterations=rep.iterations, pcg_iterations_oracle=its_o,
                  pcg_true_residual=rep.final_true_residual, pcg_target=p.tol,
                  max_orth_error=st["max_orth_error"], validate_seconds=st["validate_seconds"])
     _report(entry)
     assert all(near), f"level-1 rank flips away from the threshold: {flips[:10]}"
-    assert sig_l1 <= SIGMA_TOL, entry
+    assert sig_l1 <= sig_allowed, entry
     assert abs(rep.iterations - its_o) <= 1 and rep.converged and rep.final_true_residual <= p.tol, entry
     assert st["max_orth_error"] <= 1e-12
 

@@ -37,10 +37,11 @@ CASES = [(1, (0, 0, 0), 2048, "reference"), (2, (64, 64, 0), 2048, "reference"),
          (2, (128, 128, 0), 512, "reference"), (4, (16, 16, 16), 512, "reference"), (5, (16, 16, 16), 512, "reference"),
          (2, (128, 128, 0), 256, "merge_all_axes"), (4, (32, 16, 16), 2048, "merge_all_axes"),
          (2, (128, 128, 0), 256, "merge_all_colored"), (5, (32, 16, 16), 2048, "merge_all_colored"),
-         (3, (96, 128, 0), 256, "merge_all_colored"), (1, (0, 0, 0), 256, "merge_all_colored")]
+         (3, (96, 128, 0), 256, "merge_all_colored"), (1, (0, 0, 0), 256, "merge_all_colored"),
+         (2, (256, 256, 0), 512, "sharded")]
 IDS = ["cfg1-128", "cfg2-64", "cfg3-64", "cfg2-128", "cfg4-16", "cfg5-16", "cfg2-128-merge_all",
        "cfg4-32x16x16-merge_all", "cfg2-128-colored", "cfg5-32x16x16-colored", "cfg3-96x128-colored",
-       "cfg1-128-colored"]
+       "cfg1-128-colored", "cfg2-256-sharded"]
 
 
 def _dump(f, d, name):
