@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the colour-major plan variant line")
+    ap.add_argument("--no-shard", action="store_true", help="skip the subdomain-sharded factorization line")
     ap.add_argument("--plan", default="reference", choices=["reference", "merge_all_axes", "merge_all_colored", "sharded"],
                     help="plan family: the reference's geometric_block_ordering (join 2, one axis per level) or "
                          "every axis merging by 2 per level (J = 2^d; the 3-D configs at full size, DESIGN.md)")
@@ -263,12 +264,20 @@ def run_product(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test scaffolding (tests/test_bench_contract.py): every rank on GPU 0 with the gloo backend,
+    # to run the N > 1 code path on a one-GPU box; the driver's runs use one GPU per rank + NCCL
+    if os.environ.get("CE_BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("CE_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if dist:
@@ -363,7 +372,7 @@ def run_product(args):
         rep2, x2 = ce.pcg(a2, n, pin_b, f2, popts)
         e2e_t.append(time.time() - t0)
         del f2, a2
-    e2e_val = world * n / allmax(statistics.mean(e2e_t))
+    e2e_val = world * n / allmax(statistics.mean(e2e_t)) if e2e_t else None
 
     # Preconditioner apply and matvec on their own (PCG's two operators), CUDA events on the
     # library stream, against the HBM roofline with SURVEY.md §8d's apply byte count.
@@ -455,6 +464,42 @@ def run_product(args):
             variant["cpu_baseline_value"] = r["unknowns_per_sec"]
         del va, vb
 
+    # Subdomain-sharded factorization: ALL ranks factor ONE
+    # CE_PLAN_SHARDED problem of this config together (strong scaling), exchanging blocks over
+    # NCCL; at N=1 the same plan on one GPU is the reference point of the scaling series.
+    shard_line = None
+    if not args.no_shard:
+        try:
+            sprob = ce.Problem(args.cfg, *args.grid, plan="sharded")
+            sa = ce.DeviceMatrix(sprob.matrix(), ctx)
+            comm = ce.ShardComm(device=dev) if dist else ce.LocalShardComm()
+            srec, sst = [], None
+            for k in range(5):
+                barrier()
+                with torch.cuda.stream(stream):
+                    e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+                    e0.record(stream)
+                    sf = ce.ce_factorize_sharded(sa, sprob.plan, sprob.strategy(), sprob.box_of_block, comm,
+                                                 ce.FactorOptions(), ctx=ctx)
+                    e1.record(stream)
+                e1.synchronize()
+                if k >= 2:  # 2 warm-up, 3 timed
+                    srec.append(e0.elapsed_time(e1) * 1e-3)
+                    sst = sf.stats
+                del sf
+            st_t = allmax(sum(srec))
+            shard_line = {"plan": "sharded", "scaling": "strong", "n_gpus": world, "steps": len(srec), "warmup": 2,
+                          "value": sprob.n * len(srec) / st_t, "unit": "unknowns/s",
+                          "factor_ms": 1e3 * st_t / len(srec),
+                          "interior_rows": sst["shard_phase1_rows"], "own_rows_rank0": sst["shard_own_rows"],
+                          "interface_rows": sst["shard_phase3_rows"],
+                          "exchange_bytes_rank0": sst["shard_exchange_bytes"],
+                          "exchange_ms_rank0": 1e3 * sst["shard_exchange_seconds"],
+                          "comm": "NCCL broadcast (torch.distributed)" if dist else "none (1 rank)"}
+            del sa
+        except Exception as e:  # noqa: BLE001 -- reported, never fatal to the headline line
+            shard_line = {"plan": "sharded", "error": repr(e)[:400]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         grid = CPU_SAMPLE_GRID[args.cfg]
@@ -501,6 +546,8 @@ def run_product(args):
             line["plan_variant"] = variant
         if extra:
             line["extra_configs"] = extra
+        if shard_line:
+            line["sharded"] = shard_line
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -18,6 +18,7 @@ from .ce import (  # noqa: F401
     Context,
     DeviceMatrix,
     FactorOptions,
+    LocalShardComm,
     MinresOptions,
     PcgOptions,
     Problem,
@@ -40,6 +41,7 @@ __all__ = [
     "Context",
     "DeviceMatrix",
     "FactorOptions",
+    "LocalShardComm",
     "MinresOptions",
     "PcgOptions",
     "Problem",

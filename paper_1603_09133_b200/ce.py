@@ -409,6 +409,19 @@ class ShardComm:
             return 1
 
 
+class LocalShardComm:
+    """The one-rank communicator: ce_factorize_sharded on a single GPU (every box owned here,
+    every broadcast a no-op) -- the 1-GPU point of a sharded scaling series."""
+
+    def __init__(self):
+        self.rank, self.world, self.error, self.calls, self.bytes = 0, 1, None, 0, 0
+
+        def _b(user, ptr, nbytes, root):
+            self.calls += 1
+            return 0
+        self.fn = L.BcastFn(_b)
+
+
 def ce_factorize_sharded(a, plan: CoarseningPlan, strategy: CompressionStrategy, box_of_block, comm: ShardComm,
                          opts: Optional[FactorOptions] = None, n_boxes: int = 8,
                          ctx: Optional[Context] = None) -> CEFactorization:

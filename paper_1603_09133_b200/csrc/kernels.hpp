@@ -17,9 +17,12 @@ constexpr int kApplyWmax = 256;
 // while the row has few panels (the wave needs the parallelism: A/B on cfg2, g = 2 / 3 / 5 lose
 // 4 / 8 / 20%), more once a row has hundreds of panels (3-D deep levels, each panel is staged
 // once per pair otherwise).
+#ifndef CE_PAIR_DIV
+#define CE_PAIR_DIV 48  // panels per extra pair in a Schur task (A/B builds: -DCE_PAIR_DIV=...)
+#endif
 __host__ __device__ inline int row_pair_group(int forced, int np) {
   if (forced > 0) return forced;
-  const int g = np / 48;
+  const int g = np / CE_PAIR_DIV;
   return g < 1 ? 1 : (g > 8 ? 8 : g);
 }  // largest eliminated width per block the apply sweeps stage in shared memory
 

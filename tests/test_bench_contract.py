@@ -49,3 +49,26 @@ def test_product_line_cfg1():
     assert ra["bound"] == "hbm" and ra["algorithmic_bytes"] > 0 and 0 < ra["frac"] < 1 and ra["matvec"]["ms"] > 0
     assert d["validate"]["max_orth_error"] <= 1e-12 and d["validate"]["seconds"] > 0
     assert "extra_configs" not in d
+    sh = d["sharded"]
+    assert "error" not in sh, sh
+    assert sh["value"] > 0 and sh["scaling"] == "strong" and sh["interior_rows"] > 0
+
+
+@pytest.mark.gpu
+def test_product_line_two_ranks_one_gpu():
+    """bench.py's N > 1 code path (barriers, max-over-ranks, the sharded factorization's
+    exchanges) with 2 ranks on the test box's one GPU over gloo."""
+    port = 29500 + os.getpid() % 1000
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--cfg", "1",
+           "--steps", "2", "--warmup", "3", "--e2e-steps", "1", "--no-cpu-baseline", "--no-extra", "--no-variants"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
+                         env=dict(os.environ, CE_BENCH_SAME_DEVICE="1", CE_BENCH_BACKEND="gloo"))
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    sh = d["sharded"]
+    assert "error" not in sh, sh
+    assert sh["n_gpus"] == 2 and sh["own_rows_rank0"] < sh["interior_rows"] and sh["exchange_bytes_rank0"] > 0
