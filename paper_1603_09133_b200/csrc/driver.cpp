@@ -378,8 +378,10 @@ void build_tickets(const LevelPlan& P, const std::vector<char>* mask, std::vecto
                    std::vector<int>& item_part) {
   const int64_t M = P.M;
   const std::vector<int64_t>& wave = P.wave;
-  item_row.clear();
-  item_part.clear();
+  // The order is, for every wave w: [leaves(w)] [rest(w-1)] [combines(w)] [A2(w)] [strips(w)]
+  // [urgent(w)], rows in `order` within each segment.  Every row's share of each segment is
+  // known up front, so segment starts come from prefix sums over the rows and the rows fill
+  // their slots in parallel (the tickets of one level are millions of items).
   std::vector<int64_t> wstart;
   for (int64_t k = 0; k < M;) {
     wstart.push_back(k);
@@ -388,27 +390,69 @@ void build_tickets(const LevelPlan& P, const std::vector<char>* mask, std::vecto
   }
   wstart.push_back(M);
   const int64_t nw = static_cast<int64_t>(wstart.size()) - 1;
-  auto emit_rows = [&](int64_t w, auto&& parts) {
-    if (w < 0) return;
-    for (int64_t k = wstart[static_cast<size_t>(w)]; k < wstart[static_cast<size_t>(w + 1)]; ++k) {
-      const int row = P.order[static_cast<size_t>(k)];
-      if (mask && !(*mask)[static_cast<size_t>(row)]) continue;
-      parts(row, static_cast<size_t>(row));
+  auto cnt = [&](int row, int seg) -> int64_t {  // items of `row` in segment seg (0..5)
+    const size_t r = static_cast<size_t>(row);
+    if (mask && !(*mask)[r]) return 0;
+    switch (seg) {
+      case 0: return P.nleaf[r];
+      case 1: return static_cast<int64_t>(P.rest_of[r].size());
+      case 2: return P.nA1[r] - P.nleaf[r];
+      case 3: return 1;
+      case 4: return P.nA3[r];
+      default: return static_cast<int64_t>(P.urg_of[r].size());
     }
   };
-  auto push = [&](int row, int p) {
-    item_row.push_back(row);
-    item_part.push_back(p);
+  // start[k * 6 + seg]: first ticket of the row at order position k in segment seg
+  std::vector<int64_t> start(static_cast<size_t>(M) * 6, 0), segsum(static_cast<size_t>(nw) * 6, 0);
+  parallel_rows(nw, [&](int64_t w0, int64_t w1) {
+    for (int64_t w = w0; w < w1; ++w)
+      for (int seg = 0; seg < 6; ++seg) {
+        int64_t t = 0;
+        for (int64_t k = wstart[static_cast<size_t>(w)]; k < wstart[static_cast<size_t>(w + 1)]; ++k) {
+          start[static_cast<size_t>(k) * 6 + static_cast<size_t>(seg)] = t;
+          t += cnt(P.order[static_cast<size_t>(k)], seg);
+        }
+        segsum[static_cast<size_t>(w) * 6 + static_cast<size_t>(seg)] = t;
+      }
+  });
+  // segment bases in emission order
+  std::vector<int64_t> base(static_cast<size_t>(nw) * 6, 0);
+  int64_t at = 0;
+  auto place = [&](int64_t w, int seg) {
+    base[static_cast<size_t>(w) * 6 + static_cast<size_t>(seg)] = at;
+    at += segsum[static_cast<size_t>(w) * 6 + static_cast<size_t>(seg)];
   };
   for (int64_t w = 0; w <= nw; ++w) {
-    if (w < nw) emit_rows(w, [&](int row, size_t r) { for (int p = 0; p < P.nleaf[r]; ++p) push(row, p); });
-    emit_rows(w - 1, [&](int row, size_t r) { for (int p : P.rest_of[r]) push(row, p); });
+    if (w < nw) place(w, 0);
+    if (w > 0) place(w - 1, 1);
     if (w == nw) break;
-    emit_rows(w, [&](int row, size_t r) { for (int p = P.nleaf[r]; p < P.nA1[r]; ++p) push(row, p); });
-    emit_rows(w, [&](int row, size_t r) { push(row, P.nA1[r]); });
-    emit_rows(w, [&](int row, size_t r) { for (int p = P.nA1[r] + 1; p <= P.nA1[r] + P.nA3[r]; ++p) push(row, p); });
-    emit_rows(w, [&](int row, size_t r) { for (int p : P.urg_of[r]) push(row, p); });
+    place(w, 2);
+    place(w, 3);
+    place(w, 4);
+    place(w, 5);
   }
+  item_row.assign(static_cast<size_t>(at), 0);
+  item_part.assign(static_cast<size_t>(at), 0);
+  parallel_rows(nw, [&](int64_t w0, int64_t w1) {
+    for (int64_t w = w0; w < w1; ++w)
+      for (int64_t k = wstart[static_cast<size_t>(w)]; k < wstart[static_cast<size_t>(w + 1)]; ++k) {
+        const int row = P.order[static_cast<size_t>(k)];
+        const size_t r = static_cast<size_t>(row);
+        if (mask && !(*mask)[r]) continue;
+        auto put = [&](int seg, int64_t j, int part) {
+          const size_t idx = static_cast<size_t>(base[static_cast<size_t>(w) * 6 + static_cast<size_t>(seg)] +
+                                                 start[static_cast<size_t>(k) * 6 + static_cast<size_t>(seg)] + j);
+          item_row[idx] = row;
+          item_part[idx] = part;
+        };
+        for (int p = 0; p < P.nleaf[r]; ++p) put(0, p, p);
+        for (size_t j = 0; j < P.rest_of[r].size(); ++j) put(1, static_cast<int64_t>(j), P.rest_of[r][j]);
+        for (int p = P.nleaf[r]; p < P.nA1[r]; ++p) put(2, p - P.nleaf[r], p);
+        put(3, 0, P.nA1[r]);
+        for (int p = 0; p < P.nA3[r]; ++p) put(4, p, P.nA1[r] + 1 + p);
+        for (size_t j = 0; j < P.urg_of[r].size(); ++j) put(5, static_cast<int64_t>(j), P.urg_of[r][j]);
+      }
+  });
 }
 
 // Numeric part: everything that depends on the block sizes.
@@ -422,32 +466,47 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
   P.bmax = 0;
   for (int b : P.bsz) P.bmax = std::max(P.bmax, b);
   P.slot_off.assign(static_cast<size_t>(P.nslots), 0);
-  int64_t off = 0;
-  for (int64_t i = 0; i < M; ++i)
-    for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e) {
-      const int j = P.scol[static_cast<size_t>(e)];
-      if (j > i) break;
-      P.slot_off[static_cast<size_t>(P.sslot[static_cast<size_t>(e)])] = off;
-      off += static_cast<int64_t>(P.bsz[static_cast<size_t>(i)]) * P.bsz[static_cast<size_t>(j)];
+  // stored lower blocks in row order: per-row sizes, prefix, then every row's offsets (parallel)
+  std::vector<int64_t> row_doubles(static_cast<size_t>(M) + 1, 0);
+  parallel_rows(M, [&](int64_t r0, int64_t r1) {
+    for (int64_t i = r0; i < r1; ++i) {
+      int64_t t = 0;
+      for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e) {
+        const int j = P.scol[static_cast<size_t>(e)];
+        if (j > i) break;
+        t += static_cast<int64_t>(P.bsz[static_cast<size_t>(i)]) * P.bsz[static_cast<size_t>(j)];
+      }
+      row_doubles[static_cast<size_t>(i) + 1] = t;
     }
-  P.store_doubles = off;
+  });
+  for (int64_t i = 0; i < M; ++i) row_doubles[static_cast<size_t>(i) + 1] += row_doubles[static_cast<size_t>(i)];
   P.csum.assign(static_cast<size_t>(M), 0);
   P.fsum.assign(static_cast<size_t>(M), 0);
   P.croff.assign(P.ccol.size(), 0);
-  P.fmax = 0;
-  for (int64_t i = 0; i < M; ++i) {
-    int64_t c = 0;
-    for (int64_t k = P.cptr[static_cast<size_t>(i)]; k < P.cptr[static_cast<size_t>(i + 1)]; ++k) {
-      P.croff[static_cast<size_t>(k)] = static_cast<int>(c);
-      c += P.bsz[static_cast<size_t>(P.ccol[static_cast<size_t>(k)])];
+  parallel_rows(M, [&](int64_t r0, int64_t r1) {
+    for (int64_t i = r0; i < r1; ++i) {
+      int64_t off = row_doubles[static_cast<size_t>(i)];
+      for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e) {
+        const int j = P.scol[static_cast<size_t>(e)];
+        if (j > i) break;
+        P.slot_off[static_cast<size_t>(P.sslot[static_cast<size_t>(e)])] = off;
+        off += static_cast<int64_t>(P.bsz[static_cast<size_t>(i)]) * P.bsz[static_cast<size_t>(j)];
+      }
+      int64_t c = 0;
+      for (int64_t k = P.cptr[static_cast<size_t>(i)]; k < P.cptr[static_cast<size_t>(i + 1)]; ++k) {
+        P.croff[static_cast<size_t>(k)] = static_cast<int>(c);
+        c += P.bsz[static_cast<size_t>(P.ccol[static_cast<size_t>(k)])];
+      }
+      P.csum[static_cast<size_t>(i)] = c;
+      int64_t f = 0;
+      for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e)
+        if (P.skind[static_cast<size_t>(e)] >= 2) f += P.bsz[static_cast<size_t>(P.scol[static_cast<size_t>(e)])];
+      P.fsum[static_cast<size_t>(i)] = f;
     }
-    P.csum[static_cast<size_t>(i)] = c;
-    int64_t f = 0;
-    for (int64_t e = P.sptr[static_cast<size_t>(i)]; e < P.sptr[static_cast<size_t>(i + 1)]; ++e)
-      if (P.skind[static_cast<size_t>(e)] >= 2) f += P.bsz[static_cast<size_t>(P.scol[static_cast<size_t>(e)])];
-    P.fsum[static_cast<size_t>(i)] = f;
-    P.fmax = std::max(P.fmax, f);
-  }
+  });
+  P.store_doubles = row_doubles[static_cast<size_t>(M)];
+  P.fmax = 0;
+  for (int64_t i = 0; i < M; ++i) P.fmax = std::max(P.fmax, P.fsum[static_cast<size_t>(i)]);
   P.chol_off.resize(static_cast<size_t>(M));
   P.g_off.resize(static_cast<size_t>(M));
   P.basis_off.resize(static_cast<size_t>(M));
@@ -947,13 +1006,19 @@ struct DevPlan {
       CE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&st.p), st.cap, cudaHostAllocDefault));
     }
     size_t off = 0;
+    // the staging copies run in parallel on the host threads (one 200 MB level plan was a
+    // 30-60 ms single-thread memcpy on the critical path between two sweeps), then every
+    // array's DMA is queued on the stream
+    struct Job {
+      void* dst;
+      const void* src;
+      size_t bytes, at;
+    };
+    std::vector<Job> jobs;
     auto put = [&](auto& d, const auto& h) {
       const size_t bytes = h.size() * sizeof(h[0]);
       d.alloc(h.size());
-      if (bytes) {
-        std::memcpy(st.p + off, h.data(), bytes);
-        CE_CUDA(cudaMemcpyAsync(d.p, st.p + off, bytes, cudaMemcpyHostToDevice, s));
-      }
+      if (bytes) jobs.push_back({d.p, h.data(), bytes, off});
       off += (bytes + 255) / 256 * 256;
     };
     put(order, P.order); put(item_row, P.item_row); put(item_part, P.item_part); put(nA1, P.nA1); put(nleaf, P.nleaf);
@@ -964,6 +1029,19 @@ struct DevPlan {
     put(offsets, P.offsets); put(skind, P.skind); put(sboff, P.sboff); put(sbsz, P.sbsz); put(sroff, P.sroff);
     put(sdiag, P.sdiag); put(target, P.target); put(leaf_ptr, P.leaf_ptr); put(leaf_e, P.leaf_e);
     put(strip_ptr, P.strip_ptr); put(strip_e, P.strip_e); put(sq_pan, P.sq_pan);
+    constexpr size_t kChunk = size_t{1} << 20;
+    std::vector<std::pair<size_t, size_t>> pieces;  // (job, first byte) of 1 MB pieces
+    for (size_t j = 0; j < jobs.size(); ++j)
+      for (size_t b = 0; b < jobs[j].bytes; b += kChunk) pieces.emplace_back(j, b);
+    char* const stage = st.p;  // `st` is thread_local: the worker threads must not name it
+    parallel_rows(static_cast<int64_t>(pieces.size()), [&](int64_t r0, int64_t r1) {
+      for (int64_t k = r0; k < r1; ++k) {
+        const Job& jb = jobs[pieces[static_cast<size_t>(k)].first];
+        const size_t b = pieces[static_cast<size_t>(k)].second, n = std::min(kChunk, jb.bytes - b);
+        std::memcpy(stage + jb.at + b, static_cast<const char*>(jb.src) + b, n);
+      }
+    });
+    for (const Job& jb : jobs) CE_CUDA(cudaMemcpyAsync(jb.dst, stage + jb.at, jb.bytes, cudaMemcpyHostToDevice, s));
   }
 };
 
@@ -1715,8 +1793,15 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
         std::fclose(fp);
       }
     }
+    Events ev_pend;
+    if (profile) CE_CUDA(cudaEventRecord(ev_pend.a, s));
     launch_pending_rotation(a, s);
     CE_CUDA(cudaGetLastError());
+    if (profile) {
+      CE_CUDA(cudaEventRecord(ev_pend.b, s));
+      CE_CUDA(cudaStreamSynchronize(s));
+      std::fprintf(stderr, "[ce-profile] level %zu pending-rotation kernel %.2f ms\n", li + 1, 1e3 * ev_pend.seconds());
+    }
     if (shard_post) {
       shard_post();
       shard_post = nullptr;
@@ -1784,6 +1869,20 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
         at += LF.rank[static_cast<size_t>(b)];
       }
     }
+    // next level's numeric plan on a host thread (it is on the critical path to the next sweep);
+    // the gathers, their checks and uploads below run meanwhile
+    LevelPlan next;
+    std::future<void> next_fut;
+    if (nM > 0)
+      next_fut = std::async(std::launch::async, [&]() {
+        LevelPlan sp = spec.get();
+        if (nM == ng) {
+          next = std::move(sp);
+          plan_numeric(next, nbsz);
+        } else {
+          next = plan_level(nbsz, nptr, ncol);
+        }
+      });
     // gathers (factorization.cpp:76-85)
     std::vector<int64_t> elim, kept;
     for (int64_t b = 0; b < cur.M; ++b)
@@ -1805,23 +1904,25 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     LF.d_elim_gather.upload(elim, s);
     LF.d_kept_gather.upload(kept, s);
 
-    LevelPlan next;
     DevPlan dnext;
     const double h_t2 = now_s();
     double h_t3 = h_t2;
     if (nM > 0) {
-      LevelPlan sp = spec.get();
-      if (nM == ng) {
-        next = std::move(sp);
-        plan_numeric(next, nbsz);
-      } else {
-        next = plan_level(nbsz, nptr, ncol);
-      }
+      next_fut.get();
       h_t3 = now_s();
       dnext.upload(next, s);
+      const double h_up = now_s();
       if (nstore.n < static_cast<size_t>(next.store_doubles)) nstore.alloc(static_cast<size_t>(next.store_doubles));
       if (next.store_doubles > 0)
         CE_CUDA(cudaMemsetAsync(nstore.p, 0, static_cast<size_t>(next.store_doubles) * sizeof(double), s));
+      const double h_al = now_s();
+      Events ev_rem;
+      if (profile) {
+        CE_CUDA(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "[ce-profile] level %zu next plan: upload(host) %.1f ms, alloc+memset %.1f ms, drained %.1f ms\n",
+                     li + 1, 1e3 * (h_up - h_t3), 1e3 * (h_al - h_up), 1e3 * (now_s() - h_al));
+        CE_CUDA(cudaEventRecord(ev_rem.a, s));
+      }
       DevArray<int> d_nb, d_nl;
       d_nb.upload(next_block, s);
       d_nl.upload(next_loc, s);
@@ -1845,6 +1946,11 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       ra.err = d_err.p;
       launch_remainder(ra, s);
       CE_CUDA(cudaGetLastError());
+      if (profile) {
+        CE_CUDA(cudaEventRecord(ev_rem.b, s));
+        CE_CUDA(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "[ce-profile] level %zu remainder kernel %.2f ms\n", li + 1, 1e3 * ev_rem.seconds());
+      }
       CE_CUDA(cudaEventRecord(ev_lvl.b, s));
       CE_CUDA(cudaMemcpyAsync(herr, d_err.p, sizeof herr, cudaMemcpyDeviceToHost, s));
       CE_CUDA(cudaStreamSynchronize(s));

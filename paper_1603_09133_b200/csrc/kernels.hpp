@@ -18,7 +18,7 @@ constexpr int kApplyWmax = 256;
 // 4 / 8 / 20%), more once a row has hundreds of panels (3-D deep levels, each panel is staged
 // once per pair otherwise).
 #ifndef CE_PAIR_DIV
-#define CE_PAIR_DIV 48  // panels per extra pair in a Schur task (A/B builds: -DCE_PAIR_DIV=...)
+#define CE_PAIR_DIV 16  // panels per extra pair in a Schur task (A/B builds: -DCE_PAIR_DIV=...)
 #endif
 __host__ __device__ inline int row_pair_group(int forced, int np) {
   if (forced > 0) return forced;
