@@ -149,6 +149,19 @@ int64_t ce_launch_count(void);
 /* ---- operator: BlockSparseMatrix on the device ---- */
 /* Upload a host CSB (replaces BlockSparseMatrix construction, block_matrix.cpp:11-27). */
 int ce_matrix_upload(ce_ctx* ctx, const ce_csb_host* a, ce_matrix** out);
+/* BlockSparseMatrix::from_triplets (block_matrix.cpp:48-90) on the device: scalar COO triplets
+ * (duplicates summed in input order, bit-identical to the reference's std::map accumulation),
+ * mirror_lower != 0 = MirrorMode::Lower (the transposed entries are generated), else the input must
+ * be symmetric to 1e-12 max|a|; every touched block is inserted symmetrically, plus the full
+ * diagonal.  The values never leave the device; the block structure is kept on the host for the
+ * planner.  on_device != 0: rows / cols / vals are device pointers.  Errors: CE_EUSAGE with the
+ * reference's message ("triplet index outside matrix dimension", "asymmetric input: ..."). */
+int ce_matrix_from_triplets(ce_ctx* ctx, int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                            const double* vals, int64_t m, const int64_t* offsets, int mirror_lower, int on_device,
+                            ce_matrix** out);
+/* The matrix's CSB: structure views (valid while the matrix lives; out->values = NULL) and, when
+ * values != NULL, a copy of the block values (val_ptr[nnzb] doubles) into it. */
+int ce_matrix_csb(const ce_matrix* a, ce_csb_host* out, double* values);
 void ce_matrix_free(ce_matrix* a);
 int64_t ce_matrix_dim(const ce_matrix* a);
 /* y = A x (replaces BlockSparseMatrix::matvec, block_matrix.cpp:92-105; ApplyFn at cli.cpp:198).

@@ -230,6 +230,47 @@ class DeviceMatrix:
             lib.ce_matrix_free(self.handle)
             self.handle = None
 
+    @classmethod
+    def from_triplets(cls, n: int, rows, cols, vals, offsets, mirror_lower: bool = False,
+                      ctx: Optional[Context] = None) -> "DeviceMatrix":
+        """BlockSparseMatrix::from_triplets (block_matrix.cpp:48-90) built on the GPU
+        (ce_matrix_from_triplets); numpy arrays or CUDA tensors (int64 rows / cols, float64 vals)."""
+        ctx = ctx or Context.get()
+        offsets = _i64(offsets)
+        if _is_torch(vals):
+            import torch
+            rows = rows.to(torch.int64).contiguous()
+            cols = cols.to(torch.int64).contiguous()
+            vals = vals.to(torch.float64).contiguous()
+            nnz, dev = vals.numel(), 1
+            ptrs = [C.c_void_p(t.data_ptr()) for t in (rows, cols, vals)]
+        else:
+            rows, cols, vals = _i64(rows), _i64(cols), _f64(vals)
+            nnz, dev = vals.size, 0
+            ptrs = [C.c_void_p(x.ctypes.data) for x in (rows, cols, vals)]
+        h = C.c_void_p()
+        _check(lib.ce_matrix_from_triplets(ctx.handle, int(n), int(nnz), *ptrs, len(offsets) - 1,
+                                           _ptr(offsets, C.c_int64), int(mirror_lower), dev, C.byref(h)))
+        self = cls.__new__(cls)
+        self.ctx, self.handle, self.n = ctx, h, int(n)
+        self.host = self.csb(values=False)
+        return self
+
+    def csb(self, values: bool = True) -> BlockSparseMatrix:
+        """The CSB of this device matrix (ce_matrix_csb): structure, and the block values copied
+        back when `values` (else zeros of the right size)."""
+        v = L.CsbHost()
+        _check(lib.ce_matrix_csb(self.handle, C.byref(v), None))
+        m = v.m
+        nnzb = int(np.ctypeslib.as_array(v.row_ptr, (m + 1,))[-1])
+        val_ptr = np.ctypeslib.as_array(v.val_ptr, (nnzb + 1,)).copy()
+        vals = np.zeros(int(val_ptr[-1]))
+        if values:
+            _check(lib.ce_matrix_csb(self.handle, C.byref(v), _ptr(vals, C.c_double)))
+        return BlockSparseMatrix(np.ctypeslib.as_array(v.offsets, (m + 1,)).copy(),
+                                 np.ctypeslib.as_array(v.row_ptr, (m + 1,)).copy(),
+                                 np.ctypeslib.as_array(v.col_idx, (nnzb,)).copy(), val_ptr, vals)
+
     def matvec(self, x):
         if _is_torch(x):
             import torch

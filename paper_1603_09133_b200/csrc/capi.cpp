@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/ce_gpu.h"
+#include "assemble.hpp"
 #include "driver.hpp"
 #include "kernels.hpp"
 
@@ -257,6 +258,84 @@ int ce_matrix_upload(ce_ctx* ctx, const ce_csb_host* a, ce_matrix** out) {
                             cudaMemcpyHostToDevice, s));
     CE_CUDA(cudaStreamSynchronize(s));
     *out = h.release();
+  });
+}
+
+int ce_matrix_from_triplets(ce_ctx* ctx, int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                            const double* vals, int64_t m, const int64_t* offsets, int mirror_lower, int on_device,
+                            ce_matrix** out) {
+  return guarded([&] {
+    if (!ctx || !out || !offsets || (nnz > 0 && (!rows || !cols || !vals))) throw std::invalid_argument("null argument");
+    if (m < 1 || n < 1) throw std::invalid_argument("empty partition");
+    std::vector<int64_t> offs(offsets, offsets + m + 1);  // BlockPartition::from_offsets (partition.cpp)
+    if (offs.front() != 0 || offs.back() != n) throw std::invalid_argument("partition offsets must span [0, n)");
+    for (int64_t i = 0; i < m; ++i)
+      if (offs[static_cast<size_t>(i + 1)] <= offs[static_cast<size_t>(i)])
+        throw std::invalid_argument("partition offsets must be strictly increasing");
+    CE_CUDA(cudaSetDevice(ctx->ctx.device));
+    cudaStream_t s = ctx->ctx.stream;
+    ceg::DevArray<int64_t> d_r, d_c, d_off;
+    ceg::DevArray<double> d_v;
+    const int64_t *pr = rows, *pc = cols;
+    const double* pv = vals;
+    if (!on_device && nnz > 0) {
+      d_r.alloc(static_cast<size_t>(nnz));
+      d_c.alloc(static_cast<size_t>(nnz));
+      d_v.alloc(static_cast<size_t>(nnz));
+      CE_CUDA(cudaMemcpyAsync(d_r.p, rows, static_cast<size_t>(nnz) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      CE_CUDA(cudaMemcpyAsync(d_c.p, cols, static_cast<size_t>(nnz) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      CE_CUDA(cudaMemcpyAsync(d_v.p, vals, static_cast<size_t>(nnz) * sizeof(double), cudaMemcpyHostToDevice, s));
+      pr = d_r.p;
+      pc = d_c.p;
+      pv = d_v.p;
+    }
+    d_off.upload(offs, s);
+    ceg::AssembleResult R = ceg::assemble_from_triplets(n, nnz, pr, pc, pv, m, d_off.p, mirror_lower != 0, s);
+    if (!R.error.empty()) throw std::invalid_argument(R.error);
+    auto h = std::make_unique<ce_matrix>();
+    ceg::Matrix& M = h->m;
+    M.ctx = &ctx->ctx;
+    M.n = n;
+    M.m = m;
+    M.offsets = std::move(offs);
+    M.row_ptr = std::move(R.row_ptr);
+    M.nnzb = M.row_ptr.back();
+    M.col_idx = std::move(R.col_idx);
+    M.val_ptr = std::move(R.val_ptr);
+    M.d_offsets = std::move(d_off);
+    M.d_row_ptr.upload(M.row_ptr, s);
+    M.d_val_ptr.upload(M.val_ptr, s);
+    std::vector<int> col(M.col_idx.begin(), M.col_idx.end()), bsz(static_cast<size_t>(m));
+    for (int64_t i = 0; i < m; ++i)
+      bsz[static_cast<size_t>(i)] = static_cast<int>(M.offsets[static_cast<size_t>(i + 1)] - M.offsets[static_cast<size_t>(i)]);
+    M.d_col_idx.upload(col, s);
+    M.d_bsz.upload(bsz, s);
+    std::vector<int64_t> row_of(static_cast<size_t>(n));
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t p = M.offsets[static_cast<size_t>(i)]; p < M.offsets[static_cast<size_t>(i + 1)]; ++p) row_of[static_cast<size_t>(p)] = i;
+    M.d_row_of.upload(row_of, s);
+    M.d_values = std::move(R.values);
+    CE_CUDA(cudaStreamSynchronize(s));
+    *out = h.release();
+  });
+}
+
+int ce_matrix_csb(const ce_matrix* a, ce_csb_host* view, double* values) {
+  return guarded([&] {
+    if (!a || !view) throw std::invalid_argument("null argument");
+    const ceg::Matrix& M = a->m;
+    view->n = M.n;
+    view->m = M.m;
+    view->offsets = M.offsets.data();
+    view->row_ptr = M.row_ptr.data();
+    view->col_idx = M.col_idx.data();
+    view->val_ptr = M.val_ptr.data();
+    view->values = nullptr;
+    if (values && M.val_ptr.back() > 0) {
+      CE_CUDA(cudaSetDevice(M.ctx->device));
+      CE_CUDA(cudaMemcpy(values, M.d_values.p, static_cast<size_t>(M.val_ptr.back()) * sizeof(double),
+                         cudaMemcpyDeviceToHost));
+    }
   });
 }
 
