@@ -25,6 +25,13 @@ constexpr size_t kSweepSmem = (kWmax + 2 * kWmax * kApplyWarps) * sizeof(double)
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldcg(p); }
 
+#ifndef CE_APPLY_SLEEP
+#define CE_APPLY_SLEEP 32  // ns of __nanosleep between dependency polls (0: spin; A/B builds)
+#endif
+__device__ __forceinline__ void apply_backoff() {
+  if (CE_APPLY_SLEEP > 0) __nanosleep(CE_APPLY_SLEEP);
+}
+
 // Pull [p, p + n doubles) into L2 (one prefetch per 128-byte line, lanes of the calling
 // warp split the lines).  Issued before a task waits for its dependencies: the factor
 // data does not depend on them, so after the wait its loads hit L2 instead of HBM.
@@ -81,7 +88,7 @@ __global__ void __launch_bounds__(T) forward_kernel(ApplyLevelArgs A) {
     const int j = A.order[jl];
     const int64_t k0 = A.in_ptr[j], k1 = k0 + A.in_split[j];
     for (int64_t k = k0 + threadIdx.x; k < k1; k += T)
-      while (ld_acquire(A.flags + A.in_src[k]) == 0) __nanosleep(32);
+      while (ld_acquire(A.flags + A.in_src[k]) == 0) apply_backoff();
     __threadfence();
     __syncthreads();
     const int w = A.width[j];
@@ -211,7 +218,7 @@ __global__ void __launch_bounds__(T) backward_kernel(ApplyLevelArgs A) {
     if (tk >= A.M) break;
     const int j = A.order[tk];
     for (int64_t k = A.dep_ptr[j] + threadIdx.x; k < A.dep_ptr[j + 1]; k += T)
-      while (ld_acquire(A.flags + A.dep_t[k]) == 0) __nanosleep(32);
+      while (ld_acquire(A.flags + A.dep_t[k]) == 0) apply_backoff();
     __threadfence();
     __syncthreads();
     const int w = A.width[j];
@@ -311,7 +318,7 @@ __global__ void __launch_bounds__(T) forward_task_kernel(ApplyLevelArgs A) {
       }
       if (fused && warp == kApplyWarps - 1) prefetch_l2(A.linv + A.linv_off[j], static_cast<int64_t>(w) * w, lane);
       for (int64_t k = k0 + threadIdx.x; k < k1; k += T)
-        while (ld_acquire(A.flags + A.in_src[k]) == 0) __nanosleep(32);
+        while (ld_acquire(A.flags + A.in_src[k]) == 0) apply_backoff();
       if (threadIdx.x == 0) __threadfence();
       __syncthreads();
       double* pw = z + kWmax + warp * 2 * kWmax;
@@ -365,7 +372,7 @@ __global__ void __launch_bounds__(T) forward_task_kernel(ApplyLevelArgs A) {
       if (!fused) {
         if (warp == 1) prefetch_l2(A.linv + A.linv_off[j], static_cast<int64_t>(w) * w, lane);
         if (threadIdx.x == 0) {
-          while (ld_acquire(A.parts_done + j) < P) __nanosleep(32);
+          while (ld_acquire(A.parts_done + j) < P) apply_backoff();
           __threadfence();
         }
         __syncthreads();
@@ -432,7 +439,7 @@ __global__ void __launch_bounds__(T) backward_task_kernel(ApplyLevelArgs A) {
         if (sgi == 0) continue;
         const int t = A.cl_col[c0 + sgi - 1];
         if (t > j && A.width[t] > 0)
-          while (ld_acquire(A.flags + t) == 0) __nanosleep(32);
+          while (ld_acquire(A.flags + t) == 0) apply_backoff();
       }
       if (threadIdx.x == 0) __threadfence();
       __syncthreads();
@@ -500,7 +507,7 @@ __global__ void __launch_bounds__(T) backward_task_kernel(ApplyLevelArgs A) {
       if (!fused) {
         if (warp == 1) prefetch_l2(A.linv + A.linv_off[j], static_cast<int64_t>(w) * w, lane);
         if (threadIdx.x == 0) {
-          while (ld_acquire(A.parts_done + j) < P) __nanosleep(32);
+          while (ld_acquire(A.parts_done + j) < P) apply_backoff();
           __threadfence();
         }
         __syncthreads();

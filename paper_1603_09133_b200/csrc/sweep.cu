@@ -51,6 +51,13 @@ constexpr int kPanelRows = 260;       // g rows per Schur panel (<= 256 + paddin
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldcg(p); }
 
+#ifndef CE_SWEEP_SLEEP
+#define CE_SWEEP_SLEEP 64  // ns of __nanosleep between dependency polls (0: spin; A/B builds)
+#endif
+__device__ __forceinline__ void sweep_backoff() {
+  if (CE_SWEEP_SLEEP > 0) __nanosleep(CE_SWEEP_SLEEP);
+}
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -2121,7 +2121,7 @@ __global__ void __launch_bounds__(T, CE_SWEEP_MIN_BLOCKS) sweep_kernel(SweepArgs
             s_stop = 1;
             break;
           }
-          __nanosleep(64);
+          sweep_backoff();
         }
         if (s_stop) break;
       }
@@ -2140,7 +2140,7 @@ __global__ void __launch_bounds__(T, CE_SWEEP_MIN_BLOCKS) sweep_kernel(SweepArgs
               s_stop = 1;
               break;
             }
-            __nanosleep(64);
+            sweep_backoff();
           }
           if (s_stop) break;
         }
@@ -2158,7 +2158,7 @@ __global__ void __launch_bounds__(T, CE_SWEEP_MIN_BLOCKS) sweep_kernel(SweepArgs
             s_stop = 1;
             break;
           }
-          __nanosleep(64);
+          sweep_backoff();
         }
       }
       __threadfence();
