@@ -538,6 +538,242 @@ __global__ void __launch_bounds__(T) backward_task_kernel(ApplyLevelArgs A) {
   }
 }
 
+// ---- warp-granular split-row sweeps (CE_APPLY_WARP) ----
+// The same items, dependencies and arithmetic as forward/backward_task_kernel, but every warp
+// is an independent worker: it takes its own ticket and runs the item alone with warp-level
+// synchronisation only.  The sweeps are latency chains (one dependency hop per wave, ~500-1500
+// waves per level on the reference plan), so an item's latency, not its work, sets the time:
+// no CTA-wide barriers on the path, and four items in flight per CTA instead of one.  A row's
+// inputs are summed by one warp in ascending entry order (deterministic).
+constexpr int kQm = kWmax / 32;  // columns q per lane
+constexpr size_t kWarpSmem = 2 * kWmax * kApplyWarps * sizeof(double);
+
+__global__ void __launch_bounds__(T) forward_warp_kernel(ApplyLevelArgs A) {
+  extern __shared__ double sh[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* z = sh + warp * 2 * kWmax;
+  double* ub = z + kWmax;
+  for (;;) {
+    long long it = 0;
+    if (lane == 0) it = static_cast<long long>(atomicAdd(A.ticket, 1ULL));
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= A.n_items) break;
+    const int j = A.item_row[it], part0 = A.item_part[it];
+    const int64_t pp = A.part_ptr[j];
+    const int P = static_cast<int>(A.part_ptr[j + 1] - pp) - 1;
+    const int w = A.width[j], r = A.rank[j];
+    double* scr = A.scratch + A.scr_off[j];
+    double* vj = A.v + A.offsets[j];
+    const bool fused = part0 < 0;
+    const int part = fused ? 0 : part0;
+    if (part < P) {
+      const int64_t k0 = A.part_b[pp + part], k1 = A.part_b[pp + part + 1];
+      for (int64_t k = k0; k < k1; ++k) {
+        const int wi = A.in_w[k];
+        prefetch_l2(A.fac + A.in_goff[k] + static_cast<int64_t>(r) * wi, static_cast<int64_t>(w) * wi, lane);
+      }
+      if (fused) prefetch_l2(A.linv + A.linv_off[j], static_cast<int64_t>(w) * w, lane);
+      for (int64_t k = k0 + lane; k < k1; k += 32)
+        while (ld_acquire(A.flags + A.in_src[k]) == 0) apply_backoff();
+      __threadfence();
+      __syncwarp();
+      double acc[kQm];
+#pragma unroll
+      for (int m = 0; m < kQm; ++m) acc[m] = 0.0;
+      for (int64_t k = k0; k < k1; ++k) {
+        const int wi = A.in_w[k];
+        const double* ui = A.v + A.in_uoff[k];
+        for (int p = lane; p < wi; p += 32) ub[p] = ldg(ui + p);
+        __syncwarp();
+        const double* g = A.fac + A.in_goff[k] + static_cast<int64_t>(r) * wi;
+#pragma unroll
+        for (int m = 0; m < kQm; ++m) {
+          const int q = lane + 32 * m;
+          if (q < w) {
+            const double* gq = g + static_cast<int64_t>(q) * wi;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int p = 0;
+            for (; p + 3 < wi; p += 4) {
+              a0 = fma(__ldg(gq + p), ub[p], a0);
+              a1 = fma(__ldg(gq + p + 1), ub[p + 1], a1);
+              a2 = fma(__ldg(gq + p + 2), ub[p + 2], a2);
+              a3 = fma(__ldg(gq + p + 3), ub[p + 3], a3);
+            }
+            for (; p < wi; ++p) a0 = fma(__ldg(gq + p), ub[p], a0);
+            acc[m] += (a0 + a1) + (a2 + a3);
+          }
+        }
+        __syncwarp();
+      }
+      if (!fused) {
+#pragma unroll
+        for (int m = 0; m < kQm; ++m)
+          if (lane + 32 * m < w) scr[static_cast<int64_t>(part) * w + lane + 32 * m] = acc[m];
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(A.parts_done + j, 1);
+        }
+        continue;
+      }
+#pragma unroll
+      for (int m = 0; m < kQm; ++m)
+        if (lane + 32 * m < w) z[lane + 32 * m] = ldg(vj + r + lane + 32 * m) - acc[m];
+      __syncwarp();
+    } else {
+      prefetch_l2(A.linv + A.linv_off[j], static_cast<int64_t>(w) * w, lane);
+      if (lane == 0)
+        while (ld_acquire(A.parts_done + j) < P) apply_backoff();
+      __threadfence();
+      __syncwarp();
+      for (int q = lane; q < w; q += 32) {
+        double a = ldg(vj + r + q);
+        for (int k = 0; k < P; ++k) a -= ldg(scr + static_cast<int64_t>(k) * w + q);
+        z[q] = a;
+      }
+      __syncwarp();
+    }
+    const double* Li = A.linv + A.linv_off[j];
+    for (int q = lane; q < w; q += 32) {
+      const double* lq = Li + static_cast<int64_t>(q) * w;
+      double a0 = 0.0, a1 = 0.0;
+      int p = 0;
+      for (; p + 1 <= q; p += 2) {
+        a0 = fma(__ldg(lq + p), z[p], a0);
+        a1 = fma(__ldg(lq + p + 1), z[p + 1], a1);
+      }
+      if (p <= q) a0 = fma(__ldg(lq + p), z[p], a0);
+      vj[r + q] = a0 + a1;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      atomicExch(A.flags + j, 1);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(T) backward_warp_kernel(ApplyLevelArgs A) {
+  extern __shared__ double sh[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* sbw = sh + warp * 2 * kWmax;
+  double* vbuf = sbw + kWmax;
+  for (;;) {
+    long long it = 0;
+    if (lane == 0) it = static_cast<long long>(atomicAdd(A.ticket, 1ULL));
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= A.n_items) break;
+    const int j = A.item_row[it], part0 = A.item_part[it];
+    const int64_t pp = A.part_ptr[j];
+    const int P = static_cast<int>(A.part_ptr[j + 1] - pp) - 1;
+    const int w = A.width[j], r = A.rank[j];
+    double* scr = A.scratch + A.scr_off[j];
+    const int64_t c0 = A.cl_ptr[j];
+    double* vj = A.v + A.offsets[j];
+    const double* G = A.fac + A.g_off[j];
+    const bool fused = part0 < 0;
+    const int part = fused ? 0 : part0;
+    if (part < P) {
+      const int s0 = static_cast<int>(A.part_b[pp + part]), s1 = static_cast<int>(A.part_b[pp + part + 1]);
+      for (int sgi = s0; sgi < s1; ++sgi) {
+        if (sgi == 0) prefetch_l2(G, static_cast<int64_t>(r) * w, lane);
+        else prefetch_l2(G + static_cast<int64_t>(r + A.cl_roff[c0 + sgi - 1]) * w,
+                         static_cast<int64_t>(A.cl_nt[c0 + sgi - 1]) * w, lane);
+      }
+      if (fused) prefetch_l2(A.linv + A.linv_off[j], static_cast<int64_t>(w) * w, lane);
+      for (int sgi = s0 + lane; sgi < s1; sgi += 32) {
+        if (sgi == 0) continue;
+        const int t = A.cl_col[c0 + sgi - 1];
+        if (t > j && A.width[t] > 0)
+          while (ld_acquire(A.flags + t) == 0) apply_backoff();
+      }
+      __threadfence();
+      __syncwarp();
+      double acc[kQm];
+#pragma unroll
+      for (int m = 0; m < kQm; ++m) acc[m] = 0.0;
+      for (int sgi = s0; sgi < s1; ++sgi) {
+        const double* rows;
+        const double* vt;
+        int nt;
+        if (sgi == 0) {
+          rows = G;
+          vt = vj;
+          nt = r;
+        } else {
+          const int64_t e = c0 + sgi - 1;
+          nt = A.cl_nt[e];
+          rows = G + static_cast<int64_t>(r + A.cl_roff[e]) * w;
+          vt = A.v + A.offsets[A.cl_col[e]];
+        }
+        for (int a = lane; a < nt; a += 32) vbuf[a] = ldg(vt + a);
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < kQm; ++m) {
+          const int q = lane + 32 * m;
+          if (q < w) {
+            const double* gq = rows + q;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int a = 0;
+            for (; a + 3 < nt; a += 4) {
+              a0 = fma(__ldg(gq + static_cast<int64_t>(a) * w), vbuf[a], a0);
+              a1 = fma(__ldg(gq + static_cast<int64_t>(a + 1) * w), vbuf[a + 1], a1);
+              a2 = fma(__ldg(gq + static_cast<int64_t>(a + 2) * w), vbuf[a + 2], a2);
+              a3 = fma(__ldg(gq + static_cast<int64_t>(a + 3) * w), vbuf[a + 3], a3);
+            }
+            for (; a < nt; ++a) a0 = fma(__ldg(gq + static_cast<int64_t>(a) * w), vbuf[a], a0);
+            acc[m] += (a0 + a1) + (a2 + a3);
+          }
+        }
+        __syncwarp();
+      }
+      if (!fused) {
+#pragma unroll
+        for (int m = 0; m < kQm; ++m)
+          if (lane + 32 * m < w) scr[static_cast<int64_t>(part) * w + lane + 32 * m] = acc[m];
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(A.parts_done + j, 1);
+        }
+        continue;
+      }
+#pragma unroll
+      for (int m = 0; m < kQm; ++m)
+        if (lane + 32 * m < w) sbw[lane + 32 * m] = ldg(vj + r + lane + 32 * m) - acc[m];
+      __syncwarp();
+    } else {
+      prefetch_l2(A.linv + A.linv_off[j], static_cast<int64_t>(w) * w, lane);
+      if (lane == 0)
+        while (ld_acquire(A.parts_done + j) < P) apply_backoff();
+      __threadfence();
+      __syncwarp();
+      for (int q = lane; q < w; q += 32) {
+        double a = ldg(vj + r + q);
+        for (int k = 0; k < P; ++k) a -= ldg(scr + static_cast<int64_t>(k) * w + q);
+        sbw[q] = a;
+      }
+      __syncwarp();
+    }
+    const double* Li = A.linv + A.linv_off[j];
+    for (int p = lane; p < w; p += 32) {
+      double a0 = 0.0, a1 = 0.0;
+      int q = p;
+      for (; q + 1 < w; q += 2) {
+        a0 = fma(__ldg(Li + static_cast<int64_t>(q) * w + p), sbw[q], a0);
+        a1 = fma(__ldg(Li + static_cast<int64_t>(q + 1) * w + p), sbw[q + 1], a1);
+      }
+      if (q < w) a0 = fma(__ldg(Li + static_cast<int64_t>(q) * w + p), sbw[q], a0);
+      vj[r + p] = a0 + a1;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      atomicExch(A.flags + j, 1);
+    }
+  }
+}
+
 // L^{-1} of each row's w x w pivot factor: thread per column, forward substitution.
 __global__ void pivot_inverse_kernel(int64_t M, const int* width, const double* fac, const int64_t* chol_off,
                                      double* linv, const int64_t* linv_off) {
@@ -658,16 +894,18 @@ void launch_forward_sweep(const ApplyLevelArgs& a, int grid, cudaStream_t s) {
   forward_kernel<<<grid, T, kSweepSmem, s>>>(a);
 }
 
-void launch_forward_tasks(const ApplyLevelArgs& a, int grid, cudaStream_t s) {
+void launch_forward_tasks(const ApplyLevelArgs& a, int grid, bool warp_items, cudaStream_t s) {
   if (a.n_items == 0) return;
   note_launch();
-  forward_task_kernel<<<grid, T, kSweepSmem, s>>>(a);
+  if (warp_items) forward_warp_kernel<<<grid, T, kWarpSmem, s>>>(a);
+  else forward_task_kernel<<<grid, T, kSweepSmem, s>>>(a);
 }
 
-void launch_backward_tasks(const ApplyLevelArgs& a, int grid, cudaStream_t s) {
+void launch_backward_tasks(const ApplyLevelArgs& a, int grid, bool warp_items, cudaStream_t s) {
   if (a.n_items == 0) return;
   note_launch();
-  backward_task_kernel<<<grid, T, kSweepSmem, s>>>(a);
+  if (warp_items) backward_warp_kernel<<<grid, T, kWarpSmem, s>>>(a);
+  else backward_task_kernel<<<grid, T, kSweepSmem, s>>>(a);
 }
 
 void launch_forward_retained(const ApplyLevelArgs& a, cudaStream_t s) {

@@ -2274,7 +2274,11 @@ void apply_device(const Factor& f, const double* d_b, double* d_x, cudaStream_t 
     a.part_b = L.d_fpart_b.p;
     a.scr_off = L.d_fscr_off.p;
     if (aprof) CE_CUDA(cudaEventRecord(evs[2 * l].a, s));
-    launch_forward_tasks(a, static_cast<int>(std::min<int64_t>(grid, std::max<int64_t>(L.n_fitems, 1))), s);
+    // warp-granular items where the level is throughput-bound (many independent rows per wave:
+    // colour-major / sharded plans, A/B -33% apply time); CTA items where it is a latency chain
+    // (the reference plan's ~500-1500 waves: the 4-warp split of a row's inputs is shorter)
+    const bool warp_items = L.max_close <= CE_APPLY_WARP_MAX_CLOSE && L.M >= CE_APPLY_WARP_ROWS_PER_WAVE * std::max<int64_t>(L.n_waves, 1);
+    launch_forward_tasks(a, static_cast<int>(std::min<int64_t>(grid, std::max<int64_t>(L.n_fitems, 1))), warp_items, s);
     if (aprof) CE_CUDA(cudaEventRecord(evs[2 * l].b, s));
     launch_forward_retained(a, s);
     launch_gather(v, L.d_elim_gather.p, f.w_elim.p + f.elim_base[l], L.n_elim, s);
@@ -2300,7 +2304,10 @@ void apply_device(const Factor& f, const double* d_b, double* d_x, cudaStream_t 
     a.part_b = L.d_bpart_b.p;
     a.scr_off = L.d_bscr_off.p;
     if (aprof) CE_CUDA(cudaEventRecord(evs[2 * l + 1].a, s));
-    launch_backward_tasks(a, static_cast<int>(std::min<int64_t>(grid, std::max<int64_t>(L.n_bitems, 1))), s);
+    launch_backward_tasks(a, static_cast<int>(std::min<int64_t>(grid, std::max<int64_t>(L.n_bitems, 1))),
+                          L.max_close <= CE_APPLY_WARP_MAX_CLOSE &&
+                              L.M >= CE_APPLY_WARP_ROWS_PER_WAVE * std::max<int64_t>(L.n_waves, 1),
+                          s);
     if (aprof) CE_CUDA(cudaEventRecord(evs[2 * l + 1].b, s));
     launch_basis_apply(a, 0, s);
     CE_CUDA(cudaMemcpyAsync(active, v, static_cast<size_t>(L.dim) * sizeof(double), cudaMemcpyDeviceToDevice, s));

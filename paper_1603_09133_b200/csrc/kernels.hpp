@@ -13,6 +13,12 @@ namespace ceg {
 constexpr int kSweepThreads = CE_SWEEP_THREADS;
 constexpr int kApplyThreads = 128;
 constexpr int kApplyWmax = 256;
+#ifndef CE_APPLY_WARP_MAX_CLOSE
+#define CE_APPLY_WARP_MAX_CLOSE 16  // warp apply items only for levels of short rows (<= this many neighbours)
+#endif
+#ifndef CE_APPLY_WARP_ROWS_PER_WAVE
+#define CE_APPLY_WARP_ROWS_PER_WAVE 512  // ... that are throughput-bound (>= this many rows per sweep wave)
+#endif
 // Schur pairs per B task of a row with np panels (forced > 0, else adaptive): one pair per task
 // while the row has few panels (the wave needs the parallelism: A/B on cfg2, g = 2 / 3 / 5 lose
 // 4 / 8 / 20%), more once a row has hundreds of panels (3-D deep levels, each panel is staged
@@ -236,8 +242,10 @@ void launch_pivot_inverse(int64_t M, const int* width, const double* fac, const 
                           const int64_t* linv_off, cudaStream_t s);
 void launch_basis_apply(const ApplyLevelArgs& a, int transpose, cudaStream_t s);
 void launch_forward_sweep(const ApplyLevelArgs& a, int grid, cudaStream_t s);
-void launch_forward_tasks(const ApplyLevelArgs& a, int grid, cudaStream_t s);
-void launch_backward_tasks(const ApplyLevelArgs& a, int grid, cudaStream_t s);
+// warp_items: every warp an independent worker (levels of short rows: the sweep is a latency
+// chain and CTA barriers sit on it); else one 4-warp CTA per item (levels of long rows).
+void launch_forward_tasks(const ApplyLevelArgs& a, int grid, bool warp_items, cudaStream_t s);
+void launch_backward_tasks(const ApplyLevelArgs& a, int grid, bool warp_items, cudaStream_t s);
 void launch_forward_retained(const ApplyLevelArgs& a, cudaStream_t s);
 void launch_backward_sweep(const ApplyLevelArgs& a, int grid, cudaStream_t s);
 // operator tool (apply_operator) pieces

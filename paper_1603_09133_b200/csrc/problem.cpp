@@ -9,7 +9,8 @@
 //              3-D cell_shape (problems.cpp:184-191) or the 2-D analogue
 //   RNG      : counter-based splitmix64 + Box-Muller, stream 0 = g, stream 1 = b
 // The oracle (oracle/problems.cpp) restates the same conventions independently;
-// tests/test_problem_parity.py checks the two CSBs agree bit for bit.
+// tests/test_library_cpu.py (test_generator_matches_oracle_bitwise, test_merge_all_axes_plan_matches_oracle) and
+// tests/test_shard_cpu.py check the two CSBs and plans agree bit for bit.
 #include <algorithm>
 #include <array>
 #include <cmath>
