@@ -159,6 +159,15 @@ int ce_matrix_upload(ce_ctx* ctx, const ce_csb_host* a, ce_matrix** out);
 int ce_matrix_from_triplets(ce_ctx* ctx, int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
                             const double* vals, int64_t m, const int64_t* offsets, int mirror_lower, int on_device,
                             ce_matrix** out);
+/* Symbolic planner pieces on the device, CSR patterns with sorted rows:
+ * pattern_square (proj/src/pattern.cpp:64-86) and coarsen_pattern (pattern.cpp:97-118; group_of[b]
+ * = -1 drops block b, as a dead group).  Outputs: rows + 1 row pointers and up to cap columns,
+ * *nnz = the result's entry count (CE_EUSAGE if it exceeds cap).  ce_factorize uses them for the
+ * plans it makes while the device is idle. */
+int ce_pattern_square(ce_ctx* ctx, int64_t m, const int64_t* row_ptr, const int64_t* cols, int64_t* out_row_ptr,
+                      int64_t* out_cols, int64_t cap, int64_t* nnz);
+int ce_pattern_coarsen(ce_ctx* ctx, int64_t m, const int64_t* row_ptr, const int64_t* cols, int64_t ng,
+                       const int64_t* group_of, int64_t* out_row_ptr, int64_t* out_cols, int64_t cap, int64_t* nnz);
 /* The matrix's CSB: structure views (valid while the matrix lives; out->values = NULL) and, when
  * values != NULL, a copy of the block values (val_ptr[nnzb] doubles) into it. */
 int ce_matrix_csb(const ce_matrix* a, ce_csb_host* out, double* values);

@@ -28,6 +28,8 @@ from .ce import (  # noqa: F401
     ce_factorize_sharded,
     device_count,
     minres,
+    pattern_coarsen,
+    pattern_square,
     pcg,
     shard_plan_summary,
 )
@@ -51,6 +53,8 @@ __all__ = [
     "ce_factorize_sharded",
     "device_count",
     "minres",
+    "pattern_coarsen",
+    "pattern_square",
     "pcg",
     "shard_plan_summary",
 ]

@@ -97,6 +97,8 @@ SIGNATURES = {
     "ce_matvec": (C.c_int, [vp, vp, vp, i64, C.c_int, vp]),
     "ce_matrix_from_triplets": (C.c_int, [vp, i64, i64, vp, vp, vp, i64, i64p, C.c_int, C.c_int, C.POINTER(vp)]),
     "ce_matrix_csb": (C.c_int, [vp, C.POINTER(CsbHost), C.POINTER(C.c_double)]),
+    "ce_pattern_square": (C.c_int, [vp, i64, i64p, i64p, i64p, i64p, i64, i64p]),
+    "ce_pattern_coarsen": (C.c_int, [vp, i64, i64p, i64p, i64, i64p, i64p, i64p, i64, i64p]),
     "ce_factorize": (C.c_int, [vp, vp, C.POINTER(PlanHost), C.POINTER(Strategy), C.POINTER(FactorOpts),
                                C.POINTER(vp), C.POINTER(Status)]),
     "ce_factor_free": (None, [vp]),

@@ -495,6 +495,30 @@ def ce_factorize_sharded(a, plan: CoarseningPlan, strategy: CompressionStrategy,
     return f
 
 
+def _pattern_call(fn, rows_out: int, row_ptr, cols, *extra, square: bool = True, ctx: Optional[Context] = None):
+    ctx = ctx or Context.get()
+    row_ptr, cols = _i64(row_ptr), _i64(cols)
+    m = len(row_ptr) - 1
+    # output bound: the candidate count (square: sum of deg(k) over the entries; coarsen: nnz)
+    cap = max(1, int(np.sum(np.diff(row_ptr)[cols])) if square else len(cols))
+    optr, ocol, nnz = np.zeros(rows_out + 1, np.int64), np.zeros(cap, np.int64), C.c_int64()
+    _check(fn(ctx.handle, m, _ptr(row_ptr, C.c_int64), _ptr(cols, C.c_int64), *extra, _ptr(optr, C.c_int64),
+              _ptr(ocol, C.c_int64), cap, C.byref(nnz)))
+    return optr, ocol[:nnz.value].copy()
+
+
+def pattern_square(row_ptr, cols, ctx: Optional[Context] = None):
+    """pattern_square (proj/src/pattern.cpp:64-86) on the GPU: CSR (sorted rows) -> CSR of P^2."""
+    return _pattern_call(lib.ce_pattern_square, len(row_ptr) - 1, row_ptr, cols, ctx=ctx)
+
+
+def pattern_coarsen(row_ptr, cols, group_of, ng: int, ctx: Optional[Context] = None):
+    """coarsen_pattern (pattern.cpp:97-118) on the GPU; group_of[b] = -1 drops block b."""
+    g = _i64(group_of)
+    return _pattern_call(lib.ce_pattern_coarsen, int(ng), row_ptr, cols, int(ng), _ptr(g, C.c_int64), square=False,
+                         ctx=ctx)
+
+
 def shard_plan_summary(problem: "Problem", n_ranks: int, max_levels: int = 64) -> List[dict]:
     """Symbolic phase split of a "sharded"-plan problem over n_ranks (host only, no GPU):
     per level the block count, the box-interior (phase-1) rows and the rows each rank sweeps

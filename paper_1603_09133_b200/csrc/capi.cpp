@@ -12,6 +12,7 @@
 
 #include "../../include/ce_gpu.h"
 #include "assemble.hpp"
+#include "pattern.hpp"
 #include "driver.hpp"
 #include "kernels.hpp"
 
@@ -317,6 +318,47 @@ int ce_matrix_from_triplets(ce_ctx* ctx, int64_t n, int64_t nnz, const int64_t* 
     M.d_values = std::move(R.values);
     CE_CUDA(cudaStreamSynchronize(s));
     *out = h.release();
+  });
+}
+
+namespace {
+int pattern_out(const std::vector<int64_t>& ptr, const std::vector<int>& col, int64_t rows, int64_t* out_ptr,
+                int64_t* out_col, int64_t cap, int64_t* nnz) {
+  *nnz = ptr[static_cast<size_t>(rows)];
+  if (*nnz > cap) throw std::invalid_argument("output capacity too small");
+  for (int64_t i = 0; i <= rows; ++i) out_ptr[i] = ptr[static_cast<size_t>(i)];
+  for (int64_t k = 0; k < *nnz; ++k) out_col[k] = col[static_cast<size_t>(k)];
+  return CE_OK;
+}
+}  // namespace
+
+int ce_pattern_square(ce_ctx* ctx, int64_t m, const int64_t* row_ptr, const int64_t* cols, int64_t* out_row_ptr,
+                      int64_t* out_cols, int64_t cap, int64_t* nnz) {
+  return guarded([&] {
+    if (!ctx || !row_ptr || !out_row_ptr || !nnz || m < 1) throw std::invalid_argument("null argument");
+    CE_CUDA(cudaSetDevice(ctx->ctx.device));
+    std::vector<int64_t> ptr(row_ptr, row_ptr + m + 1);
+    std::vector<int> col(cols, cols + ptr.back());
+    std::vector<int64_t> sp;
+    std::vector<int> sc;
+    ceg::device_square(m, ptr, col, ctx->ctx.stream, sp, sc);
+    pattern_out(sp, sc, m, out_row_ptr, out_cols, cap, nnz);
+  });
+}
+
+int ce_pattern_coarsen(ce_ctx* ctx, int64_t m, const int64_t* row_ptr, const int64_t* cols, int64_t ng,
+                       const int64_t* group_of, int64_t* out_row_ptr, int64_t* out_cols, int64_t cap, int64_t* nnz) {
+  return guarded([&] {
+    if (!ctx || !row_ptr || !group_of || !out_row_ptr || !nnz || m < 1 || ng < 1) throw std::invalid_argument("null argument");
+    CE_CUDA(cudaSetDevice(ctx->ctx.device));
+    std::vector<int64_t> ptr(row_ptr, row_ptr + m + 1), gof(group_of, group_of + m);
+    std::vector<int> col(cols, cols + ptr.back());
+    for (int64_t g : gof)
+      if (g < -1 || g >= ng) throw std::invalid_argument("group index out of range");
+    std::vector<int64_t> cp;
+    std::vector<int> cc;
+    ceg::device_coarsen(m, ptr, col, ng, gof, ctx->ctx.stream, cp, cc);
+    pattern_out(cp, cc, ng, out_row_ptr, out_cols, cap, nnz);
   });
 }
 

@@ -19,6 +19,7 @@
 #include <sstream>
 
 #include "kernels.hpp"
+#include "pattern.hpp"
 
 namespace ceg {
 
@@ -301,7 +302,9 @@ int64_t csr_find(const std::vector<int64_t>& ptr, const std::vector<int>& col, i
 // stored-slot numbering, close lists and the wave order of the row DAG.  Runs on a host
 // thread for level l+1 while level l sweeps on the device (speculating that every group
 // of level l keeps a nonzero rank).
-LevelPlan plan_symbolic(int64_t M, std::vector<int64_t> bptr, std::vector<int> bcol) {
+// dev != nullptr: the caller's device is idle (first level, re-plan after dead groups), so the
+// square runs on the GPU (pattern.cu) when the level is large and not dense.
+LevelPlan plan_symbolic(int64_t M, std::vector<int64_t> bptr, std::vector<int> bcol, cudaStream_t dev = nullptr) {
   LevelPlan P;
   P.M = M;
   P.bptr = std::move(bptr);
@@ -312,7 +315,10 @@ LevelPlan plan_symbolic(int64_t M, std::vector<int64_t> bptr, std::vector<int> b
 
   const bool prof = std::getenv("CE_PROFILE") && std::getenv("CE_PROFILE")[0] == '1';
   const double t0 = now_s();
-  square_pattern(M, P.bptr, P.bcol, P.sptr, P.scol);
+  if (dev && M >= 16384 && square_candidates(M, P.bptr, P.bcol) <= (int64_t{1} << 26))
+    device_square(M, P.bptr, P.bcol, dev, P.sptr, P.scol);
+  else
+    square_pattern(M, P.bptr, P.bcol, P.sptr, P.scol);
   const double t1 = now_s();
   const int64_t nnz = static_cast<int64_t>(P.scol.size());
   P.skind.resize(static_cast<size_t>(nnz));
@@ -848,8 +854,8 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
                  1e3 * (tp4 - tp3), 1e3 * (tp5 - tp4), 1e3 * (now_s() - tp5));
 }
 
-LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vector<int> bcol) {
-  LevelPlan P = plan_symbolic(static_cast<int64_t>(bsz.size()), std::move(bptr), std::move(bcol));
+LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vector<int> bcol, cudaStream_t dev) {
+  LevelPlan P = plan_symbolic(static_cast<int64_t>(bsz.size()), std::move(bptr), std::move(bcol), dev);
   plan_numeric(P, std::move(bsz));
   return P;
 }
@@ -1464,7 +1470,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
   std::vector<int> bsz(static_cast<size_t>(A->m));
   for (int64_t i = 0; i < A->m; ++i) bsz[static_cast<size_t>(i)] = static_cast<int>(A->offsets[static_cast<size_t>(i + 1)] - A->offsets[static_cast<size_t>(i)]);
   std::vector<int> bcol(A->col_idx.begin(), A->col_idx.end());
-  LevelPlan cur = plan_level(bsz, A->row_ptr, bcol);
+  LevelPlan cur = plan_level(bsz, A->row_ptr, bcol, s);  // device idle: squares on the GPU
   DevPlan dcur;
   dcur.upload(cur, s);
   DevArray<double> store(static_cast<size_t>(cur.store_doubles));
@@ -1941,7 +1947,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
           next = std::move(sp);
           plan_numeric(next, nbsz);
         } else {
-          next = plan_level(nbsz, nptr, ncol);
+          next = plan_level(nbsz, nptr, ncol, s);  // after the sweep: the device is idle
         }
       });
     // gathers (factorization.cpp:76-85)

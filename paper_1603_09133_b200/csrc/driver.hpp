@@ -9,7 +9,7 @@
 
 namespace ceg {
 
-LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vector<int> bcol);
+LevelPlan plan_level(std::vector<int> bsz, std::vector<int64_t> bptr, std::vector<int> bcol, cudaStream_t dev = nullptr);
 
 // shard != nullptr: this rank's part of a subdomain-sharded factorization; the
 // returned factor is complete and identical on every rank.
