@@ -138,6 +138,21 @@ def test_level_stats_identical_when_forced(runs, name):
 
 
 @pytest.mark.parametrize("name", IDS)
+def test_matvec_parity(runs, name):
+    """BlockSparseMatrix::matvec (block_matrix.cpp:92-108) on the device (ce_matvec) against the oracle's, same
+    block order of accumulation: bitwise up to FMA contraction, asserted at 32 eps max|y|."""
+    r = runs[name]
+    rng = np.random.default_rng(11)
+    for _ in range(2):
+        x = rng.standard_normal(r["p"].n)
+        yg, yo = r["a"].matvec(x), r["op"].matvec(x)
+        assert np.max(np.abs(yg - yo)) <= 32 * np.finfo(float).eps * np.max(np.abs(yo))
+    e = np.zeros(r["p"].n)
+    e[r["p"].n // 3] = 1.0  # a single column of A: exact products, no rounding at all
+    assert np.array_equal(r["a"].matvec(e), r["op"].matvec(e))
+
+
+@pytest.mark.parametrize("name", IDS)
 def test_operator_parity(runs, name):
     """solve(x) = M^-1 x and apply_operator(x) = M x agree with the oracle (gauge invariant, §8c item 4)."""
     R = runs[name]
