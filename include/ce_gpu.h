@@ -231,6 +231,34 @@ int64_t ce_factor_row_sigma(const ce_factor* f, int64_t level, int64_t row, doub
 /* Binary factor dump in the oracle's format, for parity checks. */
 int ce_factor_dump(const ce_factor* f, const char* path);
 
+/* ---- CSV reports of the reference CLI (proj/src/csv.cpp, proj/src/cli.cpp) ----
+ * Text builders: each writes a NUL-terminated table (header row + rows, '\n' line ends, no
+ * quoting: CsvTable::to_string, csv.cpp:37-42) into buf when it fits in cap and returns the text
+ * length (call with cap = 0 to size the buffer; < 0 on error).  Numbers are formatted like
+ * fmt_double / fmt_index (csv.cpp:84-96): the shortest text that round-trips. */
+int ce_fmt_double(double v, char* buf, int cap);
+/* CompressionStrategy::describe (compression.cpp:10-18): "eps=1e-06", "abseps=...", "rank=8"; NULL -> "none". */
+int ce_strategy_describe(const ce_strategy* s, char* buf, int cap);
+/* factor_stats.csv (factor_stats_table, cli.cpp:60-71): level, blocks_eliminated, l_blocks, max_rank,
+ * mean_rank, seconds, bytes -- one row per level. */
+int64_t ce_factor_stats_csv(const ce_factor* f, char* buf, int64_t cap);
+/* factor_summary.csv (run_factor, cli.cpp:167-182); recon_error may be NULL / "" (n > 4096). */
+int64_t ce_factor_summary_csv(const ce_factor* f, int64_t block, const ce_strategy* s, double seconds,
+                              const char* recon_error, char* buf, int64_t cap);
+/* solve_report.csv (run_solve, cli.cpp:233-247); mode "minres" | "pcg" | "direct", s NULL = "none". */
+int64_t ce_solve_report_csv(int64_t n, const char* mode, const ce_strategy* s, int preconditioned,
+                            const ce_solve_report* rep, double factor_seconds, double solve_seconds, char* buf,
+                            int64_t cap);
+/* trace.csv (trace_table, cli.cpp:73-80) from IterationSample arrays. */
+int64_t ce_trace_csv(int64_t count, const int64_t* iter, const double* recurrence, const double* true_resid,
+                     const double* seconds, char* buf, int64_t cap);
+/* IterationTrace (minres.hpp:12-23) of the context's last ce_pcg / ce_minres: one sample per
+ * iteration preceded by the iteration-0 sample (minres.cpp:55); true_resid = -1 where it was not
+ * tracked (the last sample always carries the final true residual, minres.cpp:112-113).  Returns
+ * the sample count (writes min(count, cap)). */
+int64_t ce_ctx_last_trace(const ce_ctx* ctx, int64_t* iter, double* recurrence, double* true_resid, double* seconds,
+                          int64_t cap);
+
 /* ---- Krylov ---- */
 /* PCG with the minres contract (minres.hpp:46-47): x0 = 0, stop when the
  * recurrence ||r||/||b|| <= tol, iterations = number of A*p products.  precond may be NULL

@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdint>
 #include <functional>
 #include <memory>
@@ -142,6 +143,11 @@ struct CompressionStrategy {  // compression.hpp:15-38
     c.s = {1, 0.0, 0, rank};
     return c;
   }
+  std::string describe() const {  // compression.cpp:10-18
+    char buf[96];
+    ce_strategy_describe(&s, buf, static_cast<int>(sizeof buf));
+    return buf;
+  }
 };
 
 struct FactorOptions {  // factorization.hpp:74-77
@@ -167,6 +173,17 @@ class CEFactorization {
   Vector apply_q(const Vector& x) const { return tool(1, x); }
   Vector apply_q_transpose(const Vector& y) const { return tool(2, y); }
   const ce_factor* get() const { return f_.get(); }
+  // FactorStats / LevelStats (factorization.hpp:38-72) as the C structs of ce_gpu.h
+  ce_factor_stats stats() const {
+    ce_factor_stats st{};
+    check(ce_factor_get_stats(f_.get(), &st));
+    return st;
+  }
+  ce_level_stats level_stats(index_t level) const {
+    ce_level_stats ls{};
+    check(ce_factor_get_level_stats(f_.get(), level, &ls));
+    return ls;
+  }
 
  private:
   Vector tool(int which, const Vector& x) const {
@@ -240,8 +257,10 @@ inline SolveReport pcg(const ApplyFn& a, index_t n, const Vector& b, const Apply
   const double bnorm = norm(b);
   if (bnorm == 0.0) {
     rep.converged = true;
+    rep.trace.samples.push_back({0, 0.0, 0.0, elapsed()});
     return rep;
   }
+  rep.trace.samples.push_back({0, 1.0, o.track_true_residual ? 1.0 : -1.0, elapsed()});
   Vector r = b;
   Vector z = precond ? precond(r) : r;
   double rz = checked_inner(r, z);
@@ -290,6 +309,7 @@ inline SolveReport minres(const ApplyFn& a, index_t n, const Vector& b, const Ap
   const double bnorm = norm(b);
   if (bnorm == 0.0) {
     rep.converged = true;
+    rep.trace.samples.push_back({0, 0.0, 0.0, elapsed()});  // minres.cpp:32-36
     return rep;
   }
   Vector r1 = b;
@@ -297,9 +317,11 @@ inline SolveReport minres(const ApplyFn& a, index_t n, const Vector& b, const Ap
   double beta1 = checked_inner(r1, y);
   if (beta1 == 0.0) {
     rep.converged = true;
+    rep.trace.samples.push_back({0, 0.0, 1.0, elapsed()});  // minres.cpp:43-47
     return rep;
   }
   beta1 = std::sqrt(beta1);
+  rep.trace.samples.push_back({0, 1.0, o.track_true_residual ? 1.0 : -1.0, elapsed()});  // minres.cpp:55
   double oldb = 0.0, beta = beta1, dbar = 0.0, epsln = 0.0, phibar = beta1, cs = -1.0, sn = 0.0;
   Vector r2 = r1, w = make_vector(n), w1 = make_vector(n), w2 = make_vector(n), v = make_vector(n);
   for (index_t itn = 1; itn <= o.maxit; ++itn) {
@@ -344,6 +366,24 @@ inline SolveReport minres(const ApplyFn& a, index_t n, const Vector& b, const Ap
   return rep;
 }
 
+namespace detail {
+inline SolveReport device_report(Context& ctx, const ce_solve_report& rep) {
+  SolveReport out;
+  out.converged = rep.converged != 0;
+  out.iterations = rep.iterations;
+  out.final_recurrence_residual = rep.final_recurrence_residual;
+  out.final_true_residual = rep.final_true_residual;
+  const int64_t k = ce_ctx_last_trace(ctx.get(), nullptr, nullptr, nullptr, nullptr, 0);
+  if (k > 0) {
+    std::vector<int64_t> it(static_cast<size_t>(k));
+    std::vector<double> rec(it.size()), tru(it.size()), sec(it.size());
+    ce_ctx_last_trace(ctx.get(), it.data(), rec.data(), tru.data(), sec.data(), k);
+    for (size_t j = 0; j < it.size(); ++j) out.trace.samples.push_back({it[j], rec[j], tru[j], sec[j]});
+  }
+  return out;
+}
+}  // namespace detail
+
 // ---------------------------------------------------------------- device-resident fast path
 // Same contract with the operator and the factor as objects: the whole loop stays on the GPU
 // (one 32-byte read per iteration for the stopping test); x is returned on the host.
@@ -355,12 +395,7 @@ inline SolveReport pcg(Context& ctx, const BlockSparseMatrix& a, index_t n, cons
   const int rc =
       ce_pcg(ctx.get(), a.get(), precond ? precond->get() : nullptr, b.data(), x.data(), n, 0, &opts, &rep, nullptr);
   if (rc != CE_OK && rc != CE_ENOCONV) check(rc);
-  SolveReport out;
-  out.converged = rep.converged != 0;
-  out.iterations = rep.iterations;
-  out.final_recurrence_residual = rep.final_recurrence_residual;
-  out.final_true_residual = rep.final_true_residual;
-  return out;
+  return detail::device_report(ctx, rep);
 }
 
 inline SolveReport minres(Context& ctx, const BlockSparseMatrix& a, index_t n, const Vector& b,
@@ -371,12 +406,122 @@ inline SolveReport minres(Context& ctx, const BlockSparseMatrix& a, index_t n, c
   const int rc = ce_minres(ctx.get(), a.get(), precond ? precond->get() : nullptr, b.data(), x.data(), n, 0, &opts,
                            &rep, nullptr);
   if (rc != CE_OK && rc != CE_ENOCONV) check(rc);
-  SolveReport out;
-  out.converged = rep.converged != 0;
-  out.iterations = rep.iterations;
-  out.final_recurrence_residual = rep.final_recurrence_residual;
-  out.final_true_residual = rep.final_true_residual;
-  return out;
+  return detail::device_report(ctx, rep);
+}
+
+// ---------------------------------------------------------------- CSV reports (csv.hpp, cli.cpp)
+// CsvTable with the reference's semantics (csv.hpp:11-24: no quoting; parse followed by to_string
+// reproduces the input bytes) and the report tables of the reference CLI, built by the library's
+// text builders so that every binding formats numbers identically (fmt_double: std::to_chars).
+struct CsvTable {
+  std::vector<std::string> header;
+  std::vector<std::vector<std::string>> rows;
+
+  std::string to_string() const {
+    std::string out;
+    auto put = [&](const std::vector<std::string>& row) {
+      for (size_t k = 0; k < row.size(); ++k) {
+        if (k) out.push_back(',');
+        out += row[k];
+      }
+      out.push_back('\n');
+    };
+    put(header);
+    for (const auto& r : rows) put(r);
+    return out;
+  }
+  static CsvTable parse(const std::string& text) {
+    if (text.empty()) throw std::invalid_argument("csv text has no header row");
+    CsvTable t;
+    bool first = true;
+    for (size_t start = 0; start < text.size();) {
+      size_t nl = text.find('\n', start);
+      if (nl == std::string::npos) nl = text.size();
+      std::vector<std::string> cells;
+      for (size_t c0 = start;;) {
+        const size_t comma = text.find(',', c0);
+        if (comma == std::string::npos || comma >= nl) {
+          cells.push_back(text.substr(c0, nl - c0));
+          break;
+        }
+        cells.push_back(text.substr(c0, comma - c0));
+        c0 = comma + 1;
+      }
+      if (first) t.header = std::move(cells);
+      else t.rows.push_back(std::move(cells));
+      first = false;
+      start = nl + 1;
+    }
+    return t;
+  }
+  void write(const std::string& path) const {
+    std::FILE* fp = std::fopen(path.c_str(), "wb");
+    if (!fp) throw std::runtime_error("cannot open " + path + " for writing");
+    const std::string text = to_string();
+    const bool ok = std::fwrite(text.data(), 1, text.size(), fp) == text.size();
+    if (std::fclose(fp) != 0 || !ok) throw std::runtime_error("write failed for " + path);
+  }
+  static CsvTable load(const std::string& path) {
+    std::FILE* fp = std::fopen(path.c_str(), "rb");
+    if (!fp) throw std::runtime_error("cannot open " + path);
+    std::string text;
+    char buf[4096];
+    for (size_t k; (k = std::fread(buf, 1, sizeof buf, fp)) > 0;) text.append(buf, k);
+    std::fclose(fp);
+    return parse(text);
+  }
+};
+
+namespace detail {
+template <class F>
+inline std::string text_of(F&& call) {  // C text builder (buf, cap) -> length: size, then fill
+  const int64_t n = call(nullptr, 0);
+  if (n < 0) throw std::invalid_argument(ce_last_error());
+  std::string t(static_cast<size_t>(n) + 1, '\0');
+  call(&t[0], n + 1);
+  t.resize(static_cast<size_t>(n));
+  return t;
+}
+}  // namespace detail
+
+inline std::string fmt_double(double v) {  // csv.cpp:84-88
+  return detail::text_of([&](char* b, int64_t c) { return int64_t(ce_fmt_double(v, b, static_cast<int>(c))); });
+}
+inline std::string fmt_index(index_t v) { return std::to_string(v); }  // csv.cpp:90-94
+
+// cli.cpp:60-71
+inline CsvTable factor_stats_table(const CEFactorization& f) {
+  return CsvTable::parse(detail::text_of([&](char* b, int64_t c) { return ce_factor_stats_csv(f.get(), b, c); }));
+}
+// cli.cpp:167-182 (recon_error: fmt_double of the relative reconstruction error, or "" above n = 4096)
+inline CsvTable factor_summary_table(const CEFactorization& f, index_t block, const CompressionStrategy& s,
+                                     double seconds, const std::string& recon_error = "") {
+  return CsvTable::parse(detail::text_of(
+      [&](char* b, int64_t c) { return ce_factor_summary_csv(f.get(), block, &s.s, seconds, recon_error.c_str(), b, c); }));
+}
+// cli.cpp:73-80
+inline CsvTable trace_table(const IterationTrace& trace) {
+  std::vector<int64_t> it;
+  std::vector<double> rec, tru, sec;
+  for (const auto& smp : trace.samples) {
+    it.push_back(smp.iter);
+    rec.push_back(smp.recurrence_resid);
+    tru.push_back(smp.true_resid);
+    sec.push_back(smp.seconds);
+  }
+  return CsvTable::parse(detail::text_of([&](char* b, int64_t c) {
+    return ce_trace_csv(static_cast<int64_t>(it.size()), it.data(), rec.data(), tru.data(), sec.data(), b, c);
+  }));
+}
+// cli.cpp:233-247; strategy == nullptr prints "none" (no factorization was made)
+inline CsvTable solve_report_table(index_t n, const std::string& mode, const CompressionStrategy* strategy,
+                                   bool preconditioned, const SolveReport& rep, double factor_seconds,
+                                   double solve_seconds) {
+  ce_solve_report r{rep.converged ? 1 : 0, rep.iterations, rep.final_recurrence_residual, rep.final_true_residual, 0.0};
+  return CsvTable::parse(detail::text_of([&](char* b, int64_t c) {
+    return ce_solve_report_csv(n, mode.c_str(), strategy ? &strategy->s : nullptr, preconditioned ? 1 : 0, &r,
+                               factor_seconds, solve_seconds, b, c);
+  }));
 }
 
 }  // namespace ce_b200

@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include "ce/cli.hpp"
+#include "ce/csv.hpp"
 #include "ce/factorization.hpp"
 #include "ce/minres.hpp"
 #include "ce/problems.hpp"
@@ -225,6 +227,70 @@ int ceref_krylov(void* hp, void* hf, int method, const double* b, double* x, dou
   } catch (const std::exception& e) {
     return fail(e);
   }
+}
+
+// ---- the reference CLI's `file` flow and CSV reports (cli.cpp:114-133,153-247; csv.cpp) ----
+static ce::BenchConfig file_config(const char* matrix, const char* rhs, const char* plan, long long block,
+                                   int use_rank, long long rank, double eps, int absolute,
+                                   long long dense_threshold, const char* out_dir) {
+  ce::BenchConfig cfg;
+  cfg.problem = "file";
+  cfg.matrix_path = matrix ? matrix : "";
+  cfg.rhs_path = rhs ? rhs : "";
+  cfg.plan_path = plan ? plan : "";
+  cfg.block = block;
+  cfg.use_rank = use_rank != 0;
+  cfg.rank = rank;
+  cfg.eps = eps;
+  cfg.eps_absolute = absolute != 0;
+  cfg.dense_threshold = dense_threshold;
+  cfg.out_dir = out_dir;
+  return cfg;
+}
+
+// run_factor on a `file` problem: writes factor_stats.csv and factor_summary.csv into out_dir;
+// returns the CLI exit code.
+int ceref_run_factor(const char* matrix, const char* rhs, const char* plan, long long block, int use_rank,
+                     long long rank, double eps, int absolute, long long dense_threshold, const char* out_dir) {
+  return ce::run_factor(file_config(matrix, rhs, plan, block, use_rank, rank, eps, absolute, dense_threshold, out_dir));
+}
+
+// run_solve on a `file` problem: x.txt, trace.csv, solve_report.csv into out_dir.
+int ceref_run_solve(const char* matrix, const char* rhs, const char* plan, long long block, int use_rank,
+                    long long rank, double eps, int absolute, long long dense_threshold, double tol,
+                    long long maxit, int direct, int no_precond, const char* out_dir) {
+  ce::BenchConfig cfg = file_config(matrix, rhs, plan, block, use_rank, rank, eps, absolute, dense_threshold, out_dir);
+  cfg.tol = tol;
+  cfg.maxit = maxit;
+  cfg.direct = direct != 0;
+  cfg.no_precond = no_precond != 0;
+  return ce::run_solve(cfg);
+}
+
+int ceref_fmt_double(double v, char* buf, int cap) {
+  const std::string t = ce::fmt_double(v);
+  if (static_cast<int>(t.size()) < cap) std::memcpy(buf, t.c_str(), t.size() + 1);
+  return static_cast<int>(t.size());
+}
+
+// CsvTable::parse followed by to_string (csv.hpp: reproduces the input bytes); returns the length
+// written (< 0: parse threw).
+long long ceref_csv_roundtrip(const char* text, char* buf, long long cap) {
+  try {
+    const std::string t = ce::CsvTable::parse(text).to_string();
+    if (static_cast<long long>(t.size()) < cap) std::memcpy(buf, t.c_str(), t.size() + 1);
+    return static_cast<long long>(t.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int ceref_describe(int use_rank, long long rank, double eps, int absolute, char* buf, int cap) {
+  const std::string t = (use_rank ? ce::CompressionStrategy::fixed_rank(rank)
+                                  : ce::CompressionStrategy::adaptive(eps, absolute != 0)).describe();
+  if (static_cast<int>(t.size()) < cap) std::memcpy(buf, t.c_str(), t.size() + 1);
+  return static_cast<int>(t.size());
 }
 
 }  // extern "C"

@@ -16,6 +16,7 @@ from .ce import (  # noqa: F401
     CEFactorization,
     CompressionStrategy,
     Context,
+    CsvTable,
     DeviceMatrix,
     FactorOptions,
     LocalShardComm,
@@ -27,11 +28,17 @@ from .ce import (  # noqa: F401
     ce_factorize,
     ce_factorize_sharded,
     device_count,
+    factor_stats_table,
+    factor_summary_table,
+    fmt_double,
+    fmt_index,
     minres,
     pattern_coarsen,
     pattern_square,
     pcg,
     shard_plan_summary,
+    solve_report_table,
+    trace_table,
 )
 
 __all__ = [
@@ -41,6 +48,7 @@ __all__ = [
     "CEFactorization",
     "CompressionStrategy",
     "Context",
+    "CsvTable",
     "DeviceMatrix",
     "FactorOptions",
     "LocalShardComm",
@@ -52,9 +60,15 @@ __all__ = [
     "ce_factorize",
     "ce_factorize_sharded",
     "device_count",
+    "factor_stats_table",
+    "factor_summary_table",
+    "fmt_double",
+    "fmt_index",
     "minres",
     "pattern_coarsen",
     "pattern_square",
     "pcg",
     "shard_plan_summary",
+    "solve_report_table",
+    "trace_table",
 ]

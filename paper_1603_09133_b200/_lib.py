@@ -112,6 +112,14 @@ SIGNATURES = {
     "ce_factor_dump": (C.c_int, [vp, C.c_char_p]),
     "ce_pcg": (C.c_int, [vp, vp, vp, vp, vp, i64, C.c_int, C.POINTER(PcgOpts), C.POINTER(Report), vp]),
     "ce_minres": (C.c_int, [vp, vp, vp, vp, vp, i64, C.c_int, C.POINTER(PcgOpts), C.POINTER(Report), vp]),
+    "ce_fmt_double": (C.c_int, [C.c_double, C.c_char_p, C.c_int]),
+    "ce_strategy_describe": (C.c_int, [C.POINTER(Strategy), C.c_char_p, C.c_int]),
+    "ce_factor_stats_csv": (i64, [vp, C.c_char_p, i64]),
+    "ce_factor_summary_csv": (i64, [vp, i64, C.POINTER(Strategy), C.c_double, C.c_char_p, C.c_char_p, i64]),
+    "ce_solve_report_csv": (i64, [i64, C.c_char_p, C.POINTER(Strategy), C.c_int, C.POINTER(Report), C.c_double,
+                                  C.c_double, C.c_char_p, i64]),
+    "ce_trace_csv": (i64, [i64, i64p, dblp, dblp, dblp, C.c_char_p, i64]),
+    "ce_ctx_last_trace": (i64, [vp, i64p, dblp, dblp, dblp, i64]),
     "ce_problem_create": (C.c_int, [C.c_int, i64, i64, i64, C.POINTER(vp)]),
     "ce_problem_create_plan": (C.c_int, [C.c_int, i64, i64, i64, C.c_int, C.POINTER(vp)]),
     "ce_problem_free": (None, [vp]),

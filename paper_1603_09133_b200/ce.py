@@ -102,9 +102,8 @@ class CompressionStrategy:
         return L.Strategy(1 if self.mode == "rank" else 0, float(self.eps), int(self.absolute), int(self.rank))
 
     def describe(self) -> str:
-        if self.mode == "rank":
-            return f"rank={self.rank}"
-        return f"{'abseps' if self.absolute else 'eps'}={self.eps:g}"
+        """CompressionStrategy::describe (compression.cpp:10-18)."""
+        return _text(lambda buf, cap: lib.ce_strategy_describe(C.byref(self._c()), buf, cap))
 
 
 @dataclass
@@ -135,6 +134,8 @@ class SolveReport:
     final_recurrence_residual: float
     final_true_residual: float
     seconds: float
+    # IterationTrace (minres.hpp:12-23): (iter, recurrence_resid, true_resid or -1, seconds) per iteration
+    trace: List[tuple] = field(default_factory=list)
 
 
 class CoarseningPlan:
@@ -553,8 +554,13 @@ def _krylov(entry, what, a, n, b, precond, opts):
         rc = entry(a.ctx.handle, a.handle, ph, b.ctypes.data, x.ctypes.data, n, 0, C.byref(co), C.byref(rep), None)
     if rc not in (CE_OK, CE_ENOCONV):
         _check(rc)
+    k = int(lib.ce_ctx_last_trace(a.ctx.handle, None, None, None, None, 0))
+    it, rec, tru, sec = np.empty(k, np.int64), np.empty(k), np.empty(k), np.empty(k)
+    lib.ce_ctx_last_trace(a.ctx.handle, _ptr(it, C.c_int64), _ptr(rec, C.c_double), _ptr(tru, C.c_double),
+                          _ptr(sec, C.c_double), k)
     return SolveReport(bool(rep.converged), int(rep.iterations), rep.final_recurrence_residual,
-                       rep.final_true_residual, rep.seconds), x
+                       rep.final_true_residual, rep.seconds,
+                       [(int(i), float(r), float(t), float(q)) for i, r, t, q in zip(it, rec, tru, sec)]), x
 
 
 def pcg(a: DeviceMatrix, n: int, b, precond: Optional[CEFactorization], opts: Optional[PcgOptions] = None):
@@ -571,6 +577,94 @@ def minres(a: DeviceMatrix, n: int, b, precond: Optional[CEFactorization], opts:
     (SolveReport, x).  Same contract as pcg: x0 = 0, recurrence stopping rule relative to
     the starting preconditioned residual, non-convergence reported, not raised."""
     return _krylov(lib.ce_minres, "minres", a, n, b, precond, opts or MinresOptions())
+
+
+# ---- CSV reports of the reference CLI (proj/src/csv.cpp, proj/src/cli.cpp:60-80,153-247) ----
+def _text(call) -> str:
+    """Run a C text builder (buf, cap) -> length twice: size, then fill."""
+    n = int(call(None, 0))
+    if n < 0:
+        _check(CE_EUSAGE)
+    buf = C.create_string_buffer(n + 1)
+    call(buf, n + 1)
+    return buf.value.decode()
+
+
+def fmt_double(v: float) -> str:
+    """Shortest text that round-trips (csv.cpp:84-88, std::to_chars)."""
+    return _text(lambda buf, cap: lib.ce_fmt_double(float(v), buf, cap))
+
+
+def fmt_index(v: int) -> str:
+    return str(int(v))
+
+
+@dataclass
+class CsvTable:
+    """Comma-separated table with a header row, no quoting (csv.hpp:11-24): parse followed by
+    to_string reproduces the input bytes."""
+
+    header: List[str] = field(default_factory=list)
+    rows: List[List[str]] = field(default_factory=list)
+
+    def to_string(self) -> str:
+        return "".join(",".join(r) + "\n" for r in [self.header] + self.rows)
+
+    @staticmethod
+    def parse(text: str) -> "CsvTable":
+        if not text:
+            raise ValueError("csv text has no header row")
+        lines = text.split("\n")
+        if text.endswith("\n"):
+            lines.pop()
+        return CsvTable(lines[0].split(","), [ln.split(",") for ln in lines[1:]])
+
+    def write(self, path: str) -> None:
+        try:
+            with open(path, "wb") as fh:
+                fh.write(self.to_string().encode())
+        except OSError as e:
+            raise OSError(f"cannot open {path} for writing") from e
+
+    @staticmethod
+    def load(path: str) -> "CsvTable":
+        try:
+            with open(path, "rb") as fh:
+                return CsvTable.parse(fh.read().decode())
+        except OSError as e:
+            raise OSError(f"cannot open {path}") from e
+
+
+def factor_stats_table(f: "CEFactorization") -> CsvTable:
+    """factor_stats.csv (factor_stats_table, cli.cpp:60-71)."""
+    return CsvTable.parse(_text(lambda buf, cap: lib.ce_factor_stats_csv(f.handle, buf, cap)))
+
+
+def factor_summary_table(f: "CEFactorization", block: int, strategy: CompressionStrategy, seconds: float,
+                         recon_error: str = "") -> CsvTable:
+    """factor_summary.csv (run_factor, cli.cpp:167-182)."""
+    return CsvTable.parse(_text(lambda buf, cap: lib.ce_factor_summary_csv(
+        f.handle, int(block), C.byref(strategy._c()), float(seconds), recon_error.encode(), buf, cap)))
+
+
+def trace_table(rep: SolveReport) -> CsvTable:
+    """trace.csv (trace_table, cli.cpp:73-80)."""
+    k = len(rep.trace)
+    it = _i64([t[0] for t in rep.trace] or [0])
+    cols = [np.ascontiguousarray([t[j] for t in rep.trace] or [0.0], np.float64) for j in (1, 2, 3)]
+    return CsvTable.parse(_text(lambda buf, cap: lib.ce_trace_csv(
+        k, _ptr(it, C.c_int64), *[_ptr(c, C.c_double) for c in cols], buf, cap)))
+
+
+def solve_report_table(n: int, mode: str, strategy: Optional[CompressionStrategy], preconditioned: bool,
+                       rep: SolveReport, factor_seconds: float, solve_seconds: float) -> CsvTable:
+    """solve_report.csv (run_solve, cli.cpp:233-247); strategy None = "none" (no factorization)."""
+    r = L.Report(int(rep.converged), int(rep.iterations), rep.final_recurrence_residual, rep.final_true_residual,
+                 rep.seconds)
+    sp = C.byref(strategy._c()) if strategy is not None else None
+    return CsvTable.parse(_text(lambda buf, cap: lib.ce_solve_report_csv(
+        int(n), mode.encode(), sp, int(preconditioned), C.byref(r), float(factor_seconds), float(solve_seconds),
+        buf, cap)))
 
 
 class Problem:

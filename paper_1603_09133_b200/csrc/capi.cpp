@@ -2,7 +2,9 @@
 // return codes follow the reference CLI exit codes (proj/include/ce/cli.hpp:16-19,
 // exception mapping of proj/src/cli.cpp:82-95).
 #include <algorithm>
+#include <charconv>
 #include <cstring>
+#include <sstream>
 #include <exception>
 #include <map>
 #include <memory>
@@ -18,6 +20,7 @@
 
 struct ce_ctx {
   ceg::Context ctx;
+  ceg::SolveOut last_solve;  // the last ce_pcg / ce_minres of this context (ce_ctx_last_trace)
 };
 struct ce_matrix {
   ceg::Matrix m;
@@ -673,6 +676,7 @@ int krylov(bool use_minres, ce_ctx* ctx, const ce_matrix* a, const ce_factor* pr
     }
   });
   if (rc != CE_OK) return rc;
+  ctx->last_solve = so;
   if (rep) {
     rep->converged = so.converged ? 1 : 0;
     rep->iterations = so.iterations;
@@ -696,6 +700,113 @@ int ce_pcg(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const doub
 int ce_minres(ce_ctx* ctx, const ce_matrix* a, const ce_factor* precond, const double* b, double* x, int64_t n,
               int on_device, const ce_pcg_opts* opts, ce_solve_report* rep, void* stream) {
   return krylov(true, ctx, a, precond, b, x, n, on_device, opts, rep, stream);
+}
+
+int64_t ce_ctx_last_trace(const ce_ctx* ctx, int64_t* iter, double* recurrence, double* true_resid, double* seconds,
+                          int64_t cap) {
+  if (!ctx) return -1;
+  const ceg::SolveOut& so = ctx->last_solve;
+  const int64_t k = static_cast<int64_t>(so.trace_rec.size());
+  for (int64_t j = 0; j < k && j < cap; ++j) {
+    const size_t u = static_cast<size_t>(j);
+    if (iter) iter[j] = so.trace_iter[u];
+    if (recurrence) recurrence[j] = so.trace_rec[u];
+    if (true_resid) true_resid[j] = so.trace_true[u];
+    if (seconds) seconds[j] = so.trace_sec[u];
+  }
+  return k;
+}
+
+// ---- CSV reports (csv.cpp:84-96; cli.cpp:60-80,153-183,233-247) ----
+namespace {
+std::string fmt_double(double v) {  // shortest text that round-trips (csv.cpp:84-88)
+  char buf[64];
+  const auto res = std::to_chars(buf, buf + sizeof buf, v);
+  return std::string(buf, res.ptr);
+}
+std::string fmt_index(int64_t v) { return std::to_string(v); }
+std::string describe(const ce_strategy* s) {  // CompressionStrategy::describe (compression.cpp:10-18)
+  if (!s) return "none";
+  std::ostringstream os;
+  if (s->mode == 1) os << "rank=" << s->rank;
+  else os << (s->absolute ? "abseps=" : "eps=") << s->eps;
+  return os.str();
+}
+std::string csv_row(const std::vector<std::string>& cells) {
+  std::string out;
+  for (size_t k = 0; k < cells.size(); ++k) {
+    if (k) out.push_back(',');
+    out += cells[k];
+  }
+  out.push_back('\n');
+  return out;
+}
+int64_t emit(const std::string& t, char* buf, int64_t cap) {
+  if (buf && static_cast<int64_t>(t.size()) < cap) std::memcpy(buf, t.c_str(), t.size() + 1);
+  return static_cast<int64_t>(t.size());
+}
+}  // namespace
+
+int ce_fmt_double(double v, char* buf, int cap) { return static_cast<int>(emit(fmt_double(v), buf, cap)); }
+
+int ce_strategy_describe(const ce_strategy* s, char* buf, int cap) {
+  return static_cast<int>(emit(describe(s), buf, cap));
+}
+
+int64_t ce_factor_stats_csv(const ce_factor* f, char* buf, int64_t cap) {
+  std::string t;
+  const int rc = guarded([&] {
+    if (!f) throw std::invalid_argument("null argument");
+    t = csv_row({"level", "blocks_eliminated", "l_blocks", "max_rank", "mean_rank", "seconds", "bytes"});
+    const int64_t nl = static_cast<int64_t>(f->f->levels.size());
+    for (int64_t l = 0; l < nl; ++l) {
+      ce_level_stats ls;
+      if (ce_factor_get_level_stats(f, l, &ls) != CE_OK) throw std::runtime_error(g_err);
+      t += csv_row({fmt_index(l + 1), fmt_index(ls.eliminated), fmt_index(ls.factor_blocks), fmt_index(ls.max_rank),
+                    fmt_double(ls.mean_rank), fmt_double(ls.seconds), fmt_index(ls.l_bytes + ls.q_bytes)});
+    }
+  });
+  return rc == CE_OK ? emit(t, buf, cap) : -1;
+}
+
+int64_t ce_factor_summary_csv(const ce_factor* f, int64_t block, const ce_strategy* s, double seconds,
+                              const char* recon_error, char* buf, int64_t cap) {
+  std::string t;
+  const int rc = guarded([&] {
+    if (!f || !s) throw std::invalid_argument("null argument");
+    ce_factor_stats st;
+    if (ce_factor_get_stats(f, &st) != CE_OK) throw std::runtime_error(g_err);
+    t = csv_row({"n", "block", "strategy", "levels", "tail_dim", "l_blocks", "predicted_l_blocks", "block_ratio",
+                 "l_scalar_nnz", "l_bytes", "q_bytes", "tail_bytes", "total_bytes", "seconds", "recon_error"});
+    const double ratio = st.predicted_factor_blocks > 0 ? st.factor_blocks / st.predicted_factor_blocks : 0.0;
+    t += csv_row({fmt_index(f->f->n), fmt_index(block), describe(s), fmt_index(st.n_levels), fmt_index(st.tail_dim),
+                  fmt_double(st.factor_blocks), fmt_double(st.predicted_factor_blocks), fmt_double(ratio),
+                  fmt_index(st.l_scalar_nnz), fmt_index(st.l_payload_bytes), fmt_index(st.q_payload_bytes),
+                  fmt_index(st.tail_bytes), fmt_index(st.l_payload_bytes + st.q_payload_bytes + st.tail_bytes),
+                  fmt_double(seconds), recon_error ? recon_error : ""});
+  });
+  return rc == CE_OK ? emit(t, buf, cap) : -1;
+}
+
+int64_t ce_solve_report_csv(int64_t n, const char* mode, const ce_strategy* s, int preconditioned,
+                            const ce_solve_report* rep, double factor_seconds, double solve_seconds, char* buf,
+                            int64_t cap) {
+  if (!rep || !mode) return -1;
+  std::string t = csv_row({"n", "mode", "strategy", "preconditioned", "converged", "iterations", "recurrence_resid",
+                           "true_resid", "factor_seconds", "solve_seconds"});
+  t += csv_row({fmt_index(n), mode, describe(s), preconditioned ? "1" : "0", rep->converged ? "1" : "0",
+                fmt_index(rep->iterations), fmt_double(rep->final_recurrence_residual),
+                fmt_double(rep->final_true_residual), fmt_double(factor_seconds), fmt_double(solve_seconds)});
+  return emit(t, buf, cap);
+}
+
+int64_t ce_trace_csv(int64_t count, const int64_t* iter, const double* recurrence, const double* true_resid,
+                     const double* seconds, char* buf, int64_t cap) {
+  std::string t = csv_row({"iter", "recurrence_resid", "true_resid", "seconds"});
+  for (int64_t j = 0; j < count; ++j)
+    t += csv_row({fmt_index(iter ? iter[j] : j + 1), fmt_double(recurrence[j]), fmt_double(true_resid[j]),
+                  fmt_double(seconds[j])});
+  return emit(t, buf, cap);
 }
 
 int ce_problem_create(int cfg, int64_t nx, int64_t ny, int64_t nz, ce_problem** out) {

@@ -2438,11 +2438,19 @@ SolveOut pcg_device(const Matrix& A, const Factor* M, const double* d_b, double*
   double hb = 0.0;
   fetch(&hb, 4, 1);
   const double bnorm = std::sqrt(hb);
+  auto sample = [&](int64_t it, double rec, double tru) {  // IterationSample (minres.hpp:12-20)
+    out.trace_iter.push_back(it);
+    out.trace_rec.push_back(rec);
+    out.trace_true.push_back(tru);
+    out.trace_sec.push_back(now_s() - t0);
+  };
   if (bnorm == 0.0) {
     out.converged = true;
+    sample(0, 0.0, 0.0);
     out.seconds = now_s() - t0;
     return out;
   }
+  sample(0, 1.0, track_true ? 1.0 : -1.0);
   launch_copy(r.p, d_b, n, s);
   precond(r.p, z.p);
   dot(r.p, z.p, 0);
@@ -2462,8 +2470,7 @@ SolveOut pcg_device(const Matrix& A, const Factor* M, const double* d_b, double*
     if (!std::isfinite(h[2]) || h[2] <= 0.0) throw std::runtime_error("operator is not positive definite: p' A p <= 0");
     rel = std::sqrt(h[3]) / bnorm;
     out.iterations = itn;
-    if (track_true) out.trace_true.push_back(true_resid(bnorm));
-    out.trace_rec.push_back(rel);
+    sample(itn, rel, track_true ? true_resid(bnorm) : -1.0);
     if (rel <= tol) {
       out.converged = true;
       break;
@@ -2479,6 +2486,7 @@ SolveOut pcg_device(const Matrix& A, const Factor* M, const double* d_b, double*
   }
   out.final_rec = rel;
   out.final_true = true_resid(bnorm);
+  if (!out.trace_true.empty() && !track_true) out.trace_true.back() = out.final_true;
   CE_CUDA(cudaGetLastError());
   out.seconds = now_s() - t0;
   return out;
@@ -2524,8 +2532,15 @@ SolveOut minres_device(const Matrix& A, const Factor* M, const double* d_b, doub
   };
   CE_CUDA(cudaMemsetAsync(d_x, 0, static_cast<size_t>(n) * sizeof(double), s));
   const double bnorm = std::sqrt(dot(d_b, d_b));
+  auto sample = [&](int64_t it, double rec, double tru) {  // IterationSample (minres.hpp:12-20)
+    out.trace_iter.push_back(it);
+    out.trace_rec.push_back(rec);
+    out.trace_true.push_back(tru);
+    out.trace_sec.push_back(now_s() - t0);
+  };
   if (bnorm == 0.0) {
     out.converged = true;
+    sample(0, 0.0, 0.0);  // minres.cpp:32-36
     out.seconds = now_s() - t0;
     return out;
   }
@@ -2534,10 +2549,12 @@ SolveOut minres_device(const Matrix& A, const Factor* M, const double* d_b, doub
   double beta1 = checked_inner(r1, y);
   if (beta1 == 0.0) {  // minres.cpp:43-47: report left at its defaults
     out.converged = true;
+    sample(0, 0.0, 1.0);
     out.seconds = now_s() - t0;
     return out;
   }
   beta1 = std::sqrt(beta1);
+  sample(0, 1.0, track_true ? 1.0 : -1.0);  // minres.cpp:55
   double oldb = 0.0, beta = beta1, dbar = 0.0, epsln = 0.0, qrnorm = beta1, phibar = beta1, cs = -1.0, sn = 0.0;
   launch_copy(r2, r1, n, s);
   CE_CUDA(cudaMemsetAsync(w, 0, static_cast<size_t>(n) * sizeof(double), s));
@@ -2573,8 +2590,7 @@ SolveOut minres_device(const Matrix& A, const Factor* M, const double* d_b, doub
     qrnorm = phibar;
     const double rec = qrnorm / beta1;
     out.iterations = itn;
-    out.trace_rec.push_back(rec);
-    if (track_true) out.trace_true.push_back(true_resid(bnorm));
+    sample(itn, rec, track_true ? true_resid(bnorm) : -1.0);
     if (rec <= tol || beta / beta1 < 1e-30) {
       out.converged = true;
       break;
@@ -2582,6 +2598,7 @@ SolveOut minres_device(const Matrix& A, const Factor* M, const double* d_b, doub
   }
   out.final_rec = qrnorm / beta1;
   out.final_true = true_resid(bnorm);
+  if (!out.trace_true.empty() && !track_true) out.trace_true.back() = out.final_true;
   CE_CUDA(cudaGetLastError());
   out.seconds = now_s() - t0;
   return out;

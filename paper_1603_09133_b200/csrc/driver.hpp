@@ -27,7 +27,9 @@ struct SolveOut {
   bool converged = false;
   int64_t iterations = 0;
   double final_rec = 0.0, final_true = 0.0, seconds = 0.0;
-  std::vector<double> trace_rec, trace_true;
+  // IterationTrace (minres.hpp:12-23): sample 0 before the loop, then one per iteration; true = -1 untracked
+  std::vector<int64_t> trace_iter;
+  std::vector<double> trace_rec, trace_true, trace_sec;
 };
 // Both Krylov loops run on stream `s` (the caller's, so its producers of b / consumers of x
 // are ordered against the solve).
