@@ -139,11 +139,15 @@ enum : int {
 
 // smem doubles needed by one sweep CTA for a level
 int64_t sweep_smem_doubles(int bmax, int kcap);
-// Largest block the level sweep accepts (static shared chunk maps / cluster table); the
-// driver rejects larger levels with an error instead of overrunning them.
+// Largest block the level sweep accepts: the Schur panels hold whole neighbours in kPanelRows
+// (260) compacted rows (sweep.cu), the chunk maps / cluster table are static shared arrays of this
+// size, and the apply sweeps stage kApplyWmax = 256 eliminated columns.  The driver rejects larger
+// levels with an error instead of overrunning them.  (Round 1 accepted 512 here, which the panel
+// tables did not cover: a neighbour with more than 260 live rows overran them.)
 #ifndef CE_SWEEP_BLOCK_MAX
-#define CE_SWEEP_BLOCK_MAX 512  // 1024 costs ~1.5% on cfg2 (static shared chunk maps), A/B this round
+#define CE_SWEEP_BLOCK_MAX 256
 #endif
+static_assert(CE_SWEEP_BLOCK_MAX <= 256, "Schur panel tables (kPanelRows) hold at most 256 + 4 rows per neighbour");
 constexpr int kSweepBlockMax = CE_SWEEP_BLOCK_MAX;
 int sweep_kcap(int bmax);  // F^T chunk height for a level
 void launch_sweep(const SweepArgs& a, int grid, size_t smem_bytes, cudaStream_t s);

@@ -108,7 +108,7 @@ def test_colored_plan_fullsize_properties(gpu_ctx, cfg):
 
 def test_block_limit_fails_loudly(gpu_ctx):
     """3-D all-axis merges grow blocks with the cell surface: cfg4's stencil at 32^3 reaches
-    b ~ 580 at level 3, above the sweep's kSweepBlockMax (512).  The library must refuse with a
+    b ~ 580 at level 3, above the sweep's kSweepBlockMax (256).  The library must refuse with a
     clear error instead of overrunning its shared-memory chunk maps."""
     p = ce.Problem(4, 32, 32, 32, plan="merge_all_axes")
     a = ce.DeviceMatrix(p.matrix())

