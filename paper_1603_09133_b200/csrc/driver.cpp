@@ -4,6 +4,7 @@
 #include "driver.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -44,6 +45,11 @@ struct Thresholds {
   bool small_panels = false;               // one close neighbour per Schur panel
   bool no_tri_table = false;               // CE_NO_TRI=1: binary-search slot lookups at every level
   int64_t panel_cap = 0;                   // Schur panel height limit in rows (0: buffer-derived)
+  double chain_frac = 0.4;                 // share of rest(w-1) over which wave w's chain tickets are spread
+                                           // (build_tickets; 1: the chain follows rest(w-1), the round-1 order;
+                                           // A/B on cfg3: 1.0 7250 ms, 0.6 6250, 0.4 6080, 0.25 6180)
+  double strip_frac = 1.0;                 // share of rest(w-1) emitted before wave w's strips (>= chain_frac)
+  int64_t pre_leaf = 0;                    // rest(w-1) tickets emitted before wave w's TSQR leaves
   int64_t pair_group = 0;                  // Schur panel pairs (P, Q..Q+g-1) per task, panel P staged once;
                                            // 0: per row, kernels.hpp row_pair_group(np)
                                            // (A/B on cfg2: g=1 1.82 s, 2 1.89, 3 1.97, 5 2.19: per-wave parallelism wins)
@@ -75,6 +81,12 @@ struct Thresholds {
     env("CE_PAIR_GROUP", pair_group);
     env("CE_PANEL_CAP", panel_cap);
     if (pair_group < 0) pair_group = 0;
+    if (const char* e = std::getenv("CE_CHAIN_FRAC")) chain_frac = std::atof(e);
+    if (!(chain_frac >= 0.0 && chain_frac <= 1.0)) chain_frac = 0.4;
+    if (const char* e = std::getenv("CE_STRIP_FRAC")) strip_frac = std::atof(e);
+    if (!(strip_frac >= 0.0 && strip_frac <= 1.0)) strip_frac = 1.0;
+    env("CE_PRE_LEAF", pre_leaf);
+    if (pre_leaf < 0) pre_leaf = 0;
   }
 };
 const Thresholds& thresholds() {
@@ -439,10 +451,29 @@ void build_tickets(const LevelPlan& P, const std::vector<char>* mask, std::vecto
                    std::vector<int>& item_part) {
   const int64_t M = P.M;
   const std::vector<int64_t>& wave = P.wave;
-  // The order is, for every wave w: [leaves(w)] [rest(w-1)] [combines(w)] [A2(w)] [strips(w)]
-  // [urgent(w)], rows in `order` within each segment.  Every row's share of each segment is
+  // Segments of a wave w: leaves(w), rest(w-1), the TSQR combines of w by tree level (kLv
+  // segments; deeper levels share the last one, row-major, so a node still follows its
+  // children), A2(w), strips(w), urgent(w).  The emitted order is
+  //   [leaves(w)] [rest(w-1) with w's chain stages -- combine levels, then A2 -- interleaved]
+  //   [strips(w)] [urgent(w)],
+  // rows in `order` within each segment.  The chain of a wave is a handful of short serial
+  // tasks (one CTA each) while rest(w-1) is hundreds of independent Schur tasks: with the chain
+  // after rest(w-1) its tickets are only taken once every rest ticket is out, so the chain
+  // runs when the grid has nothing else left and every wave pays it in idle CTAs.  Chain stage
+  // s of S is instead placed after the first chain_frac (s+1)/S of rest(w-1): it is taken
+  // about when it becomes ready, a too-early pick parks one CTA, and rest(w-1) keeps the other
+  // CTAs busy meanwhile.  (The strips stay behind rest(w-1): there are hundreds per row, and
+  // parked strip tickets would hold the whole grid.)  Every row's share of each segment is
   // known up front, so segment starts come from prefix sums over the rows and the rows fill
   // their slots in parallel (the tickets of one level are millions of items).
+  constexpr int kLv = 8;
+  constexpr int kSeg = 5 + kLv;  // 0 leaves, 1 rest, 2..2+kLv-1 combine levels, then A2, strips, urgent
+  constexpr int sA2 = 2 + kLv, sStrip = 3 + kLv, sUrg = 4 + kLv;
+  constexpr int kStage = kLv + 3;  // stages inserted into rest(w-1): leaves, combine levels, A2, strips
+  auto stage_seg = [](int st) { return st == 0 ? 0 : (st == kStage - 1 ? sStrip : 1 + st); };
+  const double frac = thresholds().chain_frac;
+  const double sfrac = std::max(thresholds().strip_frac, frac);
+  const int64_t kcap = sweep_kcap(std::max(P.bmax, 1));
   std::vector<int64_t> wstart;
   for (int64_t k = 0; k < M;) {
     wstart.push_back(k);
@@ -451,67 +482,132 @@ void build_tickets(const LevelPlan& P, const std::vector<char>* mask, std::vecto
   }
   wstart.push_back(M);
   const int64_t nw = static_cast<int64_t>(wstart.size()) - 1;
-  auto cnt = [&](int row, int seg) -> int64_t {  // items of `row` in segment seg (0..5)
-    const size_t r = static_cast<size_t>(row);
-    if (mask && !(*mask)[r]) return 0;
-    switch (seg) {
-      case 0: return P.nleaf[r];
-      case 1: return static_cast<int64_t>(P.rest_of[r].size());
-      case 2: return P.nA1[r] - P.nleaf[r];
-      case 3: return 1;
-      case 4: return P.nA3[r];
-      default: return static_cast<int64_t>(P.urg_of[r].size());
+  // combine nodes of `row` per tree level (sweep_body.cuh sweep_kernel: leaves first, then
+  // levels of F-way combines down to one triangle)
+  auto comb_levels = [&](size_t r, int64_t* lv) {
+    for (int l = 0; l < kLv; ++l) lv[l] = 0;
+    if (P.nA1[r] <= P.nleaf[r]) return;
+    const int64_t F = std::max<int64_t>(2, kcap / std::max<int64_t>(P.bsz[r], 1));
+    int l = 0;
+    for (int64_t n = (P.nleaf[r] + F - 1) / F;; n = (n + F - 1) / F) {
+      lv[std::min(l, kLv - 1)] += n;
+      ++l;
+      if (n == 1) break;
     }
   };
-  // start[k * 6 + seg]: first ticket of the row at order position k in segment seg
-  std::vector<int64_t> start(static_cast<size_t>(M) * 6, 0), segsum(static_cast<size_t>(nw) * 6, 0);
-  parallel_rows(nw, [&](int64_t w0, int64_t w1) {
-    for (int64_t w = w0; w < w1; ++w)
-      for (int seg = 0; seg < 6; ++seg) {
-        int64_t t = 0;
-        for (int64_t k = wstart[static_cast<size_t>(w)]; k < wstart[static_cast<size_t>(w + 1)]; ++k) {
-          start[static_cast<size_t>(k) * 6 + static_cast<size_t>(seg)] = t;
-          t += cnt(P.order[static_cast<size_t>(k)], seg);
-        }
-        segsum[static_cast<size_t>(w) * 6 + static_cast<size_t>(seg)] = t;
-      }
-  });
-  // segment bases in emission order
-  std::vector<int64_t> base(static_cast<size_t>(nw) * 6, 0);
-  int64_t at = 0;
-  auto place = [&](int64_t w, int seg) {
-    base[static_cast<size_t>(w) * 6 + static_cast<size_t>(seg)] = at;
-    at += segsum[static_cast<size_t>(w) * 6 + static_cast<size_t>(seg)];
+  auto counts = [&](int row, int64_t* c) {
+    const size_t r = static_cast<size_t>(row);
+    for (int s = 0; s < kSeg; ++s) c[s] = 0;
+    if (mask && !(*mask)[r]) return;
+    c[0] = P.nleaf[r];
+    c[1] = static_cast<int64_t>(P.rest_of[r].size());
+    comb_levels(r, c + 2);
+    c[sA2] = 1;
+    c[sStrip] = P.nA3[r];
+    c[sUrg] = static_cast<int64_t>(P.urg_of[r].size());
   };
+  // start[k * kSeg + seg]: first ticket of the row at order position k inside segment seg
+  std::vector<int64_t> start(static_cast<size_t>(M) * kSeg, 0), segsum(static_cast<size_t>(nw) * kSeg, 0);
+  parallel_rows(nw, [&](int64_t w0, int64_t w1) {
+    int64_t c[kSeg], t[kSeg];
+    for (int64_t w = w0; w < w1; ++w) {
+      for (int s = 0; s < kSeg; ++s) t[s] = 0;
+      for (int64_t k = wstart[static_cast<size_t>(w)]; k < wstart[static_cast<size_t>(w + 1)]; ++k) {
+        counts(P.order[static_cast<size_t>(k)], c);
+        for (int s = 0; s < kSeg; ++s) {
+          start[static_cast<size_t>(k) * kSeg + static_cast<size_t>(s)] = t[s];
+          t[s] += c[s];
+        }
+      }
+      for (int s = 0; s < kSeg; ++s) segsum[static_cast<size_t>(w) * kSeg + static_cast<size_t>(s)] = t[s];
+    }
+  });
+  // segment bases in emission order.  Section w holds rest(w-1) with the stages of wave w
+  // inserted at cut[w][st] (rest items emitted before stage st), then urgent(w); a rest item g of
+  // wave w-1 lands at base + g + (items of the stages cut at or before g).  Stages: leaves,
+  // combine levels, A2, strips.  urgent(w) follows all of rest(w-1): a row's Schur tasks wait
+  // for every task of its predecessors, rest(w-1) included.
+  std::vector<int64_t> base(static_cast<size_t>(nw + 1) * kSeg, 0);
+  std::vector<int64_t> cut(static_cast<size_t>(nw + 1) * kStage, 0);
+  int64_t at = 0;
+  auto seg_n = [&](int64_t w, int s) { return segsum[static_cast<size_t>(w) * kSeg + static_cast<size_t>(s)]; };
   for (int64_t w = 0; w <= nw; ++w) {
-    if (w < nw) place(w, 0);
-    if (w > 0) place(w - 1, 1);
+    const int64_t R = w > 0 ? seg_n(w - 1, 1) : 0;
+    if (w > 0) base[static_cast<size_t>(w - 1) * kSeg + 1] = at;  // rest(w-1): position of its item 0
+    int64_t done = 0;  // rest items already emitted
+    if (w < nw) {
+      // chain stages (combine levels, A2) present in this wave
+      int S = 0, si = 0;
+      for (int s = 0; s <= kLv; ++s)
+        if (seg_n(w, 2 + s) > 0) ++S;
+      const int64_t pre = std::min<int64_t>(R, thresholds().pre_leaf);
+      for (int st = 0; st < kStage; ++st) {
+        const int seg = stage_seg(st);
+        const int64_t n = seg_n(w, seg);
+        int64_t c = done;  // an empty stage cuts nothing
+        if (n > 0) {
+          if (st == 0) {
+            c = pre;
+          } else if (st == kStage - 1) {
+            c = sfrac >= 1.0 ? R : pre + static_cast<int64_t>(sfrac * static_cast<double>(R - pre));
+          } else {
+            ++si;
+            c = frac >= 1.0 ? R : pre + static_cast<int64_t>(frac * static_cast<double>(R - pre) * si / S);
+          }
+          c = std::max(std::min(c, R), done);
+        }
+        cut[static_cast<size_t>(w) * kStage + static_cast<size_t>(st)] = c;
+        at += c - done;
+        done = c;
+        base[static_cast<size_t>(w) * kSeg + static_cast<size_t>(seg)] = at;
+        at += n;
+      }
+    }
+    at += R - done;
     if (w == nw) break;
-    place(w, 2);
-    place(w, 3);
-    place(w, 4);
-    place(w, 5);
+    base[static_cast<size_t>(w) * kSeg + sUrg] = at;
+    at += seg_n(w, sUrg);
   }
   item_row.assign(static_cast<size_t>(at), 0);
   item_part.assign(static_cast<size_t>(at), 0);
   parallel_rows(nw, [&](int64_t w0, int64_t w1) {
+    int64_t lv[kLv];
     for (int64_t w = w0; w < w1; ++w)
       for (int64_t k = wstart[static_cast<size_t>(w)]; k < wstart[static_cast<size_t>(w + 1)]; ++k) {
         const int row = P.order[static_cast<size_t>(k)];
         const size_t r = static_cast<size_t>(row);
         if (mask && !(*mask)[r]) continue;
         auto put = [&](int seg, int64_t j, int part) {
-          const size_t idx = static_cast<size_t>(base[static_cast<size_t>(w) * 6 + static_cast<size_t>(seg)] +
-                                                 start[static_cast<size_t>(k) * 6 + static_cast<size_t>(seg)] + j);
-          item_row[idx] = row;
-          item_part[idx] = part;
+          int64_t idx = base[static_cast<size_t>(w) * kSeg + static_cast<size_t>(seg)] +
+                        start[static_cast<size_t>(k) * kSeg + static_cast<size_t>(seg)] + j;
+          if (seg == 1 && w + 1 < nw) {
+            // rest item g of wave w: shifted by the chain stages of wave w+1 cut at or before g
+            const int64_t g = start[static_cast<size_t>(k) * kSeg + 1] + j;
+            for (int st = 0; st < kStage; ++st)
+              if (cut[static_cast<size_t>(w + 1) * kStage + static_cast<size_t>(st)] <= g)
+                idx += seg_n(w + 1, stage_seg(st));
+          }
+          item_row[static_cast<size_t>(idx)] = row;
+          item_part[static_cast<size_t>(idx)] = part;
         };
         for (int p = 0; p < P.nleaf[r]; ++p) put(0, p, p);
         for (size_t j = 0; j < P.rest_of[r].size(); ++j) put(1, static_cast<int64_t>(j), P.rest_of[r][j]);
-        for (int p = P.nleaf[r]; p < P.nA1[r]; ++p) put(2, p - P.nleaf[r], p);
-        put(3, 0, P.nA1[r]);
-        for (int p = 0; p < P.nA3[r]; ++p) put(4, p, P.nA1[r] + 1 + p);
-        for (size_t j = 0; j < P.urg_of[r].size(); ++j) put(5, static_cast<int64_t>(j), P.urg_of[r][j]);
+        if (P.nA1[r] > P.nleaf[r]) {
+          comb_levels(r, lv);
+          // tree levels in part order; levels >= kLv - 1 share the last segment
+          const int64_t F = std::max<int64_t>(2, kcap / std::max<int64_t>(P.bsz[r], 1));
+          int p = P.nleaf[r], l = 0;
+          int64_t in_last = 0;
+          for (int64_t n = (P.nleaf[r] + F - 1) / F;; n = (n + F - 1) / F, ++l) {
+            const int seg = std::min(l, kLv - 1);
+            for (int64_t q = 0; q < n; ++q, ++p) put(2 + seg, (seg == kLv - 1 ? in_last : 0) + q, p);
+            if (seg == kLv - 1) in_last += n;
+            if (n == 1) break;
+          }
+        }
+        put(sA2, 0, P.nA1[r]);
+        for (int p = 0; p < P.nA3[r]; ++p) put(sStrip, p, P.nA1[r] + 1 + p);
+        for (size_t j = 0; j < P.urg_of[r].size(); ++j) put(sUrg, static_cast<int64_t>(j), P.urg_of[r][j]);
       }
   });
 }
@@ -825,6 +921,51 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
     });
     build_tickets(P, nullptr, P.item_row, P.item_part);
     if (static_cast<int64_t>(P.item_row.size()) != it) throw std::logic_error("ticket order lost items");
+    if (std::getenv("CE_CHECK_TICKETS") && std::getenv("CE_CHECK_TICKETS")[0] == '1') {
+      // development check: every (row, part) exactly once, and inside a row the A stages in
+      // dependency order (tree nodes after every node of the level below, then A2, then the
+      // strips; Schur tasks after the strips)
+      std::vector<int64_t> pos(static_cast<size_t>(it), -1), row_item0(static_cast<size_t>(M), 0);
+      for (int64_t k = 0; k < M; ++k) row_item0[static_cast<size_t>(P.order[static_cast<size_t>(k)])] = P.item_start[static_cast<size_t>(k)];
+      for (int64_t t = 0; t < it; ++t) {
+        const size_t r = static_cast<size_t>(P.item_row[static_cast<size_t>(t)]);
+        const int part = P.item_part[static_cast<size_t>(t)];
+        const int64_t n = 1 + P.nA1[r] + P.nA3[r] + P.nB[r];
+        if (part < 0 || part >= n) throw std::logic_error("ticket check: part out of range");
+        int64_t& slot = pos[static_cast<size_t>(row_item0[r] + part)];
+        if (slot >= 0) throw std::logic_error("ticket check: duplicate item");
+        slot = t;
+      }
+      const int64_t kc = sweep_kcap(std::max(P.bmax, 1));
+      for (int64_t i = 0; i < M; ++i) {
+        const size_t r = static_cast<size_t>(i);
+        const int64_t* q = pos.data() + row_item0[r];
+        const int nA1 = P.nA1[r], nA3 = P.nA3[r], nB = P.nB[r];
+        int64_t lo_prev = -1;  // latest ticket of the tree level below
+        if (nA1 > 0) {
+          const int64_t F = std::max<int64_t>(2, kc / std::max<int64_t>(P.bsz[r], 1));
+          int p = 0;
+          for (int64_t n = P.nleaf[r];; n = (n + F - 1) / F) {
+            int64_t hi = -1;
+            for (int64_t c = 0; c < n; ++c, ++p) {
+              if (q[p] <= lo_prev) throw std::logic_error("ticket check: tree node before its children's level");
+              hi = std::max(hi, q[p]);
+            }
+            lo_prev = hi;
+            if (n == 1) break;
+          }
+          if (p != nA1) throw std::logic_error("ticket check: tree size");
+        }
+        if (q[nA1] <= lo_prev) throw std::logic_error("ticket check: A2 before the tree root");
+        int64_t last = q[nA1];
+        for (int p = 0; p < nA3; ++p) {
+          if (q[nA1 + 1 + p] <= q[nA1]) throw std::logic_error("ticket check: strip before A2");
+          last = std::max(last, q[nA1 + 1 + p]);
+        }
+        for (int p = 0; p < nB; ++p)
+          if (q[nA1 + 1 + nA3 + p] <= last) throw std::logic_error("ticket check: Schur task before the strips");
+      }
+    }
     tp5 = now_s();
     // sq_pan: panel of j inside close(i) for each close predecessor entry (j, i), i < j
     P.sq_pan.assign(P.scol.size(), -1);
@@ -1037,6 +1178,7 @@ struct DevPlan {
   DevArray<int64_t> sptr, sslot, slot_off, cptr, chol_off, g_off, basis_off, sigma_off, item_start, offsets, cl_slot,
       fsum, rs_off, pan_ptr, sboff, sdiag, leaf_ptr, leaf_e, strip_ptr, strip_e;  // (cl_slot unused)
   DevArray<unsigned char> skind;
+  DevArray<char> arena;  // backing store of every array above (views)
   // All plan arrays go through one pinned staging buffer (grow-only, per host thread): the
   // host copies them in and the DMAs run asynchronously (pageable copies would stage
   // synchronously).  The buffer is reused by the next level's upload, which happens
@@ -1050,6 +1192,7 @@ struct DevPlan {
       }
     };
     thread_local Stage st;
+    const double tu_start = now_s();
     size_t total = 0;
     auto add = [&](size_t bytes) { total += (bytes + 255) / 256 * 256; };
     auto sz = [](const auto& v) { return v.size() * sizeof(v[0]); };
@@ -1066,6 +1209,18 @@ struct DevPlan {
       st.cap = total + total / 4;
       CE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&st.p), st.cap, cudaHostAllocDefault));
     }
+    const double tu0 = now_s();
+    // one device arena for all plan arrays, laid out like the staging buffer: one allocation
+    // (every level asks for the high-water size, so the cached block of the previous level or
+    // factorization always fits; 36 separate arrays used to miss the allocator cache whenever
+    // a level's sizes moved by more than its rounding, a cudaMalloc of up to 100 ms between
+    // two sweeps) and one DMA
+    static std::atomic<size_t> arena_hwm{0};
+    size_t want = arena_hwm.load();
+    while (want < total && !arena_hwm.compare_exchange_weak(want, total)) {
+    }
+    want = std::max(want, total);
+    if (arena.n < total) arena.alloc(want);
     size_t off = 0;
     // the staging copies run in parallel on the host threads (one 200 MB level plan was a
     // 30-60 ms single-thread memcpy on the critical path between two sweeps), then every
@@ -1076,20 +1231,27 @@ struct DevPlan {
       size_t bytes, at;
     };
     std::vector<Job> jobs;
-    auto put = [&](auto& d, const auto& h) {
+    std::vector<size_t> owned;  // jobs whose array outlives the plan (moved into the level factor)
+    auto put = [&](auto& d, const auto& h, bool keep = false) {
       const size_t bytes = h.size() * sizeof(h[0]);
-      d.alloc(h.size());
+      if (keep) {
+        d.alloc(h.size());
+        if (bytes) owned.push_back(jobs.size());
+      } else {
+        d.set_view(arena.p + off, h.size());
+      }
       if (bytes) jobs.push_back({d.p, h.data(), bytes, off});
       off += (bytes + 255) / 256 * 256;
     };
     put(order, P.order); put(item_row, P.item_row); put(item_part, P.item_part); put(nA1, P.nA1); put(nleaf, P.nleaf);
     put(nA3, P.nA3); put(nB, P.nB); put(pan_start, P.pan_start); put(fsum, P.fsum); put(rs_off, P.rs_off);
-    put(pan_ptr, P.pan_ptr); put(bsz, P.bsz); put(scol, P.scol); put(ccol, P.ccol); put(croff, P.croff);
-    put(sptr, P.sptr); put(sslot, P.sslot); put(slot_off, P.slot_off); put(cptr, P.cptr); put(chol_off, P.chol_off);
-    put(g_off, P.g_off); put(basis_off, P.basis_off); put(sigma_off, P.sigma_off); put(item_start, P.item_start);
-    put(offsets, P.offsets); put(skind, P.skind); put(sboff, P.sboff); put(sbsz, P.sbsz); put(sroff, P.sroff);
+    put(pan_ptr, P.pan_ptr); put(bsz, P.bsz, true); put(scol, P.scol); put(ccol, P.ccol, true); put(croff, P.croff, true);
+    put(sptr, P.sptr); put(sslot, P.sslot); put(slot_off, P.slot_off); put(cptr, P.cptr, true); put(chol_off, P.chol_off, true);
+    put(g_off, P.g_off, true); put(basis_off, P.basis_off, true); put(sigma_off, P.sigma_off, true); put(item_start, P.item_start);
+    put(offsets, P.offsets, true); put(skind, P.skind); put(sboff, P.sboff); put(sbsz, P.sbsz); put(sroff, P.sroff);
     put(sdiag, P.sdiag); put(target, P.target); put(leaf_ptr, P.leaf_ptr); put(leaf_e, P.leaf_e);
     put(strip_ptr, P.strip_ptr); put(strip_e, P.strip_e); put(sq_pan, P.sq_pan);
+    const double tu1 = now_s();
     constexpr size_t kChunk = size_t{1} << 20;
     std::vector<std::pair<size_t, size_t>> pieces;  // (job, first byte) of 1 MB pieces
     for (size_t j = 0; j < jobs.size(); ++j)
@@ -1102,7 +1264,12 @@ struct DevPlan {
         std::memcpy(stage + jb.at + b, static_cast<const char*>(jb.src) + b, n);
       }
     });
-    for (const Job& jb : jobs) CE_CUDA(cudaMemcpyAsync(jb.dst, stage + jb.at, jb.bytes, cudaMemcpyHostToDevice, s));
+    const double tu2 = now_s();
+    if (total) CE_CUDA(cudaMemcpyAsync(arena.p, stage, total, cudaMemcpyHostToDevice, s));
+    for (size_t j : owned) CE_CUDA(cudaMemcpyAsync(jobs[j].dst, stage + jobs[j].at, jobs[j].bytes, cudaMemcpyHostToDevice, s));
+    if (std::getenv("CE_PROFILE") && std::getenv("CE_PROFILE")[0] == '1')
+      std::fprintf(stderr, "[ce-profile] plan upload %.1f MB: stage buffer %.1f ms, device arrays %.1f ms, staging copy %.1f ms, enqueue %.1f ms\n",
+                   total / 1e6, 1e3 * (tu0 - tu_start), 1e3 * (tu1 - tu0), 1e3 * (tu2 - tu1), 1e3 * (now_s() - tu2));
   }
 };
 
@@ -1471,7 +1638,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
   for (int64_t i = 0; i < A->m; ++i) bsz[static_cast<size_t>(i)] = static_cast<int>(A->offsets[static_cast<size_t>(i + 1)] - A->offsets[static_cast<size_t>(i)]);
   std::vector<int> bcol(A->col_idx.begin(), A->col_idx.end());
   LevelPlan cur = plan_level(bsz, A->row_ptr, bcol, s);  // device idle: squares on the GPU
-  DevPlan dcur;
+  DevPlan dcur, dprev;
   dcur.upload(cur, s);
   DevArray<double> store(static_cast<size_t>(cur.store_doubles));
   store.zero(s);
@@ -2123,6 +2290,10 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
 
     if (spec.valid()) spec.wait();  // the speculative planner reads `cur`
     cur = std::move(next);
+    // the remainder kernel queued above still reads this level's device plan: keep it (and
+    // its arena, out of the allocator cache that other host threads draw from) until the
+    // next level's sweep has completed
+    dprev = std::move(dcur);
     dcur = std::move(dnext);
     std::swap(store, nstore);
     if (nM == 0) break;

@@ -38,18 +38,21 @@ template <class T>
 struct DevArray {
   T* p = nullptr;
   size_t n = 0;
+  bool view = false;  // p points into another allocation (set_view): never freed here
   DevArray() = default;
   explicit DevArray(size_t count) { alloc(count); }
   DevArray(const DevArray&) = delete;
   DevArray& operator=(const DevArray&) = delete;
-  DevArray(DevArray&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevArray(DevArray&& o) noexcept : p(o.p), n(o.n), view(o.view) { o.p = nullptr; o.n = 0; o.view = false; }
   DevArray& operator=(DevArray&& o) noexcept {
     if (this != &o) {
       release();
       p = o.p;
       n = o.n;
+      view = o.view;
       o.p = nullptr;
       o.n = 0;
+      o.view = false;
     }
     return *this;
   }
@@ -60,9 +63,17 @@ struct DevArray {
     if (count) p = static_cast<T*>(pool_alloc(count * sizeof(T)));
   }
   void release() {
-    if (p) pool_free(p, n * sizeof(T));
+    if (p && !view) pool_free(p, n * sizeof(T));
     p = nullptr;
     n = 0;
+    view = false;
+  }
+  // non-owning window into a larger device allocation (the level plan's arena)
+  void set_view(void* ptr, size_t count) {
+    release();
+    p = count ? static_cast<T*>(ptr) : nullptr;
+    n = count;
+    view = count != 0;
   }
   void upload(const std::vector<T>& h, cudaStream_t s) {
     alloc(h.size());
