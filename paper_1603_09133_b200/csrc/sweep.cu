@@ -36,6 +36,9 @@
 #ifndef CE_NO_WIDE_JACOBI
 #define CE_NO_WIDE_JACOBI 0
 #endif
+#ifndef CE_STAGE_ASYNC
+#define CE_STAGE_ASYNC 1  // Schur panels staged with cp.async in the shared-memory build
+#endif
 #ifndef CE_SWEEP_MIN_BLOCKS
 #define CE_SWEEP_MIN_BLOCKS 1  // resident sweep CTAs per SM the register allocation must allow
 #endif

@@ -1671,9 +1671,38 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
         if (di[u] >= 0) dst[di[u]] = v[u];
     }
   };
+#if CE_SMEM_BUFFER && CE_STAGE_ASYNC
+  // shared-memory build: every element is an 8-byte cp.async (LDGSTS), so a thread's whole share
+  // of the panel is in flight at once with no register staging -- one global-memory latency per
+  // panel instead of one per batch of 8 loads; padding rows are plain zero stores
+  auto stage_async = [&](double* dst, int ld, int n, const int* roff, const unsigned char* blk,
+                         const unsigned short* loc) {
+    // 8 lanes along a g row (64 contiguous bytes), 32 rows per pass: the row's source address
+    // is looked up once and reused for its w / 8 elements (no division by w, no per-element
+    // table lookups)
+    const int ql = tid & 7;
+    for (int y = tid >> 3; y < ld; y += T / 8) {
+      double* d = dst + y;
+      if (y < n) {
+        const double* src = G + static_cast<int64_t>(r + roff[blk[y]] + loc[y]) * w;
+        const unsigned da = static_cast<unsigned>(__cvta_generic_to_shared(d));
+        for (int q = ql; q < w; q += 8)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(da + static_cast<unsigned>(q * ld) * 8u), "l"(src + q)
+                       : "memory");
+      } else {
+        for (int q = ql; q < w; q += 8) d[q * ld] = 0.0;
+      }
+    }
+  };
+  if (!reuse_s) stage_async(GsT, lds, rsn, roff_s, yblk, yloc);
+  if (P != Q) stage_async(GtT, ldt, rtn, roff_t, xblk, xloc);
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+#else
   if (!reuse_s) stage(GsT, lds, rsn, roff_s, yblk, yloc);
   if (P != Q) stage(GtT, ldt, rtn, roff_t, xblk, xloc);
   __syncthreads();
+#endif
   const long long tb2 = clock64();
   prof_add(A, kProfBStage, tb2 - tb1);
   for (int wt = warp; wt < ntx * nty; wt += T / 32) {

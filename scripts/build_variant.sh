@@ -9,5 +9,5 @@ mkdir -p $O
 for f in sweep apply dense krylov; do
   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC "$@" -c $D/$f.cu -o $O/$f.o
 done
-nvcc -shared -gencode arch=compute_100a,code=sm_100a -Xcompiler -static-libstdc++ -Xcompiler -static-libgcc -Xlinker --exclude-libs,ALL -o $O.so $O/*.o $D/build/driver.o $D/build/capi.o $D/build/problem.o $D/build/io.o -lcudart_static -lrt -lpthread -ldl
+nvcc -shared -gencode arch=compute_100a,code=sm_100a -Xcompiler -static-libstdc++ -Xcompiler -static-libgcc -Xlinker --exclude-libs,ALL -o $O.so $O/*.o $D/build/validate.o $D/build/shard.o $D/build/assemble.o $D/build/pattern.o $D/build/driver.o $D/build/capi.o $D/build/problem.o $D/build/io.o -lcudart_static -lrt -lpthread -ldl
 echo built $O.so
