@@ -86,7 +86,6 @@ struct Thresholds {
     if (const char* e = std::getenv("CE_STRIP_FRAC")) strip_frac = std::atof(e);
     if (!(strip_frac >= 0.0 && strip_frac <= 1.0)) strip_frac = 1.0;
     env("CE_PRE_LEAF", pre_leaf);
-    if (pre_leaf < 0) pre_leaf = 0;
   }
 };
 const Thresholds& thresholds() {
@@ -482,6 +481,12 @@ void build_tickets(const LevelPlan& P, const std::vector<char>* mask, std::vecto
   }
   wstart.push_back(M);
   const int64_t nw = static_cast<int64_t>(wstart.size()) - 1;
+  // rest(w-1) tickets emitted before leaves(w) (development knob CE_PRE_LEAF, default 0): the
+  // leaves wait for urgent(w-1), and a round or two of rest tickets fills that gap on levels
+  // with thousands of rows and 2-4 rows per wave (cfg3 levels 7 / 8: -3% / -6%), but delays the
+  // chain everywhere else (cfg3 levels 5 / 6 / 9, cfg2 levels 7 / 8: +1-5%); no rule found that
+  // wins on both configs, so it stays off
+  const int64_t pre_leaf = std::max<int64_t>(0, thresholds().pre_leaf);
   // combine nodes of `row` per tree level (sweep_body.cuh sweep_kernel: leaves first, then
   // levels of F-way combines down to one triangle)
   auto comb_levels = [&](size_t r, int64_t* lv) {
@@ -540,7 +545,7 @@ void build_tickets(const LevelPlan& P, const std::vector<char>* mask, std::vecto
       int S = 0, si = 0;
       for (int s = 0; s <= kLv; ++s)
         if (seg_n(w, 2 + s) > 0) ++S;
-      const int64_t pre = std::min<int64_t>(R, thresholds().pre_leaf);
+      const int64_t pre = std::min<int64_t>(R, pre_leaf);
       for (int st = 0; st < kStage; ++st) {
         const int seg = stage_seg(st);
         const int64_t n = seg_n(w, seg);
