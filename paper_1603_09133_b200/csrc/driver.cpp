@@ -1721,30 +1721,47 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       d_forced.upload(fr, s);
     }
 
-    // speculative symbolic plan of the next level on a host thread (assumes every group
-    // keeps a nonzero rank; checked after the sweep, recomputed if not)
-    std::future<LevelPlan> spec = std::async(std::launch::async, [&cur, &cur_groups]() {
-      const int64_t ng = static_cast<int64_t>(cur_groups.size());
-      std::vector<int64_t> gof(static_cast<size_t>(cur.M), 0);
-      for (int64_t g = 0; g < ng; ++g)
-        for (int64_t b : cur_groups[static_cast<size_t>(g)]) gof[static_cast<size_t>(b)] = g;
-      std::vector<int64_t> nptr(static_cast<size_t>(ng + 1), 0), mark(static_cast<size_t>(ng), -1);
-      std::vector<int> ncol, row;
-      for (int64_t g = 0; g < ng; ++g) {
-        row.clear();
-        for (int64_t b : cur_groups[static_cast<size_t>(g)])
-          for (int64_t e = cur.sptr[static_cast<size_t>(b)]; e < cur.sptr[static_cast<size_t>(b + 1)]; ++e) {
-            const int64_t h = gof[static_cast<size_t>(cur.scol[static_cast<size_t>(e)])];
-            if (mark[static_cast<size_t>(h)] == g) continue;
-            mark[static_cast<size_t>(h)] = g;
-            row.push_back(static_cast<int>(h));
+    // speculative symbolic plan of the next level on a host thread while this level sweeps.  It
+    // assumes every group keeps a nonzero rank except the groups that are dead by structure:
+    // with an eps strategy a row whose far blocks are all absent or still structurally zero
+    // (kind 3) gets rank 0 (compression.cpp:20-36: an empty / zero far concat retains nothing), so a
+    // group of such rows vanishes from the next level.  The assumed alive set is checked after
+    // the sweep and the plan recomputed if it was wrong.
+    const bool predict_dead = !st || st->mode != 1;
+    std::future<std::pair<LevelPlan, std::vector<char>>> spec =
+        std::async(std::launch::async, [&cur, &cur_groups, predict_dead]() {
+          const int64_t ng = static_cast<int64_t>(cur_groups.size());
+          std::vector<int64_t> gof(static_cast<size_t>(cur.M), 0), amap(static_cast<size_t>(ng), -1);
+          std::vector<char> alive(static_cast<size_t>(ng), 1);
+          int64_t nA = 0;
+          for (int64_t g = 0; g < ng; ++g) {
+            bool any = !predict_dead;
+            for (int64_t b : cur_groups[static_cast<size_t>(g)]) {
+              gof[static_cast<size_t>(b)] = g;
+              for (int64_t e = cur.sptr[static_cast<size_t>(b)]; !any && e < cur.sptr[static_cast<size_t>(b + 1)]; ++e)
+                any = cur.skind[static_cast<size_t>(e)] == 2;
+            }
+            alive[static_cast<size_t>(g)] = any ? 1 : 0;
+            if (any) amap[static_cast<size_t>(g)] = nA++;
           }
-        std::sort(row.begin(), row.end());
-        ncol.insert(ncol.end(), row.begin(), row.end());
-        nptr[static_cast<size_t>(g + 1)] = static_cast<int64_t>(ncol.size());
-      }
-      return plan_symbolic(ng, std::move(nptr), std::move(ncol));
-    });
+          std::vector<int64_t> nptr(static_cast<size_t>(nA + 1), 0), mark(static_cast<size_t>(ng), -1);
+          std::vector<int> ncol, row;
+          for (int64_t g = 0; g < ng; ++g) {
+            if (!alive[static_cast<size_t>(g)]) continue;
+            row.clear();
+            for (int64_t b : cur_groups[static_cast<size_t>(g)])
+              for (int64_t e = cur.sptr[static_cast<size_t>(b)]; e < cur.sptr[static_cast<size_t>(b + 1)]; ++e) {
+                const int64_t h = gof[static_cast<size_t>(cur.scol[static_cast<size_t>(e)])];
+                if (!alive[static_cast<size_t>(h)] || mark[static_cast<size_t>(h)] == g) continue;
+                mark[static_cast<size_t>(h)] = g;
+                row.push_back(static_cast<int>(amap[static_cast<size_t>(h)]));
+              }
+            std::sort(row.begin(), row.end());
+            ncol.insert(ncol.end(), row.begin(), row.end());
+            nptr[static_cast<size_t>(amap[static_cast<size_t>(g)] + 1)] = static_cast<int64_t>(ncol.size());
+          }
+          return std::make_pair(plan_symbolic(nA, std::move(nptr), std::move(ncol)), std::move(alive));
+        });
 
     SweepArgs a{};
     a.dbg = std::getenv("CE_DBG") ? std::atoi(std::getenv("CE_DBG")) : 0;
@@ -2075,7 +2092,11 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     const int64_t nM = static_cast<int64_t>(nbsz.size());
     std::vector<int64_t> nptr(static_cast<size_t>(nM + 1), 0);
     std::vector<int> ncol;
-    if (nM != ng) {  // some group died: the speculative plan does not apply
+    // the speculative plan applies when it assumed exactly this alive set
+    std::pair<LevelPlan, std::vector<char>> sp = spec.get();
+    bool spec_ok = true;
+    for (int64_t g = 0; g < ng && spec_ok; ++g) spec_ok = (alive[static_cast<size_t>(g)] >= 0) == (sp.second[static_cast<size_t>(g)] != 0);
+    if (!spec_ok) {  // a group died (or survived) against the structural prediction: plan again
       // coarse rows of the alive groups, in parallel (one mark array per host thread)
       std::vector<std::vector<int>> rows(static_cast<size_t>(ng));
       parallel_rows(ng, [&](int64_t g0, int64_t g1) {
@@ -2114,9 +2135,8 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
     std::future<void> next_fut;
     if (nM > 0)
       next_fut = std::async(std::launch::async, [&]() {
-        LevelPlan sp = spec.get();
-        if (nM == ng) {
-          next = std::move(sp);
+        if (spec_ok) {
+          next = std::move(sp.first);
           plan_numeric(next, nbsz);
         } else {
           next = plan_level(nbsz, nptr, ncol, s);  // after the sweep: the device is idle
@@ -2293,7 +2313,7 @@ Factor* factorize(Context* ctx, const Matrix* A, const ce_plan_host* plan_host, 
       std::fprintf(stderr, "[ce-profile] level %zu host: apply lists %.1f ms, stats+rest %.1f ms, iteration %.1f ms\n", li + 1,
                    1e3 * (h_tb - h_ta), 1e3 * (now_s() - h_tb), 1e3 * (now_s() - h_t0));
 
-    if (spec.valid()) spec.wait();  // the speculative planner reads `cur`
+    if (spec.valid()) spec.wait();  // the speculative planner reads `cur` (early exits above)
     cur = std::move(next);
     // the remainder kernel queued above still reads this level's device plan: keep it (and
     // its arena, out of the allocator cache that other host threads draw from) until the
