@@ -827,14 +827,16 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
       for (int64_t i = r0; i < r1; ++i) {
         const size_t iu = static_cast<size_t>(i);
         int64_t nf = 0, ns = 0;
+        int64_t kc = P.cptr[iu];  // close(i) is the ascending sub-list of sq(i) with kind 1: walk both
         for (int64_t e = P.sptr[iu]; e < P.sptr[iu + 1]; ++e) {
           const size_t eu = static_cast<size_t>(e);
           const int j = P.scol[eu];
           P.sboff[eu] = P.slot_off[static_cast<size_t>(P.sslot[eu])];
           P.sbsz[eu] = P.bsz[static_cast<size_t>(j)];
           if (P.skind[eu] == 1) {
-            const int64_t k = csr_find(P.cptr, P.ccol, i, j);
-            P.sroff[eu] = P.croff[static_cast<size_t>(k)];
+            while (kc < P.cptr[iu + 1] && P.ccol[static_cast<size_t>(kc)] < j) ++kc;
+            if (kc == P.cptr[iu + 1] || P.ccol[static_cast<size_t>(kc)] != j) throw std::logic_error("close entry missing from the close list");
+            P.sroff[eu] = P.croff[static_cast<size_t>(kc)];
           }
           nf += P.skind[eu] == 2;
           ns += P.skind[eu] == 1 || P.skind[eu] == 2;
@@ -984,8 +986,9 @@ void plan_numeric(LevelPlan& P, std::vector<int> bsz) {
             if (P.nB[iu] <= 1) continue;
             const int64_t q = csr_find(P.cptr, P.ccol, i, static_cast<int>(j)) - P.cptr[iu];
             const int np = static_cast<int>(P.pan_ptr[iu + 1] - P.pan_ptr[iu]) - 1;
-            int p = 0;
-            while (p + 1 < np && P.pan_start[static_cast<size_t>(P.pan_ptr[iu] + p + 1)] <= q) ++p;
+            // panel p with pan_start[p] <= q < pan_start[p + 1]
+            const int* ps = P.pan_start.data() + P.pan_ptr[iu];
+            const int p = static_cast<int>(std::upper_bound(ps, ps + np, static_cast<int>(q)) - ps) - 1;
             P.sq_pan[static_cast<size_t>(e)] = p;
           }
         }
