@@ -39,9 +39,11 @@ namespace {
 struct Thresholds {
   int64_t pair_inline = int64_t{1} << 19;  // FMA below which a row's Schur pairs stay in A2
   int64_t leaf_work = int64_t{1} << 15;    // far gather f*b^2 above which TSQR leaves are split off
-  int64_t leaf_cols = 0;                   // far columns per TSQR leaf (0: sqrt(f / b) leaves)
+  int64_t leaf_cols = 192;                 // far columns per TSQR leaf (0: min(kcap, 128), the round-1 value)
   int64_t strip_work = int64_t{1} << 15;   // strip rotation S*b^2 above which the strip is split off
-  int64_t strip_cols = 64;                 // strip columns per task
+  int64_t strip_cols = 192;                // strip columns per task (64 until the chain tickets moved: with the
+                                           // chain overlapped, fewer and larger strip / leaf tasks win -- per-level
+                                           // A/B in profiles/r2_summary.md: cfg3 sweep 5101 -> 4660 ms)
   bool small_panels = false;               // one close neighbour per Schur panel
   bool no_tri_table = false;               // CE_NO_TRI=1: binary-search slot lookups at every level
   int64_t panel_cap = 0;                   // Schur panel height limit in rows (0: buffer-derived)
