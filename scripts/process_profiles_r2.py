@@ -44,7 +44,7 @@ if os.path.exists(os.path.join(OUT, "launches_cfg3.csv")):
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in rows(os.path.join(OUT, "launches_cfg3.csv")):
         if r.get("Metric Name") == "gpu__time_duration.sum":
-            k = r["Kernel Name"].split("(")[0].split("<")[0][-60:]
+            k = r["Kernel Name"].replace("(anonymous namespace)::", "").replace("<unnamed>::", "").split("(")[0].split("<")[0][-60:]
             agg[k][0] += 1
             agg[k][1] += to_ms(r["Metric Value"], r["Metric Unit"])
     tot = sum(v[1] for v in agg.values())
