@@ -264,6 +264,11 @@ def run_product(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU: the ranks of the node share its host cores for the level planning
+    # (read by the library when it loads)
+    lws = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    if lws > 1 and "CE_HOST_THREADS" not in os.environ:
+        os.environ["CE_HOST_THREADS"] = str(max(2, min(16, (os.cpu_count() or 16) // lws)))
     # test scaffolding (tests/test_bench_contract.py): every rank on GPU 0 with the gloo backend,
     # to run the N > 1 code path on a one-GPU box; the driver's runs use one GPU per rank + NCCL
     if os.environ.get("CE_BENCH_SAME_DEVICE") == "1":

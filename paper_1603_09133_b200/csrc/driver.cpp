@@ -173,8 +173,14 @@ namespace {
 // Run f(r0, r1) over row chunks on up to 16 host threads (small ranges run inline).
 template <class F>
 void parallel_rows(int64_t M, F&& f) {
-  const int64_t hw = std::max<int64_t>(1, static_cast<int64_t>(std::thread::hardware_concurrency()));
-  const int64_t nt = std::min<int64_t>(16, hw);
+  // CE_HOST_THREADS: host planning threads of this process (one process per GPU: the ranks of a
+  // node share its cores, bench.py divides them)
+  static const int64_t nt = [] {
+    const int64_t hw = std::max<int64_t>(1, static_cast<int64_t>(std::thread::hardware_concurrency()));
+    int64_t n = std::min<int64_t>(16, hw);
+    if (const char* e = std::getenv("CE_HOST_THREADS")) n = std::max<int64_t>(1, std::min<int64_t>(64, std::atoll(e)));
+    return n;
+  }();
   if (M < 64 || nt <= 1) {
     f(int64_t{0}, M);
     return;

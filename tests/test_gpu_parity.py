@@ -398,3 +398,21 @@ def test_slot_table_and_zero_far_skip_paths(gpu_ctx):
     print(f"skip vs full gather {e_full:.2e}, vs oracle {e_o:.2e}")
     # deep levels amplify roundoff: the same bound as test_task_split_paths_agree
     assert e_full <= 1e-6 and e_o <= 1e-6
+
+
+def test_ticket_order_is_schedule_only(gpu_ctx):
+    """The sweep's ticket order (build_tickets) only schedules the task graph: the
+    round-1 order (chain after rest), the default interleaved order, an early-strip / pre-leaf
+    order and the 64-column task split of round 1 all pass the planner's self-check
+    (CE_CHECK_TICKETS: every task once, every wait on an earlier ticket) and give the
+    bit-identical operator for the same task split."""
+    chk = {"CE_CHECK_TICKETS": "1"}
+    kw = dict(cfg=3, grid=(128, 96), dth=64)
+    y0 = _solve_in_subprocess(chk, **kw)
+    y1 = _solve_in_subprocess(dict(chk, CE_CHAIN_FRAC="1.0"), **kw)
+    y2 = _solve_in_subprocess(dict(chk, CE_CHAIN_FRAC="0.2", CE_STRIP_FRAC="0.6", CE_PRE_LEAF="37"), **kw)
+    assert np.array_equal(y0, y1) and np.array_equal(y0, y2)
+    # forced task splits exercise every stage kind on a small problem
+    f0 = _solve_in_subprocess(dict(chk, CE_FORCE_TASKS="7", CE_CHAIN_FRAC="1.0"), **kw)
+    f1 = _solve_in_subprocess(dict(chk, CE_FORCE_TASKS="7", CE_CHAIN_FRAC="0.3", CE_PRE_LEAF="5"), **kw)
+    assert np.array_equal(f0, f1)
