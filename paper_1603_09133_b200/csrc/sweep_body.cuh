@@ -2218,12 +2218,20 @@ __global__ void __launch_bounds__(T, CE_SWEEP_MIN_BLOCKS) sweep_kernel(SweepArgs
         if (w > 0) all_panels(A, i, __ldcg(A.rank + i), w, s.R);
       } else {
         // task k -> panel P and pairs (P, Q0 .. Q0 + g - 1), Q0 >= P (driver.cpp pair_tasks)
+        // Panel P has ceil((np - P) / g) tasks, so the last m panels have
+        // T(m) = g q (q + 1) / 2 + (q + 1) r tasks (m = q g + r): closed-form inverse instead of a
+        // walk over the panels (hundreds of panels per row at the deep levels, every thread)
         const int g = row_pair_group(A.pair_group, np);
-        int P = 0, kk = k;
-        while (kk >= (np - P + g - 1) / g) {
-          kk -= (np - P + g - 1) / g;
-          ++P;
-        }
+        const int qn = np / g, rn = np - qn * g;
+        const int ntask = g * qn * (qn + 1) / 2 + (qn + 1) * rn;
+        const int need = ntask - k;  // tasks from this one to the row's last: smallest m with T(m) >= need
+        int q = static_cast<int>((sqrt(1.0 + 8.0 * static_cast<double>(need) / g) - 1.0) * 0.5);
+        while (q > 0 && g * q * (q + 1) / 2 >= need) --q;
+        while (g * (q + 1) * (q + 2) / 2 < need) ++q;
+        const int rem = need - g * q * (q + 1) / 2;  // 1 .. g (q + 1)
+        const int m = q * g + (rem + q) / (q + 1);
+        const int tm = g * q * (q + 1) / 2 + (q + 1) * (m - q * g);
+        const int P = np - m, kk = k - (ntask - tm);
         const int q0 = P + kk * g, q1 = min(np, q0 + g);
         for (int Q = q0; Q < q1; ++Q)
           if (w > 0) panel_update(A, i, __ldcg(A.rank + i), w, P, Q, s.R, Q > q0);
