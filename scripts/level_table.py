@@ -1,5 +1,5 @@
 """Per-level sweep table (LevelStats + SURVEY §8d algorithmic counts + CUDA-event sweep time):
-python scripts/level_table.py CFG PLAN  -> JSON lines, one per level, then a summary line."""
+python scripts/level_table.py CFG PLAN [NX NY NZ] -> JSON lines, one per level, then a summary line."""
 import json
 import os
 import sys
@@ -8,7 +8,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1603_09133_b200 as ce  # noqa: E402
 
 cfg, plan = int(sys.argv[1]), sys.argv[2]
-p = ce.Problem(cfg, plan=plan)
+grid = [int(v) for v in sys.argv[3:6]] if len(sys.argv) >= 6 else []  # optional nx ny nz override
+p = ce.Problem(cfg, *grid, plan=plan)
 a = ce.DeviceMatrix(p.matrix())
 for _ in range(2):
     f = ce.ce_factorize(a, p.plan, p.strategy())
