@@ -436,7 +436,9 @@ def run_product(args):
                       "steps": len(erec), "warmup": 2, "factor_ms": 1e3 * efac / len(erec),
                       "pcg_solve_ms": 1e3 * sum(x[1] for x in erec) / len(erec), "pcg_iterations": erep.iterations,
                       "pcg_true_residual": erep.final_true_residual,
-                      "sweep_hbm_frac": erec[-1][3] / esw / 1e9 / peaks["hbm_gbs"]})
+                      "sweep_hbm_frac": erec[-1][3] / esw / 1e9 / peaks["hbm_gbs"],
+                      # the like-for-like CPU number: the single-thread oracle on the WHOLE config
+                      "cpu_full_size": fullsize_cpu_reference(2, args.plan)})
         del ea, eb
 
     # The same config under the colour-major all-axis-merge plan:
