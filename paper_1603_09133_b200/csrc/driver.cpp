@@ -51,7 +51,7 @@ struct Thresholds {
                                            // (build_tickets; 1: the chain follows rest(w-1), the round-1 order;
                                            // A/B on cfg3: 1.0 7250 ms, 0.6 6250, 0.4 6080, 0.25 6180)
   double strip_frac = 1.0;                 // share of rest(w-1) emitted before wave w's strips (>= chain_frac)
-  int64_t pre_leaf = 0;                    // rest(w-1) tickets emitted before wave w's TSQR leaves
+  int64_t pre_leaf = -1;                   // rest(w-1) tickets emitted before wave w's TSQR leaves (-1: per-wave rule)
   int64_t pair_group = 0;                  // Schur panel pairs (P, Q..Q+g-1) per task, panel P staged once;
                                            // 0: per row, kernels.hpp row_pair_group(np)
                                            // (A/B on cfg2: g=1 1.82 s, 2 1.89, 3 1.97, 5 2.19: per-wave parallelism wins)
@@ -489,12 +489,14 @@ void build_tickets(const LevelPlan& P, const std::vector<char>* mask, std::vecto
   }
   wstart.push_back(M);
   const int64_t nw = static_cast<int64_t>(wstart.size()) - 1;
-  // rest(w-1) tickets emitted before leaves(w) (development knob CE_PRE_LEAF, default 0): the
-  // leaves wait for urgent(w-1), and a round or two of rest tickets fills that gap on levels
-  // with thousands of rows and 2-4 rows per wave (cfg3 levels 7 / 8: -3% / -6%), but delays the
-  // chain everywhere else (cfg3 levels 5 / 6 / 9, cfg2 levels 7 / 8: +1-5%); no rule found that
-  // wins on both configs, so it stays off
-  const int64_t pre_leaf = std::max<int64_t>(0, thresholds().pre_leaf);
+  // rest(w-1) tickets emitted before leaves(w).  The leaves wait for urgent(w-1); when that
+  // segment has fewer tickets than the grid has CTAs, the other CTAs would park on the leaves for
+  // about one Schur task, and a round of rest tickets fills the gap -- if rest(w-1) is large
+  // enough that the chain placed in it is not delayed (cfg3 levels 7 / 8: -3% / -6%).  A fixed
+  // count everywhere loses on the other levels (+1-5%: cfg3 levels 5, 6, 9, cfg2 levels 7, 8), so
+  // the rule is per wave; CE_PRE_LEAF >= 0 forces a count.
+  const int64_t pre_force = thresholds().pre_leaf;
+  constexpr int64_t kGrid = 148;  // CTAs of the persistent sweep on a B200 (a scheduling hint only)
   // combine nodes of `row` per tree level (sweep_body.cuh sweep_kernel: leaves first, then
   // levels of F-way combines down to one triangle)
   auto comb_levels = [&](size_t r, int64_t* lv) {
@@ -553,7 +555,11 @@ void build_tickets(const LevelPlan& P, const std::vector<char>* mask, std::vecto
       int S = 0, si = 0;
       for (int s = 0; s <= kLv; ++s)
         if (seg_n(w, 2 + s) > 0) ++S;
-      const int64_t pre = std::min<int64_t>(R, pre_leaf);
+      const int64_t U = w > 0 ? seg_n(w - 1, sUrg) : 0;
+      int64_t pre = 0;
+      if (pre_force >= 0) pre = pre_force;
+      else if (U > 0 && U < kGrid && R > 4 * kGrid) pre = std::min<int64_t>(R / 4, 2 * kGrid);
+      pre = std::min<int64_t>(R, pre);
       for (int st = 0; st < kStage; ++st) {
         const int seg = stage_seg(st);
         const int64_t n = seg_n(w, seg);
