@@ -1575,35 +1575,26 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
     }
     if (lane == 31) n_live[warp] = incl;
   }
-  if (!A.tri_off) {
-    // binary search of the squared pattern (large levels): a chain of dependent loads per
-    // pair, started before the panel columns are known to the other warps
-    for (int idx = tid; idx < nt * ns; idx += T) {
-      const int kt = idx / ns, ks = idx % ns;
-      long long off = -1;
-      if (!(P == Q && ks > kt)) {
-        const int t = A.cl_col[c0 + t0 + kt], s = A.cl_col[c0 + s0 + ks];
+  // value offsets of the stored (t, s) blocks: every thread reads its pair's columns from the
+  // close list itself, so this chain of dependent loads runs beside the table warps' chain
+  // instead of behind it (one barrier and one load latency less per pair)
+  for (int idx = tid; idx < nt * ns; idx += T) {
+    const int kt = idx / ns, ks = idx % ns;
+    long long off = -1;
+    if (!(P == Q && ks > kt)) {
+      const int t = A.cl_col[c0 + t0 + kt], s = A.cl_col[c0 + s0 + ks];
+      if (A.tri_off) {  // dense triangular table (levels with M <= 8192): one load
+        off = __ldg(A.tri_off + static_cast<int64_t>(t) * (t + 1) / 2 + s);
+        if (off < 0) set_error(A.err, kErrPattern, A.level, i);
+      } else {  // binary search of the squared pattern
         const int64_t slot = find_slot(A.sq_ptr, A.sq_col, A.sq_slot, t, s);
         if (slot < 0) set_error(A.err, kErrPattern, A.level, i);
         else off = A.slot_off[slot];
       }
-      slot_tab[idx] = off;
     }
+    slot_tab[idx] = off;
   }
   __syncthreads();
-  if (A.tri_off) {  // one independent load per pair
-    for (int idx = tid; idx < nt * ns; idx += T) {
-      const int kt = idx / ns, ks = idx % ns;
-      long long off = -1;
-      if (!(P == Q && ks > kt)) {
-        const int t = col_t[kt], s = col_s[ks];
-        off = __ldg(A.tri_off + static_cast<int64_t>(t) * (t + 1) / 2 + s);
-        if (off < 0) set_error(A.err, kErrPattern, A.level, i);
-      }
-      slot_tab[idx] = off;
-    }
-    __syncthreads();
-  }
   const long long tb1 = clock64();
   prof_add(A, kProfBSetup, tb1 - tb0);
   const int rsn = n_live[0], rtn = n_live[1];
