@@ -36,6 +36,9 @@
 #ifndef CE_NO_WIDE_JACOBI
 #define CE_NO_WIDE_JACOBI 0
 #endif
+#ifndef CE_TILE_TRANSPOSED
+#define CE_TILE_TRANSPOSED 1  // Schur tiles with the s panel along the accumulator rows (coalesced X accesses)
+#endif
 #ifndef CE_STAGE_ASYNC
 #define CE_STAGE_ASYNC 1  // Schur panels staged with cp.async in the shared-memory build
 #endif

@@ -1606,6 +1606,43 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
   // the epilogue scatters into the (t, s) blocks.
   const int g = lane >> 2, t4 = lane & 3;
   const int ntx = (rtn + 15) / 16, nty = (rsn + 31) / 32;
+#if CE_TILE_TRANSPOSED
+  // Transposed fragments: the warp's 16 x 32 tile (16 compacted t-rows x, 32 compacted s-rows y)
+  // is computed as (G_s G_t^T)^T, i.e. the accumulator fragments have y along their rows.  Lane
+  // (g, t4) then owns y = yb + 8 fy + g and x = xb + 8 fx + 2 t4 + e: one load instruction reads,
+  // for each of 4 X rows, 8 CONTIGUOUS doubles across the lanes g (every 32-byte sector of an X
+  // row is requested from L2 once per tile; with x along the fragment rows a lane's two adjacent
+  // columns came from two instructions and every sector was requested twice).  Same products
+  // summed in the same order: bit-identical results.
+  int ktv[4], xlv[4], ksv[4], ylv[4], bsv[4];
+  double xv[4][4];  // [2 fx + e][fy]
+  auto load_tile = [&](int wt) {
+    const int xb = (wt / nty) * 16, yb = (wt % nty) * 32;
+#pragma unroll
+    for (int xi = 0; xi < 4; ++xi) {
+      const int x = xb + 8 * (xi >> 1) + 2 * t4 + (xi & 1);
+      ktv[xi] = x < rtn ? xblk[x] : -1;
+      xlv[xi] = x < rtn ? xloc[x] : 0;
+    }
+#pragma unroll
+    for (int fy = 0; fy < 4; ++fy) {
+      const int y = yb + 8 * fy + g;
+      ksv[fy] = y < rsn ? yblk[y] : -1;
+      ylv[fy] = y < rsn ? yloc[y] : 0;
+      bsv[fy] = ksv[fy] >= 0 ? tab_bs[ksv[fy]] : 0;
+    }
+#pragma unroll
+    for (int xi = 0; xi < 4; ++xi)
+#pragma unroll
+      for (int fy = 0; fy < 4; ++fy) {
+        xv[xi][fy] = 0.0;
+        if (ktv[xi] >= 0 && ksv[fy] >= 0) {
+          const long long off = slot_tab[ktv[xi] * ns + ksv[fy]];
+          if (off >= 0) xv[xi][fy] = ldg(A.store + off + static_cast<int64_t>(xlv[xi]) * bsv[fy] + ylv[fy]);
+        }
+      }
+  };
+#else
   int ktv[2], xlv[2], ksv[8], ylv[8], bsv[8];
   double xv[2][8];
   auto load_tile = [&](int wt) {
@@ -1634,6 +1671,7 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
         }
       }
   };
+#endif
   // first tile's X in flight while the panels are staged
   if (warp < ntx * nty) load_tile(warp);
   // g rows transposed into shared memory: GsT[q][y], GtT[q][x] (live rows only)
@@ -1696,6 +1734,47 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
 #endif
   const long long tb2 = clock64();
   prof_add(A, kProfBStage, tb2 - tb1);
+#if CE_TILE_TRANSPOSED
+  for (int wt = warp; wt < ntx * nty; wt += T / 32) {
+    if (wt != warp) load_tile(wt);
+    const int xb = (wt / nty) * 16, yb = (wt % nty) * 32;
+    double acc[4][2][2];  // [fy][fx][e]
+#pragma unroll
+    for (int fy = 0; fy < 4; ++fy)
+#pragma unroll
+      for (int fx = 0; fx < 2; ++fx) acc[fy][fx][0] = acc[fy][fx][1] = 0.0;
+    for (int q0 = 0; q0 < w; q0 += 4) {
+      const int q = q0 + t4;
+      double af[4], bf[2];
+#pragma unroll
+      for (int fy = 0; fy < 4; ++fy) {
+        const int y = yb + 8 * fy + g;
+        af[fy] = (q < w && y < lds) ? GsT[q * lds + y] : 0.0;
+      }
+#pragma unroll
+      for (int fx = 0; fx < 2; ++fx) {
+        const int x = xb + 8 * fx + g;
+        bf[fx] = (q < w && x < ldt) ? GtT[q * ldt + x] : 0.0;
+      }
+#pragma unroll
+      for (int fy = 0; fy < 4; ++fy)
+#pragma unroll
+        for (int fx = 0; fx < 2; ++fx)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[fy][fx][0]), "+d"(acc[fy][fx][1])
+                       : "d"(af[fy]), "d"(bf[fx]));
+    }
+#pragma unroll
+    for (int xi = 0; xi < 4; ++xi)
+#pragma unroll
+      for (int fy = 0; fy < 4; ++fy)
+        if (ktv[xi] >= 0 && ksv[fy] >= 0) {
+          const long long off = slot_tab[ktv[xi] * ns + ksv[fy]];
+          if (off >= 0)
+            A.store[off + static_cast<int64_t>(xlv[xi]) * bsv[fy] + ylv[fy]] = xv[xi][fy] - acc[fy][xi >> 1][xi & 1];
+        }
+  }
+#else
   for (int wt = warp; wt < ntx * nty; wt += T / 32) {
     if (wt != warp) load_tile(wt);
     const int xb = (wt / nty) * 16, yb = (wt % nty) * 32;
@@ -1735,6 +1814,7 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
             A.store[off + static_cast<int64_t>(xlv[i2]) * bsv[j2] + ylv[j2]] = xv[i2][j2] - acc[i2][j2];
         }
   }
+#endif
   __syncthreads();
   prof_add(A, kProfBTiles, clock64() - tb2);
 }
