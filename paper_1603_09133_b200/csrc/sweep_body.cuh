@@ -1614,9 +1614,10 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
   // row is requested from L2 once per tile; with x along the fragment rows a lane's two adjacent
   // columns came from two instructions and every sector was requested twice).  Same products
   // summed in the same order: bit-identical results.
-  int ktv[4], xlv[4], ksv[4], ylv[4], bsv[4];
-  double xv[4][4];  // [2 fx + e][fy]
+  double* px[4][4];  // element addresses of the lane's 16 X entries (nullptr: outside the live tile)
+  double xv[4][4];   // [2 fx + e][fy]
   auto load_tile = [&](int wt) {
+    int ktv[4], xlv[4], ksv[4], ylv[4], bsv[4];
     const int xb = (wt / nty) * 16, yb = (wt % nty) * 32;
 #pragma unroll
     for (int xi = 0; xi < 4; ++xi) {
@@ -1636,9 +1637,13 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
 #pragma unroll
       for (int fy = 0; fy < 4; ++fy) {
         xv[xi][fy] = 0.0;
+        px[xi][fy] = nullptr;
         if (ktv[xi] >= 0 && ksv[fy] >= 0) {
           const long long off = slot_tab[ktv[xi] * ns + ksv[fy]];
-          if (off >= 0) xv[xi][fy] = ldg(A.store + off + static_cast<int64_t>(xlv[xi]) * bsv[fy] + ylv[fy]);
+          if (off >= 0) {
+            px[xi][fy] = A.store + off + static_cast<int64_t>(xlv[xi]) * bsv[fy] + ylv[fy];
+            xv[xi][fy] = ldg(px[xi][fy]);
+          }
         }
       }
   };
@@ -1768,11 +1773,7 @@ __device__ __noinline__ void panel_update(const SweepArgs& A, int i, int r, int 
     for (int xi = 0; xi < 4; ++xi)
 #pragma unroll
       for (int fy = 0; fy < 4; ++fy)
-        if (ktv[xi] >= 0 && ksv[fy] >= 0) {
-          const long long off = slot_tab[ktv[xi] * ns + ksv[fy]];
-          if (off >= 0)
-            A.store[off + static_cast<int64_t>(xlv[xi]) * bsv[fy] + ylv[fy]] = xv[xi][fy] - acc[fy][xi >> 1][xi & 1];
-        }
+        if (px[xi][fy]) *px[xi][fy] = xv[xi][fy] - acc[fy][xi >> 1][xi & 1];
   }
 #else
   for (int wt = warp; wt < ntx * nty; wt += T / 32) {
